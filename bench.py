@@ -1,0 +1,361 @@
+#!/usr/bin/env python
+"""Benchmark of the fused SymPhase sampling hot path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2] [--impl ours|reference]
+
+A step = one fused sampling pass (Philox draws + GF(2) product + bit-packed
+measurement records written to HBM) over this rank's shot range of the
+workload. Default workload: BASELINE.json configs[1] (rotated surface code
+d=5, 5 rounds, p=1e-3, 10^7 shots per GPU). For N > 1 every rank samples a
+disjoint global shot range (weak scaling) and the per-measurement flip counts
+are all-reduced over NCCL (the path's only exchange).
+
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "sampled measurement bits/sec"
+UNIT = "bits/s"
+R_INT_PLANNING = 148 * 64 * 1.965e9  # LOP3-class ops/s (SURVEY §8(d) planning value)
+
+WORKLOADS = {
+    "cfg1": ("cfg1: repetition code d=5, 5 rounds, p=0.01 (BASELINE.json configs[0])", 10**6),
+    "cfg2": ("cfg2: rotated surface-code memory-Z d=5, 5 rounds, 49 qubits, p=1e-3 "
+             "(BASELINE.json configs[1])", 10**7),
+    "cfg3": ("cfg3: rotated surface-code memory-Z d=15, 15 rounds, 449 qubits, p=1e-3 "
+             "(BASELINE.json configs[2])", 10**8),
+    "cfg4": ("cfg4: random Clifford n=1000, 100 layers, DEPOLARIZE1(1e-3) "
+             "(BASELINE.json configs[3])", 10**6),
+}
+
+
+def circuit_text(cfg: str) -> str:
+    from paper_2311_03906_b200 import circuits as CI
+    return CI.CONFIGS[cfg]["text"]()
+
+
+def measured_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def algorithmic(init, n_shots: int):
+    """bytes = ceil(n_m N / 8) + CSR-of-variables M_sym bytes;
+    ops = N * sum_v min(c_v/32, q_v * min(c_v, ceil(n_m/32)))."""
+    nbytes = (init.n_meas * n_shots + 7) // 8 + 4 * init.nnz + 8 * (init.n_sym + 1)
+    col = np.bincount(init.sym_idx.astype(np.int64), minlength=init.n_sym).astype(np.float64)
+    q = np.zeros(init.n_sym)
+    g = init.groups
+    for d, p, f, a in zip(g["dist"], g["param"], g["first_symbol"], g["arity"]):
+        if d == 0:
+            continue
+        if d == 2:
+            q[f] = 0.5
+        elif d == 1:
+            q[f] = p
+        elif d == 3:
+            q[f:f + 2] = 2 * p / 3
+        elif d == 4:
+            q[f:f + 4] = 8 * p / 15
+    per_shot = np.minimum(col / 32.0, q * np.minimum(col, (init.n_meas + 31) // 32)).sum()
+    return nbytes, per_shot * n_shots
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in self.lines:
+            f = [x.strip() for x in l.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_reference_rate(init_text: str, n_meas: int, target_s: float, seed: int = 42):
+    """The reference CPU sampler on this host: oracle/_ref (the unmodified
+    reference library), draw_assignments + sample + encode_shots(b8) per
+    shot chunk on every host thread; else the C port (1 thread)."""
+    import oracle
+    threads = os.cpu_count() or 1
+    if oracle.have_ref():
+        c = oracle.Ref().circuit(init_text)
+        chunk = 16384
+        probe = max(chunk * threads, chunk)
+        t = c.time(probe, chunk, threads, seed, 1)
+        shots = int(max(probe, min(probe * target_s / max(t, 1e-6), 2e8)))
+        shots = (shots + chunk - 1) // chunk * chunk
+        t = c.time(shots, chunk, threads, seed, 1)
+        sample = (f"{shots} shots of the workload circuit, {chunk}-shot chunks over {threads} "
+                  f"threads; each chunk = reference draw_assignments + sample(threads=1) + "
+                  f"encode_shots(b8) (cliffsym.cpp:108-113 timed region)")
+        return n_meas * shots / t, threads, "reference", sample, t
+    from paper_2311_03906_b200 import run_initialization
+    port = oracle.Port()
+    init = run_initialization(init_text)
+    shots = 20000
+    t0 = time.perf_counter()
+    S = port.draw_assignments(init, shots, seed)
+    m = port.sample(init.row_ptr, init.sym_idx, S, shots)
+    port.encode(m, init.n_meas, shots, "b8")
+    t = time.perf_counter() - t0
+    return n_meas * shots / t, 1, "port", f"{shots} shots, oracle C port, 1 thread", t
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    desc, shots_per_gpu = WORKLOADS[args.config]
+    text = circuit_text(args.config)
+    from paper_2311_03906_b200 import run_initialization
+    n_meas = run_initialization(text).n_meas
+    rates, cores, kind, sample = [], 1, "port", ""
+    per_step = float(os.environ.get("SP_REF_STEP_SECONDS", "4"))
+    for i in range(args.warmup + args.steps):
+        r, cores, kind, sample, _ = cpu_reference_rate(text, n_meas, per_step, seed=42 + i)
+        if i >= args.warmup:
+            rates.append(r)
+    value = statistics.median(rates)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": per_step * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "config": {"workload": desc, "shots_per_gpu": shots_per_gpu,
+                   "parallelism": "host threads (reference has no GPU path)"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    torch.cuda.set_device(local)
+    dev = torch.device(f"cuda:{local}")
+
+    from paper_2311_03906_b200 import Sampler, run_initialization
+
+    desc, shots = WORKLOADS[args.config]
+    if args.shots:
+        shots = args.shots
+    text = circuit_text(args.config)
+    t0 = time.perf_counter()
+    init = run_initialization(text)
+    init_s = time.perf_counter() - t0
+    smp = Sampler(init, device=local)
+    T = smp.shot_tile
+    shots = (shots + T - 1) // T * T
+    shot_begin = rank * shots  # disjoint global shot ranges, tile-aligned
+    out = smp.empty_bits(init.n_meas, shots)
+    counts = torch.zeros(init.n_meas, dtype=torch.int64, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    stream = torch.cuda.current_stream()
+
+    def step(i):
+        smp.sample(shots, 1000 + i, shot_begin=shot_begin, out=out, counts=counts)
+        if world > 1:
+            dist.all_reduce(counts)
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches0 = smp.launches
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        wall0 = time.perf_counter()
+        for i in range(args.steps):
+            flush.zero_()  # L2 flush between timed iterations, outside the events
+            evs[i][0].record(stream)
+            step(args.warmup + i)
+            evs[i][1].record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        wall = time.perf_counter() - wall0
+    launches = smp.launches - launches0
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    t_step = sum(step_ms) / len(step_ms) / 1e3
+    t_tensor = torch.tensor([t_step], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_tensor, op=dist.ReduceOp.MAX)
+    t_max = float(t_tensor.item())
+    value = init.n_meas * shots * world / t_max
+
+    # Kernel-only timing (no collective) for the roofline, same stream.
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(max(3, args.steps))]
+    for i, (a, b) in enumerate(kev):
+        flush.zero_()
+        a.record(stream)
+        smp.sample(shots, 5000 + i, shot_begin=shot_begin, out=out)
+        b.record(stream)
+    torch.cuda.synchronize()
+    k_ms = statistics.mean(a.elapsed_time(b) for a, b in kev)
+
+    # End to end through the public API with HOST buffers: each step uploads
+    # the model (M_sym CSR + group table) from host memory, samples, encodes
+    # the reference's b8 records on the device and copies them to pinned host
+    # memory (cmd_sample's timed region, cliffsym.cpp:108-113).
+    e2e_n = shots
+    host_out = torch.empty(smp.encoded_size(e2e_n, "b8"), dtype=torch.uint8, pin_memory=True)
+    h2d = init.row_ptr.nbytes + init.sym_idx.nbytes + init.groups.nbytes
+    e2e_t = []
+    for i in range(args.warmup + args.steps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        smp.load(init)
+        _, written = smp.sample_to_host(e2e_n, 9000 + i, "b8", shot_begin=shot_begin,
+                                        out=host_out)
+        t = time.perf_counter() - t0
+        if i >= args.warmup:
+            e2e_t.append(t)
+    e2e_tensor = torch.tensor([statistics.mean(e2e_t)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_tensor, op=dist.ReduceOp.MAX)
+    e2e_value = init.n_meas * e2e_n * world / float(e2e_tensor.item())
+
+    if rank == 0:
+        peak, peak_src = measured_peaks()
+        nbytes, ops = algorithmic(init, shots)
+        achieved = nbytes / (k_ms / 1e3) / 1e9
+        t_hbm, t_int = nbytes / (peak * 1e9), ops / R_INT_PLANNING
+        traffic = None
+        tp = ROOT / "profiles" / "ncu_traffic.json"
+        if tp.exists():
+            tr = json.loads(tp.read_text()).get(args.config)
+            if tr and tr.get("shots") == shots:
+                traffic = tr.get("dram_bytes")
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+            "data": "synthetic (seeded circuit generators, SURVEY Appendix A; seeds 1000+i)",
+            "config": {
+                "workload": desc, "shots_per_gpu": shots, "n_meas": init.n_meas,
+                "n_sym": init.n_sym, "nnz": init.nnz, "shot_tile": T,
+                "parallelism": f"shot-range sharding x{world}" + (", NCCL all_reduce of "
+                               "per-measurement counts" if world > 1 else ""),
+                "output": "measurement-major u64 bit-sliced records in HBM + per-row counts",
+                "l2": "flushed between timed steps (256 MiB memset outside the events); "
+                      "output per step > L2",
+                "init_seconds": round(init_s, 4),
+            },
+            "roofline": {
+                "bound": "hbm" if t_hbm >= t_int else "int", "achieved": achieved,
+                "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                "kernel": "k1_fused", "kernel_ms": k_ms, "alg_bytes": nbytes,
+                "alg_int_ops": ops, "t_hbm_ms": t_hbm * 1e3, "t_int_ms": t_int * 1e3,
+                "frac_of_roofline_time": max(t_hbm, t_int) * 1e3 / k_ms,
+                "frac_vs_8TBs": (nbytes / (k_ms / 1e3)) / 8.0e12,
+                "peak_source": peak_src,
+            },
+            "clocks": clk.summary(),
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(written),
+                    "path": "Sampler.load + Sampler.sample_to_host (C ABI sp_load_msym_csr/"
+                            "sp_load_groups/sp_sample_to_host), b8 records to pinned host"},
+            "gpu_launches": launches,
+            "wall_s_timed": wall,
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            r, cores, kind, sample, t = cpu_reference_rate(text, init.n_meas, 10.0)
+            line["cpu_baseline"] = {"value": r, "unit": UNIT, "cores": cores, "kind": kind,
+                                    "sample": sample, "seconds": round(t, 3)}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="cfg2", choices=sorted(WORKLOADS))
+    ap.add_argument("--shots", type=int, default=0, help="override shots per GPU")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,168 @@
+/*
+ * symphase_b200.h — C ABI of the B200-native SymPhase sampling hot path.
+ *
+ * Drop-in boundary for the reference's sampler operator API (cliffsym,
+ * proj/core/include/cliffsym/sampler.hpp). The reference has no C ABI of its
+ * own; each entry point below names the reference call it replaces.
+ *
+ * Conventions
+ *   - Return SP_OK (0) or a negative sp_status; sp_last_error() returns a
+ *     thread-local message for the last failure on the calling thread.
+ *   - Exception mapping of the reference (sampler.cpp:50, 63-67;
+ *     bit_matrix.cpp:288, 322): std::invalid_argument -> SP_ERR_INVALID_ARGUMENT,
+ *     std::out_of_range -> SP_ERR_OUT_OF_RANGE, ParseError -> SP_ERR_PARSE,
+ *     std::logic_error -> SP_ERR_LOGIC.
+ *   - One host thread per context, one context per device. Device work is
+ *     asynchronous on the context's stream (sp_set_stream); pointers named
+ *     d_* are device pointers, h_* host pointers. The caller owns every
+ *     buffer it passes in.
+ *   - Bit-sliced layout ("measurement-major" for results, "symbol-major" for
+ *     assignments): u64 words, row-major with leading dimension ld (in
+ *     words); bit j%64 of word j/64 of row r is element (r, j). Rows are
+ *     measurements (or symbols), columns are shots. This is the logical
+ *     orientation of the reference's SampleMatrix / SymbolAssignmentBatch
+ *     (sampler.hpp:32-46) with the BitVec bit order (bitvec.hpp:21-23).
+ *     Padding bits past n_shots are written as zero.
+ */
+#ifndef SYMPHASE_B200_H
+#define SYMPHASE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SP_ABI_VERSION 1
+
+typedef enum {
+  SP_OK = 0,
+  SP_ERR_INVALID_ARGUMENT = -1, /* std::invalid_argument */
+  SP_ERR_OUT_OF_RANGE = -2,     /* std::out_of_range */
+  SP_ERR_PARSE = -3,            /* cliffsym::ParseError (circuit.hpp:42-47) */
+  SP_ERR_LOGIC = -4,            /* std::logic_error */
+  SP_ERR_CUDA = -5,             /* CUDA runtime failure */
+  SP_ERR_NOT_LOADED = -6,       /* M_sym / channel table not loaded yet */
+  SP_ERR_UNSUPPORTED = -7       /* shape outside what a kernel handles */
+} sp_status;
+
+/* GroupDistribution, symbols.hpp:19-25 (same numbering). */
+enum {
+  SP_DIST_CONSTANT = 0,
+  SP_DIST_BERNOULLI = 1,
+  SP_DIST_COIN = 2,
+  SP_DIST_DEPOLARIZE1 = 3,
+  SP_DIST_DEPOLARIZE2 = 4
+};
+
+/* SymbolGroup, symbols.hpp:36-42 (instruction_index dropped). */
+typedef struct {
+  uint8_t dist;
+  uint8_t reserved[7];
+  double param;
+  uint32_t first_symbol;
+  uint32_t arity;
+} sp_group;
+
+typedef enum {
+  SP_RNG_PHILOX = 0,          /* counter-based Philox4x32-10 + geometric skip (default) */
+  SP_RNG_COMPAT_SPLITMIX = 1  /* bit-exact keyed_draw/fill_group (sampler.hpp:14-28, sampler.cpp:11-44) */
+} sp_rng;
+
+typedef enum { SP_FMT_01 = 0, SP_FMT_B8 = 1 } sp_format; /* ShotFormat, sampler.hpp:60-63 */
+
+typedef enum {
+  SP_PRODUCT_AUTO = 0,
+  SP_PRODUCT_SPARSE = 1, /* CSR over measurements (expression lists) */
+  SP_PRODUCT_DENSE = 2   /* dense row-major M_sym words, Four-Russians tables */
+} sp_product;
+
+typedef struct sp_ctx sp_ctx;
+typedef struct sp_model sp_model;
+
+const char* sp_last_error(void);
+int sp_abi_version(void);
+
+/* ---- host front end: parse_circuit (circuit.hpp:55) + run_initialization
+ *      (tableau.hpp:101). Produces InitResult.expressions (CSR rows of M_sym,
+ *      sorted symbol ids) and InitResult.registry (the group table). ------- */
+int sp_model_from_text(const char* text, sp_model** out);
+void sp_model_destroy(sp_model* m);
+int sp_model_dims(const sp_model* m, uint64_t* n_qubits, uint64_t* n_meas, uint64_t* n_sym,
+                  uint64_t* n_groups, uint64_t* nnz);
+/* row_ptr[n_meas+1], sym_idx[nnz], groups[n_groups]; any may be NULL. */
+int sp_model_export(const sp_model* m, uint64_t* row_ptr, uint32_t* sym_idx, sp_group* groups);
+
+/* ---- device context ---------------------------------------------------- */
+int sp_ctx_create(int device, sp_ctx** out);
+void sp_ctx_destroy(sp_ctx* ctx);
+int sp_set_stream(sp_ctx* ctx, void* cuda_stream); /* cudaStream_t; NULL = legacy default */
+int sp_set_rng(sp_ctx* ctx, sp_rng rng);
+int sp_set_product(sp_ctx* ctx, sp_product variant);
+
+/* M_sym as the reference's expression list: row k = sorted symbol ids of
+ * measurement k (MeasurementExpression, symbols.hpp:90-100). Host pointers.
+ * The library derives CSR-of-variables (per-symbol measurement lists), the
+ * dense row-major words and the per-channel sampling plan on the device. */
+int sp_load_msym_csr(sp_ctx* ctx, uint64_t n_meas, uint64_t n_sym, const uint64_t* h_row_ptr,
+                     const uint32_t* h_sym_idx);
+/* M_sym as dense row-major words [n_meas][ld_words] (bit s of row k = 1 iff
+ * symbol s appears in measurement k). Host pointer. */
+int sp_load_msym_dense(sp_ctx* ctx, uint64_t n_meas, uint64_t n_sym, const uint64_t* h_words,
+                       uint64_t ld_words);
+/* SymbolRegistry groups (symbols.hpp:47-86). Host pointer; group 0 must be
+ * the constant group. */
+int sp_load_groups(sp_ctx* ctx, uint64_t n_groups, const sp_group* h_groups);
+int sp_load_model(sp_ctx* ctx, const sp_model* m); /* = csr + groups */
+
+/* Shot-tile size T of the fused sampler for the loaded model. Random streams
+ * are keyed by (seed, global T-shot tile), so any split of a shot range into
+ * calls whose shot_begin is a multiple of T — one GPU or many — yields the
+ * same bits. */
+int sp_shot_tile(sp_ctx* ctx, uint64_t* tile);
+
+/* K1 — fused sampler: draw_assignments + sample (sampler.cpp:48-112) in one
+ * kernel. d_out: measurement-major [n_meas][ld], ld >= ceil(n_shots/64).
+ * Column j of d_out is global shot shot_begin + j; shot_begin % T == 0.
+ * d_counts (nullable): u64 [n_meas], += number of shots with outcome 1. */
+int sp_sample(sp_ctx* ctx, uint64_t seed, uint64_t shot_begin, uint64_t n_shots,
+              uint64_t* d_out, uint64_t ld, uint64_t* d_counts);
+
+/* draw_assignments (sampler.hpp:51-52) on the device: the exact assignment
+ * matrix S the fused sampler uses for these shots (row 0 = constant = all
+ * ones). d_S: [n_sym][ldS]. With SP_RNG_COMPAT_SPLITMIX it is bit-identical
+ * to the reference's draw_assignments(registry, n, seed) when shot_begin=0. */
+int sp_draw_assignments(sp_ctx* ctx, uint64_t seed, uint64_t shot_begin, uint64_t n_shots,
+                        uint64_t* d_S, uint64_t ldS);
+
+/* K2 — sample(expressions, batch) / gf2_multiply_sparse on a supplied
+ * batch (sampler.cpp:61-112, bit_matrix.cpp:314-328). d_S: [n_sym_S][ldS].
+ * SP_ERR_OUT_OF_RANGE if an expression names a symbol >= n_sym_S
+ * (sampler.cpp:63-67). */
+int sp_sample_given_S(sp_ctx* ctx, const uint64_t* d_S, uint64_t n_sym_S, uint64_t ldS,
+                      uint64_t n_shots, uint64_t* d_out, uint64_t ld);
+
+/* K3 — encode_shots (sampler.cpp:118-140) on the device. Writes
+ * sp_encoded_size() bytes to d_bytes. */
+uint64_t sp_encoded_size(uint64_t n_meas, uint64_t n_shots, sp_format fmt);
+int sp_encode(sp_ctx* ctx, const uint64_t* d_m, uint64_t ld, uint64_t n_meas, uint64_t n_shots,
+              sp_format fmt, uint8_t* d_bytes);
+
+/* The cmd_sample timed region (cliffsym.cpp:108-113) with a HOST output:
+ * fused sample + device encode + device->host copy into h_out (pinned or
+ * pageable), synchronous. cap = capacity of h_out in bytes. */
+int sp_sample_to_host(sp_ctx* ctx, uint64_t seed, uint64_t shot_begin, uint64_t n_shots,
+                      sp_format fmt, uint8_t* h_out, uint64_t cap, uint64_t* written);
+
+/* Test hook: one Philox4x32-10 block on the device. ctr_key = {c0,c1,c2,c3,k0,k1}. */
+int sp_debug_philox(sp_ctx* ctx, const uint32_t* ctr_key, uint32_t* out);
+
+/* Number of kernel launches this context has issued so far. */
+uint64_t sp_launch_count(const sp_ctx* ctx);
+int sp_synchronize(sp_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SYMPHASE_B200_H */

@@ -1,0 +1,239 @@
+"""Synthetic circuit generators for the BASELINE.json configurations.
+
+The reference ships none of these workloads (its own generators,
+circuit_gen.cpp:56-106, are the paper's Fig. 3 families), so these follow
+SURVEY.md Appendix A. All circuits use only instructions the reference parser
+accepts (circuit.cpp:51-69): H S S_DAG X Y Z CX M R X_ERROR Y_ERROR Z_ERROR
+DEPOLARIZE1 DEPOLARIZE2 TICK.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+
+class MT19937_64:
+    """std::mt19937_64 (the reference's test RNG), for seeded generators."""
+
+    _N, _M = 312, 156
+    _MATRIX_A = 0xB5026F5AA96619E9
+    _UM, _LM = 0xFFFFFFFF80000000, 0x7FFFFFFF
+    _MASK = (1 << 64) - 1
+
+    def __init__(self, seed: int = 5489):
+        self.mt = [0] * self._N
+        self.mt[0] = seed & self._MASK
+        for i in range(1, self._N):
+            prev = self.mt[i - 1]
+            self.mt[i] = (6364136223846793005 * (prev ^ (prev >> 62)) + i) & self._MASK
+        self.idx = self._N
+
+    def _twist(self):
+        mt, N, M = self.mt, self._N, self._M
+        for i in range(N):
+            x = (mt[i] & self._UM) | (mt[(i + 1) % N] & self._LM)
+            xa = x >> 1
+            if x & 1:
+                xa ^= self._MATRIX_A
+            mt[i] = mt[(i + M) % N] ^ xa
+        self.idx = 0
+
+    def __call__(self) -> int:
+        if self.idx >= self._N:
+            self._twist()
+        x = self.mt[self.idx]
+        self.idx += 1
+        x ^= (x >> 29) & 0x5555555555555555
+        x ^= (x << 17) & 0x71D67FFFEDA60000
+        x ^= (x << 37) & 0xFFF7EEE000000000
+        x ^= x >> 43
+        return x & self._MASK
+
+    def below(self, n: int) -> int:
+        """Uniform integer in [0, n) by rejection (no modulo bias)."""
+        lim = (1 << 64) - ((1 << 64) % n)
+        while True:
+            v = self()
+            if v < lim:
+                return v % n
+
+
+def _fmt(name, targets, p=None):
+    head = name if p is None else f"{name}({p!r})"
+    return head + " " + " ".join(str(t) for t in targets)
+
+
+def repetition_code(distance: int = 5, rounds: int = 5, p: float = 0.01) -> str:
+    """BASELINE config 1: data on even, ancillas on odd qubits."""
+    data = [2 * i for i in range(distance)]
+    anc = [2 * i + 1 for i in range(distance - 1)]
+    left = [(2 * i, 2 * i + 1) for i in range(distance - 1)]
+    right = [(2 * i + 2, 2 * i + 1) for i in range(distance - 1)]
+    out = []
+    for _ in range(rounds):
+        out.append(_fmt("R", anc))
+        out.append(_fmt("X_ERROR", anc, p))
+        for pairs in (left, right):
+            flat = [q for pr in pairs for q in pr]
+            out.append(_fmt("CX", flat))
+            out.append(_fmt("DEPOLARIZE2", flat, p))
+        out.append(_fmt("X_ERROR", anc, p))
+        out.append(_fmt("M", anc))
+    out.append(_fmt("X_ERROR", data, p))
+    out.append(_fmt("M", data))
+    return "\n".join(out) + "\n"
+
+
+@dataclass
+class SurfaceLayout:
+    data: list
+    xanc: list
+    zanc: list
+    index: dict
+
+
+def surface_layout(d: int) -> SurfaceLayout:
+    data = [(x, y) for x in range(1, 2 * d, 2) for y in range(1, 2 * d, 2)]
+    dset = set(data)
+    xanc, zanc = [], []
+    for x in range(0, 2 * d + 1, 2):
+        for y in range(0, 2 * d + 1, 2):
+            is_x = ((x + y) // 2) % 2 == 0
+            nb = sum((x + dx, y + dy) in dset for dx in (-1, 1) for dy in (-1, 1))
+            boundary = (y in (0, 2 * d)) if is_x else (x in (0, 2 * d))
+            if nb == 4 or (nb == 2 and boundary):
+                (xanc if is_x else zanc).append((x, y))
+    order = data + xanc + zanc
+    return SurfaceLayout(data, xanc, zanc, {c: i for i, c in enumerate(order)})
+
+
+def surface_code(d: int = 5, rounds: int | None = None, p: float = 1e-3) -> str:
+    """BASELINE configs 2/3: rotated surface-code memory-Z."""
+    rounds = d if rounds is None else rounds
+    L = surface_layout(d)
+    ix = L.index
+    dset = set(L.data)
+    data = [ix[c] for c in L.data]
+    xa = [ix[c] for c in L.xanc]
+    za = [ix[c] for c in L.zanc]
+    anc = xa + za
+    allq = sorted(ix.values())
+    x_off = [(1, 1), (-1, 1), (1, -1), (-1, -1)]
+    z_off = [(1, 1), (1, -1), (-1, 1), (-1, -1)]
+    layers = []
+    for l in range(4):
+        pairs = []
+        for (x, y) in L.xanc:
+            nb = (x + x_off[l][0], y + x_off[l][1])
+            if nb in dset:
+                pairs.append((ix[(x, y)], ix[nb]))
+        for (x, y) in L.zanc:
+            nb = (x + z_off[l][0], y + z_off[l][1])
+            if nb in dset:
+                pairs.append((ix[nb], ix[(x, y)]))
+        layers.append(pairs)
+    out = []
+    for _ in range(rounds):
+        out.append(_fmt("R", anc))
+        out.append(_fmt("X_ERROR", anc, p))
+        out.append(_fmt("DEPOLARIZE1", data, p))
+        out.append(_fmt("H", xa))
+        out.append(_fmt("DEPOLARIZE1", allq, p))
+        for pairs in layers:
+            flat = [q for pr in pairs for q in pr]
+            busy = set(flat)
+            out.append(_fmt("CX", flat))
+            out.append(_fmt("DEPOLARIZE2", flat, p))
+            idle = [q for q in allq if q not in busy]
+            if idle:
+                out.append(_fmt("DEPOLARIZE1", idle, p))
+        out.append(_fmt("H", xa))
+        out.append(_fmt("DEPOLARIZE1", allq, p))
+        out.append(_fmt("X_ERROR", anc, p))
+        out.append(_fmt("M", anc))
+        out.append(_fmt("DEPOLARIZE1", data, p))
+    out.append(_fmt("X_ERROR", data, p))
+    out.append(_fmt("M", data))
+    return "\n".join(out) + "\n"
+
+
+def random_clifford(n: int = 1000, layers: int = 100, p: float = 1e-3, seed: int = 1,
+                    measure_every: int = 10, measure_frac: float = 0.1) -> str:
+    """BASELINE config 4: layered random Clifford circuit."""
+    rng = MT19937_64(seed)
+    out = []
+    for layer in range(1, layers + 1):
+        hs, ss = [], []
+        for q in range(n):
+            if rng() & 1:
+                (hs if rng() & 1 else ss).append(q)
+        if hs:
+            out.append(_fmt("H", hs))
+        if ss:
+            out.append(_fmt("S", ss))
+        perm = list(range(n))
+        for i in range(n - 1, 0, -1):
+            j = rng.below(i + 1)
+            perm[i], perm[j] = perm[j], perm[i]
+        flat = []
+        for i in range(0, n - 1, 2):
+            a, b = perm[i], perm[i + 1]
+            if rng() & 1:
+                a, b = b, a
+            flat += [a, b]
+        if flat:
+            out.append(_fmt("CX", flat))
+        out.append(_fmt("DEPOLARIZE1", range(n), p))
+        if layer % measure_every == 0 and layer < layers:
+            k = max(1, int(round(measure_frac * n)))
+            pool = list(range(n))
+            for i in range(k):
+                j = i + rng.below(n - i)
+                pool[i], pool[j] = pool[j], pool[i]
+            out.append(_fmt("M", sorted(pool[:k])))
+    out.append(_fmt("M", range(n)))
+    return "\n".join(out) + "\n"
+
+
+def random_test_circuit(rng: MT19937_64, n_qubits: int = 4, n_instr: int = 40,
+                        noise: bool = True, resets: bool = True) -> str:
+    """Random mixed circuits exercising every instruction kind (for parity tests)."""
+    kinds = ["H", "S", "S_DAG", "X", "Y", "Z", "CX", "M", "TICK"]
+    if resets:
+        kinds.append("R")
+    if noise:
+        kinds += ["X_ERROR", "Y_ERROR", "Z_ERROR", "DEPOLARIZE1", "DEPOLARIZE2"]
+    probs = [0.0, 0.01, 0.1, 0.25, 0.5, 1.0]
+    out = []
+    for _ in range(n_instr):
+        k = kinds[rng.below(len(kinds))]
+        if k == "TICK":
+            out.append("TICK")
+            continue
+        if k in ("CX", "DEPOLARIZE2"):
+            if n_qubits < 2:
+                continue
+            npairs = 1 + rng.below(2)
+            flat = []
+            for _ in range(npairs):
+                a = rng.below(n_qubits)
+                b = (a + 1 + rng.below(n_qubits - 1)) % n_qubits
+                flat += [a, b]
+            tg = flat
+        else:
+            tg = [rng.below(n_qubits) for _ in range(1 + rng.below(3))]
+        p = probs[rng.below(len(probs))] if k.endswith("ERROR") or k.startswith("DEPOL") else None
+        out.append(_fmt(k, tg, p))
+    out.append(_fmt("M", range(n_qubits)))
+    return "\n".join(out) + "\n"
+
+
+CONFIGS = {
+    "cfg1": dict(name="repetition d=5, 5 rounds", text=lambda: repetition_code(5, 5, 0.01),
+                 shots=10**6),
+    "cfg2": dict(name="rotated surface d=5, 5 rounds, p=1e-3",
+                 text=lambda: surface_code(5, 5, 1e-3), shots=10**7),
+    "cfg3": dict(name="rotated surface d=15, 15 rounds, p=1e-3",
+                 text=lambda: surface_code(15, 15, 1e-3), shots=10**8),
+    "cfg4": dict(name="random Clifford n=1000, 100 layers",
+                 text=lambda: random_clifford(1000, 100, 1e-3, 1), shots=10**6),
+}

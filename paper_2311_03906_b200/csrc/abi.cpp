@@ -1,0 +1,727 @@
+// C-ABI implementation (include/symphase_b200.h): context, plan building,
+// device buffers, launches. Host C++ over the CUDA runtime; no torch types.
+#include "../../include/symphase_b200.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <new>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "frontend.hpp"
+#include "kernels.cuh"
+
+using namespace symphase;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// Owned device buffer.
+struct DBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  ~DBuf() { reset(); }
+  void reset() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  template <class T>
+  T* upload(const std::vector<T>& v, cudaStream_t s) {
+    reset();
+    bytes = std::max<size_t>(v.size() * sizeof(T), 16);
+    ck(cudaMalloc(&p, bytes), "cudaMalloc");
+    if (!v.empty()) ck(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s),
+                       "cudaMemcpyAsync H2D");
+    return static_cast<T*>(p);
+  }
+  void* ensure(size_t b) {
+    if (bytes >= b && p) return p;
+    reset();
+    ck(cudaMalloc(&p, b), "cudaMalloc");
+    bytes = b;
+    return p;
+  }
+};
+
+// Host-side sampling plan derived from M_sym + the group table.
+struct HostPlan {
+  uint64_t n_meas = 0, n_sym = 0, n_groups = 0, nnz = 0;
+  std::vector<uint64_t> row_ptr;
+  std::vector<uint32_t> sym_idx;
+  uint64_t max_sym_plus1 = 0;
+  std::vector<sp_group> groups;
+  std::vector<uint64_t> dense_words;  // only if dense product requested / loaded
+  uint64_t ldm = 0;
+};
+
+}  // namespace
+
+struct sp_model {
+  Model m;
+};
+
+struct sp_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  sp_rng rng = SP_RNG_PHILOX;
+  sp_product product = SP_PRODUCT_AUTO;
+  LaunchCfg L;
+  bool have_msym = false, have_groups = false, plan_ready = false, fused_ok = false;
+  std::string fused_why;
+  HostPlan hp;
+  DevPlan dp;
+  // plan buffers
+  DBuf b_row_ptr, b_sym_idx, b_col_ptr, b_col_rows, b_dense, b_first, b_arity, b_dist, b_param,
+      b_row_const, b_row_const_compat, b_ones, b_dense_sym, b_drow_ptr, b_drow_slot, b_ch_class,
+      b_ch_lo, b_ch_hi, b_cls_dist, b_cls_inv, b_cls_goff, b_cls_groups, b_live_groups;
+  // scratch for sp_sample_to_host
+  DBuf s_out, s_bytes;
+  uint64_t launches = 0;
+};
+
+namespace {
+
+int set_device(sp_ctx* c) {
+  cudaError_t e = cudaSetDevice(c->device);
+  if (e != cudaSuccess) return fail(SP_ERR_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+  return SP_OK;
+}
+
+// Chooses the shot tile T (power of two, 128..4096): the largest whose
+// accumulation tile + coin words + counters fit a shared-memory budget that
+// leaves room for two CTAs per SM; failing that, one CTA per SM.
+int choose_tile_log2(uint64_t n_meas, uint64_t n_dense, size_t smem_optin) {
+  const size_t budgets[2] = {100 * 1024, smem_optin - 2048};
+  for (size_t budget : budgets) {
+    for (int lg = 12; lg >= 7; --lg) {
+      uint32_t tw = 1u << (lg - 5);
+      if (fused_smem_bytes(static_cast<uint32_t>(n_meas), static_cast<uint32_t>(n_dense), tw, true) <=
+          budget)
+        return lg;
+    }
+  }
+  return -1;
+}
+
+void build_plan(sp_ctx* c) {
+  HostPlan& h = c->hp;
+  DevPlan& d = c->dp;
+  cudaStream_t s = c->stream;
+  const uint64_t n_meas = h.n_meas, n_sym = h.n_sym, G = h.groups.size();
+
+  // Symbol -> group map; the registry tiles [0, n_sym) with its groups.
+  std::vector<uint32_t> sym_group(n_sym, UINT32_MAX);
+  for (uint64_t g = 0; g < G; ++g) {
+    const sp_group& gr = h.groups[g];
+    for (uint32_t b = 0; b < gr.arity; ++b) {
+      uint64_t sidx = uint64_t{gr.first_symbol} + b;
+      if (sidx >= n_sym || sym_group[sidx] != UINT32_MAX)
+        throw std::invalid_argument("group table does not tile the symbol range");
+      sym_group[sidx] = static_cast<uint32_t>(g);
+    }
+  }
+  for (uint64_t sidx = 0; sidx < n_sym; ++sidx)
+    if (sym_group[sidx] == UINT32_MAX) throw std::invalid_argument("symbol without a group");
+
+  // CSR over symbols (CSR-of-variables).
+  std::vector<uint64_t> col_ptr(n_sym + 1, 0);
+  for (uint32_t sidx : h.sym_idx) col_ptr[sidx + 1]++;
+  for (uint64_t i = 0; i < n_sym; ++i) col_ptr[i + 1] += col_ptr[i];
+  std::vector<uint32_t> col_rows(h.nnz);
+  {
+    std::vector<uint64_t> fillp(col_ptr.begin(), col_ptr.end() - 1);
+    for (uint64_t k = 0; k < n_meas; ++k)
+      for (uint64_t i = h.row_ptr[k]; i < h.row_ptr[k + 1]; ++i)
+        col_rows[fillp[h.sym_idx[i]]++] = static_cast<uint32_t>(k);
+  }
+  auto live_sym = [&](uint64_t sidx) { return col_ptr[sidx + 1] > col_ptr[sidx]; };
+
+  const size_t cw = (n_meas + 31) / 32 + 1;
+  std::vector<uint32_t> row_const(cw, 0), row_const_compat(cw, 0);
+  auto xor_rows = [&](std::vector<uint32_t>& mask, uint64_t sidx) {
+    for (uint64_t i = col_ptr[sidx]; i < col_ptr[sidx + 1]; ++i)
+      mask[col_rows[i] >> 5] ^= 1u << (col_rows[i] & 31);
+  };
+  std::vector<uint32_t> ones{0};
+  xor_rows(row_const, 0);
+  xor_rows(row_const_compat, 0);
+
+  std::vector<uint32_t> dense_live, dense_dead;
+  struct Cls {
+    uint8_t dist;
+    double p;
+    std::vector<uint32_t> groups;
+  };
+  std::vector<Cls> live_cls, dead_cls;
+  std::map<std::pair<uint8_t, uint64_t>, size_t> live_key, dead_key;
+  std::vector<uint32_t> live_groups;
+
+  for (uint64_t g = 1; g < G; ++g) {
+    const sp_group& gr = h.groups[g];
+    bool live = false;
+    for (uint32_t b = 0; b < gr.arity; ++b) live |= live_sym(gr.first_symbol + b);
+    if (live) live_groups.push_back(static_cast<uint32_t>(g));
+    const double p = gr.param;
+    switch (gr.dist) {
+      case SP_DIST_CONSTANT:
+        throw std::invalid_argument("constant group other than group 0");
+      case SP_DIST_COIN:
+        (live ? dense_live : dense_dead).push_back(gr.first_symbol);
+        continue;
+      case SP_DIST_BERNOULLI:
+        if (p == 0.5) {
+          (live ? dense_live : dense_dead).push_back(gr.first_symbol);
+          continue;
+        }
+        if (p >= 1.0) {
+          ones.push_back(gr.first_symbol);
+          xor_rows(row_const, gr.first_symbol);
+          continue;
+        }
+        break;
+      case SP_DIST_DEPOLARIZE1:
+      case SP_DIST_DEPOLARIZE2:
+        break;
+      default:
+        throw std::invalid_argument("unknown group distribution");
+    }
+    if (!(p > 0.0)) continue;  // never fires (p == 0, or NaN)
+    uint64_t pbits;
+    std::memcpy(&pbits, &p, 8);
+    auto key = std::make_pair(gr.dist, pbits);
+    auto& keymap = live ? live_key : dead_key;
+    auto& cls = live ? live_cls : dead_cls;
+    auto it = keymap.find(key);
+    if (it == keymap.end()) {
+      it = keymap.emplace(key, cls.size()).first;
+      cls.push_back(Cls{gr.dist, std::min(p, 1.0), {}});
+    }
+    cls[it->second].groups.push_back(static_cast<uint32_t>(g));
+  }
+
+  const uint64_t n_dense_live = dense_live.size();
+  int lg = choose_tile_log2(n_meas, n_dense_live, c->L.smem_optin);
+  c->fused_ok = lg >= 0;
+  if (lg < 0) {
+    c->fused_why = "M_sym has too many measurement rows for an on-chip shot tile; use "
+                   "sp_draw_assignments + sp_sample_given_S";
+    lg = 7;
+  }
+  const uint64_t T = 1ull << lg;
+
+  // Chains: each class's flattened (group, shot) space of a tile is cut
+  // into slices of ~kEvents expected firings (<= 2^24 trials).
+  constexpr double kEvents = 8.0;
+  std::vector<uint32_t> ch_class;
+  std::vector<uint64_t> ch_lo, ch_hi, cls_goff;
+  std::vector<uint8_t> cls_dist;
+  std::vector<float> cls_inv;
+  std::vector<uint32_t> cls_groups;
+  uint64_t n_chains_live = 0;
+  auto add_classes = [&](const std::vector<Cls>& cls) {
+    for (const Cls& cl : cls) {
+      const uint32_t ci = static_cast<uint32_t>(cls_dist.size());
+      cls_dist.push_back(cl.dist);
+      const double neg_ln_q = -std::log1p(-cl.p);
+      cls_inv.push_back(static_cast<float>(1.0 / neg_ln_q));  // p == 1 -> 0: fire every trial
+      cls_goff.push_back(cls_groups.size());
+      cls_groups.insert(cls_groups.end(), cl.groups.begin(), cl.groups.end());
+      const uint64_t trials = cl.groups.size() * T;
+      double len = std::ceil(kEvents / cl.p);
+      len = std::min(std::max(len, 64.0), 16777216.0);
+      uint64_t n_ch = (trials + static_cast<uint64_t>(len) - 1) / static_cast<uint64_t>(len);
+      n_ch = std::max<uint64_t>(n_ch, 1);
+      const uint64_t L = (trials + n_ch - 1) / n_ch;
+      for (uint64_t i = 0; i < n_ch; ++i) {
+        ch_class.push_back(ci);
+        ch_lo.push_back(i * L);
+        ch_hi.push_back(std::min(trials, (i + 1) * L));
+      }
+    }
+  };
+  add_classes(live_cls);
+  n_chains_live = ch_class.size();
+  add_classes(dead_cls);
+
+  // Dense slots: live first; per-row slot lists for the output pass.
+  std::vector<uint32_t> dense_sym = dense_live;
+  dense_sym.insert(dense_sym.end(), dense_dead.begin(), dense_dead.end());
+  std::vector<uint32_t> slot_of(n_sym, UINT32_MAX);
+  for (uint32_t i = 0; i < n_dense_live; ++i) slot_of[dense_live[i]] = i;
+  std::vector<uint32_t> drow_ptr(n_meas + 1, 0), drow_slot;
+  for (uint64_t k = 0; k < n_meas; ++k) {
+    for (uint64_t i = h.row_ptr[k]; i < h.row_ptr[k + 1]; ++i)
+      if (slot_of[h.sym_idx[i]] != UINT32_MAX) drow_slot.push_back(slot_of[h.sym_idx[i]]);
+    drow_ptr[k + 1] = static_cast<uint32_t>(drow_slot.size());
+  }
+
+  std::vector<uint32_t> g_first(G), g_arity(G);
+  std::vector<uint8_t> g_dist(G);
+  std::vector<double> g_param(G);
+  for (uint64_t g = 0; g < G; ++g) {
+    g_first[g] = h.groups[g].first_symbol;
+    g_arity[g] = h.groups[g].arity;
+    g_dist[g] = h.groups[g].dist;
+    g_param[g] = h.groups[g].param;
+  }
+
+  d = DevPlan{};
+  d.n_meas = static_cast<uint32_t>(n_meas);
+  d.n_sym = static_cast<uint32_t>(n_sym);
+  d.n_groups = static_cast<uint32_t>(G);
+  d.t_log2 = static_cast<uint32_t>(lg);
+  d.tw = static_cast<uint32_t>(T / 32);
+  d.row_ptr = c->b_row_ptr.upload(h.row_ptr, s);
+  d.sym_idx = c->b_sym_idx.upload(h.sym_idx, s);
+  d.col_ptr = c->b_col_ptr.upload(col_ptr, s);
+  d.col_rows = c->b_col_rows.upload(col_rows, s);
+  if (!h.dense_words.empty()) {
+    d.dense = c->b_dense.upload(h.dense_words, s);
+    d.ldm = h.ldm;
+  }
+  d.g_first = c->b_first.upload(g_first, s);
+  d.g_arity = c->b_arity.upload(g_arity, s);
+  d.g_dist = c->b_dist.upload(g_dist, s);
+  d.g_param = c->b_param.upload(g_param, s);
+  d.row_const = c->b_row_const.upload(row_const, s);
+  d.row_const_compat = c->b_row_const_compat.upload(row_const_compat, s);
+  d.n_ones = static_cast<uint32_t>(ones.size());
+  d.ones_syms = c->b_ones.upload(ones, s);
+  d.n_dense_live = static_cast<uint32_t>(n_dense_live);
+  d.n_dense_all = static_cast<uint32_t>(dense_sym.size());
+  d.dense_sym = c->b_dense_sym.upload(dense_sym, s);
+  d.drow_ptr = c->b_drow_ptr.upload(drow_ptr, s);
+  d.drow_slot = c->b_drow_slot.upload(drow_slot, s);
+  d.n_chains_live = static_cast<uint32_t>(n_chains_live);
+  d.n_chains_all = static_cast<uint32_t>(ch_class.size());
+  d.ch_class = c->b_ch_class.upload(ch_class, s);
+  d.ch_lo = c->b_ch_lo.upload(ch_lo, s);
+  d.ch_hi = c->b_ch_hi.upload(ch_hi, s);
+  d.cls_dist = c->b_cls_dist.upload(cls_dist, s);
+  d.cls_inv = c->b_cls_inv.upload(cls_inv, s);
+  d.cls_goff = c->b_cls_goff.upload(cls_goff, s);
+  d.cls_groups = c->b_cls_groups.upload(cls_groups, s);
+  d.n_live_groups = static_cast<uint32_t>(live_groups.size());
+  d.live_groups = c->b_live_groups.upload(live_groups, s);
+  ck(cudaStreamSynchronize(s), "plan upload");
+  c->plan_ready = true;
+}
+
+int ensure_plan(sp_ctx* c) {
+  if (!c->have_msym || !c->have_groups)
+    return fail(SP_ERR_NOT_LOADED, "load M_sym and the group table first");
+  if (c->plan_ready) return SP_OK;
+  try {
+    uint64_t total = 0;
+    for (const sp_group& g : c->hp.groups) total += g.arity;
+    if (total != c->hp.n_sym)
+      return fail(SP_ERR_INVALID_ARGUMENT, "group arities do not add up to n_sym");
+    build_plan(c);
+  } catch (const std::invalid_argument& e) {
+    return fail(SP_ERR_INVALID_ARGUMENT, e.what());
+  } catch (const CudaError& e) {
+    return fail(SP_ERR_CUDA, e.what());
+  } catch (const std::bad_alloc&) {
+    return fail(SP_ERR_INVALID_ARGUMENT, "host allocation failed while building the plan");
+  }
+  return SP_OK;
+}
+
+int launched(sp_ctx* c, int r, const char* what) {
+  if (r < 0) {
+    cudaError_t e = cudaGetLastError();
+    return fail(SP_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  }
+  c->launches += static_cast<uint64_t>(r);
+  return SP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* sp_last_error(void) { return g_err.c_str(); }
+int sp_abi_version(void) { return SP_ABI_VERSION; }
+
+int sp_model_from_text(const char* text, sp_model** out) {
+  if (!text || !out) return fail(SP_ERR_INVALID_ARGUMENT, "null argument");
+  try {
+    auto m = new sp_model;
+    try {
+      m->m = run_initialization(parse_circuit(text));
+    } catch (...) {
+      delete m;
+      throw;
+    }
+    *out = m;
+    return SP_OK;
+  } catch (const ParseError& e) {
+    return fail(SP_ERR_PARSE, e.what());
+  } catch (const std::logic_error& e) {
+    return fail(SP_ERR_LOGIC, e.what());
+  } catch (const std::exception& e) {
+    return fail(SP_ERR_INVALID_ARGUMENT, e.what());
+  }
+}
+
+void sp_model_destroy(sp_model* m) { delete m; }
+
+int sp_model_dims(const sp_model* m, uint64_t* n_qubits, uint64_t* n_meas, uint64_t* n_sym,
+                  uint64_t* n_groups, uint64_t* nnz) {
+  if (!m) return fail(SP_ERR_INVALID_ARGUMENT, "null model");
+  if (n_qubits) *n_qubits = m->m.n_qubits;
+  if (n_meas) *n_meas = m->m.n_meas();
+  if (n_sym) *n_sym = m->m.n_sym;
+  if (n_groups) *n_groups = m->m.groups.size();
+  if (nnz) *nnz = m->m.sym_idx.size();
+  return SP_OK;
+}
+
+int sp_model_export(const sp_model* m, uint64_t* row_ptr, uint32_t* sym_idx, sp_group* groups) {
+  if (!m) return fail(SP_ERR_INVALID_ARGUMENT, "null model");
+  if (row_ptr) std::memcpy(row_ptr, m->m.row_ptr.data(), m->m.row_ptr.size() * 8);
+  if (sym_idx && !m->m.sym_idx.empty())
+    std::memcpy(sym_idx, m->m.sym_idx.data(), m->m.sym_idx.size() * 4);
+  if (groups) {
+    for (size_t g = 0; g < m->m.groups.size(); ++g) {
+      sp_group o{};
+      o.dist = m->m.groups[g].dist;
+      o.param = m->m.groups[g].param;
+      o.first_symbol = m->m.groups[g].first;
+      o.arity = m->m.groups[g].arity;
+      groups[g] = o;
+    }
+  }
+  return SP_OK;
+}
+
+int sp_ctx_create(int device, sp_ctx** out) {
+  if (!out) return fail(SP_ERR_INVALID_ARGUMENT, "null out");
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0)
+    return fail(SP_ERR_CUDA, std::string("no CUDA device: ") + cudaGetErrorString(e));
+  if (device < 0 || device >= n) return fail(SP_ERR_INVALID_ARGUMENT, "device index out of range");
+  auto c = new sp_ctx;
+  c->device = device;
+  if (int r = set_device(c)) {
+    delete c;
+    return r;
+  }
+  cudaDeviceProp prop{};
+  cudaGetDeviceProperties(&prop, device);
+  if (prop.major < 10) {
+    delete c;
+    return fail(SP_ERR_UNSUPPORTED, "this library is built for sm_100a (B200)");
+  }
+  c->L.num_sms = prop.multiProcessorCount;
+  c->L.smem_optin = prop.sharedMemPerBlockOptin;
+  *out = c;
+  return SP_OK;
+}
+
+void sp_ctx_destroy(sp_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  delete ctx;
+}
+
+int sp_set_stream(sp_ctx* ctx, void* stream) {
+  if (!ctx) return fail(SP_ERR_INVALID_ARGUMENT, "null ctx");
+  ctx->stream = static_cast<cudaStream_t>(stream);
+  ctx->L.stream = ctx->stream;
+  return SP_OK;
+}
+
+int sp_set_rng(sp_ctx* ctx, sp_rng rng) {
+  if (!ctx) return fail(SP_ERR_INVALID_ARGUMENT, "null ctx");
+  if (rng != SP_RNG_PHILOX && rng != SP_RNG_COMPAT_SPLITMIX)
+    return fail(SP_ERR_INVALID_ARGUMENT, "unknown rng");
+  ctx->rng = rng;
+  return SP_OK;
+}
+
+int sp_set_product(sp_ctx* ctx, sp_product v) {
+  if (!ctx) return fail(SP_ERR_INVALID_ARGUMENT, "null ctx");
+  if (v != SP_PRODUCT_AUTO && v != SP_PRODUCT_SPARSE && v != SP_PRODUCT_DENSE)
+    return fail(SP_ERR_INVALID_ARGUMENT, "unknown product variant");
+  if (v == SP_PRODUCT_DENSE && ctx->hp.dense_words.empty() && ctx->have_msym) {
+    // Build the dense words from the CSR rows on first request.
+    HostPlan& h = ctx->hp;
+    h.ldm = std::max<uint64_t>((h.n_sym + 63) / 64, 1);
+    h.dense_words.assign(h.n_meas * h.ldm, 0);
+    for (uint64_t k = 0; k < h.n_meas; ++k)
+      for (uint64_t i = h.row_ptr[k]; i < h.row_ptr[k + 1]; ++i)
+        h.dense_words[k * h.ldm + h.sym_idx[i] / 64] |= uint64_t{1} << (h.sym_idx[i] % 64);
+    ctx->plan_ready = false;
+  }
+  ctx->product = v;
+  return SP_OK;
+}
+
+int sp_load_msym_csr(sp_ctx* ctx, uint64_t n_meas, uint64_t n_sym, const uint64_t* row_ptr,
+                     const uint32_t* sym_idx) {
+  if (!ctx || !row_ptr) return fail(SP_ERR_INVALID_ARGUMENT, "null argument");
+  if (n_meas >= (1ull << 31) || n_sym >= (1ull << 32) - 1)
+    return fail(SP_ERR_UNSUPPORTED, "M_sym dimensions exceed 32-bit indexing");
+  HostPlan& h = ctx->hp;
+  h.n_meas = n_meas;
+  h.n_sym = n_sym;
+  h.row_ptr.assign(row_ptr, row_ptr + n_meas + 1);
+  if (h.row_ptr[0] != 0) return fail(SP_ERR_INVALID_ARGUMENT, "row_ptr[0] must be 0");
+  h.nnz = h.row_ptr[n_meas];
+  h.sym_idx.assign(sym_idx, sym_idx + h.nnz);
+  h.max_sym_plus1 = 0;
+  for (uint64_t k = 0; k < n_meas; ++k) {
+    if (h.row_ptr[k + 1] < h.row_ptr[k]) return fail(SP_ERR_INVALID_ARGUMENT, "row_ptr not monotone");
+    for (uint64_t i = h.row_ptr[k]; i < h.row_ptr[k + 1]; ++i) {
+      if (i > h.row_ptr[k] && h.sym_idx[i] <= h.sym_idx[i - 1])
+        return fail(SP_ERR_INVALID_ARGUMENT, "expression symbols must be strictly increasing");
+      h.max_sym_plus1 = std::max<uint64_t>(h.max_sym_plus1, uint64_t{h.sym_idx[i]} + 1);
+    }
+  }
+  h.dense_words.clear();
+  h.ldm = 0;
+  ctx->have_msym = true;
+  ctx->plan_ready = false;
+  if (ctx->product == SP_PRODUCT_DENSE) sp_set_product(ctx, SP_PRODUCT_DENSE);
+  return SP_OK;
+}
+
+int sp_load_msym_dense(sp_ctx* ctx, uint64_t n_meas, uint64_t n_sym, const uint64_t* words,
+                       uint64_t ld_words) {
+  if (!ctx || (!words && n_meas)) return fail(SP_ERR_INVALID_ARGUMENT, "null argument");
+  if (ld_words < (n_sym + 63) / 64) return fail(SP_ERR_INVALID_ARGUMENT, "ld_words too small");
+  std::vector<uint64_t> rp{0};
+  std::vector<uint32_t> si;
+  for (uint64_t k = 0; k < n_meas; ++k) {
+    for (uint64_t w = 0; w < (n_sym + 63) / 64; ++w) {
+      uint64_t x = words[k * ld_words + w];
+      if (w == (n_sym - 1) / 64 && n_sym % 64) x &= (uint64_t{1} << (n_sym % 64)) - 1;
+      while (x) {
+        si.push_back(static_cast<uint32_t>(w * 64 + __builtin_ctzll(x)));
+        x &= x - 1;
+      }
+    }
+    rp.push_back(si.size());
+  }
+  int r = sp_load_msym_csr(ctx, n_meas, n_sym, rp.data(), si.data());
+  if (r) return r;
+  HostPlan& h = ctx->hp;
+  h.ldm = std::max<uint64_t>((n_sym + 63) / 64, 1);
+  h.dense_words.assign(n_meas * h.ldm, 0);
+  for (uint64_t k = 0; k < n_meas; ++k)
+    for (uint64_t w = 0; w < (n_sym + 63) / 64; ++w) h.dense_words[k * h.ldm + w] = words[k * ld_words + w];
+  if (n_sym % 64)
+    for (uint64_t k = 0; k < n_meas; ++k)
+      h.dense_words[k * h.ldm + (n_sym - 1) / 64] &= (uint64_t{1} << (n_sym % 64)) - 1;
+  return SP_OK;
+}
+
+int sp_load_groups(sp_ctx* ctx, uint64_t n_groups, const sp_group* groups) {
+  if (!ctx || !groups || n_groups == 0) return fail(SP_ERR_INVALID_ARGUMENT, "need >= 1 group");
+  const sp_group& g0 = groups[0];
+  if (g0.dist != SP_DIST_CONSTANT || g0.first_symbol != 0 || g0.arity != 1)
+    return fail(SP_ERR_INVALID_ARGUMENT, "group 0 must be the constant symbol s0");
+  for (uint64_t g = 1; g < n_groups; ++g) {
+    const sp_group& x = groups[g];
+    uint32_t want = x.dist == SP_DIST_DEPOLARIZE1 ? 2 : x.dist == SP_DIST_DEPOLARIZE2 ? 4 : 1;
+    if (x.dist > SP_DIST_DEPOLARIZE2 || x.arity != want)
+      return fail(SP_ERR_INVALID_ARGUMENT, "group arity does not match its distribution");
+  }
+  ctx->hp.groups.assign(groups, groups + n_groups);
+  ctx->hp.n_groups = n_groups;
+  ctx->have_groups = true;
+  ctx->plan_ready = false;
+  return SP_OK;
+}
+
+int sp_load_model(sp_ctx* ctx, const sp_model* m) {
+  if (!ctx || !m) return fail(SP_ERR_INVALID_ARGUMENT, "null argument");
+  int r = sp_load_msym_csr(ctx, m->m.n_meas(), m->m.n_sym, m->m.row_ptr.data(), m->m.sym_idx.data());
+  if (r) return r;
+  std::vector<sp_group> g(m->m.groups.size());
+  sp_model_export(m, nullptr, nullptr, g.data());
+  return sp_load_groups(ctx, g.size(), g.data());
+}
+
+int sp_shot_tile(sp_ctx* ctx, uint64_t* tile) {
+  if (!ctx || !tile) return fail(SP_ERR_INVALID_ARGUMENT, "null argument");
+  if (int r = set_device(ctx)) return r;
+  if (int r = ensure_plan(ctx)) return r;
+  *tile = 1ull << ctx->dp.t_log2;
+  return SP_OK;
+}
+
+int sp_sample(sp_ctx* ctx, uint64_t seed, uint64_t shot_begin, uint64_t n_shots, uint64_t* d_out,
+              uint64_t ld, uint64_t* d_counts) {
+  if (!ctx) return fail(SP_ERR_INVALID_ARGUMENT, "null ctx");
+  if (n_shots == 0) return fail(SP_ERR_INVALID_ARGUMENT, "need at least one shot");  // sampler.cpp:50
+  if (int r = set_device(ctx)) return r;
+  if (int r = ensure_plan(ctx)) return r;
+  if (!ctx->fused_ok) return fail(SP_ERR_UNSUPPORTED, ctx->fused_why);
+  const uint64_t T = 1ull << ctx->dp.t_log2;
+  if (shot_begin % T) return fail(SP_ERR_INVALID_ARGUMENT, "shot_begin must be a multiple of the shot tile");
+  if (ctx->hp.n_meas == 0) return SP_OK;
+  if (!d_out || ld < (n_shots + 63) / 64) return fail(SP_ERR_INVALID_ARGUMENT, "output too small");
+  const uint64_t tile0 = shot_begin / T;
+  int r = ctx->rng == SP_RNG_PHILOX
+              ? launch_fused_sample(ctx->dp, ctx->L, seed, tile0, n_shots, d_out, ld, d_counts)
+              : launch_fused_sample_compat(ctx->dp, ctx->L, seed, tile0, n_shots, d_out, ld, d_counts);
+  return launched(ctx, r, "fused sampler launch");
+}
+
+int sp_draw_assignments(sp_ctx* ctx, uint64_t seed, uint64_t shot_begin, uint64_t n_shots,
+                        uint64_t* d_S, uint64_t ldS) {
+  if (!ctx) return fail(SP_ERR_INVALID_ARGUMENT, "null ctx");
+  if (n_shots == 0) return fail(SP_ERR_INVALID_ARGUMENT, "need at least one shot");  // sampler.cpp:50
+  if (int r = set_device(ctx)) return r;
+  if (int r = ensure_plan(ctx)) return r;
+  const uint64_t T = 1ull << ctx->dp.t_log2;
+  if (shot_begin % T) return fail(SP_ERR_INVALID_ARGUMENT, "shot_begin must be a multiple of the shot tile");
+  if (!d_S || ldS < (n_shots + 63) / 64) return fail(SP_ERR_INVALID_ARGUMENT, "output too small");
+  int r = launch_draw(ctx->dp, ctx->L, ctx->rng == SP_RNG_COMPAT_SPLITMIX, seed, shot_begin / T,
+                      n_shots, d_S, ldS);
+  return launched(ctx, r, "draw launch");
+}
+
+int sp_sample_given_S(sp_ctx* ctx, const uint64_t* d_S, uint64_t n_sym_S, uint64_t ldS,
+                      uint64_t n_shots, uint64_t* d_out, uint64_t ld) {
+  if (!ctx) return fail(SP_ERR_INVALID_ARGUMENT, "null ctx");
+  if (!ctx->have_msym) return fail(SP_ERR_NOT_LOADED, "load M_sym first");
+  if (ctx->hp.max_sym_plus1 > n_sym_S)
+    return fail(SP_ERR_OUT_OF_RANGE, "symbol id out of range");  // sampler.cpp:63-67
+  if (int r = set_device(ctx)) return r;
+  if (n_shots == 0 || ctx->hp.n_meas == 0) return SP_OK;
+  if (!d_S || ldS < (n_shots + 63) / 64 || !d_out || ld < (n_shots + 63) / 64)
+    return fail(SP_ERR_INVALID_ARGUMENT, "buffer too small");
+  // K2 only needs the row lists (and dense words); no group table required.
+  bool dense = ctx->product == SP_PRODUCT_DENSE;
+  if (!ctx->plan_ready) {
+    if (ctx->have_groups) {
+      if (int r = ensure_plan(ctx)) return r;
+    } else {
+      try {
+        ctx->dp.n_meas = static_cast<uint32_t>(ctx->hp.n_meas);
+        ctx->dp.n_sym = static_cast<uint32_t>(ctx->hp.n_sym);
+        ctx->dp.row_ptr = ctx->b_row_ptr.upload(ctx->hp.row_ptr, ctx->stream);
+        ctx->dp.sym_idx = ctx->b_sym_idx.upload(ctx->hp.sym_idx, ctx->stream);
+        if (!ctx->hp.dense_words.empty()) {
+          ctx->dp.dense = ctx->b_dense.upload(ctx->hp.dense_words, ctx->stream);
+          ctx->dp.ldm = ctx->hp.ldm;
+        }
+      } catch (const CudaError& e) {
+        return fail(SP_ERR_CUDA, e.what());
+      }
+    }
+  }
+  if (dense && !ctx->dp.dense) return fail(SP_ERR_NOT_LOADED, "dense M_sym words not built");
+  int r = launch_product(ctx->dp, ctx->L, dense, d_S, ldS, n_shots, d_out, ld);
+  return launched(ctx, r, "product launch");
+}
+
+uint64_t sp_encoded_size(uint64_t n_meas, uint64_t n_shots, sp_format fmt) {
+  return fmt == SP_FMT_01 ? n_shots * (n_meas + 1) : n_shots * ((n_meas + 7) / 8);
+}
+
+int sp_encode(sp_ctx* ctx, const uint64_t* d_m, uint64_t ld, uint64_t n_meas, uint64_t n_shots,
+              sp_format fmt, uint8_t* d_bytes) {
+  if (!ctx) return fail(SP_ERR_INVALID_ARGUMENT, "null ctx");
+  if (fmt != SP_FMT_01 && fmt != SP_FMT_B8) return fail(SP_ERR_INVALID_ARGUMENT, "unknown format");
+  if (int r = set_device(ctx)) return r;
+  if (n_meas && n_shots && ld < (n_shots + 63) / 64) return fail(SP_ERR_INVALID_ARGUMENT, "ld too small");
+  int r = launch_encode(ctx->L, d_m, ld, n_meas, n_shots, fmt, d_bytes);
+  return launched(ctx, r, "encode launch");
+}
+
+int sp_sample_to_host(sp_ctx* ctx, uint64_t seed, uint64_t shot_begin, uint64_t n_shots,
+                      sp_format fmt, uint8_t* h_out, uint64_t cap, uint64_t* written) {
+  if (!ctx) return fail(SP_ERR_INVALID_ARGUMENT, "null ctx");
+  if (n_shots == 0) return fail(SP_ERR_INVALID_ARGUMENT, "need at least one shot");
+  if (int r = set_device(ctx)) return r;
+  if (int r = ensure_plan(ctx)) return r;
+  const uint64_t n_meas = ctx->hp.n_meas;
+  const uint64_t need = sp_encoded_size(n_meas, n_shots, fmt);
+  if (cap < need || (!h_out && need)) return fail(SP_ERR_INVALID_ARGUMENT, "host buffer too small");
+  const uint64_t T = 1ull << ctx->dp.t_log2;
+  if (shot_begin % T) return fail(SP_ERR_INVALID_ARGUMENT, "shot_begin must be a multiple of the shot tile");
+  // Chunks of ~64 MB of records, a multiple of the shot tile.
+  const uint64_t per_shot = std::max<uint64_t>(sp_encoded_size(n_meas, 1, fmt), 1);
+  uint64_t chunk = std::max<uint64_t>((64ull << 20) / per_shot / T, 1) * T;
+  chunk = std::min(chunk, (n_shots + T - 1) / T * T);
+  const uint64_t ld = chunk / 64;
+  try {
+    uint64_t* d_m = static_cast<uint64_t*>(ctx->s_out.ensure(std::max<uint64_t>(n_meas * ld * 8, 16)));
+    uint8_t* d_b = static_cast<uint8_t*>(ctx->s_bytes.ensure(std::max<uint64_t>(chunk * per_shot, 16)));
+    uint64_t off = 0;
+    for (uint64_t done = 0; done < n_shots; done += chunk) {
+      const uint64_t n = std::min(chunk, n_shots - done);
+      if (n_meas) {
+        int r = sp_sample(ctx, seed, shot_begin + done, n, d_m, ld, nullptr);
+        if (r) return r;
+      }
+      int r = sp_encode(ctx, d_m, ld, n_meas, n, fmt, d_b);
+      if (r) return r;
+      const uint64_t nb = sp_encoded_size(n_meas, n, fmt);
+      if (nb) ck(cudaMemcpyAsync(h_out + off, d_b, nb, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+      off += nb;
+    }
+    ck(cudaStreamSynchronize(ctx->stream), "sync");
+    if (written) *written = off;
+  } catch (const CudaError& e) {
+    return fail(SP_ERR_CUDA, e.what());
+  }
+  return SP_OK;
+}
+
+uint64_t sp_launch_count(const sp_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int sp_synchronize(sp_ctx* ctx) {
+  if (!ctx) return fail(SP_ERR_INVALID_ARGUMENT, "null ctx");
+  if (int r = set_device(ctx)) return r;
+  cudaError_t e = cudaStreamSynchronize(ctx->stream);
+  if (e != cudaSuccess) return fail(SP_ERR_CUDA, std::string("sync: ") + cudaGetErrorString(e));
+  return SP_OK;
+}
+
+int sp_debug_philox(sp_ctx* ctx, const uint32_t* ctr_key, uint32_t* out) {
+  if (!ctx || !ctr_key || !out) return fail(SP_ERR_INVALID_ARGUMENT, "null argument");
+  if (int r = set_device(ctx)) return r;
+  try {
+    DBuf in, o;
+    uint32_t* din = static_cast<uint32_t*>(in.ensure(6 * 4));
+    uint32_t* dout = static_cast<uint32_t*>(o.ensure(4 * 4));
+    ck(cudaMemcpy(din, ctr_key, 6 * 4, cudaMemcpyHostToDevice), "H2D");
+    int r = launch_debug_philox(ctx->L, din, dout);
+    if (int e = launched(ctx, r, "philox launch")) return e;
+    ck(cudaMemcpy(out, dout, 4 * 4, cudaMemcpyDeviceToHost), "D2H");
+  } catch (const CudaError& e) {
+    return fail(SP_ERR_CUDA, e.what());
+  }
+  return SP_OK;
+}
+
+}  // extern "C"

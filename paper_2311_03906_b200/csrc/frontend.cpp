@@ -1,0 +1,367 @@
+// Host front end — see frontend.hpp for scope. Independent implementation of
+// the reference's parse_circuit (circuit.cpp:79-168), summarize
+// (circuit.cpp:188-226), decompose_noise (circuit.cpp:228-281) and the
+// one-pass symbolic tableau (tableau.cpp:17-198, 318-382).
+#include "frontend.hpp"
+
+#include <algorithm>
+#include <cctype>
+#include <charconv>
+#include <cstring>
+#include <optional>
+
+namespace symphase {
+
+namespace {
+
+bool is_noise(Op k) {
+  return k == Op::XErr || k == Op::YErr || k == Op::ZErr || k == Op::Dep1 || k == Op::Dep2;
+}
+bool is_pair_op(Op k) { return k == Op::CX || k == Op::Dep2; }
+
+std::optional<Op> op_from_name(std::string name) {
+  for (auto& c : name) c = static_cast<char>(std::toupper(static_cast<unsigned char>(c)));
+  static const struct { const char* n; Op op; } kTable[] = {
+      {"H", Op::H},         {"S", Op::S},           {"S_DAG", Op::SDag},
+      {"X", Op::X},         {"Y", Op::Y},           {"Z", Op::Z},
+      {"CX", Op::CX},       {"CNOT", Op::CX},       {"M", Op::M},
+      {"MZ", Op::M},        {"R", Op::R},           {"X_ERROR", Op::XErr},
+      {"Y_ERROR", Op::YErr}, {"Z_ERROR", Op::ZErr}, {"DEPOLARIZE1", Op::Dep1},
+      {"DEPOLARIZE2", Op::Dep2}, {"TICK", Op::Tick}};
+  for (const auto& e : kTable)
+    if (name == e.n) return e.op;
+  return std::nullopt;
+}
+
+// Whitespace set of operator>> on a C-locale istringstream.
+bool is_ws(char c) {
+  return c == ' ' || c == '\t' || c == '\n' || c == '\v' || c == '\f' || c == '\r';
+}
+
+}  // namespace
+
+std::vector<Instr> parse_circuit(std::string_view text) {
+  std::vector<Instr> prog;
+  size_t line_no = 0, pos = 0;
+  while (pos <= text.size()) {
+    size_t eol = text.find('\n', pos);
+    std::string_view line =
+        text.substr(pos, eol == std::string_view::npos ? text.size() - pos : eol - pos);
+    pos = eol == std::string_view::npos ? text.size() + 1 : eol + 1;
+    ++line_no;
+    if (size_t h = line.find('#'); h != std::string_view::npos) line = line.substr(0, h);
+
+    std::vector<std::string> tok;
+    for (size_t i = 0; i < line.size();) {
+      while (i < line.size() && is_ws(line[i])) ++i;
+      size_t j = i;
+      while (j < line.size() && !is_ws(line[j])) ++j;
+      if (j > i) tok.emplace_back(line.substr(i, j - i));
+      i = j;
+    }
+    if (tok.empty()) continue;
+
+    std::string head = tok[0];
+    std::optional<double> prob;
+    if (size_t open = head.find('('); open != std::string::npos) {
+      if (head.back() != ')') throw ParseError(line_no, "malformed parameter");
+      std::string body = head.substr(open + 1, head.size() - open - 2);
+      double v = 0;
+      auto r = std::from_chars(body.data(), body.data() + body.size(), v);
+      if (r.ec != std::errc{} || r.ptr != body.data() + body.size())
+        throw ParseError(line_no, "bad probability '" + body + "'");
+      prob = v;
+      head = head.substr(0, open);
+    }
+    auto op = op_from_name(head);
+    if (!op) {
+      if (head == "REPEAT" || head == "DETECTOR" || head == "OBSERVABLE_INCLUDE" ||
+          head == "QUBIT_COORDS" || head == "SHIFT_COORDS")
+        throw ParseError(line_no, "unsupported instruction '" + head +
+                                      "' (flat gate/noise/measure circuits only)");
+      throw ParseError(line_no, "unknown instruction '" + head + "'");
+    }
+    Instr in;
+    in.op = *op;
+    in.line = line_no;
+    for (size_t i = 1; i < tok.size(); ++i) {
+      uint32_t t = 0;
+      const std::string& s = tok[i];
+      auto r = std::from_chars(s.data(), s.data() + s.size(), t);
+      if (r.ec != std::errc{} || r.ptr != s.data() + s.size())
+        throw ParseError(line_no, "bad target '" + s + "'");
+      in.targets.push_back(t);
+    }
+    if (is_noise(in.op)) {
+      if (!prob) throw ParseError(line_no, "noise instruction needs a probability");
+      if (*prob < 0.0 || *prob > 1.0) throw ParseError(line_no, "probability out of [0,1]");
+      in.p = *prob;
+    } else if (prob) {
+      throw ParseError(line_no, "unexpected parameter on non-noise instruction");
+    }
+    if (in.op == Op::Tick) {
+      if (!in.targets.empty()) throw ParseError(line_no, "TICK takes no targets");
+    } else if (in.targets.empty()) {
+      throw ParseError(line_no, "missing targets");
+    }
+    if (is_pair_op(in.op)) {
+      if (in.targets.size() % 2 != 0)
+        throw ParseError(line_no, "odd number of targets for a two-qubit instruction");
+      for (size_t i = 0; i < in.targets.size(); i += 2)
+        if (in.targets[i] == in.targets[i + 1])
+          throw ParseError(line_no, "pair targets the same qubit twice");
+    }
+    prog.push_back(std::move(in));
+  }
+  return prog;
+}
+
+namespace {
+
+// Stabilizer tableau with symbolic phases on the stabilizer half only.
+// Rows [0, n) destabilizers, [n, 2n) stabilizers; x/z row-major packed.
+class SymTableau {
+ public:
+  SymTableau(size_t n, size_t capacity)
+      : n_(n), wq_((n + 63) / 64), ws_((capacity + 63) / 64),
+        x_(2 * n * wq_, 0), z_(2 * n * wq_, 0), ph_(n * ws_, 0), hi_(n, 0) {
+    for (size_t i = 0; i < n; ++i) {
+      x_[i * wq_ + i / 64] |= bit(i);              // destabilizer X_i
+      z_[(n + i) * wq_ + i / 64] |= bit(i);        // stabilizer Z_i
+    }
+  }
+
+  // H, S, S_DAG, CX: tableau.cpp:38-78 (phase term into the constant symbol).
+  void h(uint32_t a) {
+    const size_t w = a / 64; const uint64_t m = bit(a);
+    for (size_t r = 0; r < 2 * n_; ++r) {
+      uint64_t& xr = x_[r * wq_ + w]; uint64_t& zr = z_[r * wq_ + w];
+      bool xa = xr & m, za = zr & m;
+      if (xa && za && r >= n_) flip_phase(r - n_, 0);
+      if (xa != za) { xr ^= m; zr ^= m; }
+    }
+  }
+  void s(uint32_t a) {
+    const size_t w = a / 64; const uint64_t m = bit(a);
+    for (size_t r = 0; r < 2 * n_; ++r) {
+      uint64_t& xr = x_[r * wq_ + w]; uint64_t& zr = z_[r * wq_ + w];
+      bool xa = xr & m, za = zr & m;
+      if (xa && za && r >= n_) flip_phase(r - n_, 0);
+      if (xa) zr ^= m;
+    }
+  }
+  void s_dag(uint32_t a) {
+    const size_t w = a / 64; const uint64_t m = bit(a);
+    for (size_t r = 0; r < 2 * n_; ++r) {
+      uint64_t& xr = x_[r * wq_ + w]; uint64_t& zr = z_[r * wq_ + w];
+      bool xa = xr & m, za = zr & m;
+      if (xa && !za && r >= n_) flip_phase(r - n_, 0);
+      if (xa) zr ^= m;
+    }
+  }
+  void cx(uint32_t a, uint32_t b) {
+    const size_t wa = a / 64, wb = b / 64; const uint64_t ma = bit(a), mb = bit(b);
+    for (size_t r = 0; r < 2 * n_; ++r) {
+      uint64_t* xr = &x_[r * wq_]; uint64_t* zr = &z_[r * wq_];
+      bool xa = xr[wa] & ma, za = zr[wa] & ma, xb = xr[wb] & mb, zb = zr[wb] & mb;
+      if (r >= n_ && xa && zb && !(xb ^ za)) flip_phase(r - n_, 0);
+      if (xa) xr[wb] ^= mb;
+      if (zb) zr[wa] ^= ma;
+    }
+  }
+
+  // Symbol-conditioned Paulis (tableau.cpp:80-100): XOR symbol s into the
+  // phase of every stabilizer row the Pauli anticommutes with.
+  void pauli(uint32_t a, bool px, bool pz, uint32_t sym) {
+    const size_t w = a / 64; const uint64_t m = bit(a);
+    for (size_t i = 0; i < n_; ++i) {
+      size_t r = n_ + i;
+      bool xa = x_[r * wq_ + w] & m, za = z_[r * wq_ + w] & m;
+      bool anti = (px && za) ^ (pz && xa);
+      if (anti) flip_phase(i, sym);
+    }
+  }
+
+  // Z-basis measurement (tableau.cpp:146-198). Returns sorted symbol ids.
+  std::vector<uint32_t> measure(uint32_t a, uint64_t& n_sym, std::vector<Group>& groups) {
+    const size_t w = a / 64; const uint64_t m = bit(a);
+    size_t pivot = 2 * n_;
+    for (size_t r = n_; r < 2 * n_; ++r)
+      if (x_[r * wq_ + w] & m) { pivot = r; break; }
+
+    if (pivot < 2 * n_) {
+      for (size_t r = 0; r < 2 * n_; ++r) {
+        if (r == pivot || r + n_ == pivot) continue;
+        if (x_[r * wq_ + w] & m) rowsum(r, pivot);
+      }
+      std::memcpy(&x_[(pivot - n_) * wq_], &x_[pivot * wq_], wq_ * 8);
+      std::memcpy(&z_[(pivot - n_) * wq_], &z_[pivot * wq_], wq_ * 8);
+      std::memset(&x_[pivot * wq_], 0, wq_ * 8);
+      std::memset(&z_[pivot * wq_], 0, wq_ * 8);
+      z_[pivot * wq_ + w] |= m;
+      size_t i = pivot - n_;
+      std::memset(&ph_[i * ws_], 0, hi_[i] * 8);
+      hi_[i] = 0;
+      uint32_t sym = static_cast<uint32_t>(n_sym++);  // add_measurement_symbol, symbols.hpp:73-81
+      groups.push_back(Group{kCoin, 0.5, sym, 1});
+      if (sym / 64 >= ws_) throw std::logic_error("symbol capacity exhausted (pre-pass undercount)");
+      flip_phase(i, sym);
+      return {sym};
+    }
+
+    // Determined: product of the stabilizers selected by destabilizers that
+    // anticommute with Z_a is +/-Z_a; its symbolic phase is the outcome.
+    std::vector<uint64_t> sx(wq_, 0), sz(wq_, 0), sp(ws_, 0);
+    size_t shi = 0;
+    for (size_t i = 0; i < n_; ++i) {
+      if (!(x_[i * wq_ + w] & m)) continue;
+      const uint64_t* x1 = &x_[(n_ + i) * wq_];
+      const uint64_t* z1 = &z_[(n_ + i) * wq_];
+      int res = phase_exponent(x1, z1, sx.data(), sz.data());
+      if (res & 1) throw std::logic_error("non-hermitian generator product: tableau corrupt");
+      for (size_t k = 0; k < wq_; ++k) { sx[k] ^= x1[k]; sz[k] ^= z1[k]; }
+      const uint64_t* p1 = &ph_[i * ws_];
+      for (size_t k = 0; k < hi_[i]; ++k) sp[k] ^= p1[k];
+      shi = std::max<size_t>(shi, hi_[i]);
+      if (res == 2) sp[0] ^= 1;
+    }
+    bool ok = true;
+    for (size_t k = 0; k < wq_; ++k) {
+      if (sx[k] != 0) ok = false;
+      if (sz[k] != (k == w ? m : 0)) ok = false;
+    }
+    if (!ok) throw std::logic_error("determined measurement did not reduce to Z_a");
+    std::vector<uint32_t> e;
+    for (size_t k = 0; k < std::max<size_t>(shi, 1); ++k) {
+      uint64_t v = sp[k];
+      while (v) {
+        e.push_back(static_cast<uint32_t>(k * 64 + __builtin_ctzll(v)));
+        v &= v - 1;
+      }
+    }
+    return e;
+  }
+
+ private:
+  static uint64_t bit(size_t i) { return uint64_t{1} << (i & 63); }
+
+  void flip_phase(size_t i, uint32_t sym) {
+    ph_[i * ws_ + sym / 64] ^= bit(sym);
+    hi_[i] = std::max<uint32_t>(hi_[i], sym / 64 + 1);
+  }
+
+  // i-exponent of (source * target), single_qubit_phase_exponent summed over
+  // qubits (pauli.cpp:7-12), mod 4.
+  int phase_exponent(const uint64_t* x1, const uint64_t* z1, const uint64_t* x2,
+                     const uint64_t* z2) const {
+    int64_t plus = 0, minus = 0;
+    for (size_t k = 0; k < wq_; ++k) {
+      uint64_t a = x1[k], b = z1[k], c = x2[k], d = z2[k];
+      uint64_t p = (a & ~b & ~c & d) | (a & b & c & ~d) | (~a & b & c & d);
+      uint64_t q = (a & ~b & c & d) | (a & b & ~c & d) | (~a & b & c & ~d);
+      plus += __builtin_popcountll(p);
+      minus += __builtin_popcountll(q);
+    }
+    return static_cast<int>((((plus - minus) % 4) + 4) % 4);
+  }
+
+  // dst := src * dst (rowsum_rows, tableau.cpp:113-144). Destabilizer phases
+  // are not tracked (they never reach an outcome), so only stabilizer targets
+  // pay for the phase.
+  void rowsum(size_t dst, size_t src) {
+    uint64_t* xd = &x_[dst * wq_]; uint64_t* zd = &z_[dst * wq_];
+    const uint64_t* xs = &x_[src * wq_]; const uint64_t* zs = &z_[src * wq_];
+    if (dst >= n_) {
+      int res = phase_exponent(xs, zs, xd, zd);
+      if (res & 1) throw std::logic_error("non-hermitian generator product: tableau corrupt");
+      size_t di = dst - n_, si = src - n_;
+      uint64_t* pd = &ph_[di * ws_]; const uint64_t* ps = &ph_[si * ws_];
+      for (size_t k = 0; k < hi_[si]; ++k) pd[k] ^= ps[k];
+      hi_[di] = std::max(hi_[di], hi_[si]);
+      if (res == 2) flip_phase(di, 0);
+    }
+    for (size_t k = 0; k < wq_; ++k) { xd[k] ^= xs[k]; zd[k] ^= zs[k]; }
+  }
+
+  size_t n_, wq_, ws_;
+  std::vector<uint64_t> x_, z_, ph_;
+  std::vector<uint32_t> hi_;
+};
+
+}  // namespace
+
+Model run_initialization(const std::vector<Instr>& prog) {
+  Model M;
+  M.groups.push_back(Group{});  // group 0: the constant symbol (symbols.hpp:49-52)
+  // summarize (circuit.cpp:188-226): qubit count and symbol capacity.
+  size_t n = 0, cap = 1;
+  for (const auto& in : prog) {
+    for (uint32_t t : in.targets) n = std::max<size_t>(n, size_t{t} + 1);
+    switch (in.op) {
+      case Op::M: case Op::R: cap += in.targets.size(); break;
+      case Op::XErr: case Op::YErr: case Op::ZErr: cap += in.targets.size(); break;
+      case Op::Dep1: cap += 2 * in.targets.size(); break;
+      case Op::Dep2: cap += 2 * in.targets.size(); break;
+      default: break;
+    }
+  }
+  M.n_qubits = n;
+  if (n == 0) return M;
+
+  SymTableau t(n, cap);
+  uint64_t& n_sym = M.n_sym;
+  auto add_fault = [&](uint8_t dist, double p, uint32_t arity) {
+    uint32_t first = static_cast<uint32_t>(n_sym);
+    M.groups.push_back(Group{dist, p, first, arity});
+    n_sym += arity;
+    return first;
+  };
+  auto push_row = [&](const std::vector<uint32_t>& e) {
+    M.sym_idx.insert(M.sym_idx.end(), e.begin(), e.end());
+    M.row_ptr.push_back(M.sym_idx.size());
+  };
+  for (const auto& in : prog) {
+    const auto& q = in.targets;
+    switch (in.op) {
+      case Op::H: for (uint32_t a : q) t.h(a); break;
+      case Op::S: for (uint32_t a : q) t.s(a); break;
+      case Op::SDag: for (uint32_t a : q) t.s_dag(a); break;
+      case Op::X: for (uint32_t a : q) t.pauli(a, true, false, 0); break;
+      case Op::Y: for (uint32_t a : q) t.pauli(a, true, true, 0); break;
+      case Op::Z: for (uint32_t a : q) t.pauli(a, false, true, 0); break;
+      case Op::CX: for (size_t i = 0; i + 1 < q.size(); i += 2) t.cx(q[i], q[i + 1]); break;
+      case Op::M: for (uint32_t a : q) push_row(t.measure(a, n_sym, M.groups)); break;
+      case Op::R:
+        // Reset = measure + X conditioned on the outcome (tableau.cpp:355-362).
+        for (uint32_t a : q) {
+          auto e = t.measure(a, n_sym, M.groups);
+          for (uint32_t s : e) t.pauli(a, true, false, s);
+        }
+        break;
+      // decompose_noise (circuit.cpp:228-281): one group per channel target.
+      case Op::XErr: for (uint32_t a : q) t.pauli(a, true, false, add_fault(kBernoulli, in.p, 1)); break;
+      case Op::ZErr: for (uint32_t a : q) t.pauli(a, false, true, add_fault(kBernoulli, in.p, 1)); break;
+      case Op::YErr: for (uint32_t a : q) t.pauli(a, true, true, add_fault(kBernoulli, in.p, 1)); break;
+      case Op::Dep1:
+        for (uint32_t a : q) {
+          uint32_t s = add_fault(kDep1, in.p, 2);
+          t.pauli(a, true, false, s);
+          t.pauli(a, false, true, s + 1);
+        }
+        break;
+      case Op::Dep2:
+        for (size_t i = 0; i + 1 < q.size(); i += 2) {
+          uint32_t s = add_fault(kDep2, in.p, 4);
+          t.pauli(q[i], true, false, s);
+          t.pauli(q[i], false, true, s + 1);
+          t.pauli(q[i + 1], true, false, s + 2);
+          t.pauli(q[i + 1], false, true, s + 3);
+        }
+        break;
+      case Op::Tick: break;
+    }
+  }
+  return M;
+}
+
+}  // namespace symphase

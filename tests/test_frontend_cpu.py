@@ -1,0 +1,105 @@
+"""Host front end (native parse + symbolic pass, CPU-only code in
+libsymphase_b200.so) against the reference's run_initialization."""
+import json
+
+import numpy as np
+import pytest
+
+from conftest import golden_circuit
+from paper_2311_03906_b200 import circuits as CI
+from paper_2311_03906_b200 import run_initialization
+from paper_2311_03906_b200._native import LogicError, ParseError  # noqa: F401
+
+
+def _same(a, b):
+    return (a.n_sym == b.n_sym and np.array_equal(a.row_ptr, b.row_ptr)
+            and np.array_equal(a.sym_idx, b.sym_idx)
+            and np.array_equal(a.groups["dist"], b.groups["dist"])
+            and np.array_equal(a.groups["param"], b.groups["param"])
+            and np.array_equal(a.groups["first_symbol"], b.groups["first_symbol"])
+            and np.array_equal(a.groups["arity"], b.groups["arity"]))
+
+
+def test_golden_expressions_and_registry(golden):
+    names = json.loads(str(golden["frontend"]["names"]))
+    for name in names:
+        text, want = golden_circuit(golden, name)
+        got = run_initialization(text)
+        assert _same(got, want), name
+
+
+def test_worked_example_expressions():
+    # acceptance.cpp:110-138: m1 = s3, m2 = s1 ^ s2 ^ s3 (0-based ids here).
+    init = run_initialization("H 0\nCX 0 1\nX_ERROR(0.1) 0 1\nM 0 1\n")
+    assert init.expressions == [[3], [1, 2, 3]]
+
+
+def test_four_qubit_example():
+    # acceptance.cpp:141-177: m = s1, s2, s2^s3, s3^s4
+    text = ("H 0\nCX 0 1\nCX 1 2\nCX 2 3\nZ_ERROR(0.1) 0\nX_ERROR(0.1) 1\nX_ERROR(0.1) 2\n"
+            "X_ERROR(0.1) 3\nCX 2 3\nCX 1 2\nCX 0 1\nH 0\nM 0 1 2 3\n")
+    assert run_initialization(text).expressions == [[1], [2], [2, 3], [3, 4]]
+
+
+def test_noise_symbol_numbering():
+    # test_sampler.cpp:193-196: three X_ERRORs on qubit 0 -> m = s1 ^ s2 ^ s3
+    init = run_initialization("X_ERROR(0.05) 0\nX_ERROR(0.2) 0\nX_ERROR(0.45) 0\nM 0\n")
+    assert init.expressions == [[1, 2, 3]]
+    assert init.n_sym == 4
+
+
+def test_constant_symbol_rows():
+    # test_sampler.cpp:36-46: X 0; M 0; M 0 -> both rows {s0}, registry size 1
+    init = run_initialization("X 0\nM 0\nM 0\n")
+    assert init.expressions == [[0], [0]]
+    assert init.n_sym == 1
+
+
+def test_empty_circuit():
+    init = run_initialization("")
+    assert init.n_meas == 0 and init.n_sym == 1 and len(init.groups) == 1
+
+
+@pytest.mark.parametrize("text,line", [("H 0\nFROB 1\n", 2), ("M 0\nX_ERROR 0\n", 2),
+                                       ("H(0.1) 0\n", 1), ("CX 0 0\n", 1), ("CX 0\n", 1),
+                                       ("TICK 3\n", 1), ("M\n", 1), ("X_ERROR(1.5) 0\n", 1),
+                                       ("X_ERROR(0.1 0\n", 1), ("M -1\n", 1),
+                                       ("\n\nREPEAT 3 {\n", 3), ("DETECTOR rec[-1]\n", 1)])
+def test_parse_errors_carry_line_numbers(text, line):
+    with pytest.raises(ParseError) as e:
+        run_initialization(text)
+    assert f"line {line}:" in str(e.value)
+
+
+def test_parse_accepts_aliases_case_comments():
+    # test_circuit.cpp:38-53
+    init = run_initialization("# c\n  h 5   # t\n\ncnot 0 1\nmz 2\ntick\n")
+    assert init.n_qubits == 6 and init.n_meas == 1
+
+
+def test_generator_shapes_match_survey():
+    # SURVEY.md §8 table, measured from the reference's own pass.
+    rep = run_initialization(CI.repetition_code(5, 5, 0.01))
+    assert (rep.n_meas, rep.n_sym, rep.nnz) == (25, 206, 280)
+    s5 = run_initialization(CI.surface_code(5, 5, 1e-3))
+    assert (s5.n_meas, s5.n_sym, s5.nnz) == (145, 3730, 12569)
+
+
+def test_frontend_matches_live_reference_random(ref):
+    rng = CI.MT19937_64(4242)
+    for _ in range(150):
+        text = CI.random_test_circuit(rng, n_qubits=1 + rng.below(7), n_instr=5 + rng.below(70))
+        c = ref.circuit(text)
+        got = run_initialization(text)
+        assert got.n_sym == c.n_sym
+        assert np.array_equal(got.row_ptr, c.row_ptr)
+        assert np.array_equal(got.sym_idx, c.sym_idx)
+        assert np.array_equal(got.groups["dist"], c.dist)
+        assert np.array_equal(got.groups["first_symbol"], c.first)
+
+
+def test_frontend_matches_live_reference_surface9(ref):
+    text = CI.surface_code(9, 9, 1e-3)
+    c = ref.circuit(text)
+    got = run_initialization(text)
+    assert np.array_equal(got.row_ptr, c.row_ptr) and np.array_equal(got.sym_idx, c.sym_idx)

@@ -1,0 +1,110 @@
+"""Statistical parity of the in-kernel Philox sampler (north star: per-variable
+marginals and per-measurement flip rates within 5 sigma at 10^7 shots).
+
+Analytic targets follow fill_group's pmf (sampler.cpp:11-44) and the
+piling-up form of test_sampler.cpp:189-203, computed by oracle.flip_rates."""
+import numpy as np
+import pytest
+
+import oracle
+from paper_2311_03906_b200 import circuits as CI
+from paper_2311_03906_b200 import run_initialization
+
+pytestmark = pytest.mark.gpu
+
+N = 10_000_000
+SIGMA = 5.0
+
+
+def within(hits, n, p):
+    sd = np.sqrt(max(p * (1 - p), 1e-300) / n)
+    return abs(hits / n - p) <= SIGMA * sd + 1e-12, (hits / n, p, sd)
+
+
+def host(t):
+    return t.cpu().numpy().view(np.uint64)
+
+
+CHANNELS = [("X_ERROR", p) for p in (1e-4, 1e-3, 0.01, 0.1, 0.3, 0.5, 0.9, 1.0, 0.0)] + \
+           [("DEPOLARIZE1", p) for p in (1e-3, 0.05, 0.3, 0.75, 1.0)] + \
+           [("DEPOLARIZE2", p) for p in (1e-3, 0.1, 0.8, 1.0)]
+
+
+def channel_circuit():
+    lines, q = [], 0
+    for name, p in CHANNELS:
+        if name == "DEPOLARIZE2":
+            lines.append(f"{name}({p!r}) {q} {q + 1}")
+            q += 2
+        else:
+            lines.append(f"{name}({p!r}) {q}")
+            q += 1
+    lines.append("H " + " ".join(str(i) for i in range(q, q + 3)))  # three fair coins
+    lines.append("M " + " ".join(str(i) for i in range(q + 3)))
+    return "\n".join(lines) + "\n"
+
+
+def test_per_variable_marginals_10M(gpu_sampler_factory):
+    init = run_initialization(channel_circuit())
+    s = gpu_sampler_factory(init)
+    S = host(s.draw_assignments(N, 2024))
+    tail = N % 64
+    valid = np.full(S.shape[1], ~np.uint64(0), dtype=np.uint64)
+    if tail:
+        valid[-1] = np.uint64((1 << tail) - 1)
+    pc = lambda w: int(np.bitwise_count(w & valid).sum())  # noqa: E731
+    g = init.groups
+    bad = []
+    for gi in range(1, len(g)):
+        d, p, f = int(g["dist"][gi]), float(g["param"][gi]), int(g["first_symbol"][gi])
+        if d in (1, 2):
+            q = 0.5 if d == 2 else p
+            ok, info = within(pc(S[f]), N, q)
+            if not ok:
+                bad.append((gi, d, info))
+        elif d == 3:  # patterns x, z, y each p/3; identity 1-p
+            x, z = S[f], S[f + 1]
+            for pat, w in ((1, x & ~z), (2, ~x & z), (3, x & z), (0, ~x & ~z)):
+                ok, info = within(pc(w), N, (1 - p) if pat == 0 else p / 3)
+                if not ok:
+                    bad.append((gi, d, pat, info))
+        elif d == 4:  # 15 non-identity patterns each p/15
+            rows = [S[f + b] for b in range(4)]
+            for pat in range(16):
+                w = valid.copy()
+                for b in range(4):
+                    w &= rows[b] if (pat >> b) & 1 else ~rows[b]
+                ok, info = within(pc(w), N, (1 - p) if pat == 0 else p / 15)
+                if not ok:
+                    bad.append((gi, d, pat, info))
+    assert not bad, bad
+
+
+@pytest.mark.parametrize("cfg", ["cfg1", "cfg2", "xor_conv", "channels"])
+def test_per_measurement_flip_rates_10M(gpu_sampler_factory, cfg):
+    import torch
+    text = {"cfg1": lambda: CI.repetition_code(5, 5, 0.01),
+            "cfg2": lambda: CI.surface_code(5, 5, 1e-3),
+            # test_sampler.cpp:193-194
+            "xor_conv": lambda: "X_ERROR(0.05) 0\nX_ERROR(0.2) 0\nX_ERROR(0.45) 0\nM 0\n",
+            "channels": channel_circuit}[cfg]()
+    init = run_initialization(text)
+    s = gpu_sampler_factory(init)
+    counts = torch.zeros(init.n_meas, dtype=torch.int64, device="cuda")
+    out = s.empty_bits(init.n_meas, N)
+    s.sample(N, 77, out=out, counts=counts)
+    got = counts.cpu().numpy()
+    want = oracle.flip_rates(init)
+    bad = [(k, *within(int(got[k]), N, float(want[k]))[1]) for k in range(init.n_meas)
+           if not within(int(got[k]), N, float(want[k]))[0]]
+    assert not bad, bad
+    if cfg == "xor_conv":
+        assert abs(want[0] - 0.5 * (1 - 0.9 * 0.6 * 0.1)) < 1e-12
+
+
+def test_seeds_differ_and_repeat(gpu_sampler_factory):
+    init = run_initialization(CI.surface_code(5, 5, 1e-3))
+    s = gpu_sampler_factory(init)
+    a = host(s.sample(100_000, 1))
+    assert np.array_equal(a, host(s.sample(100_000, 1)))
+    assert not np.array_equal(a, host(s.sample(100_000, 2)))
