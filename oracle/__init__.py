@@ -49,13 +49,16 @@ class Port:
         L.orc_group_bits.argtypes = [_i, _d, _u64]
         L.orc_draw_assignments.restype = _i
         L.orc_draw_assignments.argtypes = [_u64, _p, _p, _p, _p, _u64, _u64, _u64, _p, _u64]
+        L.orc_draw_assignments_range.restype = _i
+        L.orc_draw_assignments_range.argtypes = [_u64, _p, _p, _p, _p, _u64, _u64, _u64, _u64,
+                                                 _p, _u64]
         L.orc_sample_sparse.restype = _i
         L.orc_sample_sparse.argtypes = [_u64, _p, _p, _u64, _u64, _p, _u64, _p, _u64]
         L.orc_encode.restype = _u64
         L.orc_encode.argtypes = [_u64, _u64, _p, _u64, _i, _p]
         self.L = L
 
-    def draw_assignments(self, init, n_shots: int, seed: int) -> np.ndarray:
+    def draw_assignments(self, init, n_shots: int, seed: int, shot_begin: int = 0) -> np.ndarray:
         g = init.groups
         ld = max((n_shots + 63) // 64, 1)
         S = np.zeros((init.n_sym, ld), dtype=np.uint64)
@@ -63,8 +66,9 @@ class Port:
         param = np.ascontiguousarray(g["param"])
         first = np.ascontiguousarray(g["first_symbol"])
         arity = np.ascontiguousarray(g["arity"])
-        r = self.L.orc_draw_assignments(len(g), _ptr(dist), _ptr(param), _ptr(first), _ptr(arity),
-                                        init.n_sym, n_shots, seed, _ptr(S), ld)
+        r = self.L.orc_draw_assignments_range(len(g), _ptr(dist), _ptr(param), _ptr(first),
+                                              _ptr(arity), init.n_sym, shot_begin, n_shots, seed,
+                                              _ptr(S), ld)
         if r == -2:
             raise ValueError("need at least one shot")
         return S

@@ -57,6 +57,14 @@ unsigned orc_group_bits(int dist, double param, uint64_t u) {
 int orc_draw_assignments(uint64_t n_groups, const uint8_t* dist, const double* param,
                          const uint32_t* first, const uint32_t* arity, uint64_t n_sym,
                          uint64_t n_shots, uint64_t seed, uint64_t* S, uint64_t ldS) {
+  return orc_draw_assignments_range(n_groups, dist, param, first, arity, n_sym, 0, n_shots, seed,
+                                    S, ldS);
+}
+
+int orc_draw_assignments_range(uint64_t n_groups, const uint8_t* dist, const double* param,
+                               const uint32_t* first, const uint32_t* arity, uint64_t n_sym,
+                               uint64_t shot_begin, uint64_t n_shots, uint64_t seed, uint64_t* S,
+                               uint64_t ldS) {
   if (n_shots == 0) return -2; /* sampler.cpp:50 */
   memset(S, 0, (size_t)(n_sym * ldS) * sizeof(uint64_t));
   for (uint64_t shot = 0; shot < n_shots; ++shot) {
@@ -64,7 +72,7 @@ int orc_draw_assignments(uint64_t n_groups, const uint8_t* dist, const double* p
     uint64_t w = shot >> 6;
     if (n_sym > 0) S[w] |= bit; /* row 0 = constant symbol, sampler.cpp:53 */
     for (uint64_t g = 1; g < n_groups; ++g) {
-      uint64_t u = orc_keyed_draw(seed, g, shot);
+      uint64_t u = orc_keyed_draw(seed, g, shot_begin + shot); /* order-insensitive keys, sampler.hpp:21-26 */
       unsigned bits = orc_group_bits(dist[g], param[g], u);
       for (uint32_t b = 0; b < arity[g] && bits; ++b, bits >>= 1) {
         if (bits & 1u) S[(uint64_t)(first[g] + b) * ldS + w] |= bit;

@@ -39,6 +39,14 @@ int orc_draw_assignments(uint64_t n_groups, const uint8_t* dist, const double* p
                          const uint32_t* first, const uint32_t* arity, uint64_t n_sym,
                          uint64_t n_shots, uint64_t seed, uint64_t* S, uint64_t ldS);
 
+/* Same draws for global shots [shot_begin, shot_begin + n_shots): keyed_draw
+ * is keyed by the shot index (sampler.hpp:21-26), so any shot range can be
+ * drawn independently — the multi-GPU sharding invariant. */
+int orc_draw_assignments_range(uint64_t n_groups, const uint8_t* dist, const double* param,
+                               const uint32_t* first, const uint32_t* arity, uint64_t n_sym,
+                               uint64_t shot_begin, uint64_t n_shots, uint64_t seed, uint64_t* S,
+                               uint64_t ldS);
+
 /* sample(expressions, batch) / gf2_multiply_sparse (sampler.cpp:61-112,
  * bit_matrix.cpp:314-328): row k of out = XOR of S rows listed in row k.
  * Returns 0, or -1 when a symbol id >= n_sym (std::out_of_range,

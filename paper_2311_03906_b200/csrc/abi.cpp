@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <new>
@@ -95,8 +96,8 @@ struct sp_ctx {
   DevPlan dp;
   // plan buffers
   DBuf b_row_ptr, b_sym_idx, b_col_ptr, b_col_rows, b_dense, b_first, b_arity, b_dist, b_param,
-      b_row_const, b_row_const_compat, b_ones, b_dense_sym, b_drow_ptr, b_drow_slot, b_ch_class,
-      b_ch_lo, b_ch_hi, b_cls_dist, b_cls_inv, b_cls_goff, b_cls_groups, b_live_groups;
+      b_row_const_compat, b_ones, b_dense_sym, b_drow_ptr, b_drow_slot, b_cls, b_cls_groups,
+      b_desc, b_colrow, b_live_groups, b_parent, b_lvl_rows, b_lvl_ptr;
   // scratch for sp_sample_to_host
   DBuf s_out, s_bytes;
   uint64_t launches = 0;
@@ -110,20 +111,77 @@ int set_device(sp_ctx* c) {
   return SP_OK;
 }
 
-// Chooses the shot tile T (power of two, 128..4096): the largest whose
-// accumulation tile + coin words + counters fit a shared-memory budget that
-// leaves room for two CTAs per SM; failing that, one CTA per SM.
-int choose_tile_log2(uint64_t n_meas, uint64_t n_dense, size_t smem_optin) {
-  const size_t budgets[2] = {100 * 1024, smem_optin - 2048};
-  for (size_t budget : budgets) {
-    for (int lg = 12; lg >= 7; --lg) {
-      uint32_t tw = 1u << (lg - 5);
-      if (fused_smem_bytes(static_cast<uint32_t>(n_meas), static_cast<uint32_t>(n_dense), tw, true) <=
-          budget)
-        return lg;
+long env_long(const char* name, long dflt) {
+  const char* v = std::getenv(name);
+  return v && *v ? std::strtol(v, nullptr, 10) : dflt;
+}
+
+// M_sym = L·D "chain" transform. Row k gets at most one parent p(k) < k —
+// the earlier row sharing the most symbols with it — whenever
+// |row_k XOR row_p| < |row_k|; D row k is that symmetric difference (else
+// row k itself). Then out[k] = (D·S)[k] ^ out[p(k)] exactly over GF(2). For
+// repeated syndrome extraction this turns cumulative measurement rows into
+// detector-like round differences, so fault columns of D are several times
+// shorter than those of M (fewer bit flips per firing). Rows are grouped
+// into levels by parent depth so a level only reads finished rows.
+struct ChainXf {
+  std::vector<int32_t> parent;
+  std::vector<uint64_t> rp;
+  std::vector<uint32_t> si;
+  std::vector<uint32_t> depth;
+  uint32_t n_levels = 1;
+};
+
+ChainXf chain_transform(uint64_t n_meas, const std::vector<uint64_t>& row_ptr,
+                        const std::vector<uint32_t>& sym_idx, const std::vector<uint64_t>& col_ptr,
+                        const std::vector<uint32_t>& col_rows, bool enable) {
+  ChainXf x;
+  x.parent.assign(n_meas, -1);
+  x.depth.assign(n_meas, 0);
+  x.rp.assign(1, 0);
+  std::vector<uint32_t> cnt(n_meas, 0), touched;
+  for (uint64_t k = 0; k < n_meas; ++k) {
+    const uint64_t b = row_ptr[k], e = row_ptr[k + 1];
+    int64_t best = -1, best_gain = 0;
+    if (enable) {
+      for (uint64_t i = b; i < e; ++i) {
+        const uint32_t sidx = sym_idx[i];
+        for (uint64_t t = col_ptr[sidx]; t < col_ptr[sidx + 1]; ++t) {
+          const uint32_t j = col_rows[t];
+          if (j >= k) break;  // column lists are ascending
+          if (cnt[j]++ == 0) touched.push_back(j);
+        }
+      }
+      for (uint32_t j : touched) {
+        // |row_k| - |row_k XOR row_j| = 2 overlap - |row_j|
+        const int64_t gain = 2 * static_cast<int64_t>(cnt[j]) -
+                             static_cast<int64_t>(row_ptr[j + 1] - row_ptr[j]);
+        if (gain > best_gain || (gain == best_gain && gain > 0 && j > best)) {
+          best_gain = gain;
+          best = j;
+        }
+        cnt[j] = 0;
+      }
+      touched.clear();
     }
+    if (best >= 0) {
+      x.parent[k] = static_cast<int32_t>(best);
+      x.depth[k] = x.depth[best] + 1;
+      x.n_levels = std::max(x.n_levels, x.depth[k] + 1);
+      // sorted symmetric difference of row k and row best
+      uint64_t i = b, j = row_ptr[best];
+      const uint64_t je = row_ptr[best + 1];
+      while (i < e || j < je) {
+        if (j >= je || (i < e && sym_idx[i] < sym_idx[j])) x.si.push_back(sym_idx[i++]);
+        else if (i >= e || sym_idx[j] < sym_idx[i]) x.si.push_back(sym_idx[j++]);
+        else { ++i; ++j; }
+      }
+    } else {
+      x.si.insert(x.si.end(), sym_idx.begin() + b, sym_idx.begin() + e);
+    }
+    x.rp.push_back(x.si.size());
   }
-  return -1;
+  return x;
 }
 
 void build_plan(sp_ctx* c) {
@@ -157,18 +215,38 @@ void build_plan(sp_ctx* c) {
       for (uint64_t i = h.row_ptr[k]; i < h.row_ptr[k + 1]; ++i)
         col_rows[fillp[h.sym_idx[i]]++] = static_cast<uint32_t>(k);
   }
-  auto live_sym = [&](uint64_t sidx) { return col_ptr[sidx + 1] > col_ptr[sidx]; };
+  auto col_len = [&](uint64_t sidx) { return col_ptr[sidx + 1] - col_ptr[sidx]; };
+
+  // D = L^-1 M (chain transform); skipped when M is dense enough that the
+  // parent search (sum of squared column lengths) would be expensive.
+  double sq = 0;
+  for (uint64_t sidx = 0; sidx < n_sym; ++sidx) sq += static_cast<double>(col_len(sidx)) * col_len(sidx);
+  const ChainXf X = chain_transform(n_meas, h.row_ptr, h.sym_idx, col_ptr, col_rows,
+                                    sq < 2e9 && env_long("SP_NO_CHAIN", 0) == 0);
+  std::vector<uint64_t> dcol_ptr(n_sym + 1, 0);
+  for (uint32_t sidx : X.si) dcol_ptr[sidx + 1]++;
+  for (uint64_t i = 0; i < n_sym; ++i) dcol_ptr[i + 1] += dcol_ptr[i];
+  std::vector<uint32_t> dcol_rows(X.si.size());
+  {
+    std::vector<uint64_t> fillp(dcol_ptr.begin(), dcol_ptr.end() - 1);
+    for (uint64_t k = 0; k < n_meas; ++k)
+      for (uint64_t i = X.rp[k]; i < X.rp[k + 1]; ++i) dcol_rows[fillp[X.si[i]]++] = static_cast<uint32_t>(k);
+  }
+  auto dcol_len = [&](uint64_t sidx) { return dcol_ptr[sidx + 1] - dcol_ptr[sidx]; };
 
   const size_t cw = (n_meas + 31) / 32 + 1;
-  std::vector<uint32_t> row_const(cw, 0), row_const_compat(cw, 0);
+  std::vector<uint32_t> row_const(cw, 0), row_const_compat(cw, 0);  // D rows / M rows
   auto xor_rows = [&](std::vector<uint32_t>& mask, uint64_t sidx) {
-    for (uint64_t i = col_ptr[sidx]; i < col_ptr[sidx + 1]; ++i)
-      mask[col_rows[i] >> 5] ^= 1u << (col_rows[i] & 31);
+    for (uint64_t i = dcol_ptr[sidx]; i < dcol_ptr[sidx + 1]; ++i)
+      mask[dcol_rows[i] >> 5] ^= 1u << (dcol_rows[i] & 31);
   };
   std::vector<uint32_t> ones{0};
   xor_rows(row_const, 0);
-  xor_rows(row_const_compat, 0);
+  for (uint64_t i = col_ptr[0]; i < col_ptr[1]; ++i)
+    row_const_compat[col_rows[i] >> 5] ^= 1u << (col_rows[i] & 31);
 
+  // Classify groups: dense (coins, Bernoulli(1/2)), constant-folded
+  // (Bernoulli(p>=1)), never (p == 0), or a sparse class keyed by (dist, p).
   std::vector<uint32_t> dense_live, dense_dead;
   struct Cls {
     uint8_t dist;
@@ -178,11 +256,15 @@ void build_plan(sp_ctx* c) {
   std::vector<Cls> live_cls, dead_cls;
   std::map<std::pair<uint8_t, uint64_t>, size_t> live_key, dead_key;
   std::vector<uint32_t> live_groups;
-
+  double events_per_shot = 0, flips_per_shot = 0;
   for (uint64_t g = 1; g < G; ++g) {
     const sp_group& gr = h.groups[g];
     bool live = false;
-    for (uint32_t b = 0; b < gr.arity; ++b) live |= live_sym(gr.first_symbol + b);
+    uint64_t flips = 0;
+    for (uint32_t b = 0; b < gr.arity; ++b) {
+      live |= col_len(gr.first_symbol + b) > 0;
+      flips += dcol_len(gr.first_symbol + b);
+    }
     if (live) live_groups.push_back(static_cast<uint32_t>(g));
     const double p = gr.param;
     switch (gr.dist) {
@@ -209,6 +291,10 @@ void build_plan(sp_ctx* c) {
         throw std::invalid_argument("unknown group distribution");
     }
     if (!(p > 0.0)) continue;  // never fires (p == 0, or NaN)
+    if (live) {
+      events_per_shot += std::min(p, 1.0);
+      flips_per_shot += std::min(p, 1.0) * flips / gr.arity * (gr.arity == 1 ? 1.0 : gr.arity == 2 ? 4.0 / 3 : 32.0 / 15);
+    }
     uint64_t pbits;
     std::memcpy(&pbits, &p, 8);
     auto key = std::make_pair(gr.dist, pbits);
@@ -222,8 +308,64 @@ void build_plan(sp_ctx* c) {
     cls[it->second].groups.push_back(static_cast<uint32_t>(g));
   }
 
+  // Dense slots (live first) and per-row slot lists; slot n_dense_live is the
+  // all-ones slot standing for the constant term.
   const uint64_t n_dense_live = dense_live.size();
-  int lg = choose_tile_log2(n_meas, n_dense_live, c->L.smem_optin);
+  if (n_dense_live + 1 >= 65535) throw std::invalid_argument("too many fair-coin symbols");
+  std::vector<uint32_t> dense_sym = dense_live;
+  dense_sym.insert(dense_sym.end(), dense_dead.begin(), dense_dead.end());
+  std::vector<uint32_t> slot_of(n_sym, UINT32_MAX);
+  for (uint32_t i = 0; i < n_dense_live; ++i) slot_of[dense_live[i]] = i;
+  std::vector<uint32_t> drow_ptr(n_meas + 1, 0);
+  std::vector<uint16_t> drow_slot;
+  for (uint64_t k = 0; k < n_meas; ++k) {
+    if ((row_const[k >> 5] >> (k & 31)) & 1u) drow_slot.push_back(static_cast<uint16_t>(n_dense_live));
+    for (uint64_t i = X.rp[k]; i < X.rp[k + 1]; ++i)
+      if (slot_of[X.si[i]] != UINT32_MAX) drow_slot.push_back(static_cast<uint16_t>(slot_of[X.si[i]]));
+    drow_ptr[k + 1] = static_cast<uint32_t>(drow_slot.size());
+  }
+  uint64_t live_positions = 0, live_colrow = 0;
+  for (const Cls& cl : live_cls)
+    for (uint32_t g : cl.groups) {
+      ++live_positions;
+      for (uint32_t b = 0; b < h.groups[g].arity; ++b) live_colrow += dcol_len(h.groups[g].first_symbol + b);
+    }
+
+  // ---- launch shape: tile T, table staging, generator/drain warp split ----
+  d = DevPlan{};
+  d.n_meas = static_cast<uint32_t>(n_meas);
+  d.n_sym = static_cast<uint32_t>(n_sym);
+  d.n_groups = static_cast<uint32_t>(G);
+  d.n_dense_live = static_cast<uint32_t>(n_dense_live);
+  d.n_dense_all = static_cast<uint32_t>(dense_sym.size());
+  d.n_drow = static_cast<uint32_t>(drow_slot.size());
+  d.n_cls_live = static_cast<uint32_t>(live_cls.size());
+  d.n_desc_live = static_cast<uint32_t>(live_positions);
+  d.n_colrow = live_colrow;
+  d.n_levels = X.n_levels;
+  const size_t optin = c->L.smem_optin;
+  int lg = -1;
+  bool staged = false, row_staged = false;
+  const long force_lg = env_long("SP_TLOG2", 0), force_st = env_long("SP_STAGED", -1),
+             force_rs = env_long("SP_ROWSTAGED", -1);
+  // Preference: event + row tables on chip (T >= 512), row tables only, none.
+  const bool cand[3][2] = {{true, true}, {false, true}, {false, false}};
+  for (int ci = 0; ci < 3 && lg < 0; ++ci) {
+    const bool st = cand[ci][0], rs = cand[ci][1];
+    if (force_st >= 0 && st != (force_st != 0)) continue;
+    if (force_rs >= 0 && rs != (force_rs != 0)) continue;
+    for (int t = 12; t >= 7; --t) {
+      if (force_lg && t != force_lg) continue;
+      if (static_cast<uint64_t>(n_meas) * (1u << (t - 5)) >= 65536) continue;  // u16 row offsets
+      if (st && t < 9 && !force_lg) break;
+      if (fused_smem_bytes(d, t, st, rs) <= optin) {
+        lg = t;
+        staged = st;
+        row_staged = rs;
+        break;
+      }
+    }
+  }
   c->fused_ok = lg >= 0;
   if (lg < 0) {
     c->fused_why = "M_sym has too many measurement rows for an on-chip shot tile; use "
@@ -231,52 +373,73 @@ void build_plan(sp_ctx* c) {
     lg = 7;
   }
   const uint64_t T = 1ull << lg;
+  d.t_log2 = static_cast<uint32_t>(lg);
+  d.tw = static_cast<uint32_t>(T / 32);
+  d.staged = staged;
+  d.row_staged = row_staged;
+  {
+    const size_t smem = fused_smem_bytes(d, d.t_log2, staged, row_staged);
+    d.cta_per_sm = static_cast<uint32_t>(std::max<long>(
+        1, std::min<long>(env_long("SP_CTAS", 2), static_cast<long>((228 * 1024) / (smem + 1024)))));
+    const double ev = events_per_shot * T, flips = flips_per_shot * T;
+    const double gen = ev * 60.0 + flips * 4.0;
+    const double items = static_cast<double>(n_meas) * (T / 128);
+    const double drain = n_dense_live * (T / 128.0) * 60.0 +
+                         items * (12.0 + 3.0 * drow_slot.size() / std::max<uint64_t>(n_meas, 1));
+    long gw = std::lround(16.0 * gen / std::max(gen + drain, 1.0));
+    gw = env_long("SP_GEN_WARPS", gw);
+    d.gen_warps = static_cast<uint32_t>(std::min<long>(std::max<long>(gw, 1), 15));
+  }
 
-  // Chains: each class's flattened (group, shot) space of a tile is cut
-  // into slices of ~kEvents expected firings (<= 2^24 trials).
-  constexpr double kEvents = 8.0;
-  std::vector<uint32_t> ch_class;
-  std::vector<uint64_t> ch_lo, ch_hi, cls_goff;
-  std::vector<uint8_t> cls_dist;
-  std::vector<float> cls_inv;
+  // Segments: each class's flattened (group, shot) space of a tile is cut
+  // into slices of ~E expected firings (<= 2^24 trials), one warp walk each;
+  // E is chosen so each generator warp takes a few segments per tile.
+  const double ev_tile = events_per_shot * T;
+  double E = ev_tile / (3.0 * d.gen_warps);
+  E = std::min(std::max(E, 32.0), 2048.0);
+  if (const long fe = env_long("SP_SEG_EVENTS", 0)) E = static_cast<double>(fe);
+  std::vector<ClassInfo> cls_info;
   std::vector<uint32_t> cls_groups;
-  uint64_t n_chains_live = 0;
-  auto add_classes = [&](const std::vector<Cls>& cls) {
+  std::vector<uint4> desc;
+  std::vector<uint16_t> colrow16;
+  uint64_t n_chains = 0, n_chains_live = 0;
+  auto add_classes = [&](const std::vector<Cls>& cls, bool live) {
     for (const Cls& cl : cls) {
-      const uint32_t ci = static_cast<uint32_t>(cls_dist.size());
-      cls_dist.push_back(cl.dist);
-      const double neg_ln_q = -std::log1p(-cl.p);
-      cls_inv.push_back(static_cast<float>(1.0 / neg_ln_q));  // p == 1 -> 0: fire every trial
-      cls_goff.push_back(cls_groups.size());
-      cls_groups.insert(cls_groups.end(), cl.groups.begin(), cl.groups.end());
-      const uint64_t trials = cl.groups.size() * T;
-      double len = std::ceil(kEvents / cl.p);
-      len = std::min(std::max(len, 64.0), 16777216.0);
-      uint64_t n_ch = (trials + static_cast<uint64_t>(len) - 1) / static_cast<uint64_t>(len);
-      n_ch = std::max<uint64_t>(n_ch, 1);
-      const uint64_t L = (trials + n_ch - 1) / n_ch;
-      for (uint64_t i = 0; i < n_ch; ++i) {
-        ch_class.push_back(ci);
-        ch_lo.push_back(i * L);
-        ch_hi.push_back(std::min(trials, (i + 1) * L));
+      ClassInfo ci{};
+      ci.dist = cl.dist;
+      ci.inv = static_cast<float>(1.0 / -std::log1p(-cl.p));  // p == 1 -> 0: fire every trial
+      ci.goff = static_cast<uint32_t>(cls_groups.size());
+      ci.trials = cl.groups.size() * T;
+      double len = std::ceil(E / cl.p);
+      len = std::min(std::max(len, 32.0), 16777216.0);
+      uint64_t n_seg = std::max<uint64_t>((ci.trials + static_cast<uint64_t>(len) - 1) /
+                                              static_cast<uint64_t>(len), 1);
+      ci.L = (ci.trials + n_seg - 1) / n_seg;
+      ci.n_seg = static_cast<uint32_t>(n_seg);
+      ci.seg_off = static_cast<uint32_t>(n_chains);
+      n_chains += n_seg;
+      cls_info.push_back(ci);
+      for (uint32_t g : cl.groups) {
+        cls_groups.push_back(g);
+        if (!live) continue;
+        const sp_group& gr = h.groups[g];
+        uint32_t lens[4] = {0, 0, 0, 0};
+        const uint32_t base = static_cast<uint32_t>(colrow16.size());
+        for (uint32_t b = 0; b < gr.arity; ++b) {
+          const uint64_t sidx = gr.first_symbol + b;
+          lens[b] = static_cast<uint32_t>(dcol_len(sidx));
+          if (lens[b] > 0xFFFF) throw std::invalid_argument("M_sym column longer than 65535");
+          for (uint64_t i = dcol_ptr[sidx]; i < dcol_ptr[sidx + 1]; ++i)
+            colrow16.push_back(static_cast<uint16_t>(dcol_rows[i] * d.tw));
+        }
+        desc.push_back(make_uint4(base, lens[0] | (lens[1] << 16), lens[2] | (lens[3] << 16), g));
       }
     }
   };
-  add_classes(live_cls);
-  n_chains_live = ch_class.size();
-  add_classes(dead_cls);
-
-  // Dense slots: live first; per-row slot lists for the output pass.
-  std::vector<uint32_t> dense_sym = dense_live;
-  dense_sym.insert(dense_sym.end(), dense_dead.begin(), dense_dead.end());
-  std::vector<uint32_t> slot_of(n_sym, UINT32_MAX);
-  for (uint32_t i = 0; i < n_dense_live; ++i) slot_of[dense_live[i]] = i;
-  std::vector<uint32_t> drow_ptr(n_meas + 1, 0), drow_slot;
-  for (uint64_t k = 0; k < n_meas; ++k) {
-    for (uint64_t i = h.row_ptr[k]; i < h.row_ptr[k + 1]; ++i)
-      if (slot_of[h.sym_idx[i]] != UINT32_MAX) drow_slot.push_back(slot_of[h.sym_idx[i]]);
-    drow_ptr[k + 1] = static_cast<uint32_t>(drow_slot.size());
-  }
+  add_classes(live_cls, true);
+  n_chains_live = n_chains;
+  add_classes(dead_cls, false);
+  if (n_chains >= (1ull << 32)) throw std::invalid_argument("too many sampling chains");
 
   std::vector<uint32_t> g_first(G), g_arity(G);
   std::vector<uint8_t> g_dist(G);
@@ -288,12 +451,6 @@ void build_plan(sp_ctx* c) {
     g_param[g] = h.groups[g].param;
   }
 
-  d = DevPlan{};
-  d.n_meas = static_cast<uint32_t>(n_meas);
-  d.n_sym = static_cast<uint32_t>(n_sym);
-  d.n_groups = static_cast<uint32_t>(G);
-  d.t_log2 = static_cast<uint32_t>(lg);
-  d.tw = static_cast<uint32_t>(T / 32);
   d.row_ptr = c->b_row_ptr.upload(h.row_ptr, s);
   d.sym_idx = c->b_sym_idx.upload(h.sym_idx, s);
   d.col_ptr = c->b_col_ptr.upload(col_ptr, s);
@@ -306,24 +463,30 @@ void build_plan(sp_ctx* c) {
   d.g_arity = c->b_arity.upload(g_arity, s);
   d.g_dist = c->b_dist.upload(g_dist, s);
   d.g_param = c->b_param.upload(g_param, s);
-  d.row_const = c->b_row_const.upload(row_const, s);
   d.row_const_compat = c->b_row_const_compat.upload(row_const_compat, s);
   d.n_ones = static_cast<uint32_t>(ones.size());
   d.ones_syms = c->b_ones.upload(ones, s);
-  d.n_dense_live = static_cast<uint32_t>(n_dense_live);
-  d.n_dense_all = static_cast<uint32_t>(dense_sym.size());
   d.dense_sym = c->b_dense_sym.upload(dense_sym, s);
   d.drow_ptr = c->b_drow_ptr.upload(drow_ptr, s);
   d.drow_slot = c->b_drow_slot.upload(drow_slot, s);
-  d.n_chains_live = static_cast<uint32_t>(n_chains_live);
-  d.n_chains_all = static_cast<uint32_t>(ch_class.size());
-  d.ch_class = c->b_ch_class.upload(ch_class, s);
-  d.ch_lo = c->b_ch_lo.upload(ch_lo, s);
-  d.ch_hi = c->b_ch_hi.upload(ch_hi, s);
-  d.cls_dist = c->b_cls_dist.upload(cls_dist, s);
-  d.cls_inv = c->b_cls_inv.upload(cls_inv, s);
-  d.cls_goff = c->b_cls_goff.upload(cls_goff, s);
+  d.n_cls_all = static_cast<uint32_t>(cls_info.size());
+  d.n_seg_live = static_cast<uint32_t>(n_chains_live);
+  d.n_seg_all = static_cast<uint32_t>(n_chains);
+  d.cls = c->b_cls.upload(cls_info, s);
   d.cls_groups = c->b_cls_groups.upload(cls_groups, s);
+  d.desc = c->b_desc.upload(desc, s);
+  d.colrow = c->b_colrow.upload(colrow16, s);
+  {
+    std::vector<uint32_t> lvl_ptr(X.n_levels + 1, 0);
+    for (uint64_t k = 0; k < n_meas; ++k) lvl_ptr[X.depth[k] + 1]++;
+    for (uint32_t l = 0; l < X.n_levels; ++l) lvl_ptr[l + 1] += lvl_ptr[l];
+    std::vector<uint16_t> lvl_rows(std::max<uint64_t>(n_meas, 1));
+    std::vector<uint32_t> fillp(lvl_ptr.begin(), lvl_ptr.end() - 1);
+    for (uint64_t k = 0; k < n_meas; ++k) lvl_rows[fillp[X.depth[k]]++] = static_cast<uint16_t>(k);
+    d.parent = c->b_parent.upload(X.parent, s);
+    d.lvl_rows = c->b_lvl_rows.upload(lvl_rows, s);
+    d.lvl_ptr = c->b_lvl_ptr.upload(lvl_ptr, s);
+  }
   d.n_live_groups = static_cast<uint32_t>(live_groups.size());
   d.live_groups = c->b_live_groups.upload(live_groups, s);
   ck(cudaStreamSynchronize(s), "plan upload");

@@ -1,8 +1,8 @@
 // sm_100a kernels for the SymPhase sampling hot path.
 //
 //   K1  fused sampler      draw (Philox4x32-10, geometric skip) + GF(2) product +
-//                          record write, one persistent kernel (replaces
-//                          draw_assignments + sample, sampler.cpp:48-112)
+//                          record write, one persistent warp-specialised kernel
+//                          (replaces draw_assignments + sample, sampler.cpp:48-112)
 //   K4  fused, compat RNG  bit-exact keyed_draw/fill_group (sampler.hpp:14-28,
 //                          sampler.cpp:11-44) + product
 //   D   draw               the assignment matrix S of K1/K4 (draw_assignments)
@@ -10,30 +10,46 @@
 //                          (sampler.cpp:61-112, bit_matrix.cpp:314-328)
 //   K3  encode             encode_shots '01' / 'b8' (sampler.cpp:118-140)
 //
-// All of this is integer/bitwise and HBM-bound work: LOP3 XOR accumulation,
-// shared-memory tiles, coalesced u64 stores. There is no binary MMA on sm_100a
-// worth using, so no tensor-core path.
+// All of this is integer/bitwise, HBM-write-bound work: shared-memory XOR
+// tiles, LOP3 accumulation, coalesced 16-byte stores. sm_100a has no binary
+// MMA worth using, so there is no tensor-core path.
 #include "kernels.cuh"
 
 #include <algorithm>
 
 namespace symphase {
+
+RoundKeys expand_keys(uint64_t seed) {
+  RoundKeys K{};
+  uint32_t k0 = static_cast<uint32_t>(seed), k1 = static_cast<uint32_t>(seed >> 32);
+  for (int i = 0; i < 10; ++i) {
+    K.k[2 * i] = k0;
+    K.k[2 * i + 1] = k1;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  return K;
+}
+
 namespace {
 
 constexpr unsigned kFull = 0xFFFFFFFFu;
-constexpr int kFusedThreads = 512;
+// Named barriers of the fused kernel (0 is __syncthreads).
+constexpr uint32_t kBarFull0 = 1, kBarEmpty0 = 3, kBarDrain = 5;
+
+__host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) & ~size_t{15}; }
 
 // ---- random numbers -------------------------------------------------------
 
-// Philox4x32-10 (Salmon et al., SC'11), counter-based: one call -> 4 words.
-__device__ __forceinline__ uint4 philox10(uint4 c, uint32_t k0, uint32_t k1) {
+// Philox4x32-10 (Salmon et al., SC'11): one counter block -> 4 words. The
+// key schedule is expanded on the host, so each round is 2 IMAD.WIDE + 2 LOP3
+// with the round keys read straight from the parameter bank.
+__device__ __forceinline__ uint4 philox10(uint4 c, const RoundKeys& K) {
 #pragma unroll
   for (int i = 0; i < 10; ++i) {
     const uint32_t lo0 = 0xD2511F53u * c.x, hi0 = __umulhi(0xD2511F53u, c.x);
     const uint32_t lo1 = 0xCD9E8D57u * c.z, hi1 = __umulhi(0xCD9E8D57u, c.z);
-    c = make_uint4(hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0);
-    k0 += 0x9E3779B9u;
-    k1 += 0xBB67AE85u;
+    c = make_uint4(hi1 ^ c.y ^ K.k[2 * i], lo1, hi0 ^ c.w ^ K.k[2 * i + 1], lo0);
   }
   return c;
 }
@@ -80,157 +96,339 @@ __device__ __forceinline__ uint32_t group_bits_compat(uint32_t dist, double p, u
   }
 }
 
-__device__ __forceinline__ uint32_t pattern_of(uint32_t dist, uint32_t r) {
-  // Given that the channel fired: Bernoulli -> its one symbol; DEPOLARIZE1 ->
-  // X, Z, Y uniformly (bits x=1, z=2); DEPOLARIZE2 -> one of 15 non-identity
-  // Paulis uniformly (sampler.cpp:24-42 pattern encoding).
-  if (dist == 3) return 1u + __umulhi(r, 3u);
-  if (dist == 4) return 1u + __umulhi(r, 15u);
-  return 1u;
-}
+// ---- geometric-skip segments ----------------------------------------------
+//
+// A class's flattened (group, shot) trial space of one tile is cut into
+// segments; each segment is one Bernoulli(p) process walked by ONE warp in
+// lockstep. Every lane draws one Philox block per step: 4 Exp(1) skips
+// (Bernoulli) or 3 skips + one word whose three base-n digits pick the
+// non-identity Pauli of each firing (n = 3 for DEPOLARIZE1 -> X, Z, Y;
+// n = 15 for DEPOLARIZE2) — the joint channel pmf of fill_group
+// (sampler.cpp:24-42). Geometric gaps floor(Exp/-ln(1-p)) + 1 are laid
+// end to end in lane order with a warp prefix sum, so one step yields up to
+// 96-128 firing positions with no divergence. Streams are keyed by
+// (segment, global tile), independent of which warp, CTA or GPU runs them.
+struct Segment {
+  uint64_t lo;
+  uint32_t len, seg, goff, dist;
+  float inv;
+};
 
-// Runs one geometric-skip chain over its slice [lo, hi) of a class's
-// flattened (group, shot) trial space for global tile gtile, calling
-// emit(group_id, shot_in_tile, pattern) for each firing channel.
-template <class Emit>
-__device__ __forceinline__ void run_chain(const DevPlan& P, uint32_t c, uint64_t gtile,
-                                          uint32_t k0, uint32_t k1, Emit&& emit) {
-  const uint32_t cls = P.ch_class[c];
-  uint64_t pos = P.ch_lo[c];
-  const uint64_t hi = P.ch_hi[c];
-  const float inv = P.cls_inv[cls];
-  const uint32_t dist = P.cls_dist[cls];
-  const uint32_t* groups = P.cls_groups + P.cls_goff[cls];
-  const uint32_t tmask = (1u << P.t_log2) - 1u;
-  uint4 ctr = make_uint4(c, 0u, static_cast<uint32_t>(gtile),
-                         (static_cast<uint32_t>(gtile >> 32) & 0xFFFFFFu) | (kDomChain << 24));
-  for (;;) {
-    const uint4 r = philox10(ctr, k0, k1);
-    ctr.y++;
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const float sf = exp1_from_bits(h ? r.z : r.x) * inv;
-      // Chain slices are <= 2^24 trials, so (float)rem is exact.
-      if (!(sf < static_cast<float>(hi - pos))) return;
-      pos += static_cast<uint64_t>(sf);
-      if (pos >= hi) return;
-      emit(groups[pos >> P.t_log2], static_cast<uint32_t>(pos) & tmask,
-           pattern_of(dist, h ? r.w : r.y));
-      ++pos;
-    }
+__device__ __forceinline__ void segment_init(Segment& sg, const ClassInfo* cls, uint32_t n_cls,
+                                             uint32_t seg) {
+  uint32_t lo = 0, hi = n_cls;  // largest k with cls[k].seg_off <= seg
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (cls[mid].seg_off <= seg) lo = mid; else hi = mid;
   }
+  const ClassInfo& ci = cls[lo];
+  sg.lo = static_cast<uint64_t>(seg - ci.seg_off) * ci.L;
+  sg.len = static_cast<uint32_t>(min(sg.lo + ci.L, ci.trials) - sg.lo);
+  sg.seg = seg;
+  sg.goff = ci.goff;
+  sg.dist = ci.dist;
+  sg.inv = ci.inv;
 }
 
-// Output pass shared by K1/K4: tile (+ const + dense coins) -> HBM.
-template <bool kCounts>
-__device__ __forceinline__ void store_tile(const DevPlan& P, const uint32_t* tile,
-                                           const uint32_t* coin, const uint32_t* row_const,
-                                           bool use_dense, uint64_t t_local, uint64_t n_shots,
-                                           uint64_t* __restrict__ out, uint64_t ld,
-                                           unsigned long long* cnt) {
-  const uint32_t tw2_log2 = P.t_log2 - 6, tw2 = 1u << tw2_log2;
-  const uint64_t T = 1ull << P.t_log2;
-  const uint64_t first = t_local * T;
-  const uint64_t valid = min(T, n_shots - first);
-  const uint32_t vw = static_cast<uint32_t>((valid + 63) >> 6);
-  const uint64_t tail = (valid & 63) ? ((1ull << (valid & 63)) - 1) : ~0ull;
-  const uint2* t2 = reinterpret_cast<const uint2*>(tile);
-  const uint2* c2 = reinterpret_cast<const uint2*>(coin);
-  const uint32_t items = P.n_meas << tw2_log2;
-  for (uint32_t i = threadIdx.x; i < items; i += blockDim.x) {
-    const uint32_t k = i >> tw2_log2, p = i & (tw2 - 1);
-    if (p >= vw) continue;
-    uint2 v = t2[i];
-    if ((row_const[k >> 5] >> (k & 31)) & 1u) { v.x = ~v.x; v.y = ~v.y; }
-    if (use_dense) {
-      for (uint32_t j = P.drow_ptr[k], e = P.drow_ptr[k + 1]; j < e; ++j) {
-        const uint2 c = c2[(P.drow_slot[j] << tw2_log2) + p];
-        v.x ^= c.x;
-        v.y ^= c.y;
+// emit(class_position, shot_in_tile, pattern) runs on the lane that owns
+// the firing; all lanes of the warp must call segment_walk together.
+template <class Emit>
+__device__ __forceinline__ void segment_walk(const Segment& sg, const RoundKeys& K, uint64_t gtile,
+                                             uint32_t t_log2, uint32_t lane, Emit&& emit) {
+  const bool bern = sg.dist == 1;
+  const uint32_t n = sg.dist == 3 ? 3u : 15u;
+  const uint32_t magic = n == 3 ? 0x5556u : 0x1112u;  // exact /n for values < n^3
+  const uint32_t tmask = (1u << t_log2) - 1u;
+  const uint32_t c3 = (static_cast<uint32_t>(gtile >> 32) & 0xFFFFFFu) | (kDomChain << 24);
+  uint32_t pos = 0;  // trials consumed (warp-uniform), < len <= 2^24
+  for (uint32_t draw = 0;; ++draw) {
+    const uint4 r = philox10(make_uint4(sg.seg, draw * 32 + lane, static_cast<uint32_t>(gtile), c3), K);
+    const uint32_t w[4] = {r.x, r.y, r.z, r.w};
+    uint32_t incl[4];
+    uint32_t acc = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (k == 3 && !bern) break;
+      const float sf = exp1_from_bits(w[k]) * sg.inv;
+      acc += (sf < 16777216.f ? static_cast<uint32_t>(sf) : 16777216u) + 1u;  // gap to next firing
+      incl[k] = acc;
+    }
+    uint32_t scan = acc;  // warp inclusive scan of the lanes' gap sums
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(kFull, scan, o);
+      if (lane >= static_cast<uint32_t>(o)) scan += t;
+    }
+    const uint32_t total = __shfl_sync(kFull, scan, 31);
+    const uint32_t base = pos + scan - acc - 1;
+    uint32_t digits = bern ? 0u : __umulhi(r.w, n * n * n);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (k == 3 && !bern) break;
+      uint32_t pat = 1u;
+      if (!bern) {
+        const uint32_t q = (digits * magic) >> 16;
+        pat = 1u + digits - q * n;
+        digits = q;
+      }
+      const uint32_t rel = base + incl[k];
+      if (rel < sg.len) {
+        const uint64_t f = sg.lo + rel;
+        emit(sg.goff + static_cast<uint32_t>(f >> t_log2), static_cast<uint32_t>(f) & tmask, pat);
       }
     }
-    uint64_t w = (static_cast<uint64_t>(v.y) << 32) | v.x;
-    if (p == vw - 1) w &= tail;
-    out[static_cast<uint64_t>(k) * ld + (first >> 6) + p] = w;
-    if (kCounts) atomicAdd(&cnt[k], static_cast<unsigned long long>(__popcll(w)));
+    pos += total;
+    if (pos >= sg.len) return;
   }
 }
 
-// ---- K1: fused Philox sampler --------------------------------------------
-template <bool kCounts>
-__global__ void __launch_bounds__(kFusedThreads)
-k1_fused(const DevPlan P, uint64_t seed, uint64_t tile0, uint32_t n_tiles, uint64_t n_shots,
-         uint64_t* __restrict__ out, uint64_t ld, unsigned long long* __restrict__ counts) {
-  extern __shared__ __align__(16) uint32_t smem[];
-  const uint32_t tw = P.tw;
-  uint32_t* tile = smem;                                  // [n_meas][tw]
-  uint32_t* coin = tile + static_cast<size_t>(P.n_meas) * tw;  // [n_dense_live][tw]
-  unsigned long long* cnt =
-      reinterpret_cast<unsigned long long*>(coin + static_cast<size_t>(P.n_dense_live) * tw);
-  const uint32_t k0 = static_cast<uint32_t>(seed), k1 = static_cast<uint32_t>(seed >> 32);
-  if (kCounts)
-    for (uint32_t i = threadIdx.x; i < P.n_meas; i += blockDim.x) cnt[i] = 0;
+__device__ __forceinline__ void named_sync(uint32_t id, uint32_t n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void named_arrive(uint32_t id, uint32_t n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
 
-  const uint32_t tw4_log2 = P.t_log2 - 7, tw4 = 1u << tw4_log2;
-  for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-    const uint64_t gtile = tile0 + t;
-    // Phase 0: clear the accumulation tile.
-    uint4* t4 = reinterpret_cast<uint4*>(tile);
-    for (uint32_t i = threadIdx.x; i < (P.n_meas << tw4_log2); i += blockDim.x)
-      t4[i] = make_uint4(0, 0, 0, 0);
-    // Phase 1: bit-sliced fair-coin words, keyed by (symbol, global 128-shot quad).
-    uint4* c4 = reinterpret_cast<uint4*>(coin);
-    for (uint32_t i = threadIdx.x; i < (P.n_dense_live << tw4_log2); i += blockDim.x) {
-      const uint32_t slot = i >> tw4_log2, q = i & (tw4 - 1);
-      const uint64_t gq = (gtile << tw4_log2) + q;
-      c4[i] = philox10(make_uint4(P.dense_sym[slot], static_cast<uint32_t>(gq),
-                                  (static_cast<uint32_t>(gq >> 32) & 0xFFFFFFu) | (kDomCoin << 24),
-                                  0u),
-                       k0, k1);
+__device__ __forceinline__ uint4 xor4(uint4 a, uint4 b) {
+  return make_uint4(a.x ^ b.x, a.y ^ b.y, a.z ^ b.z, a.w ^ b.w);
+}
+
+// ---- K1: fused, warp-specialised Philox sampler ---------------------------
+//
+// The planner rewrites M_sym = L·D (abi.cpp, chain transform): each row k has
+// at most one earlier parent row p(k) and D row k = row k XOR row p(k), which
+// for syndrome-extraction circuits is the detector-like difference of
+// consecutive rounds — far fewer symbols per column. The kernel samples in
+// D space and rebuilds M rows level by level (out[k] = d[k] ^ out[p(k)]).
+//
+// Per CTA: two shared-memory accumulation tiles [n_meas][T/32] u32 (double
+// buffer) and two coin buffers [n_dense+1][T/32]. Generator warps walk the
+// geometric-skip segments of tile i (warp-cooperative) and XOR each fired
+// symbol's D column into tile[i&1] with shared atomics; drain warps
+// meanwhile make tile i's fair-coin words, then — once the tile is complete
+// — add dense terms and parents level by level, stream the records to HBM
+// with 16-byte stores and zero the buffer for tile i+2. Named barriers
+// FULL[b] / EMPTY[b] hand the buffers back and forth. Event tables and row
+// tables are staged in shared memory when they fit.
+template <bool kStaged, bool kRowStaged>
+__global__ void __launch_bounds__(kFusedThreads, 1)
+k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, uint64_t n_shots,
+         uint64_t* __restrict__ out, uint64_t ld, unsigned long long* __restrict__ counts,
+         bool vec) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const uint32_t tw = P.tw, tw4_log2 = P.t_log2 - 7, tw4 = 1u << tw4_log2;
+  const uint32_t tile_words = P.n_meas * tw;
+  const uint32_t n_slots = P.n_dense_live + 1;  // + the all-ones constant slot
+  const bool with_counts = counts != nullptr;
+  uint32_t* tiles = reinterpret_cast<uint32_t*>(smem);
+  uint32_t* coins = tiles + 2 * tile_words;
+  uint8_t* p = reinterpret_cast<uint8_t*>(coins + 2 * n_slots * tw);
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(p);
+  p += align16(4ull * P.n_meas);
+  uint32_t* segctr = reinterpret_cast<uint32_t*>(p);  // per-buffer segment dispensers
+  p += 16;
+
+  const ClassInfo* CLS = P.cls;
+  const uint4* DESC = P.desc;
+  const uint16_t* COLROW = P.colrow;
+  const uint32_t* DRP = P.drow_ptr;
+  const uint16_t* DRS = P.drow_slot;
+  const int32_t* PAR = P.parent;
+  const uint16_t* LVR = P.lvl_rows;
+  if (kRowStaged) {
+    uint32_t* s_drp = reinterpret_cast<uint32_t*>(p);
+    p += align16(4ull * (P.n_meas + 1));
+    uint16_t* s_drs = reinterpret_cast<uint16_t*>(p);
+    p += align16(2ull * P.n_drow);
+    int32_t* s_par = reinterpret_cast<int32_t*>(p);
+    p += align16(4ull * P.n_meas);
+    uint16_t* s_lvr = reinterpret_cast<uint16_t*>(p);
+    p += align16(2ull * P.n_meas);
+    for (uint32_t i = threadIdx.x; i <= P.n_meas; i += blockDim.x) s_drp[i] = P.drow_ptr[i];
+    for (uint32_t i = threadIdx.x; i < P.n_drow; i += blockDim.x) s_drs[i] = P.drow_slot[i];
+    for (uint32_t i = threadIdx.x; i < P.n_meas; i += blockDim.x) {
+      s_par[i] = P.parent[i];
+      s_lvr[i] = P.lvl_rows[i];
     }
-    __syncthreads();
-    // Phase 2: sparse channels — geometric-skip chains, XOR the fired
-    // symbols' M_sym columns into the tile (one bit per measurement row).
-    for (uint32_t c = threadIdx.x; c < P.n_chains_live; c += blockDim.x) {
-      run_chain(P, c, gtile, k0, k1, [&](uint32_t gid, uint32_t shot, uint32_t pat) {
-        const uint32_t bit = 1u << (shot & 31), wofs = shot >> 5;
-        uint32_t s = P.g_first[gid];
-        for (; pat; pat >>= 1, ++s) {
-          if (!(pat & 1u)) continue;
-          for (uint64_t j = P.col_ptr[s], e = P.col_ptr[s + 1]; j < e; ++j)
-            atomicXor(&tile[P.col_rows[j] * tw + wofs], bit);
-        }
-      });
-    }
-    __syncthreads();
-    // Phase 3: constant + dense terms, coalesced u64 stores.
-    store_tile<kCounts>(P, tile, coin, P.row_const, true, t, n_shots, out, ld, cnt);
-    __syncthreads();
+    DRP = s_drp;
+    DRS = s_drs;
+    PAR = s_par;
+    LVR = s_lvr;
   }
-  if (kCounts)
+  if (kStaged) {
+    ClassInfo* s_cls = reinterpret_cast<ClassInfo*>(p);
+    p += align16(sizeof(ClassInfo) * P.n_cls_live);
+    uint4* s_desc = reinterpret_cast<uint4*>(p);
+    p += 16ull * P.n_desc_live;
+    uint16_t* s_col = reinterpret_cast<uint16_t*>(p);
+    {
+      const uint32_t* src = reinterpret_cast<const uint32_t*>(P.cls);
+      uint32_t* dst = reinterpret_cast<uint32_t*>(s_cls);
+      for (uint32_t i = threadIdx.x; i < P.n_cls_live * (sizeof(ClassInfo) / 4); i += blockDim.x)
+        dst[i] = src[i];
+    }
+    for (uint32_t i = threadIdx.x; i < P.n_desc_live; i += blockDim.x) s_desc[i] = P.desc[i];
+    for (uint64_t i = threadIdx.x; i < P.n_colrow; i += blockDim.x) s_col[i] = P.colrow[i];
+    CLS = s_cls;
+    DESC = s_desc;
+    COLROW = s_col;
+  }
+  {
+    uint4* t4 = reinterpret_cast<uint4*>(tiles);
+    for (uint32_t i = threadIdx.x; i < (2 * tile_words) / 4; i += blockDim.x)
+      t4[i] = make_uint4(0, 0, 0, 0);
+    uint4* c4 = reinterpret_cast<uint4*>(coins);
+    for (uint32_t i = threadIdx.x; i < 2 * tw4; i += blockDim.x) {
+      const uint32_t b = i >> tw4_log2, q = i & (tw4 - 1);
+      c4[((b * n_slots + P.n_dense_live) << tw4_log2) + q] = make_uint4(kFull, kFull, kFull, kFull);
+    }
+    if (with_counts)
+      for (uint32_t i = threadIdx.x; i < P.n_meas; i += blockDim.x) cnt[i] = 0;
+    if (threadIdx.x < 2) segctr[threadIdx.x] = 0;
+  }
+  __syncthreads();
+
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t n_gen = P.gen_warps;
+  const uint32_t n_my =
+      n_tiles > blockIdx.x ? (n_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0u;
+
+  if (warp < n_gen) {
+    // ---------------- event generators ----------------
+    for (uint32_t i = 0; i < n_my; ++i) {
+      const uint32_t b = i & 1;
+      const uint64_t gtile = tile0 + blockIdx.x + static_cast<uint64_t>(i) * gridDim.x;
+      if (i >= 2) named_sync(kBarEmpty0 + b, kFusedThreads);
+      uint32_t* tile = tiles + b * tile_words;
+      auto apply = [&](uint32_t cpos, uint32_t shot, uint32_t pat) {
+        const uint4 d = DESC[cpos];
+        const uint32_t bit = 1u << (shot & 31);
+        uint32_t* wb = tile + (shot >> 5);
+        uint32_t off = d.x;
+        const uint32_t lens[4] = {d.y & 0xFFFFu, d.y >> 16, d.z & 0xFFFFu, d.z >> 16};
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+          if ((pat >> s) & 1u)
+            for (uint32_t j = 0; j < lens[s]; ++j) atomicXor(wb + COLROW[off + j], bit);
+          off += lens[s];
+        }
+      };
+      for (;;) {
+        uint32_t seg = 0;
+        if (lane == 0) seg = atomicAdd(&segctr[b], 1u);
+        seg = __shfl_sync(kFull, seg, 0);
+        if (seg >= P.n_seg_live) break;
+        Segment sg;
+        segment_init(sg, CLS, P.n_cls_live, seg);
+        segment_walk(sg, K, gtile, P.t_log2, lane, apply);
+      }
+      named_arrive(kBarFull0 + b, kFusedThreads);
+    }
+  } else {
+    // ---------------- drain warps ----------------
+    const uint32_t ct = threadIdx.x - n_gen * 32, nct = kFusedThreads - n_gen * 32;
+    const uint32_t seg = tw4 < 32 ? tw4 : 32;  // lanes per measurement row in a warp
+    for (uint32_t i = 0; i < n_my; ++i) {
+      const uint32_t b = i & 1;
+      const uint64_t t_local = blockIdx.x + static_cast<uint64_t>(i) * gridDim.x;
+      const uint64_t gtile = tile0 + t_local;
+      uint4* c4 = reinterpret_cast<uint4*>(coins + b * n_slots * tw);
+      for (uint32_t j = ct; j < (P.n_dense_live << tw4_log2); j += nct) {
+        const uint32_t slot = j >> tw4_log2, q = j & (tw4 - 1);
+        const uint64_t gq = (gtile << tw4_log2) + q;
+        c4[j] = philox10(make_uint4(P.dense_sym[slot], static_cast<uint32_t>(gq),
+                                    (static_cast<uint32_t>(gq >> 32) & 0xFFFFFFu) |
+                                        (kDomCoin << 24),
+                                    0u),
+                         K);
+      }
+      named_sync(kBarDrain, nct);
+      named_sync(kBarFull0 + b, kFusedThreads);
+
+      uint4* t4 = reinterpret_cast<uint4*>(tiles + b * tile_words);
+      const uint64_t first = t_local << P.t_log2;
+      const uint64_t valid = min(static_cast<uint64_t>(1) << P.t_log2, n_shots - first);
+      const uint32_t vq = static_cast<uint32_t>((valid + 127) >> 7);
+      const uint32_t rem = static_cast<uint32_t>(valid & 127);
+      // Rows in level order: a row's parent is final before the row is read.
+      for (uint32_t lv = 0; lv < P.n_levels; ++lv) {
+        const uint32_t r0 = P.lvl_ptr[lv], r1 = P.lvl_ptr[lv + 1];
+        const uint32_t items = (r1 - r0) << tw4_log2;
+        const uint32_t items_rounded = (items + nct - 1) / nct * nct;
+        for (uint32_t base = 0; base < items_rounded; base += nct) {
+          const uint32_t j = base + ct;
+          uint32_t pc = 0, k = 0;
+          if (j < items) {
+            k = LVR[r0 + (j >> tw4_log2)];
+            const uint32_t q = j & (tw4 - 1);
+            const uint32_t ti = (k << tw4_log2) + q;
+            uint4 v = t4[ti];
+            for (uint32_t s = DRP[k], e = DRP[k + 1]; s < e; ++s)
+              v = xor4(v, c4[(static_cast<uint32_t>(DRS[s]) << tw4_log2) + q]);
+            const int32_t par = PAR[k];
+            if (par >= 0) v = xor4(v, t4[(static_cast<uint32_t>(par) << tw4_log2) + q]);
+            t4[ti] = v;  // final value, read by this row's children
+            if (q < vq) {
+              bool two = true;  // whether the item's second u64 word is inside the tile
+              if (q == vq - 1 && rem) {
+                const uint32_t m[4] = {rem >= 32 ? kFull : (1u << rem) - 1,
+                                       rem >= 64 ? kFull : rem > 32 ? (1u << (rem - 32)) - 1 : 0u,
+                                       rem >= 96 ? kFull : rem > 64 ? (1u << (rem - 64)) - 1 : 0u,
+                                       rem > 96 ? (1u << (rem - 96)) - 1 : 0u};
+                v.x &= m[0]; v.y &= m[1]; v.z &= m[2]; v.w &= m[3];
+                two = rem > 64;
+              }
+              uint64_t* o = out + static_cast<uint64_t>(k) * ld + (first >> 6) + 2 * q;
+              const uint64_t w0 = (static_cast<uint64_t>(v.y) << 32) | v.x;
+              const uint64_t w1 = (static_cast<uint64_t>(v.w) << 32) | v.z;
+              if (vec && two) {
+                *reinterpret_cast<ulonglong2*>(o) = make_ulonglong2(w0, w1);
+              } else {
+                o[0] = w0;
+                if (two) o[1] = w1;
+              }
+              if (with_counts) pc = __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
+            }
+          }
+          if (with_counts) {
+            for (uint32_t o = seg >> 1; o; o >>= 1) pc += __shfl_xor_sync(kFull, pc, o);
+            if (j < items && (lane & (seg - 1)) == 0 && pc) atomicAdd(&cnt[k], pc);
+          }
+        }
+        if (P.n_levels > 1) named_sync(kBarDrain, nct);
+      }
+      for (uint32_t j = ct; j < tile_words / 4; j += nct) t4[j] = make_uint4(0, 0, 0, 0);
+      if (ct == 0) segctr[b] = 0;  // all generators are past tile i (FULL[b] completed)
+      if (i + 2 < n_my) named_arrive(kBarEmpty0 + b, kFusedThreads);
+    }
+  }
+  if (with_counts) {
+    __syncthreads();
     for (uint32_t i = threadIdx.x; i < P.n_meas; i += blockDim.x)
-      if (cnt[i]) atomicAdd(&counts[i], cnt[i]);
+      if (cnt[i]) atomicAdd(&counts[i], static_cast<unsigned long long>(cnt[i]));
+  }
 }
 
 // ---- K4: fused sampler with the reference's keyed_draw -------------------
+// Validation path (bit-exact with the CPU reference): one 64-bit keyed draw
+// per (group, shot), ballot into 32-shot symbol words, XOR into the tile.
 template <bool kCounts>
 __global__ void __launch_bounds__(kFusedThreads)
 k4_fused_compat(const DevPlan P, uint64_t seed_mix, uint64_t tile0, uint32_t n_tiles,
                 uint64_t n_shots, uint64_t* __restrict__ out, uint64_t ld,
                 unsigned long long* __restrict__ counts) {
-  extern __shared__ __align__(16) uint32_t smem[];
+  extern __shared__ __align__(16) uint32_t smem_k4[];
   const uint32_t tw = P.tw, tw_log2 = P.t_log2 - 5;
-  uint32_t* tile = smem;
-  unsigned long long* cnt =
-      reinterpret_cast<unsigned long long*>(tile + static_cast<size_t>(P.n_meas) * tw);
-  if (kCounts)
-    for (uint32_t i = threadIdx.x; i < P.n_meas; i += blockDim.x) cnt[i] = 0;
+  uint32_t* tile = smem_k4;
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
     const uint64_t gshot0 = (tile0 + t) << P.t_log2;
-    uint4* t4 = reinterpret_cast<uint4*>(tile);
-    for (uint32_t i = threadIdx.x; i < (P.n_meas << (P.t_log2 - 7)); i += blockDim.x)
-      t4[i] = make_uint4(0, 0, 0, 0);
+    for (uint32_t i = threadIdx.x; i < P.n_meas * tw; i += blockDim.x) tile[i] = 0;
     __syncthreads();
     const uint32_t tasks = P.n_live_groups << tw_log2;
     for (uint32_t task = warp; task < tasks; task += nwarps) {
@@ -248,12 +446,24 @@ k4_fused_compat(const DevPlan P, uint64_t seed_mix, uint64_t tile0, uint32_t n_t
       }
     }
     __syncthreads();
-    store_tile<kCounts>(P, tile, nullptr, P.row_const_compat, false, t, n_shots, out, ld, cnt);
+    const uint64_t first = static_cast<uint64_t>(t) << P.t_log2;
+    const uint64_t valid = min(static_cast<uint64_t>(1) << P.t_log2, n_shots - first);
+    const uint32_t vw = static_cast<uint32_t>((valid + 63) >> 6);
+    const uint64_t tail = (valid & 63) ? ((1ull << (valid & 63)) - 1) : ~0ull;
+    const uint32_t tw2_log2 = P.t_log2 - 6;
+    const uint2* t2 = reinterpret_cast<const uint2*>(tile);
+    for (uint32_t i = threadIdx.x; i < (P.n_meas << tw2_log2); i += blockDim.x) {
+      const uint32_t k = i >> tw2_log2, p = i & ((1u << tw2_log2) - 1);
+      if (p >= vw) continue;
+      uint2 v = t2[i];
+      uint64_t w = (static_cast<uint64_t>(v.y) << 32) | v.x;
+      if ((P.row_const_compat[k >> 5] >> (k & 31)) & 1u) w = ~w;
+      if (p == vw - 1) w &= tail;
+      out[static_cast<uint64_t>(k) * ld + (first >> 6) + p] = w;
+      if (kCounts && w) atomicAdd(&counts[k], static_cast<unsigned long long>(__popcll(w)));
+    }
     __syncthreads();
   }
-  if (kCounts)
-    for (uint32_t i = threadIdx.x; i < P.n_meas; i += blockDim.x)
-      if (cnt[i]) atomicAdd(&counts[i], cnt[i]);
 }
 
 // ---- D: draw_assignments -------------------------------------------------
@@ -266,9 +476,8 @@ __global__ void d_fill_ones(const uint32_t* syms, uint32_t n, uint64_t* S, uint6
   }
 }
 
-__global__ void d_coins(const DevPlan P, uint64_t seed, uint64_t quad0, uint64_t n_quads,
+__global__ void d_coins(const DevPlan P, const RoundKeys K, uint64_t quad0, uint64_t n_quads,
                         uint64_t n_words32, uint32_t last_mask, uint32_t* S32, uint64_t ld32) {
-  const uint32_t k0 = static_cast<uint32_t>(seed), k1 = static_cast<uint32_t>(seed >> 32);
   const uint64_t total = P.n_dense_all * n_quads;
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
@@ -279,7 +488,7 @@ __global__ void d_coins(const DevPlan P, uint64_t seed, uint64_t quad0, uint64_t
                                         (static_cast<uint32_t>(gq >> 32) & 0xFFFFFFu) |
                                             (kDomCoin << 24),
                                         0u),
-                             k0, k1);
+                             K);
     const uint32_t v[4] = {r.x, r.y, r.z, r.w};
     uint32_t* row = S32 + sym * ld32;
 #pragma unroll
@@ -290,19 +499,22 @@ __global__ void d_coins(const DevPlan P, uint64_t seed, uint64_t quad0, uint64_t
   }
 }
 
-__global__ void d_chains(const DevPlan P, uint64_t seed, uint64_t tile0, uint32_t n_tiles,
-                         uint64_t n_shots, uint32_t* S32, uint64_t ld32) {
-  const uint32_t k0 = static_cast<uint32_t>(seed), k1 = static_cast<uint32_t>(seed >> 32);
-  const uint64_t total = static_cast<uint64_t>(P.n_chains_all) * n_tiles;
-  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    const uint32_t t = static_cast<uint32_t>(i / P.n_chains_all);
-    const uint32_t c = static_cast<uint32_t>(i - static_cast<uint64_t>(t) * P.n_chains_all);
+__global__ void d_segments(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles,
+                           uint64_t n_shots, uint32_t* S32, uint64_t ld32) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t warp = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+  const uint64_t total = static_cast<uint64_t>(P.n_seg_all) * n_tiles;
+  for (uint64_t i = warp; i < total; i += nwarps) {
+    const uint32_t t = static_cast<uint32_t>(i / P.n_seg_all);
+    const uint32_t seg = static_cast<uint32_t>(i - static_cast<uint64_t>(t) * P.n_seg_all);
     const uint64_t base = static_cast<uint64_t>(t) << P.t_log2;
-    run_chain(P, c, tile0 + t, k0, k1, [&](uint32_t gid, uint32_t shot, uint32_t pat) {
+    Segment sg;
+    segment_init(sg, P.cls, P.n_cls_all, seg);
+    segment_walk(sg, K, tile0 + t, P.t_log2, lane, [&](uint32_t cpos, uint32_t shot, uint32_t pat) {
       const uint64_t j = base + shot;
       if (j >= n_shots) return;
-      uint32_t s = P.g_first[gid];
+      uint32_t s = P.g_first[P.cls_groups[cpos]];
       for (; pat; pat >>= 1, ++s)
         if (pat & 1u) atomicXor(&S32[s * ld32 + (j >> 5)], 1u << (j & 31));
     });
@@ -464,7 +676,15 @@ __global__ void k3_01(const uint32_t* __restrict__ m32, uint64_t ld32, uint32_t 
 }
 
 __global__ void k_debug_philox(const uint32_t* in, uint32_t* out) {
-  const uint4 r = philox10(make_uint4(in[0], in[1], in[2], in[3]), in[4], in[5]);
+  RoundKeys K;
+  uint32_t k0 = in[4], k1 = in[5];
+  for (int i = 0; i < 10; ++i) {
+    K.k[2 * i] = k0;
+    K.k[2 * i + 1] = k1;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  const uint4 r = philox10(make_uint4(in[0], in[1], in[2], in[3]), K);
   out[0] = r.x; out[1] = r.y; out[2] = r.z; out[3] = r.w;
 }
 
@@ -477,8 +697,9 @@ uint64_t host_mix64(uint64_t x) {
   return x ^ (x >> 31);
 }
 
-template <class K>
-int persistent_grid(K kernel, const LaunchCfg& L, size_t smem, uint32_t n_tiles, int* grid) {
+template <class Kern>
+int persistent_grid(Kern kernel, const LaunchCfg& L, size_t smem, uint32_t n_tiles,
+                    uint32_t max_per_sm, int* grid) {
   if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(smem)) != cudaSuccess)
     return -1;
@@ -487,34 +708,56 @@ int persistent_grid(K kernel, const LaunchCfg& L, size_t smem, uint32_t n_tiles,
           cudaSuccess ||
       per_sm < 1)
     return -1;
+  per_sm = std::min<int>(per_sm, static_cast<int>(max_per_sm));
   *grid = static_cast<int>(std::min<uint64_t>(n_tiles, static_cast<uint64_t>(per_sm) * L.num_sms));
   return 0;
 }
 
+template <bool kStaged, bool kRowStaged>
+int launch_k1(const DevPlan& P, const LaunchCfg& L, const RoundKeys& K, uint64_t tile0,
+              uint32_t n_tiles, uint64_t n_shots, uint64_t* out, uint64_t ld,
+              unsigned long long* cnt) {
+  auto kern = k1_fused<kStaged, kRowStaged>;
+  const size_t smem = fused_smem_bytes(P, P.t_log2, kStaged, kRowStaged);
+  int grid = 0;
+  if (persistent_grid(kern, L, smem, n_tiles, P.cta_per_sm, &grid)) return -1;
+  const bool vec = (ld % 2 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0);
+  kern<<<grid, kFusedThreads, smem, L.stream>>>(P, K, tile0, n_tiles, n_shots, out, ld, cnt, vec);
+  return check_launch() ? -1 : 1;
+}
+
 }  // namespace
 
-size_t fused_smem_bytes(uint32_t n_meas, uint32_t n_dense, uint32_t tw, bool counts) {
-  return (static_cast<size_t>(n_meas) + n_dense) * tw * 4 + (counts ? 8ull * n_meas : 0);
+size_t fused_smem_bytes(const DevPlan& P, uint32_t t_log2, bool staged, bool row_staged) {
+  const size_t tw = size_t{1} << (t_log2 - 5);
+  size_t b = 2 * static_cast<size_t>(P.n_meas) * tw * 4;           // tiles
+  b += 2 * static_cast<size_t>(P.n_dense_live + 1) * tw * 4;        // coin words + ones slot
+  b += align16(4ull * P.n_meas) + 16;                               // counts, dispensers
+  if (row_staged) {
+    b += align16(4ull * (P.n_meas + 1));
+    b += align16(2ull * P.n_drow);
+    b += align16(4ull * P.n_meas);
+    b += align16(2ull * P.n_meas);
+  }
+  if (staged) {
+    b += align16(sizeof(ClassInfo) * P.n_cls_live);
+    b += 16ull * P.n_desc_live;
+    b += align16(P.n_colrow * 2);
+  }
+  return b;
 }
 
 int launch_fused_sample(const DevPlan& P, const LaunchCfg& L, uint64_t seed, uint64_t tile0,
                         uint64_t n_shots, uint64_t* out, uint64_t ld, uint64_t* counts) {
   const uint64_t T = 1ull << P.t_log2;
   const uint32_t n_tiles = static_cast<uint32_t>((n_shots + T - 1) / T);
-  const bool with_counts = counts != nullptr;
-  const size_t smem = fused_smem_bytes(P.n_meas, P.n_dense_live, P.tw, with_counts);
-  int grid = 0;
+  const RoundKeys K = expand_keys(seed);
   auto* cnt = reinterpret_cast<unsigned long long*>(counts);
-  if (with_counts) {
-    if (persistent_grid(k1_fused<true>, L, smem, n_tiles, &grid)) return -1;
-    k1_fused<true><<<grid, kFusedThreads, smem, L.stream>>>(P, seed, tile0, n_tiles, n_shots, out,
-                                                            ld, cnt);
-  } else {
-    if (persistent_grid(k1_fused<false>, L, smem, n_tiles, &grid)) return -1;
-    k1_fused<false><<<grid, kFusedThreads, smem, L.stream>>>(P, seed, tile0, n_tiles, n_shots,
-                                                             out, ld, cnt);
-  }
-  return check_launch() ? -1 : 1;
+  if (P.staged)
+    return P.row_staged ? launch_k1<true, true>(P, L, K, tile0, n_tiles, n_shots, out, ld, cnt)
+                        : launch_k1<true, false>(P, L, K, tile0, n_tiles, n_shots, out, ld, cnt);
+  return P.row_staged ? launch_k1<false, true>(P, L, K, tile0, n_tiles, n_shots, out, ld, cnt)
+                      : launch_k1<false, false>(P, L, K, tile0, n_tiles, n_shots, out, ld, cnt);
 }
 
 int launch_fused_sample_compat(const DevPlan& P, const LaunchCfg& L, uint64_t seed,
@@ -522,17 +765,16 @@ int launch_fused_sample_compat(const DevPlan& P, const LaunchCfg& L, uint64_t se
                                uint64_t* counts) {
   const uint64_t T = 1ull << P.t_log2;
   const uint32_t n_tiles = static_cast<uint32_t>((n_shots + T - 1) / T);
-  const bool with_counts = counts != nullptr;
-  const size_t smem = fused_smem_bytes(P.n_meas, 0, P.tw, with_counts);
+  const size_t smem = static_cast<size_t>(P.n_meas) * P.tw * 4;
   int grid = 0;
   auto* cnt = reinterpret_cast<unsigned long long*>(counts);
   const uint64_t sm = host_mix64(seed);
-  if (with_counts) {
-    if (persistent_grid(k4_fused_compat<true>, L, smem, n_tiles, &grid)) return -1;
+  if (counts) {
+    if (persistent_grid(k4_fused_compat<true>, L, smem, n_tiles, 8, &grid)) return -1;
     k4_fused_compat<true><<<grid, kFusedThreads, smem, L.stream>>>(P, sm, tile0, n_tiles,
                                                                    n_shots, out, ld, cnt);
   } else {
-    if (persistent_grid(k4_fused_compat<false>, L, smem, n_tiles, &grid)) return -1;
+    if (persistent_grid(k4_fused_compat<false>, L, smem, n_tiles, 8, &grid)) return -1;
     k4_fused_compat<false><<<grid, kFusedThreads, smem, L.stream>>>(P, sm, tile0, n_tiles,
                                                                     n_shots, out, ld, cnt);
   }
@@ -563,17 +805,18 @@ int launch_draw(const DevPlan& P, const LaunchCfg& L, bool compat, uint64_t seed
       ++launches;
     }
   } else {
+    const RoundKeys K = expand_keys(seed);
     const uint64_t n_quads = (n_words32 + 3) / 4;
     const uint32_t last_mask = (n_shots & 31) ? ((1u << (n_shots & 31)) - 1) : ~0u;
     if (P.n_dense_all) {
-      d_coins<<<grid, 256, 0, L.stream>>>(P, seed, (tile0 << P.t_log2) >> 7, n_quads, n_words32,
+      d_coins<<<grid, 256, 0, L.stream>>>(P, K, (tile0 << P.t_log2) >> 7, n_quads, n_words32,
                                           last_mask, S32, ld32);
       ++launches;
     }
     const uint64_t T = 1ull << P.t_log2;
     const uint32_t n_tiles = static_cast<uint32_t>((n_shots + T - 1) / T);
-    if (P.n_chains_all) {
-      d_chains<<<grid, 256, 0, L.stream>>>(P, seed, tile0, n_tiles, n_shots, S32, ld32);
+    if (P.n_seg_all) {
+      d_segments<<<grid, 256, 0, L.stream>>>(P, K, tile0, n_tiles, n_shots, S32, ld32);
       ++launches;
     }
   }
@@ -586,7 +829,8 @@ int launch_product(const DevPlan& P, const LaunchCfg& L, bool dense, const uint6
   if (P.n_meas == 0 || n_words == 0) return 0;
   const uint64_t tail = (n_shots & 63) ? ((1ull << (n_shots & 63)) - 1) : ~0ull;
   const uint64_t windows = (n_words + 63) / 64;
-  dim3 grid((P.n_meas + kK2Rows - 1) / kK2Rows, static_cast<unsigned>(std::min<uint64_t>(windows, 65535)));
+  dim3 grid((P.n_meas + kK2Rows - 1) / kK2Rows,
+            static_cast<unsigned>(std::min<uint64_t>(windows, 65535)));
   if (dense) {
     const uint64_t m_words = (P.n_sym + 63) / 64;
     k2_dense<<<grid, kK2Rows * 32, 0, L.stream>>>(P.dense, P.ldm, m_words, P.n_meas, S, ldS,

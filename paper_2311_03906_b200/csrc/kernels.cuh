@@ -10,8 +10,22 @@ namespace symphase {
 constexpr uint32_t kDomChain = 1u;  // geometric-skip event chains
 constexpr uint32_t kDomCoin = 2u;   // bit-sliced fair-coin words
 
+// One class = all sparse channels sharing (distribution, p). Its trial space
+// for one shot tile is the flattened (group, shot) grid, group-major, cut into
+// n_seg segments of L trials (the last one shorter), one warp walk each.
+struct ClassInfo {
+  uint64_t L = 0;        // trials per segment (<= 2^24)
+  uint64_t trials = 0;   // groups * T
+  uint32_t seg_off = 0;  // first segment id of the class
+  uint32_t n_seg = 0;
+  uint32_t goff = 0;    // first class position (index into desc / cls_groups)
+  float inv = 0.f;      // 1 / -ln(1 - p): Exp(1) -> geometric skip
+  uint32_t dist = 0;    // 1 Bernoulli, 3 DEPOLARIZE1, 4 DEPOLARIZE2
+  uint32_t pad = 0;
+};
+
 // Everything a kernel needs about the loaded model, all device pointers.
-// Built once per sp_load_* by plan.cpp.
+// Built once per model by abi.cpp (build_plan).
 struct DevPlan {
   uint32_t n_meas = 0, n_sym = 0, n_groups = 0;
   uint32_t t_log2 = 0, tw = 0;  // shot tile T = 1 << t_log2; tw = T/32 u32 words
@@ -21,7 +35,7 @@ struct DevPlan {
   const uint32_t* sym_idx = nullptr;
   const uint64_t* col_ptr = nullptr;   // [n_sym+1]
   const uint32_t* col_rows = nullptr;  // [nnz]
-  // dense row-major M_sym words [n_meas][ldm] (only when loaded / built)
+  // dense row-major M_sym words [n_meas][ldm] (only when requested)
   const uint64_t* dense = nullptr;
   uint64_t ldm = 0;
 
@@ -31,37 +45,58 @@ struct DevPlan {
   const uint8_t* g_dist = nullptr;
   const double* g_param = nullptr;
 
-  // Constant rows: bit k set when measurement k XORs a constant 1
-  // (s0, plus Bernoulli(p>=1) symbols in Philox mode).
-  const uint32_t* row_const = nullptr;         // Philox mode
-  const uint32_t* row_const_compat = nullptr;  // s0 only (compat mode)
+  // Constant rows in compat mode (s0 only): bit k = measurement k XORs 1.
+  const uint32_t* row_const_compat = nullptr;
   // Symbols whose assignment row is identically one in Philox mode (s0 and
   // Bernoulli(p>=1)); in compat mode only s0 (== ones_syms[0]).
   uint32_t n_ones = 0;
   const uint32_t* ones_syms = nullptr;
 
-  // Dense (bit-sliced) symbols: fair coins and Bernoulli(1/2).
-  uint32_t n_dense_live = 0, n_dense_all = 0;  // live slots come first
-  const uint32_t* dense_sym = nullptr;         // slot -> symbol id
-  const uint32_t* drow_ptr = nullptr;          // [n_meas+1] -> drow_slot
-  const uint32_t* drow_slot = nullptr;
+  // Dense (bit-sliced) symbols: fair coins and Bernoulli(1/2). Live slots
+  // first; slot n_dense_live of the fused kernel's coin buffer is all ones
+  // and stands for the constant term.
+  uint32_t n_dense_live = 0, n_dense_all = 0;
+  const uint32_t* dense_sym = nullptr;  // slot -> symbol id
+  const uint32_t* drow_ptr = nullptr;   // [n_meas+1] -> drow_slot
+  const uint16_t* drow_slot = nullptr;  // dense slots (and the ones slot) per row
+  uint32_t n_drow = 0;
 
-  // Sparse channels: classes of groups sharing (distribution, p), each
-  // sampled as one Bernoulli process over its flattened (group, shot) trial
-  // space of a tile, cut into chains of roughly equal expected event count.
-  uint32_t n_chains_live = 0, n_chains_all = 0;  // live chains come first
-  const uint32_t* ch_class = nullptr;
-  const uint64_t* ch_lo = nullptr;
-  const uint64_t* ch_hi = nullptr;
-  const uint8_t* cls_dist = nullptr;
-  const float* cls_inv = nullptr;   // 1 / -ln(1 - p)
-  const uint64_t* cls_goff = nullptr;
-  const uint32_t* cls_groups = nullptr;
+  // Sparse channels (see ClassInfo). Live classes first.
+  uint32_t n_cls_live = 0, n_cls_all = 0;
+  uint32_t n_seg_live = 0, n_seg_all = 0;
+  const ClassInfo* cls = nullptr;
+  const uint32_t* cls_groups = nullptr;  // class position -> group id
+  // Fused-kernel event tables in D space (M_sym = L·D, see abi.cpp), class-
+  // position order: desc = {colrow base, len0 | len1 << 16, len2 | len3 << 16,
+  // group id}; colrow entries = D row * tw (u16: n_meas * tw < 65536).
+  uint32_t n_desc_live = 0;
+  const uint4* desc = nullptr;
+  const uint16_t* colrow = nullptr;
+  uint64_t n_colrow = 0;
+  // Row reconstruction: out[k] = d[k] ^ out[parent[k]] (parent < k or -1),
+  // rows listed level by level (lvl_rows, lvl_ptr[n_levels + 1]).
+  const int32_t* parent = nullptr;
+  const uint16_t* lvl_rows = nullptr;
+  const uint32_t* lvl_ptr = nullptr;  // [n_levels + 1]
+  uint32_t n_levels = 1;
 
-  // Compat mode: group ids (>= 1) with at least one live symbol, and all.
+  // Fused-kernel launch shape (chosen by the planner).
+  uint32_t staged = 0;       // event tables copied into shared memory
+  uint32_t row_staged = 0;   // row tables copied into shared memory
+  uint32_t gen_warps = 12;   // event-generator warps; the rest drain tiles
+  uint32_t cta_per_sm = 1;
+
+  // Compat mode: group ids (>= 1) with at least one live symbol.
   uint32_t n_live_groups = 0;
   const uint32_t* live_groups = nullptr;
 };
+
+// Philox4x32-10 round keys for one seed (host-expanded, read from the
+// kernel-parameter bank).
+struct RoundKeys {
+  uint32_t k[20];
+};
+RoundKeys expand_keys(uint64_t seed);
 
 struct LaunchCfg {
   cudaStream_t stream = nullptr;
@@ -69,8 +104,10 @@ struct LaunchCfg {
   size_t smem_optin = 227 * 1024;
 };
 
-// Shared-memory bytes the fused kernel needs per CTA for tile width tw.
-size_t fused_smem_bytes(uint32_t n_meas, uint32_t n_dense, uint32_t tw, bool counts);
+constexpr int kFusedThreads = 512;
+
+// Shared-memory bytes of the fused kernel for a plan shape.
+size_t fused_smem_bytes(const DevPlan& P, uint32_t t_log2, bool staged, bool row_staged);
 
 // K1 fused sampler (Philox). Returns number of launches issued, <0 on error.
 int launch_fused_sample(const DevPlan& P, const LaunchCfg& L, uint64_t seed, uint64_t tile0,
