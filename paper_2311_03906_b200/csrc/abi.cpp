@@ -97,7 +97,11 @@ struct sp_ctx {
   // plan buffers
   DBuf b_row_ptr, b_sym_idx, b_col_ptr, b_col_rows, b_dense, b_first, b_arity, b_dist, b_param,
       b_row_const_compat, b_ones, b_dense_sym, b_drow_ptr, b_drow_slot, b_cls, b_cls_groups,
-      b_desc, b_colrow, b_live_groups, b_parent, b_lvl_rows, b_lvl_ptr;
+      b_desc, b_colrow, b_live_groups, b_parent, b_lvl_rows, b_lvl_ptr, b_plist;
+  // K2's own copy of the rows (independent of the group table)
+  bool prod_ready = false;
+  DevPlan pp;
+  DBuf p_row_ptr, p_sym_idx, p_dense;
   // scratch for sp_sample_to_host
   DBuf s_out, s_bytes;
   uint64_t launches = 0;
@@ -402,6 +406,10 @@ void build_plan(sp_ctx* c) {
   std::vector<uint32_t> cls_groups;
   std::vector<uint4> desc;
   std::vector<uint16_t> colrow16;
+  // Exact flip lists per (group, pattern): XOR of the D columns of the
+  // pattern's set symbols, as row * tw offsets.
+  std::vector<std::vector<uint16_t>> plists;
+  size_t max_plist = 0;
   uint64_t n_chains = 0, n_chains_live = 0;
   auto add_classes = [&](const std::vector<Cls>& cls, bool live) {
     for (const Cls& cl : cls) {
@@ -418,11 +426,33 @@ void build_plan(sp_ctx* c) {
       ci.n_seg = static_cast<uint32_t>(n_seg);
       ci.seg_off = static_cast<uint32_t>(n_chains);
       n_chains += n_seg;
+      ci.npat = cl.dist == SP_DIST_DEPOLARIZE2 ? 15 : cl.dist == SP_DIST_DEPOLARIZE1 ? 3 : 1;
+      ci.pbase = static_cast<uint32_t>(plists.size());
       cls_info.push_back(ci);
       for (uint32_t g : cl.groups) {
         cls_groups.push_back(g);
         if (!live) continue;
         const sp_group& gr = h.groups[g];
+        for (uint32_t pat = 1; pat <= ci.npat; ++pat) {
+          std::vector<uint16_t> rows;
+          for (uint32_t b = 0; b < gr.arity; ++b) {
+            if (!((pat >> b) & 1u)) continue;
+            const uint64_t sidx = gr.first_symbol + b;
+            std::vector<uint16_t> merged;
+            size_t i = 0;
+            uint64_t j = dcol_ptr[sidx];
+            while (i < rows.size() || j < dcol_ptr[sidx + 1]) {
+              const uint32_t a = i < rows.size() ? rows[i] : UINT32_MAX;
+              const uint32_t c2 = j < dcol_ptr[sidx + 1] ? dcol_rows[j] * d.tw : UINT32_MAX;
+              if (a < c2) { merged.push_back(static_cast<uint16_t>(a)); ++i; }
+              else if (c2 < a) { merged.push_back(static_cast<uint16_t>(c2)); ++j; }
+              else { ++i; ++j; }
+            }
+            rows.swap(merged);
+          }
+          max_plist = std::max(max_plist, rows.size());
+          plists.push_back(std::move(rows));
+        }
         uint32_t lens[4] = {0, 0, 0, 0};
         const uint32_t base = static_cast<uint32_t>(colrow16.size());
         for (uint32_t b = 0; b < gr.arity; ++b) {
@@ -476,6 +506,20 @@ void build_plan(sp_ctx* c) {
   d.cls_groups = c->b_cls_groups.upload(cls_groups, s);
   d.desc = c->b_desc.upload(desc, s);
   d.colrow = c->b_colrow.upload(colrow16, s);
+  {
+    const long force_lp = env_long("SP_LP", -1);
+    d.lp = max_plist <= 8 ? 8 : max_plist <= 16 ? 16 : 0;
+    if (force_lp >= 0) d.lp = static_cast<uint32_t>(force_lp);
+    if (d.lp && d.lp < max_plist) d.lp = 0;
+    if (d.lp) {
+      std::vector<uint16_t> flat(plists.size() * d.lp, 0xFFFF);
+      for (size_t i = 0; i < plists.size(); ++i)
+        std::copy(plists[i].begin(), plists[i].end(), flat.begin() + i * d.lp);
+      std::vector<uint4> packed(std::max<size_t>(flat.size() / 8, 1));
+      std::memcpy(packed.data(), flat.data(), flat.size() * 2);
+      d.plist = c->b_plist.upload(packed, s);
+    }
+  }
   {
     std::vector<uint32_t> lvl_ptr(X.n_levels + 1, 0);
     for (uint64_t k = 0; k < n_meas; ++k) lvl_ptr[X.depth[k] + 1]++;
@@ -640,6 +684,7 @@ int sp_set_product(sp_ctx* ctx, sp_product v) {
       for (uint64_t i = h.row_ptr[k]; i < h.row_ptr[k + 1]; ++i)
         h.dense_words[k * h.ldm + h.sym_idx[i] / 64] |= uint64_t{1} << (h.sym_idx[i] % 64);
     ctx->plan_ready = false;
+    ctx->prod_ready = false;
   }
   ctx->product = v;
   return SP_OK;
@@ -670,6 +715,7 @@ int sp_load_msym_csr(sp_ctx* ctx, uint64_t n_meas, uint64_t n_sym, const uint64_
   h.ldm = 0;
   ctx->have_msym = true;
   ctx->plan_ready = false;
+  ctx->prod_ready = false;
   if (ctx->product == SP_PRODUCT_DENSE) sp_set_product(ctx, SP_PRODUCT_DENSE);
   return SP_OK;
 }
@@ -701,6 +747,7 @@ int sp_load_msym_dense(sp_ctx* ctx, uint64_t n_meas, uint64_t n_sym, const uint6
   if (n_sym % 64)
     for (uint64_t k = 0; k < n_meas; ++k)
       h.dense_words[k * h.ldm + (n_sym - 1) / 64] &= (uint64_t{1} << (n_sym % 64)) - 1;
+  ctx->prod_ready = false;
   return SP_OK;
 }
 
@@ -781,28 +828,27 @@ int sp_sample_given_S(sp_ctx* ctx, const uint64_t* d_S, uint64_t n_sym_S, uint64
   if (n_shots == 0 || ctx->hp.n_meas == 0) return SP_OK;
   if (!d_S || ldS < (n_shots + 63) / 64 || !d_out || ld < (n_shots + 63) / 64)
     return fail(SP_ERR_INVALID_ARGUMENT, "buffer too small");
-  // K2 only needs the row lists (and dense words); no group table required.
+  // K2 only needs the row lists (and dense words): it has its own device
+  // copy, independent of the group table and of the fused sampler's plan.
   bool dense = ctx->product == SP_PRODUCT_DENSE;
-  if (!ctx->plan_ready) {
-    if (ctx->have_groups) {
-      if (int r = ensure_plan(ctx)) return r;
-    } else {
-      try {
-        ctx->dp.n_meas = static_cast<uint32_t>(ctx->hp.n_meas);
-        ctx->dp.n_sym = static_cast<uint32_t>(ctx->hp.n_sym);
-        ctx->dp.row_ptr = ctx->b_row_ptr.upload(ctx->hp.row_ptr, ctx->stream);
-        ctx->dp.sym_idx = ctx->b_sym_idx.upload(ctx->hp.sym_idx, ctx->stream);
-        if (!ctx->hp.dense_words.empty()) {
-          ctx->dp.dense = ctx->b_dense.upload(ctx->hp.dense_words, ctx->stream);
-          ctx->dp.ldm = ctx->hp.ldm;
-        }
-      } catch (const CudaError& e) {
-        return fail(SP_ERR_CUDA, e.what());
+  if (!ctx->prod_ready) {
+    try {
+      ctx->pp = DevPlan{};
+      ctx->pp.n_meas = static_cast<uint32_t>(ctx->hp.n_meas);
+      ctx->pp.n_sym = static_cast<uint32_t>(ctx->hp.n_sym);
+      ctx->pp.row_ptr = ctx->p_row_ptr.upload(ctx->hp.row_ptr, ctx->stream);
+      ctx->pp.sym_idx = ctx->p_sym_idx.upload(ctx->hp.sym_idx, ctx->stream);
+      if (!ctx->hp.dense_words.empty()) {
+        ctx->pp.dense = ctx->p_dense.upload(ctx->hp.dense_words, ctx->stream);
+        ctx->pp.ldm = ctx->hp.ldm;
       }
+      ctx->prod_ready = true;
+    } catch (const CudaError& e) {
+      return fail(SP_ERR_CUDA, e.what());
     }
   }
-  if (dense && !ctx->dp.dense) return fail(SP_ERR_NOT_LOADED, "dense M_sym words not built");
-  int r = launch_product(ctx->dp, ctx->L, dense, d_S, ldS, n_shots, d_out, ld);
+  if (dense && !ctx->pp.dense) return fail(SP_ERR_NOT_LOADED, "dense M_sym words not built");
+  int r = launch_product(ctx->pp, ctx->L, dense, d_S, ldS, n_shots, d_out, ld);
   return launched(ctx, r, "product launch");
 }
 

@@ -110,8 +110,14 @@ __device__ __forceinline__ uint32_t group_bits_compat(uint32_t dist, double p, u
 // (segment, global tile), independent of which warp, CTA or GPU runs them.
 struct Segment {
   uint64_t lo;
-  uint32_t len, seg, goff, dist;
+  uint32_t len, seg, goff, dist, pbase, npat;
   float inv;
+};
+
+// Firings of one walk step on one lane (up to 4; slot k valid iff v & (1<<k)).
+struct Fired {
+  uint32_t v;
+  uint32_t g[4], shot[4], pat[4];  // group position in class, shot in tile, pattern
 };
 
 __device__ __forceinline__ void segment_init(Segment& sg, const ClassInfo* cls, uint32_t n_cls,
@@ -127,11 +133,13 @@ __device__ __forceinline__ void segment_init(Segment& sg, const ClassInfo* cls, 
   sg.seg = seg;
   sg.goff = ci.goff;
   sg.dist = ci.dist;
+  sg.pbase = ci.pbase;
+  sg.npat = ci.npat;
   sg.inv = ci.inv;
 }
 
-// emit(class_position, shot_in_tile, pattern) runs on the lane that owns
-// the firing; all lanes of the warp must call segment_walk together.
+// Walks one segment with the whole warp; emit(const Fired&) runs on every
+// lane after each step (lanes may have no valid firing).
 template <class Emit>
 __device__ __forceinline__ void segment_walk(const Segment& sg, const RoundKeys& K, uint64_t gtile,
                                              uint32_t t_log2, uint32_t lane, Emit&& emit) {
@@ -162,21 +170,26 @@ __device__ __forceinline__ void segment_walk(const Segment& sg, const RoundKeys&
     const uint32_t total = __shfl_sync(kFull, scan, 31);
     const uint32_t base = pos + scan - acc - 1;
     uint32_t digits = bern ? 0u : __umulhi(r.w, n * n * n);
+    Fired f;
+    f.v = 0;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      if (k == 3 && !bern) break;
-      uint32_t pat = 1u;
+      f.pat[k] = 1u;
+      f.g[k] = 0;
+      f.shot[k] = 0;
+      if (k == 3 && !bern) continue;
       if (!bern) {
         const uint32_t q = (digits * magic) >> 16;
-        pat = 1u + digits - q * n;
+        f.pat[k] = 1u + digits - q * n;
         digits = q;
       }
       const uint32_t rel = base + incl[k];
-      if (rel < sg.len) {
-        const uint64_t f = sg.lo + rel;
-        emit(sg.goff + static_cast<uint32_t>(f >> t_log2), static_cast<uint32_t>(f) & tmask, pat);
-      }
+      const uint64_t fl = sg.lo + rel;
+      f.g[k] = static_cast<uint32_t>(fl >> t_log2);
+      f.shot[k] = static_cast<uint32_t>(fl) & tmask;
+      f.v |= (rel < sg.len ? 1u : 0u) << k;
     }
+    emit(f);
     pos += total;
     if (pos >= sg.len) return;
   }
@@ -187,11 +200,6 @@ __device__ __forceinline__ void named_sync(uint32_t id, uint32_t n) {
 }
 __device__ __forceinline__ void named_arrive(uint32_t id, uint32_t n) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-__device__ __forceinline__ uint32_t lanemask_lt() {
-  uint32_t m;
-  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
-  return m;
 }
 
 __device__ __forceinline__ uint4 xor4(uint4 a, uint4 b) {
@@ -215,14 +223,15 @@ __device__ __forceinline__ uint4 xor4(uint4 a, uint4 b) {
 // with 16-byte stores and zero the buffer for tile i+2. Named barriers
 // FULL[b] / EMPTY[b] hand the buffers back and forth. Event tables and row
 // tables are staged in shared memory when they fit.
-template <bool kStaged, bool kRowStaged>
+template <bool kStaged, bool kRowStaged, int kLp>
 __global__ void __launch_bounds__(kFusedThreads, 1)
 k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, uint64_t n_shots,
          uint64_t* __restrict__ out, uint64_t ld, unsigned long long* __restrict__ counts,
          bool vec) {
   extern __shared__ __align__(16) uint8_t smem[];
   const uint32_t tw = P.tw, tw4_log2 = P.t_log2 - 7, tw4 = 1u << tw4_log2;
-  const uint32_t tile_words = P.n_meas * tw;
+  // One spare row absorbs the XORs of padded flip-list entries (never read).
+  const uint32_t tile_words = (P.n_meas + 1) * tw;
   const uint32_t n_slots = P.n_dense_live + 1;  // + the all-ones constant slot
   const bool with_counts = counts != nullptr;
   uint32_t* tiles = reinterpret_cast<uint32_t*>(smem);
@@ -239,6 +248,7 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
   const uint32_t* DRP = P.drow_ptr;
   const uint16_t* DRS = P.drow_slot;
   const int32_t* PAR = P.parent;
+  const uint4* PLIST = P.plist;
   const uint16_t* LVR = P.lvl_rows;
   if (kRowStaged) {
     uint32_t* s_drp = reinterpret_cast<uint32_t*>(p);
@@ -305,34 +315,65 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
       const uint64_t gtile = tile0 + blockIdx.x + static_cast<uint64_t>(i) * gridDim.x;
       if (i >= 2) named_sync(kBarEmpty0 + b, kFusedThreads);
       uint32_t* tile = tiles + b * tile_words;
-      auto apply = [&](uint32_t cpos, uint32_t shot, uint32_t pat) {
-        const uint4 d = DESC[cpos];
-        const uint32_t bit = 1u << (shot & 31);
-        uint32_t* wb = tile + (shot >> 5);
-        uint32_t off = d.x;
-        const uint32_t lens[4] = {d.y & 0xFFFFu, d.y >> 16, d.z & 0xFFFFu, d.z >> 16};
+      uint32_t seg = 0;
+      Segment sg;
+      auto emit = [&](const Fired& f) {
+        if constexpr (kLp > 0) {
+          // Exact flip list of (group, pattern), padded to kLp u16 rows with
+          // 0xFFFF; one or two 16-byte loads, then predicated shared atomics.
+          uint4 lst[4][kLp / 8];
 #pragma unroll
-        for (int s = 0; s < 4; ++s) {
-          if ((pat >> s) & 1u)
-            for (uint32_t j = 0; j < lens[s]; ++j) atomicXor(wb + COLROW[off + j], bit);
-          off += lens[s];
+          for (int k = 0; k < 4; ++k)
+#pragma unroll
+            for (int h = 0; h < kLp / 8; ++h)
+              lst[k][h] = ((f.v >> k) & 1u)
+                              ? __ldg(PLIST + (static_cast<uint64_t>(sg.pbase + f.g[k] * sg.npat +
+                                                                     f.pat[k] - 1) * (kLp / 8) + h))
+                              : make_uint4(kFull, kFull, kFull, kFull);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            uint32_t* wb = tile + (f.shot[k] >> 5);
+            const uint32_t bit = 1u << (f.shot[k] & 31);
+#pragma unroll
+            for (int h = 0; h < kLp / 8; ++h) {
+              const uint32_t ww[4] = {lst[k][h].x, lst[k][h].y, lst[k][h].z, lst[k][h].w};
+#pragma unroll
+              for (int e = 0; e < 8; ++e) {
+                const uint32_t row = (ww[e >> 1] >> (16 * (e & 1))) & 0xFFFFu;
+                if (row != 0xFFFFu) atomicXor(wb + row, bit);
+              }
+            }
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            if (!((f.v >> k) & 1u)) continue;
+            const uint4 d = DESC[sg.goff + f.g[k]];
+            const uint32_t bit = 1u << (f.shot[k] & 31);
+            uint32_t* wb = tile + (f.shot[k] >> 5);
+            uint32_t off = d.x;
+            const uint32_t lens[4] = {d.y & 0xFFFFu, d.y >> 16, d.z & 0xFFFFu, d.z >> 16};
+#pragma unroll
+            for (int s = 0; s < 4; ++s) {
+              if ((f.pat[k] >> s) & 1u)
+                for (uint32_t j = 0; j < lens[s]; ++j) atomicXor(wb + COLROW[off + j], bit);
+              off += lens[s];
+            }
+          }
         }
       };
       for (;;) {
-        uint32_t seg = 0;
         if (lane == 0) seg = atomicAdd(&segctr[b], 1u);
         seg = __shfl_sync(kFull, seg, 0);
         if (seg >= P.n_seg_live) break;
-        Segment sg;
         segment_init(sg, CLS, P.n_cls_live, seg);
-        segment_walk(sg, K, gtile, P.t_log2, lane, apply);
+        segment_walk(sg, K, gtile, P.t_log2, lane, emit);
       }
       named_arrive(kBarFull0 + b, kFusedThreads);
     }
   } else {
     // ---------------- drain warps ----------------
     const uint32_t ct = threadIdx.x - n_gen * 32, nct = kFusedThreads - n_gen * 32;
-    const uint32_t seg = tw4 < 32 ? tw4 : 32;  // lanes per measurement row in a warp
     for (uint32_t i = 0; i < n_my; ++i) {
       const uint32_t b = i & 1;
       const uint64_t t_local = blockIdx.x + static_cast<uint64_t>(i) * gridDim.x;
@@ -395,10 +436,7 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
               if (with_counts) pc = __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
             }
           }
-          if (with_counts) {
-            for (uint32_t o = seg >> 1; o; o >>= 1) pc += __shfl_xor_sync(kFull, pc, o);
-            if (j < items && (lane & (seg - 1)) == 0 && pc) atomicAdd(&cnt[k], pc);
-          }
+          if (with_counts && pc) atomicAdd(&cnt[k], pc);
         }
         if (P.n_levels > 1) named_sync(kBarDrain, nct);
       }
@@ -511,12 +549,15 @@ __global__ void d_segments(const DevPlan P, const RoundKeys K, uint64_t tile0, u
     const uint64_t base = static_cast<uint64_t>(t) << P.t_log2;
     Segment sg;
     segment_init(sg, P.cls, P.n_cls_all, seg);
-    segment_walk(sg, K, tile0 + t, P.t_log2, lane, [&](uint32_t cpos, uint32_t shot, uint32_t pat) {
-      const uint64_t j = base + shot;
-      if (j >= n_shots) return;
-      uint32_t s = P.g_first[P.cls_groups[cpos]];
-      for (; pat; pat >>= 1, ++s)
-        if (pat & 1u) atomicXor(&S32[s * ld32 + (j >> 5)], 1u << (j & 31));
+    segment_walk(sg, K, tile0 + t, P.t_log2, lane, [&](const Fired& f) {
+      for (int k = 0; k < 4; ++k) {
+        if (!((f.v >> k) & 1u)) continue;
+        const uint64_t j = base + f.shot[k];
+        if (j >= n_shots) continue;
+        uint32_t s = P.g_first[P.cls_groups[sg.goff + f.g[k]]];
+        for (uint32_t pat = f.pat[k]; pat; pat >>= 1, ++s)
+          if (pat & 1u) atomicXor(&S32[s * ld32 + (j >> 5)], 1u << (j & 31));
+      }
     });
   }
 }
@@ -713,11 +754,11 @@ int persistent_grid(Kern kernel, const LaunchCfg& L, size_t smem, uint32_t n_til
   return 0;
 }
 
-template <bool kStaged, bool kRowStaged>
+template <bool kStaged, bool kRowStaged, int kLp>
 int launch_k1(const DevPlan& P, const LaunchCfg& L, const RoundKeys& K, uint64_t tile0,
               uint32_t n_tiles, uint64_t n_shots, uint64_t* out, uint64_t ld,
               unsigned long long* cnt) {
-  auto kern = k1_fused<kStaged, kRowStaged>;
+  auto kern = k1_fused<kStaged, kRowStaged, kLp>;
   const size_t smem = fused_smem_bytes(P, P.t_log2, kStaged, kRowStaged);
   int grid = 0;
   if (persistent_grid(kern, L, smem, n_tiles, P.cta_per_sm, &grid)) return -1;
@@ -730,7 +771,7 @@ int launch_k1(const DevPlan& P, const LaunchCfg& L, const RoundKeys& K, uint64_t
 
 size_t fused_smem_bytes(const DevPlan& P, uint32_t t_log2, bool staged, bool row_staged) {
   const size_t tw = size_t{1} << (t_log2 - 5);
-  size_t b = 2 * static_cast<size_t>(P.n_meas) * tw * 4;           // tiles
+  size_t b = 2 * static_cast<size_t>(P.n_meas + 1) * tw * 4;       // tiles (+ spare row)
   b += 2 * static_cast<size_t>(P.n_dense_live + 1) * tw * 4;        // coin words + ones slot
   b += align16(4ull * P.n_meas) + 16;                               // counts, dispensers
   if (row_staged) {
@@ -753,11 +794,12 @@ int launch_fused_sample(const DevPlan& P, const LaunchCfg& L, uint64_t seed, uin
   const uint32_t n_tiles = static_cast<uint32_t>((n_shots + T - 1) / T);
   const RoundKeys K = expand_keys(seed);
   auto* cnt = reinterpret_cast<unsigned long long*>(counts);
-  if (P.staged)
-    return P.row_staged ? launch_k1<true, true>(P, L, K, tile0, n_tiles, n_shots, out, ld, cnt)
-                        : launch_k1<true, false>(P, L, K, tile0, n_tiles, n_shots, out, ld, cnt);
-  return P.row_staged ? launch_k1<false, true>(P, L, K, tile0, n_tiles, n_shots, out, ld, cnt)
-                      : launch_k1<false, false>(P, L, K, tile0, n_tiles, n_shots, out, ld, cnt);
+#define SP_K1(st, rs, lp) launch_k1<st, rs, lp>(P, L, K, tile0, n_tiles, n_shots, out, ld, cnt)
+  if (P.lp == 8) return P.row_staged ? SP_K1(false, true, 8) : SP_K1(false, false, 8);
+  if (P.lp == 16) return P.row_staged ? SP_K1(false, true, 16) : SP_K1(false, false, 16);
+  if (P.staged) return P.row_staged ? SP_K1(true, true, 0) : SP_K1(true, false, 0);
+  return P.row_staged ? SP_K1(false, true, 0) : SP_K1(false, false, 0);
+#undef SP_K1
 }
 
 int launch_fused_sample_compat(const DevPlan& P, const LaunchCfg& L, uint64_t seed,

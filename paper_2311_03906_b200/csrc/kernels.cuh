@@ -21,6 +21,8 @@ struct ClassInfo {
   uint32_t goff = 0;    // first class position (index into desc / cls_groups)
   float inv = 0.f;      // 1 / -ln(1 - p): Exp(1) -> geometric skip
   uint32_t dist = 0;    // 1 Bernoulli, 3 DEPOLARIZE1, 4 DEPOLARIZE2
+  uint32_t pbase = 0;   // first flip list of the class (lists in plist)
+  uint32_t npat = 1;    // non-identity patterns per group: 1, 3 or 15
   uint32_t pad = 0;
 };
 
@@ -73,6 +75,11 @@ struct DevPlan {
   const uint4* desc = nullptr;
   const uint16_t* colrow = nullptr;
   uint64_t n_colrow = 0;
+  // Exact per-(group, pattern) flip lists in D space, padded with 0xFFFF to
+  // lp u16 rows (lp = 8 or 16; 0 = lists too long, use desc/colrow loops).
+  // List of (class position g, pattern pi) = plist[(pbase + g*npat + pi-1)].
+  uint32_t lp = 0;
+  const uint4* plist = nullptr;
   // Row reconstruction: out[k] = d[k] ^ out[parent[k]] (parent < k or -1),
   // rows listed level by level (lvl_rows, lvl_ptr[n_levels + 1]).
   const int32_t* parent = nullptr;
