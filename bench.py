@@ -86,29 +86,42 @@ class ClockSampler:
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index: int):
+        import tempfile
         self.index = index
         self.proc = None
+        self.path = tempfile.mktemp(prefix="sp_clocks_", suffix=".csv")
+        self.t0 = time.perf_counter()
 
     def __enter__(self):
         try:
+            # -f writes line by line (a pipe would be block-buffered and lost
+            # on terminate).
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "--format=csv,noheader,nounits", "-lms", "100", "-f", self.path],
+                stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
         except OSError:
             self.proc = None
+        self.t0 = time.perf_counter()
         return self
+
+    def elapsed(self) -> float:
+        return time.perf_counter() - self.t0
 
     def __exit__(self, *a):
         self.lines = []
         if self.proc is not None:
             self.proc.terminate()
             try:
-                out, _ = self.proc.communicate(timeout=5)
+                self.proc.wait(timeout=5)
             except subprocess.TimeoutExpired:
                 self.proc.kill()
-                out, _ = self.proc.communicate()
-            self.lines = [l for l in out.splitlines() if l.strip()]
+            try:
+                with open(self.path) as f:
+                    self.lines = [l for l in f.read().splitlines() if l.strip()]
+                os.unlink(self.path)
+            except OSError:
+                pass
 
     def summary(self):
         sm, mx, reasons = [], None, set()
@@ -230,14 +243,20 @@ def run_ours(args):
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    launches0 = smp.launches
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(args.steps)]
     with ClockSampler(local) as clk:
+        # Keep the GPU busy (untimed) while nvidia-smi starts sampling.
+        j = 0
+        while clk.elapsed() < 0.6:
+            step(args.warmup + args.steps + j)
+            torch.cuda.synchronize()
+            j += 1
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         wall0 = time.perf_counter()
+        launches0 = smp.launches
         for i in range(args.steps):
             flush.zero_()  # L2 flush between timed iterations, outside the events
             evs[i][0].record(stream)
@@ -247,7 +266,13 @@ def run_ours(args):
         if world > 1:
             dist.barrier()
         wall = time.perf_counter() - wall0
-    launches = smp.launches - launches0
+        launches = smp.launches - launches0
+        # ... and for a short soak after the timed steps, same load.
+        t_end = clk.elapsed() + 0.5
+        while clk.elapsed() < t_end:
+            step(args.warmup + args.steps + j)
+            torch.cuda.synchronize()
+            j += 1
     step_ms = [a.elapsed_time(b) for a, b in evs]
     t_step = sum(step_ms) / len(step_ms) / 1e3
     t_tensor = torch.tensor([t_step], dtype=torch.float64, device=dev)

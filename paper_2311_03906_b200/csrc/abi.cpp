@@ -97,7 +97,7 @@ struct sp_ctx {
   // plan buffers
   DBuf b_row_ptr, b_sym_idx, b_col_ptr, b_col_rows, b_dense, b_first, b_arity, b_dist, b_param,
       b_row_const_compat, b_ones, b_dense_sym, b_drow_ptr, b_drow_slot, b_cls, b_cls_groups,
-      b_desc, b_colrow, b_live_groups, b_parent, b_lvl_rows, b_lvl_ptr, b_plist;
+      b_desc, b_colrow, b_live_groups, b_path_rows, b_path_ptr, b_path_par, b_round_ptr, b_plist;
   // K2's own copy of the rows (independent of the group table)
   bool prod_ready = false;
   DevPlan pp;
@@ -346,7 +346,7 @@ void build_plan(sp_ctx* c) {
   d.n_cls_live = static_cast<uint32_t>(live_cls.size());
   d.n_desc_live = static_cast<uint32_t>(live_positions);
   d.n_colrow = live_colrow;
-  d.n_levels = X.n_levels;
+  d.n_paths = static_cast<uint32_t>(n_meas);  // upper bound for the smem estimate
   const size_t optin = c->L.smem_optin;
   int lg = -1;
   bool staged = false, row_staged = false;
@@ -390,9 +390,12 @@ void build_plan(sp_ctx* c) {
     const double items = static_cast<double>(n_meas) * (T / 128);
     const double drain = n_dense_live * (T / 128.0) * 60.0 +
                          items * (12.0 + 3.0 * drow_slot.size() / std::max<uint64_t>(n_meas, 1));
-    long gw = std::lround(16.0 * gen / std::max(gen + drain, 1.0));
+    d.cta_threads = static_cast<uint32_t>(env_long("SP_CTA_THREADS", 512));
+    const long n_warps = d.cta_threads / 32;
+    long gw = std::lround(n_warps * 0.75 * gen / std::max(gen + drain, 1.0) / 0.75);
+    gw = std::min<long>(gw, n_warps - std::max<long>(1, n_warps / 4));
     gw = env_long("SP_GEN_WARPS", gw);
-    d.gen_warps = static_cast<uint32_t>(std::min<long>(std::max<long>(gw, 1), 15));
+    d.gen_warps = static_cast<uint32_t>(std::min<long>(std::max<long>(gw, 1), n_warps - 1));
   }
 
   // Segments: each class's flattened (group, shot) space of a tile is cut
@@ -521,15 +524,54 @@ void build_plan(sp_ctx* c) {
     }
   }
   {
-    std::vector<uint32_t> lvl_ptr(X.n_levels + 1, 0);
-    for (uint64_t k = 0; k < n_meas; ++k) lvl_ptr[X.depth[k] + 1]++;
-    for (uint32_t l = 0; l < X.n_levels; ++l) lvl_ptr[l + 1] += lvl_ptr[l];
-    std::vector<uint16_t> lvl_rows(std::max<uint64_t>(n_meas, 1));
-    std::vector<uint32_t> fillp(lvl_ptr.begin(), lvl_ptr.end() - 1);
-    for (uint64_t k = 0; k < n_meas; ++k) lvl_rows[fillp[X.depth[k]]++] = static_cast<uint16_t>(k);
-    d.parent = c->b_parent.upload(X.parent, s);
-    d.lvl_rows = c->b_lvl_rows.upload(lvl_rows, s);
-    d.lvl_ptr = c->b_lvl_ptr.upload(lvl_ptr, s);
+    // Heavy-path decomposition of the parent forest (parents precede
+    // children, so one reverse sweep gives subtree sizes).
+    std::vector<uint32_t> size(n_meas, 1);
+    std::vector<int32_t> heavy(n_meas, -1);
+    for (uint64_t k = n_meas; k-- > 0;)
+      if (X.parent[k] >= 0) size[X.parent[k]] += size[k];
+    for (uint64_t k = 0; k < n_meas; ++k) {
+      const int32_t pa = X.parent[k];
+      if (pa >= 0 && (heavy[pa] < 0 || size[k] > size[heavy[pa]])) heavy[pa] = static_cast<int32_t>(k);
+    }
+    std::vector<uint32_t> path_of(n_meas, 0), round_of_path;
+    std::vector<std::vector<uint16_t>> paths;
+    std::vector<int32_t> heads_par;
+    for (uint64_t k = 0; k < n_meas; ++k) {
+      const int32_t pa = X.parent[k];
+      if (pa >= 0 && heavy[pa] == static_cast<int32_t>(k)) continue;  // continues its parent's path
+      const uint32_t id = static_cast<uint32_t>(paths.size());
+      paths.emplace_back();
+      heads_par.push_back(pa);
+      round_of_path.push_back(pa >= 0 ? round_of_path[path_of[pa]] + 1 : 0);
+      for (int64_t r = static_cast<int64_t>(k); r >= 0; r = heavy[r]) {
+        paths[id].push_back(static_cast<uint16_t>(r));
+        path_of[r] = id;
+      }
+    }
+    uint32_t n_rounds = 1;
+    for (uint32_t r : round_of_path) n_rounds = std::max(n_rounds, r + 1);
+    std::vector<uint32_t> order(paths.size());
+    for (uint32_t i = 0; i < order.size(); ++i) order[i] = i;
+    std::stable_sort(order.begin(), order.end(),
+                     [&](uint32_t a, uint32_t b) { return round_of_path[a] < round_of_path[b]; });
+    std::vector<uint16_t> path_rows;
+    std::vector<uint32_t> path_ptr{0}, round_ptr(n_rounds + 1, 0);
+    std::vector<int32_t> path_par;
+    for (uint32_t id : order) {
+      path_rows.insert(path_rows.end(), paths[id].begin(), paths[id].end());
+      path_ptr.push_back(static_cast<uint32_t>(path_rows.size()));
+      path_par.push_back(heads_par[id]);
+      round_ptr[round_of_path[id] + 1]++;
+    }
+    for (uint32_t r = 0; r < n_rounds; ++r) round_ptr[r + 1] += round_ptr[r];
+    if (path_rows.empty()) path_rows.push_back(0);
+    d.n_paths = static_cast<uint32_t>(paths.size());
+    d.n_rounds = n_rounds;
+    d.path_rows = c->b_path_rows.upload(path_rows, s);
+    d.path_ptr = c->b_path_ptr.upload(path_ptr, s);
+    d.path_par = c->b_path_par.upload(path_par, s);
+    d.round_ptr = c->b_round_ptr.upload(round_ptr, s);
   }
   d.n_live_groups = static_cast<uint32_t>(live_groups.size());
   d.live_groups = c->b_live_groups.upload(live_groups, s);

@@ -114,10 +114,15 @@ struct Segment {
   float inv;
 };
 
-// Firings of one walk step on one lane (up to 4; slot k valid iff v & (1<<k)).
+// Philox blocks each lane draws per walk step (independent counters, so the
+// two ten-round chains interleave), and the firings one step can yield.
+constexpr int kBlocks = 2;
+constexpr int kSlots = 4 * kBlocks;
+
+// Firings of one walk step on one lane (slot k valid iff v & (1<<k)).
 struct Fired {
   uint32_t v;
-  uint32_t g[4], shot[4], pat[4];  // group position in class, shot in tile, pattern
+  uint32_t g[kSlots], shot[kSlots], pat[kSlots];  // group position, shot in tile, pattern
 };
 
 __device__ __forceinline__ void segment_init(Segment& sg, const ClassInfo* cls, uint32_t n_cls,
@@ -144,22 +149,30 @@ template <class Emit>
 __device__ __forceinline__ void segment_walk(const Segment& sg, const RoundKeys& K, uint64_t gtile,
                                              uint32_t t_log2, uint32_t lane, Emit&& emit) {
   const bool bern = sg.dist == 1;
+  const uint32_t nk = bern ? 4u : 3u;  // skips per Philox block
   const uint32_t n = sg.dist == 3 ? 3u : 15u;
   const uint32_t magic = n == 3 ? 0x5556u : 0x1112u;  // exact /n for values < n^3
   const uint32_t tmask = (1u << t_log2) - 1u;
   const uint32_t c3 = (static_cast<uint32_t>(gtile >> 32) & 0xFFFFFFu) | (kDomChain << 24);
   uint32_t pos = 0;  // trials consumed (warp-uniform), < len <= 2^24
+  uint4 r[kBlocks];
+#pragma unroll
+  for (int b = 0; b < kBlocks; ++b)
+    r[b] = philox10(make_uint4(sg.seg, b * 32 + lane, static_cast<uint32_t>(gtile), c3), K);
   for (uint32_t draw = 0;; ++draw) {
-    const uint4 r = philox10(make_uint4(sg.seg, draw * 32 + lane, static_cast<uint32_t>(gtile), c3), K);
-    const uint32_t w[4] = {r.x, r.y, r.z, r.w};
-    uint32_t incl[4];
+    uint32_t incl[kSlots];
     uint32_t acc = 0;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      if (k == 3 && !bern) break;
-      const float sf = exp1_from_bits(w[k]) * sg.inv;
-      acc += (sf < 16777216.f ? static_cast<uint32_t>(sf) : 16777216u) + 1u;  // gap to next firing
-      incl[k] = acc;
+    for (int b = 0; b < kBlocks; ++b) {
+      const uint32_t w[4] = {r[b].x, r[b].y, r[b].z, r[b].w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        incl[4 * b + k] = acc;
+        if (k == 3 && !bern) continue;
+        const float sf = exp1_from_bits(w[k]) * sg.inv;
+        acc += (sf < 16777216.f ? static_cast<uint32_t>(sf) : 16777216u) + 1u;  // gap to next firing
+        incl[4 * b + k] = acc;
+      }
     }
     uint32_t scan = acc;  // warp inclusive scan of the lanes' gap sums
 #pragma unroll
@@ -169,29 +182,44 @@ __device__ __forceinline__ void segment_walk(const Segment& sg, const RoundKeys&
     }
     const uint32_t total = __shfl_sync(kFull, scan, 31);
     const uint32_t base = pos + scan - acc - 1;
-    uint32_t digits = bern ? 0u : __umulhi(r.w, n * n * n);
     Fired f;
     f.v = 0;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      f.pat[k] = 1u;
-      f.g[k] = 0;
-      f.shot[k] = 0;
-      if (k == 3 && !bern) continue;
-      if (!bern) {
-        const uint32_t q = (digits * magic) >> 16;
-        f.pat[k] = 1u + digits - q * n;
-        digits = q;
+    for (int b = 0; b < kBlocks; ++b) {
+      uint32_t digits = bern ? 0u : __umulhi(r[b].w, n * n * n);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int sl = 4 * b + k;
+        f.pat[sl] = 1u;
+        f.g[sl] = 0;
+        f.shot[sl] = 0;
+        if (k == 3 && !bern) continue;
+        if (!bern) {
+          const uint32_t q = (digits * magic) >> 16;
+          f.pat[sl] = 1u + digits - q * n;
+          digits = q;
+        }
+        const uint32_t rel = base + incl[sl];
+        const uint64_t fl = sg.lo + rel;
+        f.g[sl] = static_cast<uint32_t>(fl >> t_log2);
+        f.shot[sl] = static_cast<uint32_t>(fl) & tmask;
+        f.v |= (rel < sg.len ? 1u : 0u) << sl;
       }
-      const uint32_t rel = base + incl[k];
-      const uint64_t fl = sg.lo + rel;
-      f.g[k] = static_cast<uint32_t>(fl >> t_log2);
-      f.shot[k] = static_cast<uint32_t>(fl) & tmask;
-      f.v |= (rel < sg.len ? 1u : 0u) << k;
+    }
+    (void)nk;
+    pos += total;
+    const bool more = pos < sg.len;
+    // The next step's Philox blocks are independent of this step's table
+    // loads and atomics: computing them first lets the two overlap.
+    if (more) {
+#pragma unroll
+      for (int b = 0; b < kBlocks; ++b)
+        r[b] = philox10(make_uint4(sg.seg, ((draw + 1) * kBlocks + b) * 32 + lane,
+                                   static_cast<uint32_t>(gtile), c3),
+                        K);
     }
     emit(f);
-    pos += total;
-    if (pos >= sg.len) return;
+    if (!more) return;
   }
 }
 
@@ -200,6 +228,16 @@ __device__ __forceinline__ void named_sync(uint32_t id, uint32_t n) {
 }
 __device__ __forceinline__ void named_arrive(uint32_t id, uint32_t n) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+// Predicated shared-memory XOR reduction: one ATOMS per active lane, no
+// branch (a C++ `if (...) atomicXor(...)` compiles to BSSY/BRA/BSYNC around
+// every call, which dominated the firing loop).
+__device__ __forceinline__ void red_xor_shared_if(uint32_t saddr, uint32_t val, uint32_t pred) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p red.shared.xor.b32 [%0], %1;\n\t}"
+      ::"r"(saddr), "r"(val), "r"(pred)
+      : "memory");
 }
 
 __device__ __forceinline__ uint4 xor4(uint4 a, uint4 b) {
@@ -247,28 +285,31 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
   const uint16_t* COLROW = P.colrow;
   const uint32_t* DRP = P.drow_ptr;
   const uint16_t* DRS = P.drow_slot;
-  const int32_t* PAR = P.parent;
   const uint4* PLIST = P.plist;
-  const uint16_t* LVR = P.lvl_rows;
+  const uint16_t* PROWS = P.path_rows;
+  const uint32_t* PPTR = P.path_ptr;
+  const int32_t* PPAR = P.path_par;
   if (kRowStaged) {
     uint32_t* s_drp = reinterpret_cast<uint32_t*>(p);
     p += align16(4ull * (P.n_meas + 1));
     uint16_t* s_drs = reinterpret_cast<uint16_t*>(p);
     p += align16(2ull * P.n_drow);
-    int32_t* s_par = reinterpret_cast<int32_t*>(p);
-    p += align16(4ull * P.n_meas);
-    uint16_t* s_lvr = reinterpret_cast<uint16_t*>(p);
+    uint16_t* s_prows = reinterpret_cast<uint16_t*>(p);
     p += align16(2ull * P.n_meas);
+    uint32_t* s_pptr = reinterpret_cast<uint32_t*>(p);
+    p += align16(4ull * (P.n_paths + 1));
+    int32_t* s_ppar = reinterpret_cast<int32_t*>(p);
+    p += align16(4ull * P.n_paths);
     for (uint32_t i = threadIdx.x; i <= P.n_meas; i += blockDim.x) s_drp[i] = P.drow_ptr[i];
     for (uint32_t i = threadIdx.x; i < P.n_drow; i += blockDim.x) s_drs[i] = P.drow_slot[i];
-    for (uint32_t i = threadIdx.x; i < P.n_meas; i += blockDim.x) {
-      s_par[i] = P.parent[i];
-      s_lvr[i] = P.lvl_rows[i];
-    }
+    for (uint32_t i = threadIdx.x; i < P.n_meas; i += blockDim.x) s_prows[i] = P.path_rows[i];
+    for (uint32_t i = threadIdx.x; i <= P.n_paths; i += blockDim.x) s_pptr[i] = P.path_ptr[i];
+    for (uint32_t i = threadIdx.x; i < P.n_paths; i += blockDim.x) s_ppar[i] = P.path_par[i];
     DRP = s_drp;
     DRS = s_drs;
-    PAR = s_par;
-    LVR = s_lvr;
+    PROWS = s_prows;
+    PPTR = s_pptr;
+    PPAR = s_ppar;
   }
   if (kStaged) {
     ClassInfo* s_cls = reinterpret_cast<ClassInfo*>(p);
@@ -313,40 +354,46 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
     for (uint32_t i = 0; i < n_my; ++i) {
       const uint32_t b = i & 1;
       const uint64_t gtile = tile0 + blockIdx.x + static_cast<uint64_t>(i) * gridDim.x;
-      if (i >= 2) named_sync(kBarEmpty0 + b, kFusedThreads);
+      if (i >= 2) named_sync(kBarEmpty0 + b, blockDim.x);
       uint32_t* tile = tiles + b * tile_words;
+      const uint32_t tile_s = static_cast<uint32_t>(__cvta_generic_to_shared(tile));
       uint32_t seg = 0;
       Segment sg;
       auto emit = [&](const Fired& f) {
         if constexpr (kLp > 0) {
           // Exact flip list of (group, pattern), padded to kLp u16 rows with
           // 0xFFFF; one or two 16-byte loads, then predicated shared atomics.
-          uint4 lst[4][kLp / 8];
 #pragma unroll
-          for (int k = 0; k < 4; ++k)
+          for (int half = 0; half < kSlots; half += 4) {
+            uint4 lst[4][kLp / 8];
 #pragma unroll
-            for (int h = 0; h < kLp / 8; ++h)
-              lst[k][h] = ((f.v >> k) & 1u)
-                              ? __ldg(PLIST + (static_cast<uint64_t>(sg.pbase + f.g[k] * sg.npat +
-                                                                     f.pat[k] - 1) * (kLp / 8) + h))
-                              : make_uint4(kFull, kFull, kFull, kFull);
+            for (int k = 0; k < 4; ++k)
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            uint32_t* wb = tile + (f.shot[k] >> 5);
-            const uint32_t bit = 1u << (f.shot[k] & 31);
+              for (int h = 0; h < kLp / 8; ++h)
+                lst[k][h] = ((f.v >> (half + k)) & 1u)
+                                ? __ldg(PLIST + (static_cast<uint64_t>(sg.pbase +
+                                                                       f.g[half + k] * sg.npat +
+                                                                       f.pat[half + k] - 1) *
+                                                     (kLp / 8) + h))
+                                : make_uint4(kFull, kFull, kFull, kFull);
 #pragma unroll
-            for (int h = 0; h < kLp / 8; ++h) {
-              const uint32_t ww[4] = {lst[k][h].x, lst[k][h].y, lst[k][h].z, lst[k][h].w};
+            for (int k = 0; k < 4; ++k) {
+              const uint32_t wb = tile_s + ((f.shot[half + k] >> 5) << 2);
+              const uint32_t bit = 1u << (f.shot[half + k] & 31);
 #pragma unroll
-              for (int e = 0; e < 8; ++e) {
-                const uint32_t row = (ww[e >> 1] >> (16 * (e & 1))) & 0xFFFFu;
-                if (row != 0xFFFFu) atomicXor(wb + row, bit);
+              for (int h = 0; h < kLp / 8; ++h) {
+                const uint32_t ww[4] = {lst[k][h].x, lst[k][h].y, lst[k][h].z, lst[k][h].w};
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                  const uint32_t row = (ww[e >> 1] >> (16 * (e & 1))) & 0xFFFFu;
+                  red_xor_shared_if(wb + (row << 2), bit, row != 0xFFFFu);
+                }
               }
             }
           }
         } else {
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
+          for (int k = 0; k < kSlots; ++k) {
             if (!((f.v >> k) & 1u)) continue;
             const uint4 d = DESC[sg.goff + f.g[k]];
             const uint32_t bit = 1u << (f.shot[k] & 31);
@@ -369,11 +416,11 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
         segment_init(sg, CLS, P.n_cls_live, seg);
         segment_walk(sg, K, gtile, P.t_log2, lane, emit);
       }
-      named_arrive(kBarFull0 + b, kFusedThreads);
+      named_arrive(kBarFull0 + b, blockDim.x);
     }
   } else {
     // ---------------- drain warps ----------------
-    const uint32_t ct = threadIdx.x - n_gen * 32, nct = kFusedThreads - n_gen * 32;
+    const uint32_t ct = threadIdx.x - n_gen * 32, nct = blockDim.x - n_gen * 32;
     for (uint32_t i = 0; i < n_my; ++i) {
       const uint32_t b = i & 1;
       const uint64_t t_local = blockIdx.x + static_cast<uint64_t>(i) * gridDim.x;
@@ -389,31 +436,34 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
                          K);
       }
       named_sync(kBarDrain, nct);
-      named_sync(kBarFull0 + b, kFusedThreads);
+      named_sync(kBarFull0 + b, blockDim.x);
 
       uint4* t4 = reinterpret_cast<uint4*>(tiles + b * tile_words);
       const uint64_t first = t_local << P.t_log2;
       const uint64_t valid = min(static_cast<uint64_t>(1) << P.t_log2, n_shots - first);
       const uint32_t vq = static_cast<uint32_t>((valid + 127) >> 7);
       const uint32_t rem = static_cast<uint32_t>(valid & 127);
-      // Rows in level order: a row's parent is final before the row is read.
-      for (uint32_t lv = 0; lv < P.n_levels; ++lv) {
-        const uint32_t r0 = P.lvl_ptr[lv], r1 = P.lvl_ptr[lv + 1];
-        const uint32_t items = (r1 - r0) << tw4_log2;
-        const uint32_t items_rounded = (items + nct - 1) / nct * nct;
-        for (uint32_t base = 0; base < items_rounded; base += nct) {
-          const uint32_t j = base + ct;
-          uint32_t pc = 0, k = 0;
-          if (j < items) {
-            k = LVR[r0 + (j >> tw4_log2)];
-            const uint32_t q = j & (tw4 - 1);
+      // Rows along parent paths (heavy-path decomposition of the L forest):
+      // one thread walks a path top-down for one 128-shot column, carrying
+      // the running row value; a path's head waits only for its parent's
+      // path, which ran in an earlier round.
+      for (uint32_t rd = 0; rd < P.n_rounds; ++rd) {
+        const uint32_t p0 = P.round_ptr[rd], p1 = P.round_ptr[rd + 1];
+        const uint32_t tasks = (p1 - p0) << tw4_log2;
+        for (uint32_t j = ct; j < tasks; j += nct) {
+          const uint32_t pth = p0 + (j >> tw4_log2);
+          const uint32_t q = j & (tw4 - 1);
+          const int32_t par = PPAR[pth];
+          uint4 prev = par >= 0 ? t4[(static_cast<uint32_t>(par) << tw4_log2) + q]
+                                : make_uint4(0, 0, 0, 0);
+          for (uint32_t x = PPTR[pth], xe = PPTR[pth + 1]; x < xe; ++x) {
+            const uint32_t k = PROWS[x];
             const uint32_t ti = (k << tw4_log2) + q;
-            uint4 v = t4[ti];
+            uint4 v = xor4(t4[ti], prev);
             for (uint32_t s = DRP[k], e = DRP[k + 1]; s < e; ++s)
               v = xor4(v, c4[(static_cast<uint32_t>(DRS[s]) << tw4_log2) + q]);
-            const int32_t par = PAR[k];
-            if (par >= 0) v = xor4(v, t4[(static_cast<uint32_t>(par) << tw4_log2) + q]);
-            t4[ti] = v;  // final value, read by this row's children
+            t4[ti] = v;  // final value, read by light children in later rounds
+            prev = v;
             if (q < vq) {
               bool two = true;  // whether the item's second u64 word is inside the tile
               if (q == vq - 1 && rem) {
@@ -433,16 +483,21 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
                 o[0] = w0;
                 if (two) o[1] = w1;
               }
-              if (with_counts) pc = __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
+              if (with_counts) {
+                const uint32_t pc = __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
+                if (pc) atomicAdd(&cnt[k], pc);
+              }
             }
           }
-          if (with_counts && pc) atomicAdd(&cnt[k], pc);
         }
-        if (P.n_levels > 1) named_sync(kBarDrain, nct);
+        // A later round must not start before every row a light child
+        // reads is final.
+        if (rd + 1 < P.n_rounds) named_sync(kBarDrain, nct);
       }
+      named_sync(kBarDrain, nct);  // every drain thread is done reading the tile
       for (uint32_t j = ct; j < tile_words / 4; j += nct) t4[j] = make_uint4(0, 0, 0, 0);
       if (ct == 0) segctr[b] = 0;  // all generators are past tile i (FULL[b] completed)
-      if (i + 2 < n_my) named_arrive(kBarEmpty0 + b, kFusedThreads);
+      if (i + 2 < n_my) named_arrive(kBarEmpty0 + b, blockDim.x);
     }
   }
   if (with_counts) {
@@ -550,7 +605,7 @@ __global__ void d_segments(const DevPlan P, const RoundKeys K, uint64_t tile0, u
     Segment sg;
     segment_init(sg, P.cls, P.n_cls_all, seg);
     segment_walk(sg, K, tile0 + t, P.t_log2, lane, [&](const Fired& f) {
-      for (int k = 0; k < 4; ++k) {
+      for (int k = 0; k < kSlots; ++k) {
         if (!((f.v >> k) & 1u)) continue;
         const uint64_t j = base + f.shot[k];
         if (j >= n_shots) continue;
@@ -740,12 +795,12 @@ uint64_t host_mix64(uint64_t x) {
 
 template <class Kern>
 int persistent_grid(Kern kernel, const LaunchCfg& L, size_t smem, uint32_t n_tiles,
-                    uint32_t max_per_sm, int* grid) {
+                    uint32_t max_per_sm, int* grid, int threads = kFusedThreads) {
   if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(smem)) != cudaSuccess)
     return -1;
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kFusedThreads, smem) !=
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem) !=
           cudaSuccess ||
       per_sm < 1)
     return -1;
@@ -761,9 +816,10 @@ int launch_k1(const DevPlan& P, const LaunchCfg& L, const RoundKeys& K, uint64_t
   auto kern = k1_fused<kStaged, kRowStaged, kLp>;
   const size_t smem = fused_smem_bytes(P, P.t_log2, kStaged, kRowStaged);
   int grid = 0;
-  if (persistent_grid(kern, L, smem, n_tiles, P.cta_per_sm, &grid)) return -1;
+  const int threads = static_cast<int>(P.cta_threads);
+  if (persistent_grid(kern, L, smem, n_tiles, P.cta_per_sm, &grid, threads)) return -1;
   const bool vec = (ld % 2 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0);
-  kern<<<grid, kFusedThreads, smem, L.stream>>>(P, K, tile0, n_tiles, n_shots, out, ld, cnt, vec);
+  kern<<<grid, threads, smem, L.stream>>>(P, K, tile0, n_tiles, n_shots, out, ld, cnt, vec);
   return check_launch() ? -1 : 1;
 }
 
@@ -777,8 +833,9 @@ size_t fused_smem_bytes(const DevPlan& P, uint32_t t_log2, bool staged, bool row
   if (row_staged) {
     b += align16(4ull * (P.n_meas + 1));
     b += align16(2ull * P.n_drow);
-    b += align16(4ull * P.n_meas);
     b += align16(2ull * P.n_meas);
+    b += align16(4ull * (P.n_paths + 1));
+    b += align16(4ull * P.n_paths);
   }
   if (staged) {
     b += align16(sizeof(ClassInfo) * P.n_cls_live);

@@ -80,18 +80,22 @@ struct DevPlan {
   // List of (class position g, pattern pi) = plist[(pbase + g*npat + pi-1)].
   uint32_t lp = 0;
   const uint4* plist = nullptr;
-  // Row reconstruction: out[k] = d[k] ^ out[parent[k]] (parent < k or -1),
-  // rows listed level by level (lvl_rows, lvl_ptr[n_levels + 1]).
-  const int32_t* parent = nullptr;
-  const uint16_t* lvl_rows = nullptr;
-  const uint32_t* lvl_ptr = nullptr;  // [n_levels + 1]
-  uint32_t n_levels = 1;
+  // Row reconstruction out[k] = d[k] ^ out[parent[k]] along the paths of a
+  // heavy-path decomposition of the parent forest: path p lists rows
+  // path_rows[path_ptr[p] .. path_ptr[p+1]) top-down; path_par[p] is the head's
+  // parent (or -1), which lies on a path of an earlier round (round_ptr).
+  const uint16_t* path_rows = nullptr;
+  const uint32_t* path_ptr = nullptr;
+  const int32_t* path_par = nullptr;
+  const uint32_t* round_ptr = nullptr;  // [n_rounds + 1] over paths
+  uint32_t n_paths = 0, n_rounds = 1;
 
   // Fused-kernel launch shape (chosen by the planner).
   uint32_t staged = 0;       // event tables copied into shared memory
   uint32_t row_staged = 0;   // row tables copied into shared memory
   uint32_t gen_warps = 12;   // event-generator warps; the rest drain tiles
   uint32_t cta_per_sm = 1;
+  uint32_t cta_threads = 512;
 
   // Compat mode: group ids (>= 1) with at least one live symbol.
   uint32_t n_live_groups = 0;
