@@ -158,6 +158,11 @@ int sp_sample_to_host(sp_ctx* ctx, uint64_t seed, uint64_t shot_begin, uint64_t 
 /* Test hook: one Philox4x32-10 block on the device. ctr_key = {c0,c1,c2,c3,k0,k1}. */
 int sp_debug_philox(sp_ctx* ctx, const uint32_t* ctr_key, uint32_t* out);
 
+/* Profiling hook: per-role cycle counters of the fused kernel (gen wait,
+ * gen work, drain wait, drain work), enabled by SP_PHASE_TIMERS=1 at plan
+ * build; copied out and cleared. */
+int sp_debug_timers(sp_ctx* ctx, long long* out4);
+
 /* Number of kernel launches this context has issued so far. */
 uint64_t sp_launch_count(const sp_ctx* ctx);
 int sp_synchronize(sp_ctx* ctx);

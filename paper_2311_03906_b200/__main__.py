@@ -1,0 +1,123 @@
+"""Command line mirroring `cliffsym sample` / `cliffsym analyze`
+(tools/cliffsym.cpp:99-149, flags at cliffsym.cpp:294-330).
+
+    python -m paper_2311_03906_b200 sample --in c.stim --shots N --seed S \
+        [--format 01|b8] [--out FILE] [--rng philox|compat] [--dump-assignments FILE]
+    python -m paper_2311_03906_b200 analyze --in c.stim [--out FILE]
+
+`sample` writes the records exactly as the reference encodes them
+(sampler.cpp:118-140) and prints the reference's timing line
+`init_seconds=%.6f sampling_seconds=%.6f` on stderr (cliffsym.cpp:126-127).
+With `--rng compat` the output is byte-identical to `cliffsym sample` for the
+same seed. Exit codes follow cliffsym.cpp:346-355: parse/usage errors 1,
+internal logic errors 2.
+"""
+from __future__ import annotations
+
+import argparse
+import sys
+import time
+
+
+def _read(path: str | None) -> str:
+    if not path or path == "-":
+        return sys.stdin.read()
+    with open(path) as f:
+        return f.read()
+
+
+def _write(path: str | None, data: bytes) -> None:
+    if not path or path == "-":
+        sys.stdout.buffer.write(data)
+        sys.stdout.buffer.flush()
+    else:
+        with open(path, "wb") as f:
+            f.write(data)
+
+
+def expression_to_string(syms) -> str:
+    """tableau.cpp:308-316: '0' for empty, '1' for s0, 's<i>' joined by ' ^ '."""
+    if len(syms) == 0:
+        return "0"
+    return " ^ ".join("1" if s == 0 else f"s{s}" for s in syms)
+
+
+def cmd_sample(a) -> int:
+    from . import Sampler, run_initialization
+    text = _read(a.input)
+    t0 = time.perf_counter()
+    init = run_initialization(text)
+    init_s = time.perf_counter() - t0
+    t1 = time.perf_counter()
+    smp = Sampler(init, device=a.device, rng=a.rng)
+    buf, n = smp.sample_to_host(a.shots, a.seed, a.format)
+    sampling_s = time.perf_counter() - t1
+    _write(a.out, bytes(buf[:n]))
+    if a.dump_assignments:
+        from .sampler import unpack_bits
+        S = smp.draw_assignments(a.shots, a.seed).cpu().numpy().view("uint64")
+        bits = unpack_bits(S, a.shots)
+        lines = "\n".join("".join("1" if b else "0" for b in row) for row in bits) + "\n"
+        _write(a.dump_assignments, lines.encode())
+    print(f"init_seconds={init_s:.6f} sampling_seconds={sampling_s:.6f}", file=sys.stderr)
+    return 0
+
+
+def cmd_analyze(a) -> int:
+    from . import run_initialization
+    from .sampler import DIST_NAMES
+    init = run_initialization(_read(a.input))
+    # cmd_analyze, cliffsym.cpp:130-149: 1-based measurement names, then a
+    # '#'-comment listing of the symbols.
+    lines = [f"m{k + 1} = {expression_to_string(e)}" for k, e in enumerate(init.expressions)]
+    if init.n_sym > 1:
+        lines.append("# symbols:")
+        for g in init.groups[1:]:
+            for b in range(int(g["arity"])):
+                sid = int(g["first_symbol"]) + b
+                kind = DIST_NAMES[int(g["dist"])]
+                p = "" if int(g["dist"]) == 2 else f"({float(g['param'])!r})"
+                lines.append(f"#   s{sid}: {kind}{p} bit {b}")
+    _write(a.out, ("\n".join(lines) + ("\n" if lines else "")).encode())
+    return 0
+
+
+def main(argv=None) -> int:
+    ap = argparse.ArgumentParser(prog="python -m paper_2311_03906_b200",
+                                 description="B200 stabilizer-circuit sampler (SymPhase)")
+    sub = ap.add_subparsers(dest="cmd", required=True)
+    s = sub.add_parser("sample", help="sample measurement outcomes")
+    s.add_argument("--in", dest="input")
+    s.add_argument("--out")
+    s.add_argument("--seed", type=int, default=0)
+    s.add_argument("--shots", type=int, default=1)
+    s.add_argument("--format", choices=["01", "b8"], default="01")
+    s.add_argument("--rng", choices=["philox", "compat"], default="philox")
+    s.add_argument("--device", type=int, default=0)
+    s.add_argument("--dump-assignments")
+    s.add_argument("--threads", type=int, default=1, help="accepted for compatibility; unused")
+    an = sub.add_parser("analyze", help="print measurement outcomes as symbol expressions")
+    an.add_argument("--in", dest="input")
+    an.add_argument("--out")
+    try:
+        a = ap.parse_args(argv)
+    except SystemExit as e:
+        return 0 if e.code == 0 else 1
+    from ._native import LogicError, SymphaseError
+    try:
+        if a.cmd == "sample":
+            if a.shots < 1:
+                print("error: --shots must be positive", file=sys.stderr)
+                return 1
+            return cmd_sample(a)
+        return cmd_analyze(a)
+    except LogicError as e:
+        print(f"internal error: {e}", file=sys.stderr)
+        return 2
+    except (SymphaseError, OSError, ValueError) as e:
+        print(f"error: {e}", file=sys.stderr)
+        return 1
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -62,6 +62,7 @@ SIGNATURES = [
     ("sp_encode", _i, [_p, _p, _u64, _u64, _u64, _i, _p]),
     ("sp_sample_to_host", _i, [_p, _u64, _u64, _u64, _i, _p, _u64, _pu64]),
     ("sp_debug_philox", _i, [_p, _p, _p]),
+    ("sp_debug_timers", _i, [_p, _p]),
     ("sp_launch_count", _u64, [_p]),
     ("sp_synchronize", _i, [_p]),
 ]

@@ -97,7 +97,7 @@ struct sp_ctx {
   // plan buffers
   DBuf b_row_ptr, b_sym_idx, b_col_ptr, b_col_rows, b_dense, b_first, b_arity, b_dist, b_param,
       b_row_const_compat, b_ones, b_dense_sym, b_drow_ptr, b_drow_slot, b_cls, b_cls_groups,
-      b_desc, b_colrow, b_live_groups, b_path_rows, b_path_ptr, b_path_par, b_round_ptr, b_plist;
+      b_desc, b_colrow, b_live_groups, b_path_rows, b_path_ptr, b_path_par, b_round_ptr, b_plist, b_pslot_ptr, b_pslots, b_keep_rows, b_timers;
   // K2's own copy of the rows (independent of the group table)
   bool prod_ready = false;
   DevPlan pp;
@@ -346,7 +346,8 @@ void build_plan(sp_ctx* c) {
   d.n_cls_live = static_cast<uint32_t>(live_cls.size());
   d.n_desc_live = static_cast<uint32_t>(live_positions);
   d.n_colrow = live_colrow;
-  d.n_paths = static_cast<uint32_t>(n_meas);  // upper bound for the smem estimate
+  d.n_paths = static_cast<uint32_t>(n_meas);  // upper bounds for the smem estimate
+  d.n_keep = static_cast<uint32_t>(n_meas);
   const size_t optin = c->L.smem_optin;
   int lg = -1;
   bool staged = false, row_staged = false;
@@ -360,7 +361,7 @@ void build_plan(sp_ctx* c) {
     if (force_rs >= 0 && rs != (force_rs != 0)) continue;
     for (int t = 12; t >= 7; --t) {
       if (force_lg && t != force_lg) continue;
-      if (static_cast<uint64_t>(n_meas) * (1u << (t - 5)) >= 65536) continue;  // u16 row offsets
+      if (static_cast<uint64_t>(n_meas + 1) * (1u << (t - 5)) >= 65536) continue;  // u16 row offsets
       if (st && t < 9 && !force_lg) break;
       if (fused_smem_bytes(d, t, st, rs) <= optin) {
         lg = t;
@@ -386,10 +387,11 @@ void build_plan(sp_ctx* c) {
     d.cta_per_sm = static_cast<uint32_t>(std::max<long>(
         1, std::min<long>(env_long("SP_CTAS", 2), static_cast<long>((228 * 1024) / (smem + 1024)))));
     const double ev = events_per_shot * T, flips = flips_per_shot * T;
-    const double gen = ev * 60.0 + flips * 4.0;
+    // Generator warps also make the coin words; drain warps only rebuild and
+    // store rows (~40 instructions per 128-shot row word).
+    const double gen = ev * 60.0 + flips * 4.0 + n_dense_live * (T / 128.0) * 60.0;
     const double items = static_cast<double>(n_meas) * (T / 128);
-    const double drain = n_dense_live * (T / 128.0) * 60.0 +
-                         items * (12.0 + 3.0 * drow_slot.size() / std::max<uint64_t>(n_meas, 1));
+    const double drain = items * (40.0 + 3.0 * drow_slot.size() / std::max<uint64_t>(n_meas, 1));
     d.cta_threads = static_cast<uint32_t>(env_long("SP_CTA_THREADS", 512));
     const long n_warps = d.cta_threads / 32;
     long gw = std::lround(n_warps * 0.75 * gen / std::max(gen + drain, 1.0) / 0.75);
@@ -402,7 +404,7 @@ void build_plan(sp_ctx* c) {
   // into slices of ~E expected firings (<= 2^24 trials), one warp walk each;
   // E is chosen so each generator warp takes a few segments per tile.
   const double ev_tile = events_per_shot * T;
-  double E = ev_tile / (3.0 * d.gen_warps);
+  double E = ev_tile / d.gen_warps;
   E = std::min(std::max(E, 32.0), 2048.0);
   if (const long fe = env_long("SP_SEG_EVENTS", 0)) E = static_cast<double>(fe);
   std::vector<ClassInfo> cls_info;
@@ -514,8 +516,13 @@ void build_plan(sp_ctx* c) {
     d.lp = max_plist <= 8 ? 8 : max_plist <= 16 ? 16 : 0;
     if (force_lp >= 0) d.lp = static_cast<uint32_t>(force_lp);
     if (d.lp && d.lp < max_plist) d.lp = 0;
+    // Unconditional padded XORs cost ATOMS throughput (~12 lanes/clk/SM on
+    // B200); they only pay off when firings per shot are few.
+    d.pad_pred = events_per_shot * d.lp > 32.0;
+    if (const long fp = env_long("SP_PAD_PRED", -1); fp >= 0) d.pad_pred = fp != 0;
     if (d.lp) {
-      std::vector<uint16_t> flat(plists.size() * d.lp, 0xFFFF);
+      // padding = the spare tile row (row n_meas), absorbed and never read
+      std::vector<uint16_t> flat(plists.size() * d.lp, static_cast<uint16_t>(n_meas * d.tw));
       for (size_t i = 0; i < plists.size(); ++i)
         std::copy(plists[i].begin(), plists[i].end(), flat.begin() + i * d.lp);
       std::vector<uint4> packed(std::max<size_t>(flat.size() / 8, 1));
@@ -555,11 +562,24 @@ void build_plan(sp_ctx* c) {
     for (uint32_t i = 0; i < order.size(); ++i) order[i] = i;
     std::stable_sort(order.begin(), order.end(),
                      [&](uint32_t a, uint32_t b) { return round_of_path[a] < round_of_path[b]; });
-    std::vector<uint16_t> path_rows;
-    std::vector<uint32_t> path_ptr{0}, round_ptr(n_rounds + 1, 0);
+    std::vector<uint8_t> keep(n_meas, 0);
+    for (uint64_t k = 0; k < n_meas; ++k) {
+      const int32_t pa = X.parent[k];
+      if (pa >= 0 && heavy[pa] != static_cast<int32_t>(k)) keep[pa] = 1;  // light child
+    }
+    std::vector<uint32_t> path_rows;
+    std::vector<uint32_t> path_ptr{0}, round_ptr(n_rounds + 1, 0), pslot_ptr;
+    std::vector<uint16_t> pslots, keep_rows;
     std::vector<int32_t> path_par;
     for (uint32_t id : order) {
-      path_rows.insert(path_rows.end(), paths[id].begin(), paths[id].end());
+      pslot_ptr.push_back(static_cast<uint32_t>(pslots.size()));
+      for (uint16_t r : paths[id]) {
+        const uint32_t ns = drow_ptr[r + 1] - drow_ptr[r];
+        if (ns > 0x7FFF) throw std::invalid_argument("too many dense symbols in one row");
+        path_rows.push_back(r | (ns << 16) | (keep[r] ? 0x80000000u : 0u));
+        pslots.insert(pslots.end(), drow_slot.begin() + drow_ptr[r], drow_slot.begin() + drow_ptr[r + 1]);
+        if (keep[r]) keep_rows.push_back(r);
+      }
       path_ptr.push_back(static_cast<uint32_t>(path_rows.size()));
       path_par.push_back(heads_par[id]);
       round_ptr[round_of_path[id] + 1]++;
@@ -568,13 +588,21 @@ void build_plan(sp_ctx* c) {
     if (path_rows.empty()) path_rows.push_back(0);
     d.n_paths = static_cast<uint32_t>(paths.size());
     d.n_rounds = n_rounds;
+    d.n_keep = static_cast<uint32_t>(keep_rows.size());
     d.path_rows = c->b_path_rows.upload(path_rows, s);
     d.path_ptr = c->b_path_ptr.upload(path_ptr, s);
     d.path_par = c->b_path_par.upload(path_par, s);
+    d.pslot_ptr = c->b_pslot_ptr.upload(pslot_ptr, s);
+    d.pslots = c->b_pslots.upload(pslots, s);
+    d.keep_rows = c->b_keep_rows.upload(keep_rows, s);
     d.round_ptr = c->b_round_ptr.upload(round_ptr, s);
   }
   d.n_live_groups = static_cast<uint32_t>(live_groups.size());
   d.live_groups = c->b_live_groups.upload(live_groups, s);
+  if (env_long("SP_PHASE_TIMERS", 0)) {
+    std::vector<long long> z(4, 0);
+    d.timers = c->b_timers.upload(z, s);
+  }
   ck(cudaStreamSynchronize(s), "plan upload");
   c->plan_ready = true;
 }
@@ -955,6 +983,17 @@ int sp_synchronize(sp_ctx* ctx) {
   if (int r = set_device(ctx)) return r;
   cudaError_t e = cudaStreamSynchronize(ctx->stream);
   if (e != cudaSuccess) return fail(SP_ERR_CUDA, std::string("sync: ") + cudaGetErrorString(e));
+  return SP_OK;
+}
+
+// Test/profiling hook: copies (and clears) the fused kernel's per-role cycle
+// counters when the plan was built with SP_PHASE_TIMERS=1.
+int sp_debug_timers(sp_ctx* ctx, long long* out4) {
+  if (!ctx || !out4) return fail(SP_ERR_INVALID_ARGUMENT, "null argument");
+  if (!ctx->dp.timers) return fail(SP_ERR_NOT_LOADED, "timers not enabled (SP_PHASE_TIMERS=1)");
+  if (cudaMemcpy(out4, ctx->dp.timers, 32, cudaMemcpyDeviceToHost) != cudaSuccess ||
+      cudaMemset(ctx->dp.timers, 0, 32) != cudaSuccess)
+    return fail(SP_ERR_CUDA, "timer copy failed");
   return SP_OK;
 }
 

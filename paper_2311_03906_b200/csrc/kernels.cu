@@ -16,6 +16,7 @@
 #include "kernels.cuh"
 
 #include <algorithm>
+#include <type_traits>
 
 namespace symphase {
 
@@ -60,8 +61,10 @@ __device__ __forceinline__ uint4 philox10(uint4 c, const RoundKeys& K) {
 __device__ __forceinline__ float exp1_from_bits(uint32_t r) {
   const uint32_t k = (r >> 8) + 1u;
   const float ux = static_cast<float>(0x1000000u - k) * 0x1.0p-24f;  // 1 - u, exact
-  if (ux < 0.03125f) return ux * (1.f + ux * (0.5f + ux * (0.33333334f + ux * 0.25f)));
-  return -__log2f(static_cast<float>(k) * 0x1.0p-24f) * 0.6931471806f;
+  const float series = ux * (1.f + ux * (0.5f + ux * (0.33333334f + ux * 0.25f)));
+  float lg;  // u >= 2^-24 is a normal float, so the flush-to-zero form is exact
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(lg) : "f"(static_cast<float>(k) * 0x1.0p-24f));
+  return ux < 0.03125f ? series : -lg * 0.6931471806f;  // branch-free select
 }
 
 // SplitMix64 finalizer and keyed draw — sampler.hpp:14-26.
@@ -145,10 +148,11 @@ __device__ __forceinline__ void segment_init(Segment& sg, const ClassInfo* cls, 
 
 // Walks one segment with the whole warp; emit(const Fired&) runs on every
 // lane after each step (lanes may have no valid firing).
-template <class Emit>
-__device__ __forceinline__ void segment_walk(const Segment& sg, const RoundKeys& K, uint64_t gtile,
-                                             uint32_t t_log2, uint32_t lane, Emit&& emit) {
-  const bool bern = sg.dist == 1;
+template <bool kBern, class Emit>
+__device__ __forceinline__ void segment_walk_t(const Segment& sg, const RoundKeys& K,
+                                               uint64_t gtile, uint32_t t_log2, uint32_t lane,
+                                               Emit&& emit) {
+  constexpr bool bern = kBern;
   const uint32_t nk = bern ? 4u : 3u;  // skips per Philox block
   const uint32_t n = sg.dist == 3 ? 3u : 15u;
   const uint32_t magic = n == 3 ? 0x5556u : 0x1112u;  // exact /n for values < n^3
@@ -218,9 +222,21 @@ __device__ __forceinline__ void segment_walk(const Segment& sg, const RoundKeys&
                                    static_cast<uint32_t>(gtile), c3),
                         K);
     }
-    emit(f);
+    emit(std::integral_constant<bool, kBern>{}, f);
     if (!more) return;
   }
+}
+
+// Bernoulli classes use all four words of a block as skips; DEPOLARIZE
+// classes use three and draw patterns from the fourth. The two shapes are
+// separate instantiations so neither pays for the other's slots.
+template <class Emit>
+__device__ __forceinline__ void segment_walk(const Segment& sg, const RoundKeys& K, uint64_t gtile,
+                                             uint32_t t_log2, uint32_t lane, Emit&& emit) {
+  if (sg.dist == 1)
+    segment_walk_t<true>(sg, K, gtile, t_log2, lane, emit);
+  else
+    segment_walk_t<false>(sg, K, gtile, t_log2, lane, emit);
 }
 
 __device__ __forceinline__ void named_sync(uint32_t id, uint32_t n) {
@@ -228,16 +244,6 @@ __device__ __forceinline__ void named_sync(uint32_t id, uint32_t n) {
 }
 __device__ __forceinline__ void named_arrive(uint32_t id, uint32_t n) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-
-// Predicated shared-memory XOR reduction: one ATOMS per active lane, no
-// branch (a C++ `if (...) atomicXor(...)` compiles to BSSY/BRA/BSYNC around
-// every call, which dominated the firing loop).
-__device__ __forceinline__ void red_xor_shared_if(uint32_t saddr, uint32_t val, uint32_t pred) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p red.shared.xor.b32 [%0], %1;\n\t}"
-      ::"r"(saddr), "r"(val), "r"(pred)
-      : "memory");
 }
 
 __device__ __forceinline__ uint4 xor4(uint4 a, uint4 b) {
@@ -261,7 +267,7 @@ __device__ __forceinline__ uint4 xor4(uint4 a, uint4 b) {
 // with 16-byte stores and zero the buffer for tile i+2. Named barriers
 // FULL[b] / EMPTY[b] hand the buffers back and forth. Event tables and row
 // tables are staged in shared memory when they fit.
-template <bool kStaged, bool kRowStaged, int kLp>
+template <bool kStaged, bool kRowStaged, int kLp, bool kPadPred>
 __global__ void __launch_bounds__(kFusedThreads, 1)
 k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, uint64_t n_shots,
          uint64_t* __restrict__ out, uint64_t ld, unsigned long long* __restrict__ counts,
@@ -283,33 +289,40 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
   const ClassInfo* CLS = P.cls;
   const uint4* DESC = P.desc;
   const uint16_t* COLROW = P.colrow;
-  const uint32_t* DRP = P.drow_ptr;
-  const uint16_t* DRS = P.drow_slot;
   const uint4* PLIST = P.plist;
-  const uint16_t* PROWS = P.path_rows;
+  const uint32_t* PROWS = P.path_rows;
   const uint32_t* PPTR = P.path_ptr;
   const int32_t* PPAR = P.path_par;
+  const uint32_t* PSLP = P.pslot_ptr;
+  const uint16_t* PSL = P.pslots;
+  const uint16_t* KEEP = P.keep_rows;
   if (kRowStaged) {
-    uint32_t* s_drp = reinterpret_cast<uint32_t*>(p);
-    p += align16(4ull * (P.n_meas + 1));
-    uint16_t* s_drs = reinterpret_cast<uint16_t*>(p);
-    p += align16(2ull * P.n_drow);
-    uint16_t* s_prows = reinterpret_cast<uint16_t*>(p);
-    p += align16(2ull * P.n_meas);
+    uint32_t* s_prows = reinterpret_cast<uint32_t*>(p);
+    p += align16(4ull * P.n_meas);
     uint32_t* s_pptr = reinterpret_cast<uint32_t*>(p);
     p += align16(4ull * (P.n_paths + 1));
     int32_t* s_ppar = reinterpret_cast<int32_t*>(p);
     p += align16(4ull * P.n_paths);
-    for (uint32_t i = threadIdx.x; i <= P.n_meas; i += blockDim.x) s_drp[i] = P.drow_ptr[i];
-    for (uint32_t i = threadIdx.x; i < P.n_drow; i += blockDim.x) s_drs[i] = P.drow_slot[i];
+    uint32_t* s_pslp = reinterpret_cast<uint32_t*>(p);
+    p += align16(4ull * P.n_paths);
+    uint16_t* s_psl = reinterpret_cast<uint16_t*>(p);
+    p += align16(2ull * P.n_drow);
+    uint16_t* s_keep = reinterpret_cast<uint16_t*>(p);
+    p += align16(2ull * P.n_keep);
     for (uint32_t i = threadIdx.x; i < P.n_meas; i += blockDim.x) s_prows[i] = P.path_rows[i];
     for (uint32_t i = threadIdx.x; i <= P.n_paths; i += blockDim.x) s_pptr[i] = P.path_ptr[i];
-    for (uint32_t i = threadIdx.x; i < P.n_paths; i += blockDim.x) s_ppar[i] = P.path_par[i];
-    DRP = s_drp;
-    DRS = s_drs;
+    for (uint32_t i = threadIdx.x; i < P.n_paths; i += blockDim.x) {
+      s_ppar[i] = P.path_par[i];
+      s_pslp[i] = P.pslot_ptr[i];
+    }
+    for (uint32_t i = threadIdx.x; i < P.n_drow; i += blockDim.x) s_psl[i] = P.pslots[i];
+    for (uint32_t i = threadIdx.x; i < P.n_keep; i += blockDim.x) s_keep[i] = P.keep_rows[i];
     PROWS = s_prows;
     PPTR = s_pptr;
     PPAR = s_ppar;
+    PSLP = s_pslp;
+    PSL = s_psl;
+    KEEP = s_keep;
   }
   if (kStaged) {
     ClassInfo* s_cls = reinterpret_cast<ClassInfo*>(p);
@@ -354,20 +367,41 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
     for (uint32_t i = 0; i < n_my; ++i) {
       const uint32_t b = i & 1;
       const uint64_t gtile = tile0 + blockIdx.x + static_cast<uint64_t>(i) * gridDim.x;
+      long long tw0 = clock64();
       if (i >= 2) named_sync(kBarEmpty0 + b, blockDim.x);
+      long long tw1 = clock64();
       uint32_t* tile = tiles + b * tile_words;
+      {  // fair-coin words of this tile (dense symbols), keyed by (symbol, 128-shot quad)
+        uint4* c4 = reinterpret_cast<uint4*>(coins + b * n_slots * tw);
+        for (uint32_t j = threadIdx.x; j < (P.n_dense_live << tw4_log2); j += n_gen * 32) {
+          const uint32_t slot = j >> tw4_log2, q = j & (tw4 - 1);
+          const uint64_t gq = (gtile << tw4_log2) + q;
+          c4[j] = philox10(make_uint4(P.dense_sym[slot], static_cast<uint32_t>(gq),
+                                      (static_cast<uint32_t>(gq >> 32) & 0xFFFFFFu) |
+                                          (kDomCoin << 24),
+                                      0u),
+                           K);
+        }
+      }
       const uint32_t tile_s = static_cast<uint32_t>(__cvta_generic_to_shared(tile));
+      const uint32_t spare = P.n_meas * tw;
+      const uint32_t spare2 = spare * 0x10001u;  // two u16 spare-row offsets
       uint32_t seg = 0;
       Segment sg;
-      auto emit = [&](const Fired& f) {
+      auto emit = [&](auto bern_tag, const Fired& f) {
+        constexpr bool kB = decltype(bern_tag)::value;
         if constexpr (kLp > 0) {
           // Exact flip list of (group, pattern), padded to kLp u16 rows with
           // 0xFFFF; one or two 16-byte loads, then predicated shared atomics.
 #pragma unroll
           for (int half = 0; half < kSlots; half += 4) {
+            // Padding entries point at the spare row, so every entry is an
+            // unconditional shared XOR; an invalid slot XORs bit 0 of the
+            // spare row's first word.
             uint4 lst[4][kLp / 8];
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
+            for (int k = 0; k < 4; ++k) {
+              if (!kB && k == 3) continue;
 #pragma unroll
               for (int h = 0; h < kLp / 8; ++h)
                 lst[k][h] = ((f.v >> (half + k)) & 1u)
@@ -375,18 +409,27 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
                                                                        f.g[half + k] * sg.npat +
                                                                        f.pat[half + k] - 1) *
                                                      (kLp / 8) + h))
-                                : make_uint4(kFull, kFull, kFull, kFull);
+                                : make_uint4(spare2, spare2, spare2, spare2);
+            }
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
+              if (!kB && k == 3) continue;
               const uint32_t wb = tile_s + ((f.shot[half + k] >> 5) << 2);
-              const uint32_t bit = 1u << (f.shot[half + k] & 31);
+              const uint32_t bit = ((f.v >> (half + k)) & 1u) << (f.shot[half + k] & 31);
 #pragma unroll
               for (int h = 0; h < kLp / 8; ++h) {
                 const uint32_t ww[4] = {lst[k][h].x, lst[k][h].y, lst[k][h].z, lst[k][h].w};
 #pragma unroll
                 for (int e = 0; e < 8; ++e) {
                   const uint32_t row = (ww[e >> 1] >> (16 * (e & 1))) & 0xFFFFu;
-                  red_xor_shared_if(wb + (row << 2), bit, row != 0xFFFFu);
+                  if (kPadPred) {
+                    // many firings per shot: skip padding so the ATOMS pipe
+                    // only carries real flips
+                    if (row != spare) atomicXor(tile + (f.shot[half + k] >> 5) + row, bit);
+                  } else {
+                    asm volatile("red.shared.xor.b32 [%0], %1;" ::"r"(wb + (row << 2)), "r"(bit)
+                                 : "memory");
+                  }
                 }
               }
             }
@@ -394,6 +437,7 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
         } else {
 #pragma unroll
           for (int k = 0; k < kSlots; ++k) {
+            if (!kB && (k & 3) == 3) continue;
             if (!((f.v >> k) & 1u)) continue;
             const uint4 d = DESC[sg.goff + f.g[k]];
             const uint32_t bit = 1u << (f.shot[k] & 31);
@@ -416,6 +460,10 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
         segment_init(sg, CLS, P.n_cls_live, seg);
         segment_walk(sg, K, gtile, P.t_log2, lane, emit);
       }
+      if (P.timers && lane == 0) {  // gen: [0] waiting EMPTY, [1] working
+        atomicAdd(reinterpret_cast<unsigned long long*>(P.timers) + 0, tw1 - tw0);
+        atomicAdd(reinterpret_cast<unsigned long long*>(P.timers) + 1, clock64() - tw1);
+      }
       named_arrive(kBarFull0 + b, blockDim.x);
     }
   } else {
@@ -425,18 +473,10 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
       const uint32_t b = i & 1;
       const uint64_t t_local = blockIdx.x + static_cast<uint64_t>(i) * gridDim.x;
       const uint64_t gtile = tile0 + t_local;
-      uint4* c4 = reinterpret_cast<uint4*>(coins + b * n_slots * tw);
-      for (uint32_t j = ct; j < (P.n_dense_live << tw4_log2); j += nct) {
-        const uint32_t slot = j >> tw4_log2, q = j & (tw4 - 1);
-        const uint64_t gq = (gtile << tw4_log2) + q;
-        c4[j] = philox10(make_uint4(P.dense_sym[slot], static_cast<uint32_t>(gq),
-                                    (static_cast<uint32_t>(gq >> 32) & 0xFFFFFFu) |
-                                        (kDomCoin << 24),
-                                    0u),
-                         K);
-      }
-      named_sync(kBarDrain, nct);
+      const uint4* c4 = reinterpret_cast<const uint4*>(coins + b * n_slots * tw);
+      long long td0 = clock64();
       named_sync(kBarFull0 + b, blockDim.x);
+      long long td1 = clock64();
 
       uint4* t4 = reinterpret_cast<uint4*>(tiles + b * tile_words);
       const uint64_t first = t_local << P.t_log2;
@@ -450,20 +490,36 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
       for (uint32_t rd = 0; rd < P.n_rounds; ++rd) {
         const uint32_t p0 = P.round_ptr[rd], p1 = P.round_ptr[rd + 1];
         const uint32_t tasks = (p1 - p0) << tw4_log2;
-        for (uint32_t j = ct; j < tasks; j += nct) {
-          const uint32_t pth = p0 + (j >> tw4_log2);
+        const uint32_t tasks_rounded = (tasks + 31) & ~31u;
+        for (uint32_t j = ct; j < tasks_rounded; j += nct) {
+          const bool act = j < tasks;
+          const uint32_t pth = act ? p0 + (j >> tw4_log2) : p0;
           const uint32_t q = j & (tw4 - 1);
-          const int32_t par = PPAR[pth];
+          const int32_t par = act ? PPAR[pth] : -1;
           uint4 prev = par >= 0 ? t4[(static_cast<uint32_t>(par) << tw4_log2) + q]
                                 : make_uint4(0, 0, 0, 0);
-          for (uint32_t x = PPTR[pth], xe = PPTR[pth + 1]; x < xe; ++x) {
-            const uint32_t k = PROWS[x];
+          uint32_t sl = act ? PSLP[pth] : 0;
+          const uint32_t xe = act ? PPTR[pth + 1] : 0;
+          uint32_t x = act ? PPTR[pth] : 0;
+          uint32_t e = x < xe ? PROWS[x] : 0u;
+          uint4 cur = x < xe ? t4[((e & 0xFFFFu) << tw4_log2) + q] : make_uint4(0, 0, 0, 0);
+          for (; x < xe; ++x) {
+            // e = row | n_slots << 16 | keep << 31; prefetch the next row's word
+            const bool has_next = x + 1 < xe;
+            const uint32_t en = has_next ? PROWS[x + 1] : 0u;
+            const uint4 nxt = has_next ? t4[((en & 0xFFFFu) << tw4_log2) + q] : make_uint4(0, 0, 0, 0);
+            const uint32_t k = e & 0xFFFFu;
             const uint32_t ti = (k << tw4_log2) + q;
-            uint4 v = xor4(t4[ti], prev);
-            for (uint32_t s = DRP[k], e = DRP[k + 1]; s < e; ++s)
-              v = xor4(v, c4[(static_cast<uint32_t>(DRS[s]) << tw4_log2) + q]);
-            t4[ti] = v;  // final value, read by light children in later rounds
+            uint4 v = xor4(cur, prev);
+            for (const uint32_t se = sl + ((e >> 16) & 0x7FFFu); sl < se; ++sl)
+              v = xor4(v, c4[(static_cast<uint32_t>(PSL[sl]) << tw4_log2) + q]);
+            // Rows with light children keep their final value for a later
+            // round; all others are cleared for tile i+2 right away.
+            t4[ti] = (e >> 31) ? v : make_uint4(0, 0, 0, 0);
             prev = v;
+            e = en;
+            cur = nxt;
+            uint32_t pc = 0;
             if (q < vq) {
               bool two = true;  // whether the item's second u64 word is inside the tile
               if (q == vq - 1 && rem) {
@@ -483,9 +539,14 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
                 o[0] = w0;
                 if (two) o[1] = w1;
               }
-              if (with_counts) {
-                const uint32_t pc = __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
-                if (pc) atomicAdd(&cnt[k], pc);
+              if (with_counts) pc = __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
+            }
+            if (with_counts) {
+              if (tw4 >= 32) {  // the whole warp walks this path: one atomic per row
+                pc = __reduce_add_sync(kFull, pc);
+                if (lane == 0 && pc) atomicAdd(&cnt[k], pc);
+              } else if (pc) {
+                atomicAdd(&cnt[k], pc);
               }
             }
           }
@@ -494,9 +555,17 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
         // reads is final.
         if (rd + 1 < P.n_rounds) named_sync(kBarDrain, nct);
       }
-      named_sync(kBarDrain, nct);  // every drain thread is done reading the tile
-      for (uint32_t j = ct; j < tile_words / 4; j += nct) t4[j] = make_uint4(0, 0, 0, 0);
+      if (P.n_keep) {
+        named_sync(kBarDrain, nct);  // all light children have read their parents
+        for (uint32_t j = ct; j < (P.n_keep << tw4_log2); j += nct)
+          t4[(static_cast<uint32_t>(KEEP[j >> tw4_log2]) << tw4_log2) + (j & (tw4 - 1))] =
+              make_uint4(0, 0, 0, 0);
+      }
       if (ct == 0) segctr[b] = 0;  // all generators are past tile i (FULL[b] completed)
+      if (P.timers && lane == 0) {  // drain: [2] waiting FULL, [3] working
+        atomicAdd(reinterpret_cast<unsigned long long*>(P.timers) + 2, td1 - td0);
+        atomicAdd(reinterpret_cast<unsigned long long*>(P.timers) + 3, clock64() - td1);
+      }
       if (i + 2 < n_my) named_arrive(kBarEmpty0 + b, blockDim.x);
     }
   }
@@ -604,7 +673,7 @@ __global__ void d_segments(const DevPlan P, const RoundKeys K, uint64_t tile0, u
     const uint64_t base = static_cast<uint64_t>(t) << P.t_log2;
     Segment sg;
     segment_init(sg, P.cls, P.n_cls_all, seg);
-    segment_walk(sg, K, tile0 + t, P.t_log2, lane, [&](const Fired& f) {
+    segment_walk(sg, K, tile0 + t, P.t_log2, lane, [&](auto, const Fired& f) {
       for (int k = 0; k < kSlots; ++k) {
         if (!((f.v >> k) & 1u)) continue;
         const uint64_t j = base + f.shot[k];
@@ -809,11 +878,11 @@ int persistent_grid(Kern kernel, const LaunchCfg& L, size_t smem, uint32_t n_til
   return 0;
 }
 
-template <bool kStaged, bool kRowStaged, int kLp>
+template <bool kStaged, bool kRowStaged, int kLp, bool kPadPred = false>
 int launch_k1(const DevPlan& P, const LaunchCfg& L, const RoundKeys& K, uint64_t tile0,
               uint32_t n_tiles, uint64_t n_shots, uint64_t* out, uint64_t ld,
               unsigned long long* cnt) {
-  auto kern = k1_fused<kStaged, kRowStaged, kLp>;
+  auto kern = k1_fused<kStaged, kRowStaged, kLp, kPadPred>;
   const size_t smem = fused_smem_bytes(P, P.t_log2, kStaged, kRowStaged);
   int grid = 0;
   const int threads = static_cast<int>(P.cta_threads);
@@ -831,11 +900,11 @@ size_t fused_smem_bytes(const DevPlan& P, uint32_t t_log2, bool staged, bool row
   b += 2 * static_cast<size_t>(P.n_dense_live + 1) * tw * 4;        // coin words + ones slot
   b += align16(4ull * P.n_meas) + 16;                               // counts, dispensers
   if (row_staged) {
-    b += align16(4ull * (P.n_meas + 1));
-    b += align16(2ull * P.n_drow);
-    b += align16(2ull * P.n_meas);
+    b += align16(4ull * P.n_meas);
     b += align16(4ull * (P.n_paths + 1));
-    b += align16(4ull * P.n_paths);
+    b += 2 * align16(4ull * P.n_paths);
+    b += align16(2ull * P.n_drow);
+    b += align16(2ull * P.n_keep);
   }
   if (staged) {
     b += align16(sizeof(ClassInfo) * P.n_cls_live);
@@ -852,11 +921,17 @@ int launch_fused_sample(const DevPlan& P, const LaunchCfg& L, uint64_t seed, uin
   const RoundKeys K = expand_keys(seed);
   auto* cnt = reinterpret_cast<unsigned long long*>(counts);
 #define SP_K1(st, rs, lp) launch_k1<st, rs, lp>(P, L, K, tile0, n_tiles, n_shots, out, ld, cnt)
+#define SP_K1P(st, rs, lp) \
+  launch_k1<st, rs, lp, true>(P, L, K, tile0, n_tiles, n_shots, out, ld, cnt)
+  if (P.lp == 8 && P.pad_pred) return P.row_staged ? SP_K1P(false, true, 8) : SP_K1P(false, false, 8);
+  if (P.lp == 16 && P.pad_pred)
+    return P.row_staged ? SP_K1P(false, true, 16) : SP_K1P(false, false, 16);
   if (P.lp == 8) return P.row_staged ? SP_K1(false, true, 8) : SP_K1(false, false, 8);
   if (P.lp == 16) return P.row_staged ? SP_K1(false, true, 16) : SP_K1(false, false, 16);
   if (P.staged) return P.row_staged ? SP_K1(true, true, 0) : SP_K1(true, false, 0);
   return P.row_staged ? SP_K1(false, true, 0) : SP_K1(false, false, 0);
 #undef SP_K1
+#undef SP_K1P
 }
 
 int launch_fused_sample_compat(const DevPlan& P, const LaunchCfg& L, uint64_t seed,

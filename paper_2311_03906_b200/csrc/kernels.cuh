@@ -79,16 +79,24 @@ struct DevPlan {
   // lp u16 rows (lp = 8 or 16; 0 = lists too long, use desc/colrow loops).
   // List of (class position g, pattern pi) = plist[(pbase + g*npat + pi-1)].
   uint32_t lp = 0;
+  uint32_t pad_pred = 0;  // skip padding entries (many firings per shot) vs XOR the spare row
   const uint4* plist = nullptr;
   // Row reconstruction out[k] = d[k] ^ out[parent[k]] along the paths of a
   // heavy-path decomposition of the parent forest: path p lists rows
   // path_rows[path_ptr[p] .. path_ptr[p+1]) top-down; path_par[p] is the head's
   // parent (or -1), which lies on a path of an earlier round (round_ptr).
-  const uint16_t* path_rows = nullptr;
+  // Entry = row | n_dense_slots << 16 | keep << 31 (keep: row has light
+  // children, so its final value stays in the tile until the tile ends);
+  // each path's dense slots (coins, the ones slot) follow in pslots from
+  // pslot_ptr[path] in row order; keep_rows lists the rows to clear at the end.
+  const uint32_t* path_rows = nullptr;
   const uint32_t* path_ptr = nullptr;
   const int32_t* path_par = nullptr;
+  const uint32_t* pslot_ptr = nullptr;
+  const uint16_t* pslots = nullptr;
+  const uint16_t* keep_rows = nullptr;
   const uint32_t* round_ptr = nullptr;  // [n_rounds + 1] over paths
-  uint32_t n_paths = 0, n_rounds = 1;
+  uint32_t n_paths = 0, n_rounds = 1, n_keep = 0;
 
   // Fused-kernel launch shape (chosen by the planner).
   uint32_t staged = 0;       // event tables copied into shared memory
@@ -96,6 +104,9 @@ struct DevPlan {
   uint32_t gen_warps = 12;   // event-generator warps; the rest drain tiles
   uint32_t cta_per_sm = 1;
   uint32_t cta_threads = 512;
+  // Optional per-role cycle counters (SP_PHASE_TIMERS=1): gen wait/work,
+  // drain wait/work, summed over warps and tiles (u64[4], device).
+  long long* timers = nullptr;
 
   // Compat mode: group ids (>= 1) with at least one live symbol.
   uint32_t n_live_groups = 0;

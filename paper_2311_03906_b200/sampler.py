@@ -67,6 +67,20 @@ class InitResult:
         rp = self.row_ptr
         return [self.sym_idx[rp[k]:rp[k + 1]].tolist() for k in range(self.n_meas)]
 
+    def save(self, path) -> None:
+        """On-disk M_sym cache: CSR rows + group table, so a
+        large circuit's one-pass init (seconds at d=15) runs once."""
+        np.savez_compressed(path, n_qubits=np.array([self.n_qubits]),
+                            n_sym=np.array([self.n_sym]), row_ptr=self.row_ptr,
+                            sym_idx=self.sym_idx, groups=self.groups.view(np.uint8))
+
+    @classmethod
+    def load(cls, path) -> "InitResult":
+        z = np.load(path)
+        groups = np.ascontiguousarray(z["groups"]).view(GROUP_DTYPE).reshape(-1)
+        return cls(int(z["n_qubits"][0]), int(z["n_sym"][0]), z["row_ptr"].astype(np.uint64),
+                   z["sym_idx"].astype(np.uint32), groups)
+
     def dense_words(self) -> np.ndarray:
         """M_sym as dense row-major u64 words [n_meas][ceil(n_sym/64)]."""
         ldm = max((self.n_sym + 63) // 64, 1)

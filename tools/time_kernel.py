@@ -40,12 +40,18 @@ def main():
         torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1))
     ts.sort()
+    timers = None
+    if os.environ.get("SP_PHASE_TIMERS"):
+        import ctypes as C
+        buf = (C.c_longlong * 4)()
+        s._L.sp_debug_timers(s._h, C.cast(buf, C.c_void_p))
+        timers = list(buf)
     ms = ts[len(ts) // 2]
     bytes_ = init.n_meas * n / 8
     env = {k: v for k, v in os.environ.items() if k.startswith("SP_")}
     print(json.dumps({"config": a.config, "shots": n, "T": T, "env": env, "ms_median": ms,
                       "ms_min": ts[0], "GBps": bytes_ / ms / 1e6,
-                      "bits_per_s": init.n_meas * n / ms * 1e3}))
+                      "bits_per_s": init.n_meas * n / ms * 1e3, "timers": timers}))
 
 
 if __name__ == "__main__":
