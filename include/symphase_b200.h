@@ -129,6 +129,22 @@ int sp_shot_tile(sp_ctx* ctx, uint64_t* tile);
 int sp_sample(sp_ctx* ctx, uint64_t seed, uint64_t shot_begin, uint64_t n_shots,
               uint64_t* d_out, uint64_t ld, uint64_t* d_counts);
 
+/* K1 with tiled records (the layout the fused kernel produces natively,
+ * cf. the reference's 512x512-bit TiledBitMatrix, bit_matrix.hpp:13-31):
+ * d_out holds ceil(n_shots/T) blocks; block b is [n_meas][T/64] u64 words
+ * for shots shot_begin + b*T .. + T (bits past n_shots are 0). Every store
+ * of the kernel is then contiguous, whatever n_meas is. Philox RNG only.
+ * sp_tiled_words gives the size in u64 words. */
+uint64_t sp_tiled_words(sp_ctx* ctx, uint64_t n_shots);
+int sp_sample_tiled(sp_ctx* ctx, uint64_t seed, uint64_t shot_begin, uint64_t n_shots,
+                    uint64_t* d_out, uint64_t* d_counts);
+/* Tiled records -> measurement-major [n_meas][ld]. */
+int sp_untile(sp_ctx* ctx, const uint64_t* d_tiled, uint64_t n_shots, uint64_t* d_out,
+              uint64_t ld);
+/* encode_shots straight from tiled records. */
+int sp_encode_tiled(sp_ctx* ctx, const uint64_t* d_tiled, uint64_t n_shots, sp_format fmt,
+                    uint8_t* d_bytes);
+
 /* draw_assignments (sampler.hpp:51-52) on the device: the exact assignment
  * matrix S the fused sampler uses for these shots (row 0 = constant = all
  * ones). d_S: [n_sym][ldS]. With SP_RNG_COMPAT_SPLITMIX it is bit-identical
@@ -157,6 +173,11 @@ int sp_sample_to_host(sp_ctx* ctx, uint64_t seed, uint64_t shot_begin, uint64_t 
 
 /* Test hook: one Philox4x32-10 block on the device. ctr_key = {c0,c1,c2,c3,k0,k1}. */
 int sp_debug_philox(sp_ctx* ctx, const uint32_t* ctr_key, uint32_t* out);
+
+/* Launch shape and table sizes of the loaded model's fused-sampler plan:
+ * {T, gen_warps, cta_threads, staged, row_staged, lp, pad_pred, n_paths,
+ *  n_rounds, n_keep, n_segments, n_classes, n_dense, nnz(D), smem_bytes, fused_ok}. */
+int sp_plan_info(sp_ctx* ctx, uint64_t* out16);
 
 /* Profiling hook: per-role cycle counters of the fused kernel (gen wait,
  * gen work, drain wait, drain work), enabled by SP_PHASE_TIMERS=1 at plan

@@ -57,12 +57,17 @@ SIGNATURES = [
     ("sp_shot_tile", _i, [_p, _pu64]),
     ("sp_sample", _i, [_p, _u64, _u64, _u64, _p, _u64, _p]),
     ("sp_draw_assignments", _i, [_p, _u64, _u64, _u64, _p, _u64]),
+    ("sp_tiled_words", _u64, [_p, _u64]),
+    ("sp_sample_tiled", _i, [_p, _u64, _u64, _u64, _p, _p]),
+    ("sp_untile", _i, [_p, _p, _u64, _p, _u64]),
+    ("sp_encode_tiled", _i, [_p, _p, _u64, _i, _p]),
     ("sp_sample_given_S", _i, [_p, _p, _u64, _u64, _u64, _p, _u64]),
     ("sp_encoded_size", _u64, [_u64, _u64, _i]),
     ("sp_encode", _i, [_p, _p, _u64, _u64, _u64, _i, _p]),
     ("sp_sample_to_host", _i, [_p, _u64, _u64, _u64, _i, _p, _u64, _pu64]),
     ("sp_debug_philox", _i, [_p, _p, _p]),
     ("sp_debug_timers", _i, [_p, _p]),
+    ("sp_plan_info", _i, [_p, _p]),
     ("sp_launch_count", _u64, [_p]),
     ("sp_synchronize", _i, [_p]),
 ]

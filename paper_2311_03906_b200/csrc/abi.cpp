@@ -98,6 +98,7 @@ struct sp_ctx {
   DBuf b_row_ptr, b_sym_idx, b_col_ptr, b_col_rows, b_dense, b_first, b_arity, b_dist, b_param,
       b_row_const_compat, b_ones, b_dense_sym, b_drow_ptr, b_drow_slot, b_cls, b_cls_groups,
       b_desc, b_colrow, b_live_groups, b_path_rows, b_path_ptr, b_path_par, b_round_ptr, b_plist, b_pslot_ptr, b_pslots, b_keep_rows, b_timers;
+  uint64_t dnnz = 0;  // nnz of D (chain transform), for reports
   // K2's own copy of the rows (independent of the group table)
   bool prod_ready = false;
   DevPlan pp;
@@ -227,6 +228,7 @@ void build_plan(sp_ctx* c) {
   for (uint64_t sidx = 0; sidx < n_sym; ++sidx) sq += static_cast<double>(col_len(sidx)) * col_len(sidx);
   const ChainXf X = chain_transform(n_meas, h.row_ptr, h.sym_idx, col_ptr, col_rows,
                                     sq < 2e9 && env_long("SP_NO_CHAIN", 0) == 0);
+  c->dnnz = X.si.size();
   std::vector<uint64_t> dcol_ptr(n_sym + 1, 0);
   for (uint32_t sidx : X.si) dcol_ptr[sidx + 1]++;
   for (uint64_t i = 0; i < n_sym; ++i) dcol_ptr[i + 1] += dcol_ptr[i];
@@ -392,9 +394,11 @@ void build_plan(sp_ctx* c) {
     const double gen = ev * 60.0 + flips * 4.0 + n_dense_live * (T / 128.0) * 60.0;
     const double items = static_cast<double>(n_meas) * (T / 128);
     const double drain = items * (40.0 + 3.0 * drow_slot.size() / std::max<uint64_t>(n_meas, 1));
-    d.cta_threads = static_cast<uint32_t>(env_long("SP_CTA_THREADS", 512));
+    d.cta_threads = static_cast<uint32_t>(env_long("SP_CTA_THREADS", kFusedThreads));
     const long n_warps = d.cta_threads / 32;
-    long gw = std::lround(n_warps * 0.75 * gen / std::max(gen + drain, 1.0) / 0.75);
+    // measured on B200: the drain's latency chains want ~15% more warps than
+    // its instruction share (cfg2 and cfg3 both peak at 10 of 16)
+    long gw = std::lround(n_warps * 0.85 * gen / std::max(gen + drain, 1.0));
     gw = std::min<long>(gw, n_warps - std::max<long>(1, n_warps / 4));
     gw = env_long("SP_GEN_WARPS", gw);
     d.gen_warps = static_cast<uint32_t>(std::min<long>(std::max<long>(gw, 1), n_warps - 1));
@@ -599,6 +603,7 @@ void build_plan(sp_ctx* c) {
   }
   d.n_live_groups = static_cast<uint32_t>(live_groups.size());
   d.live_groups = c->b_live_groups.upload(live_groups, s);
+  d.debug_mode = static_cast<uint32_t>(env_long("SP_DEBUG_MODE", 0));
   if (env_long("SP_PHASE_TIMERS", 0)) {
     std::vector<long long> z(4, 0);
     d.timers = c->b_timers.upload(z, s);
@@ -874,6 +879,51 @@ int sp_sample(sp_ctx* ctx, uint64_t seed, uint64_t shot_begin, uint64_t n_shots,
   return launched(ctx, r, "fused sampler launch");
 }
 
+uint64_t sp_tiled_words(sp_ctx* ctx, uint64_t n_shots) {
+  if (!ctx || set_device(ctx) || ensure_plan(ctx)) return 0;
+  const uint64_t T = 1ull << ctx->dp.t_log2;
+  return (n_shots + T - 1) / T * ctx->hp.n_meas * (T / 64);
+}
+
+int sp_sample_tiled(sp_ctx* ctx, uint64_t seed, uint64_t shot_begin, uint64_t n_shots,
+                    uint64_t* d_out, uint64_t* d_counts) {
+  if (!ctx) return fail(SP_ERR_INVALID_ARGUMENT, "null ctx");
+  if (n_shots == 0) return fail(SP_ERR_INVALID_ARGUMENT, "need at least one shot");
+  if (int r = set_device(ctx)) return r;
+  if (int r = ensure_plan(ctx)) return r;
+  if (!ctx->fused_ok) return fail(SP_ERR_UNSUPPORTED, ctx->fused_why);
+  if (ctx->rng != SP_RNG_PHILOX)
+    return fail(SP_ERR_UNSUPPORTED, "tiled output is produced by the Philox sampler only");
+  const uint64_t T = 1ull << ctx->dp.t_log2;
+  if (shot_begin % T) return fail(SP_ERR_INVALID_ARGUMENT, "shot_begin must be a multiple of the shot tile");
+  if (ctx->hp.n_meas == 0) return SP_OK;
+  if (!d_out) return fail(SP_ERR_INVALID_ARGUMENT, "null output");
+  int r = launch_fused_sample(ctx->dp, ctx->L, seed, shot_begin / T, n_shots, d_out, 0, d_counts,
+                              true);
+  return launched(ctx, r, "fused sampler launch");
+}
+
+int sp_untile(sp_ctx* ctx, const uint64_t* d_tiled, uint64_t n_shots, uint64_t* d_out,
+              uint64_t ld) {
+  if (!ctx || !d_tiled || !d_out) return fail(SP_ERR_INVALID_ARGUMENT, "null argument");
+  if (int r = set_device(ctx)) return r;
+  if (int r = ensure_plan(ctx)) return r;
+  if (ld < (n_shots + 63) / 64) return fail(SP_ERR_INVALID_ARGUMENT, "ld too small");
+  int r = launch_untile(ctx->L, d_tiled, ctx->hp.n_meas, 1u << ctx->dp.t_log2, n_shots, d_out, ld);
+  return launched(ctx, r, "untile launch");
+}
+
+int sp_encode_tiled(sp_ctx* ctx, const uint64_t* d_tiled, uint64_t n_shots, sp_format fmt,
+                    uint8_t* d_bytes) {
+  if (!ctx) return fail(SP_ERR_INVALID_ARGUMENT, "null ctx");
+  if (fmt != SP_FMT_01 && fmt != SP_FMT_B8) return fail(SP_ERR_INVALID_ARGUMENT, "unknown format");
+  if (int r = set_device(ctx)) return r;
+  if (int r = ensure_plan(ctx)) return r;
+  int r = launch_encode(ctx->L, d_tiled, 0, ctx->hp.n_meas, n_shots, fmt, d_bytes,
+                        1u << ctx->dp.t_log2);
+  return launched(ctx, r, "encode launch");
+}
+
 int sp_draw_assignments(sp_ctx* ctx, uint64_t seed, uint64_t shot_begin, uint64_t n_shots,
                         uint64_t* d_S, uint64_t ldS) {
   if (!ctx) return fail(SP_ERR_INVALID_ARGUMENT, "null ctx");
@@ -958,12 +1008,15 @@ int sp_sample_to_host(sp_ctx* ctx, uint64_t seed, uint64_t shot_begin, uint64_t 
     uint64_t off = 0;
     for (uint64_t done = 0; done < n_shots; done += chunk) {
       const uint64_t n = std::min(chunk, n_shots - done);
-      if (n_meas) {
-        int r = sp_sample(ctx, seed, shot_begin + done, n, d_m, ld, nullptr);
-        if (r) return r;
+      int r = SP_OK;
+      if (ctx->rng == SP_RNG_PHILOX && n_meas) {
+        // tiled records: coalesced stores for any row count
+        if ((r = sp_sample_tiled(ctx, seed, shot_begin + done, n, d_m, nullptr))) return r;
+        if ((r = sp_encode_tiled(ctx, d_m, n, fmt, d_b))) return r;
+      } else {
+        if (n_meas && (r = sp_sample(ctx, seed, shot_begin + done, n, d_m, ld, nullptr))) return r;
+        if ((r = sp_encode(ctx, d_m, ld, n_meas, n, fmt, d_b))) return r;
       }
-      int r = sp_encode(ctx, d_m, ld, n_meas, n, fmt, d_b);
-      if (r) return r;
       const uint64_t nb = sp_encoded_size(n_meas, n, fmt);
       if (nb) ck(cudaMemcpyAsync(h_out + off, d_b, nb, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
       off += nb;
@@ -983,6 +1036,22 @@ int sp_synchronize(sp_ctx* ctx) {
   if (int r = set_device(ctx)) return r;
   cudaError_t e = cudaStreamSynchronize(ctx->stream);
   if (e != cudaSuccess) return fail(SP_ERR_CUDA, std::string("sync: ") + cudaGetErrorString(e));
+  return SP_OK;
+}
+
+// Launch shape and table sizes of the fused sampler's plan (for reports):
+// {T, gen_warps, cta_threads, staged, row_staged, lp, pad_pred, n_paths,
+//  n_rounds, n_keep, n_seg_live, n_cls_live, n_dense_live, nnz(D), smem bytes, fused_ok}
+int sp_plan_info(sp_ctx* ctx, uint64_t* out16) {
+  if (!ctx || !out16) return fail(SP_ERR_INVALID_ARGUMENT, "null argument");
+  if (int r = set_device(ctx)) return r;
+  if (int r = ensure_plan(ctx)) return r;
+  const DevPlan& d = ctx->dp;
+  const uint64_t v[16] = {1ull << d.t_log2, d.gen_warps, d.cta_threads, d.staged, d.row_staged,
+                          d.lp, d.pad_pred, d.n_paths, d.n_rounds, d.n_keep, d.n_seg_live,
+                          d.n_cls_live, d.n_dense_live, ctx->dnnz,
+                          fused_smem_bytes(d, d.t_log2, d.staged, d.row_staged), ctx->fused_ok};
+  std::memcpy(out16, v, sizeof(v));
   return SP_OK;
 }
 

@@ -35,6 +35,7 @@ RoundKeys expand_keys(uint64_t seed) {
 namespace {
 
 constexpr unsigned kFull = 0xFFFFFFFFu;
+
 // Named barriers of the fused kernel (0 is __syncthreads).
 constexpr uint32_t kBarFull0 = 1, kBarEmpty0 = 3, kBarDrain = 5;
 
@@ -270,8 +271,8 @@ __device__ __forceinline__ uint4 xor4(uint4 a, uint4 b) {
 template <bool kStaged, bool kRowStaged, int kLp, bool kPadPred>
 __global__ void __launch_bounds__(kFusedThreads, 1)
 k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, uint64_t n_shots,
-         uint64_t* __restrict__ out, uint64_t ld, unsigned long long* __restrict__ counts,
-         bool vec) {
+         uint64_t* __restrict__ out, uint64_t ld, uint64_t tile_stride,
+         unsigned long long* __restrict__ counts, bool vec) {
   extern __shared__ __align__(16) uint8_t smem[];
   const uint32_t tw = P.tw, tw4_log2 = P.t_log2 - 7, tw4 = 1u << tw4_log2;
   // One spare row absorbs the XORs of padded flip-list entries (never read).
@@ -390,6 +391,10 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
       Segment sg;
       auto emit = [&](auto bern_tag, const Fired& f) {
         constexpr bool kB = decltype(bern_tag)::value;
+        if (P.debug_mode & 1u) {
+          if (f.v == 0xFFFFFFFFu) tile[0] = f.g[0] ^ f.shot[1] ^ f.pat[2];  // keep the walk alive
+          return;
+        }
         if constexpr (kLp > 0) {
           // Exact flip list of (group, pattern), padded to kLp u16 rows with
           // 0xFFFF; one or two 16-byte loads, then predicated shared atomics.
@@ -456,7 +461,7 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
       for (;;) {
         if (lane == 0) seg = atomicAdd(&segctr[b], 1u);
         seg = __shfl_sync(kFull, seg, 0);
-        if (seg >= P.n_seg_live) break;
+        if (seg >= P.n_seg_live || (P.debug_mode & 2u)) break;
         segment_init(sg, CLS, P.n_cls_live, seg);
         segment_walk(sg, K, gtile, P.t_log2, lane, emit);
       }
@@ -483,11 +488,12 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
       const uint64_t valid = min(static_cast<uint64_t>(1) << P.t_log2, n_shots - first);
       const uint32_t vq = static_cast<uint32_t>((valid + 127) >> 7);
       const uint32_t rem = static_cast<uint32_t>(valid & 127);
+      const bool fast = vec && !with_counts && (valid == (static_cast<uint64_t>(1) << P.t_log2));
       // Rows along parent paths (heavy-path decomposition of the L forest):
       // one thread walks a path top-down for one 128-shot column, carrying
       // the running row value; a path's head waits only for its parent's
       // path, which ran in an earlier round.
-      for (uint32_t rd = 0; rd < P.n_rounds; ++rd) {
+      for (uint32_t rd = 0; rd < ((P.debug_mode & 8u) ? 0u : P.n_rounds); ++rd) {
         const uint32_t p0 = P.round_ptr[rd], p1 = P.round_ptr[rd + 1];
         const uint32_t tasks = (p1 - p0) << tw4_log2;
         const uint32_t tasks_rounded = (tasks + 31) & ~31u;
@@ -501,55 +507,70 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
           uint32_t sl = act ? PSLP[pth] : 0;
           const uint32_t xe = act ? PPTR[pth + 1] : 0;
           uint32_t x = act ? PPTR[pth] : 0;
-          uint32_t e = x < xe ? PROWS[x] : 0u;
-          uint4 cur = x < xe ? t4[((e & 0xFFFFu) << tw4_log2) + q] : make_uint4(0, 0, 0, 0);
-          for (; x < xe; ++x) {
-            // e = row | n_slots << 16 | keep << 31; prefetch the next row's word
-            const bool has_next = x + 1 < xe;
-            const uint32_t en = has_next ? PROWS[x + 1] : 0u;
-            const uint4 nxt = has_next ? t4[((en & 0xFFFFu) << tw4_log2) + q] : make_uint4(0, 0, 0, 0);
-            const uint32_t k = e & 0xFFFFu;
-            const uint32_t ti = (k << tw4_log2) + q;
-            uint4 v = xor4(cur, prev);
-            for (const uint32_t se = sl + ((e >> 16) & 0x7FFFu); sl < se; ++sl)
-              v = xor4(v, c4[(static_cast<uint32_t>(PSL[sl]) << tw4_log2) + q]);
-            // Rows with light children keep their final value for a later
-            // round; all others are cleared for tile i+2 right away.
-            t4[ti] = (e >> 31) ? v : make_uint4(0, 0, 0, 0);
-            prev = v;
-            e = en;
-            cur = nxt;
-            uint32_t pc = 0;
-            if (q < vq) {
-              bool two = true;  // whether the item's second u64 word is inside the tile
-              if (q == vq - 1 && rem) {
-                const uint32_t m[4] = {rem >= 32 ? kFull : (1u << rem) - 1,
-                                       rem >= 64 ? kFull : rem > 32 ? (1u << (rem - 32)) - 1 : 0u,
-                                       rem >= 96 ? kFull : rem > 64 ? (1u << (rem - 64)) - 1 : 0u,
-                                       rem > 96 ? (1u << (rem - 96)) - 1 : 0u};
-                v.x &= m[0]; v.y &= m[1]; v.z &= m[2]; v.w &= m[3];
-                two = rem > 64;
-              }
-              uint64_t* o = out + static_cast<uint64_t>(k) * ld + (first >> 6) + 2 * q;
-              const uint64_t w0 = (static_cast<uint64_t>(v.y) << 32) | v.x;
-              const uint64_t w1 = (static_cast<uint64_t>(v.w) << 32) | v.z;
-              if (vec && two) {
-                *reinterpret_cast<ulonglong2*>(o) = make_ulonglong2(w0, w1);
+          uint64_t* obase = out + t_local * tile_stride + 2 * q;
+          // Walks the path: rebuild row (tile ^ dense terms ^ parent), keep or
+          // clear the tile word, store 16 bytes to HBM, optionally count.
+          auto walk = [&](auto fast_tag) {
+            constexpr bool kFast = decltype(fast_tag)::value;  // full tile, aligned, no counts
+            uint32_t e = x < xe ? PROWS[x] : 0u;
+            uint4 cur = x < xe ? t4[((e & 0xFFFFu) << tw4_log2) + q] : make_uint4(0, 0, 0, 0);
+            for (; x < xe; ++x) {
+              // e = row | n_slots << 16 | keep << 31; prefetch the next row's word
+              const bool has_next = x + 1 < xe;
+              const uint32_t en = has_next ? PROWS[x + 1] : 0u;
+              const uint4 nxt =
+                  has_next ? t4[((en & 0xFFFFu) << tw4_log2) + q] : make_uint4(0, 0, 0, 0);
+              const uint32_t k = e & 0xFFFFu;
+              uint4 v = xor4(cur, prev);
+              for (const uint32_t se = sl + ((e >> 16) & 0x7FFFu); sl < se; ++sl)
+                v = xor4(v, c4[(static_cast<uint32_t>(PSL[sl]) << tw4_log2) + q]);
+              // Rows with light children keep their final value for a later
+              // round; all others are cleared for tile i+2 right away.
+              t4[(k << tw4_log2) + q] = (e >> 31) ? v : make_uint4(0, 0, 0, 0);
+              prev = v;
+              e = en;
+              cur = nxt;
+              uint64_t* o = obase + static_cast<uint64_t>(k) * ld;
+              if constexpr (kFast) {
+                *reinterpret_cast<uint4*>(o) = v;
               } else {
-                o[0] = w0;
-                if (two) o[1] = w1;
+                uint32_t pc = 0;
+                if (q < vq) {
+                  bool two = true;  // whether the item's second u64 word is inside the tile
+                  if (q == vq - 1 && rem) {
+                    const uint32_t m[4] = {
+                        rem >= 32 ? kFull : (1u << rem) - 1,
+                        rem >= 64 ? kFull : rem > 32 ? (1u << (rem - 32)) - 1 : 0u,
+                        rem >= 96 ? kFull : rem > 64 ? (1u << (rem - 64)) - 1 : 0u,
+                        rem > 96 ? (1u << (rem - 96)) - 1 : 0u};
+                    v.x &= m[0]; v.y &= m[1]; v.z &= m[2]; v.w &= m[3];
+                    two = rem > 64;
+                  }
+                  const uint64_t w0 = (static_cast<uint64_t>(v.y) << 32) | v.x;
+                  const uint64_t w1 = (static_cast<uint64_t>(v.w) << 32) | v.z;
+                  if (vec && two) {
+                    *reinterpret_cast<ulonglong2*>(o) = make_ulonglong2(w0, w1);
+                  } else {
+                    o[0] = w0;
+                    if (two) o[1] = w1;
+                  }
+                  if (with_counts) pc = __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
+                }
+                if (with_counts) {
+                  if (tw4 >= 32) {  // the whole warp walks this path: one atomic per row
+                    pc = __reduce_add_sync(kFull, pc);
+                    if (lane == 0 && pc) atomicAdd(&cnt[k], pc);
+                  } else if (pc) {
+                    atomicAdd(&cnt[k], pc);
+                  }
+                }
               }
-              if (with_counts) pc = __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
             }
-            if (with_counts) {
-              if (tw4 >= 32) {  // the whole warp walks this path: one atomic per row
-                pc = __reduce_add_sync(kFull, pc);
-                if (lane == 0 && pc) atomicAdd(&cnt[k], pc);
-              } else if (pc) {
-                atomicAdd(&cnt[k], pc);
-              }
-            }
-          }
+          };
+          if (fast)
+            walk(std::true_type{});
+          else
+            walk(std::false_type{});
         }
         // A later round must not start before every row a light child
         // reads is final.
@@ -789,8 +810,18 @@ __device__ __forceinline__ uint32_t transpose32(uint32_t x) {
 // b8: ceil(n_m/8) bytes per shot, measurement k at bit k%8 of byte k/8.
 // Each warp turns one 32-shot column into 32 records, staged in shared
 // memory so the global write of the block's records is contiguous.
+// Word (row k, 32-shot column c) of a measurement-major (tw32 == 0) or
+// tiled (tw32 = T/32) record array.
+__device__ __forceinline__ uint64_t rec_word(uint32_t k, uint64_t c, uint64_t ld32,
+                                             uint32_t n_meas, uint32_t tw32) {
+  if (tw32 == 0) return k * ld32 + c;
+  return (c / tw32) * (static_cast<uint64_t>(n_meas) * tw32) + static_cast<uint64_t>(k) * tw32 +
+         (c % tw32);
+}
+
 __global__ void k3_b8(const uint32_t* __restrict__ m32, uint64_t ld32, uint32_t n_meas,
-                      uint64_t n_shots, uint32_t rec, uint8_t* __restrict__ out, bool staged) {
+                      uint64_t n_shots, uint32_t rec, uint8_t* __restrict__ out, bool staged,
+                      uint32_t tw32) {
   extern __shared__ __align__(16) uint8_t stage[];
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const uint64_t n_words32 = (n_shots + 31) >> 5;
@@ -800,7 +831,7 @@ __global__ void k3_b8(const uint32_t* __restrict__ m32, uint64_t ld32, uint32_t 
   const uint64_t my_shot = shot0 + warp * 32 + lane;
   for (uint32_t kw = 0; kw < kwords; ++kw) {
     const uint32_t k = kw * 32 + lane;
-    uint32_t x = (k < n_meas && col < n_words32) ? m32[k * ld32 + col] : 0u;
+    uint32_t x = (k < n_meas && col < n_words32) ? m32[rec_word(k, col, ld32, n_meas, tw32)] : 0u;
     x = transpose32(x);
     uint8_t* dst = staged ? stage + static_cast<uint64_t>(warp * 32 + lane) * rec
                           : out + my_shot * rec;
@@ -819,7 +850,7 @@ __global__ void k3_b8(const uint32_t* __restrict__ m32, uint64_t ld32, uint32_t 
 
 // '01': one line per shot, '0'/'1' per measurement then '\n'.
 __global__ void k3_01(const uint32_t* __restrict__ m32, uint64_t ld32, uint32_t n_meas,
-                      uint64_t n_shots, uint8_t* __restrict__ out) {
+                      uint64_t n_shots, uint8_t* __restrict__ out, uint32_t tw32) {
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const uint64_t n_words32 = (n_shots + 31) >> 5;
   const uint64_t col = static_cast<uint64_t>(blockIdx.x) * nw + warp;
@@ -829,7 +860,7 @@ __global__ void k3_01(const uint32_t* __restrict__ m32, uint64_t ld32, uint32_t 
   const uint32_t kwords = (n_meas + 31) >> 5;
   for (uint32_t kw = 0; kw < kwords; ++kw) {
     const uint32_t k = kw * 32 + lane;
-    uint32_t x = k < n_meas ? m32[k * ld32 + col] : 0u;
+    uint32_t x = k < n_meas ? m32[rec_word(k, col, ld32, n_meas, tw32)] : 0u;
     x = transpose32(x);
     if (shot < n_shots) {
       uint8_t* dst = out + shot * line + kw * 32;
@@ -838,6 +869,20 @@ __global__ void k3_01(const uint32_t* __restrict__ m32, uint64_t ld32, uint32_t 
     }
   }
   if (shot < n_shots) out[shot * line + n_meas] = '\n';
+}
+
+// Tiled [tile][row][T/64] -> measurement-major [row][ld]; one thread per u64.
+__global__ void k_untile(const uint64_t* __restrict__ in, uint32_t n_meas, uint32_t tw2,
+                         uint64_t n_words, uint64_t total, uint64_t* __restrict__ out,
+                         uint64_t ld) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t t = i / (static_cast<uint64_t>(n_meas) * tw2);
+    const uint64_t r = i - t * n_meas * tw2;
+    const uint64_t k = r / tw2, w = r - k * tw2;
+    const uint64_t col = t * tw2 + w;
+    if (col < n_words) out[k * ld + col] = in[i];
+  }
 }
 
 __global__ void k_debug_philox(const uint32_t* in, uint32_t* out) {
@@ -880,7 +925,7 @@ int persistent_grid(Kern kernel, const LaunchCfg& L, size_t smem, uint32_t n_til
 
 template <bool kStaged, bool kRowStaged, int kLp, bool kPadPred = false>
 int launch_k1(const DevPlan& P, const LaunchCfg& L, const RoundKeys& K, uint64_t tile0,
-              uint32_t n_tiles, uint64_t n_shots, uint64_t* out, uint64_t ld,
+              uint32_t n_tiles, uint64_t n_shots, uint64_t* out, uint64_t ld, uint64_t tstride,
               unsigned long long* cnt) {
   auto kern = k1_fused<kStaged, kRowStaged, kLp, kPadPred>;
   const size_t smem = fused_smem_bytes(P, P.t_log2, kStaged, kRowStaged);
@@ -888,7 +933,8 @@ int launch_k1(const DevPlan& P, const LaunchCfg& L, const RoundKeys& K, uint64_t
   const int threads = static_cast<int>(P.cta_threads);
   if (persistent_grid(kern, L, smem, n_tiles, P.cta_per_sm, &grid, threads)) return -1;
   const bool vec = (ld % 2 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0);
-  kern<<<grid, threads, smem, L.stream>>>(P, K, tile0, n_tiles, n_shots, out, ld, cnt, vec);
+  kern<<<grid, threads, smem, L.stream>>>(P, K, tile0, n_tiles, n_shots, out, ld, tstride, cnt,
+                                          vec);
   return check_launch() ? -1 : 1;
 }
 
@@ -915,14 +961,18 @@ size_t fused_smem_bytes(const DevPlan& P, uint32_t t_log2, bool staged, bool row
 }
 
 int launch_fused_sample(const DevPlan& P, const LaunchCfg& L, uint64_t seed, uint64_t tile0,
-                        uint64_t n_shots, uint64_t* out, uint64_t ld, uint64_t* counts) {
+                        uint64_t n_shots, uint64_t* out, uint64_t ld, uint64_t* counts,
+                        bool tiled) {
   const uint64_t T = 1ull << P.t_log2;
+  const uint64_t tstride = tiled ? static_cast<uint64_t>(P.n_meas) * (T / 64) : T / 64;
+  if (tiled) ld = T / 64;
   const uint32_t n_tiles = static_cast<uint32_t>((n_shots + T - 1) / T);
   const RoundKeys K = expand_keys(seed);
   auto* cnt = reinterpret_cast<unsigned long long*>(counts);
-#define SP_K1(st, rs, lp) launch_k1<st, rs, lp>(P, L, K, tile0, n_tiles, n_shots, out, ld, cnt)
+#define SP_K1(st, rs, lp) \
+  launch_k1<st, rs, lp>(P, L, K, tile0, n_tiles, n_shots, out, ld, tstride, cnt)
 #define SP_K1P(st, rs, lp) \
-  launch_k1<st, rs, lp, true>(P, L, K, tile0, n_tiles, n_shots, out, ld, cnt)
+  launch_k1<st, rs, lp, true>(P, L, K, tile0, n_tiles, n_shots, out, ld, tstride, cnt)
   if (P.lp == 8 && P.pad_pred) return P.row_staged ? SP_K1P(false, true, 8) : SP_K1P(false, false, 8);
   if (P.lp == 16 && P.pad_pred)
     return P.row_staged ? SP_K1P(false, true, 16) : SP_K1P(false, false, 16);
@@ -1017,7 +1067,8 @@ int launch_product(const DevPlan& P, const LaunchCfg& L, bool dense, const uint6
 }
 
 int launch_encode(const LaunchCfg& L, const uint64_t* m, uint64_t ld, uint64_t n_meas,
-                  uint64_t n_shots, int fmt, uint8_t* bytes) {
+                  uint64_t n_shots, int fmt, uint8_t* bytes, uint32_t tile_shots) {
+  const uint32_t tw32 = tile_shots / 32;
   if (n_shots == 0 || n_meas == 0) {
     if (fmt == 0 && n_shots) {  // n_meas == 0: one empty line per shot
       if (cudaMemsetAsync(bytes, '\n', n_shots, L.stream) != cudaSuccess) return -1;
@@ -1030,7 +1081,7 @@ int launch_encode(const LaunchCfg& L, const uint64_t* m, uint64_t ld, uint64_t n
     const uint64_t blocks = (n_words32 + 7) / 8;
     k3_01<<<static_cast<unsigned>(blocks), 256, 0, L.stream>>>(m32, 2 * ld,
                                                                static_cast<uint32_t>(n_meas),
-                                                               n_shots, bytes);
+                                                               n_shots, bytes, tw32);
   } else {
     const uint32_t rec = static_cast<uint32_t>((n_meas + 7) / 8);
     const size_t budget = 96 * 1024;
@@ -1043,8 +1094,20 @@ int launch_encode(const LaunchCfg& L, const uint64_t* m, uint64_t ld, uint64_t n
       return -1;
     const uint64_t blocks = (n_words32 + warps - 1) / warps;
     k3_b8<<<static_cast<unsigned>(blocks), warps * 32, smem, L.stream>>>(
-        m32, 2 * ld, static_cast<uint32_t>(n_meas), n_shots, rec, bytes, staged);
+        m32, 2 * ld, static_cast<uint32_t>(n_meas), n_shots, rec, bytes, staged, tw32);
   }
+  return check_launch() ? -1 : 1;
+}
+
+int launch_untile(const LaunchCfg& L, const uint64_t* in, uint64_t n_meas, uint32_t tile_shots,
+                  uint64_t n_shots, uint64_t* out, uint64_t ld) {
+  const uint64_t n_words = (n_shots + 63) / 64;
+  if (!n_meas || !n_words) return 0;
+  const uint64_t tiles = (n_shots + tile_shots - 1) / tile_shots;
+  const uint64_t total = n_meas * tiles * (tile_shots / 64);
+  const unsigned blocks = static_cast<unsigned>(std::min<uint64_t>((total + 255) / 256, 1u << 20));
+  k_untile<<<blocks, 256, 0, L.stream>>>(in, static_cast<uint32_t>(n_meas), tile_shots / 64,
+                                        n_words, total, out, ld);
   return check_launch() ? -1 : 1;
 }
 

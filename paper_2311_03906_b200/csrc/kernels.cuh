@@ -104,6 +104,10 @@ struct DevPlan {
   uint32_t gen_warps = 12;   // event-generator warps; the rest drain tiles
   uint32_t cta_per_sm = 1;
   uint32_t cta_threads = 512;
+  // Profiling switches (SP_DEBUG_MODE): bit 0 skips the firing XORs, bit 1
+  // skips the segment walks, bit 2 skips the HBM stores, bit 3 skips the row
+  // rebuild. Results are wrong when set.
+  uint32_t debug_mode = 0;
   // Optional per-role cycle counters (SP_PHASE_TIMERS=1): gen wait/work,
   // drain wait/work, summed over warps and tiles (u64[4], device).
   long long* timers = nullptr;
@@ -126,6 +130,8 @@ struct LaunchCfg {
   size_t smem_optin = 227 * 1024;
 };
 
+// 16 warps per CTA, one CTA per SM (a 32-warp variant with 64 registers per
+// thread measured slower on both cfg2 and cfg3).
 constexpr int kFusedThreads = 512;
 
 // Shared-memory bytes of the fused kernel for a plan shape.
@@ -133,7 +139,8 @@ size_t fused_smem_bytes(const DevPlan& P, uint32_t t_log2, bool staged, bool row
 
 // K1 fused sampler (Philox). Returns number of launches issued, <0 on error.
 int launch_fused_sample(const DevPlan& P, const LaunchCfg& L, uint64_t seed, uint64_t tile0,
-                        uint64_t n_shots, uint64_t* out, uint64_t ld, uint64_t* counts);
+                        uint64_t n_shots, uint64_t* out, uint64_t ld, uint64_t* counts,
+                        bool tiled = false);
 // K4 fused sampler, compat RNG (bit-exact keyed_draw / fill_group).
 int launch_fused_sample_compat(const DevPlan& P, const LaunchCfg& L, uint64_t seed,
                                uint64_t tile0, uint64_t n_shots, uint64_t* out, uint64_t ld,
@@ -145,8 +152,12 @@ int launch_draw(const DevPlan& P, const LaunchCfg& L, bool compat, uint64_t seed
 int launch_product(const DevPlan& P, const LaunchCfg& L, bool dense, const uint64_t* S,
                    uint64_t ldS, uint64_t n_shots, uint64_t* out, uint64_t ld);
 // K3 encode (fmt 0 = '01', 1 = 'b8').
+// tile_shots == 0: measurement-major input; else tiled blocks of tile_shots.
 int launch_encode(const LaunchCfg& L, const uint64_t* m, uint64_t ld, uint64_t n_meas,
-                  uint64_t n_shots, int fmt, uint8_t* bytes);
+                  uint64_t n_shots, int fmt, uint8_t* bytes, uint32_t tile_shots = 0);
+// Tiled records -> measurement-major.
+int launch_untile(const LaunchCfg& L, const uint64_t* in, uint64_t n_meas, uint32_t tile_shots,
+                  uint64_t n_shots, uint64_t* out, uint64_t ld);
 // Known-answer hook for the Philox4x32-10 implementation.
 int launch_debug_philox(const LaunchCfg& L, const uint32_t* ctr_key_dev, uint32_t* out_dev);
 

@@ -187,6 +187,16 @@ class Sampler:
         N.check(self._L.sp_shot_tile(self._h, C.byref(t)))
         return t.value
 
+    PLAN_FIELDS = ("shot_tile", "gen_warps", "cta_threads", "staged", "row_staged", "lp",
+                   "pad_pred", "n_paths", "n_rounds", "n_keep", "n_segments", "n_classes",
+                   "n_dense", "nnz_d", "smem_bytes", "fused_ok")
+
+    def plan_info(self) -> dict:
+        """Launch shape / table sizes the planner chose for the fused sampler."""
+        buf = (C.c_uint64 * 16)()
+        N.check(self._L.sp_plan_info(self._h, C.cast(buf, C.c_void_p)))
+        return dict(zip(self.PLAN_FIELDS, (int(x) for x in buf)))
+
     @property
     def launches(self) -> int:
         return int(self._L.sp_launch_count(self._h))
@@ -208,6 +218,31 @@ class Sampler:
                                   out.shape[1] if out.dim() == 2 else words(n_shots),
                                   _ptr(counts)))
         return out
+
+    def sample_tiled(self, n_shots: int, seed: int, shot_begin: int = 0, out=None, counts=None):
+        """Fused sampler with tiled records: blocks [n_meas][T/64] per T shots."""
+        if out is None:
+            nw = int(self._L.sp_tiled_words(self._h, n_shots))
+            out = self._torch.empty(max(nw, 1), dtype=self._torch.int64,
+                                    device=f"cuda:{self.device}")
+        N.check(self._L.sp_sample_tiled(self._h, seed, shot_begin, n_shots, _ptr(out),
+                                        _ptr(counts)))
+        return out
+
+    def untile(self, tiled, n_shots: int, out=None):
+        """Tiled records -> measurement-major words [n_meas, ceil(n/64)]."""
+        if out is None:
+            out = self.empty_bits(self.n_meas, n_shots)
+        N.check(self._L.sp_untile(self._h, _ptr(tiled), n_shots, _ptr(out), out.shape[1]))
+        return out
+
+    def encode_tiled(self, tiled, n_shots: int, fmt: str = "b8", out=None):
+        size = self.encoded_size(n_shots, fmt)
+        if out is None:
+            out = self._torch.empty(max(size, 1), dtype=self._torch.uint8,
+                                    device=f"cuda:{self.device}")
+        N.check(self._L.sp_encode_tiled(self._h, _ptr(tiled), n_shots, FORMATS[fmt], _ptr(out)))
+        return out[:size]
 
     def draw_assignments(self, n_shots: int, seed: int, shot_begin: int = 0, out=None):
         """draw_assignments: the symbol assignment matrix S (row 0 = ones)."""

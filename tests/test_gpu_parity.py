@@ -205,3 +205,22 @@ def test_bench_configs_parity_small(gpu_sampler_factory):
     want = Port().sample(init.row_ptr, init.sym_idx, host(S), n)
     assert np.array_equal(host(s.sample(n, 42)), want)
     torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("cfg", ["rep", "surf5", "surf9"])
+def test_tiled_layout_equals_measurement_major(gpu_sampler_factory, cfg):
+    import torch
+    text = {"rep": CI.repetition_code(5, 5, 0.01), "surf5": CI.surface_code(5, 5, 1e-3),
+            "surf9": CI.surface_code(9, 9, 1e-3)}[cfg]
+    init = run_initialization(text)
+    s = gpu_sampler_factory(init)
+    T = s.shot_tile
+    for n in (1, T + 77, 5 * T):
+        c1 = torch.zeros(init.n_meas, dtype=torch.int64, device="cuda")
+        c2 = torch.zeros(init.n_meas, dtype=torch.int64, device="cuda")
+        mm = s.sample(n, 17, counts=c1)
+        tl = s.sample_tiled(n, 17, counts=c2)
+        assert torch.equal(s.untile(tl, n), mm)
+        assert torch.equal(c1, c2)
+        for fmt in ("b8", "01"):
+            assert torch.equal(s.encode_tiled(tl, n, fmt), s.encode(mm, n, fmt))

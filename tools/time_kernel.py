@@ -19,23 +19,27 @@ def main():
     ap.add_argument("--shots", type=int, default=0)
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--counts", action="store_true")
+    ap.add_argument("--tiled", action="store_true", help="tiled record layout")
     a = ap.parse_args()
     init = run_initialization(circuits.CONFIGS[a.config]["text"]())
     n = a.shots or circuits.CONFIGS[a.config]["shots"]
     s = Sampler(init)
     T = s.shot_tile
     n = (n + T - 1) // T * T
-    out = s.empty_bits(init.n_meas, n)
+    out = (torch.empty(int(s._L.sp_tiled_words(s._h, n)), dtype=torch.int64, device="cuda")
+           if a.tiled else s.empty_bits(init.n_meas, n))
+    run = (lambda seed: s.sample_tiled(n, seed, out=out, counts=counts)) if a.tiled else \
+          (lambda seed: s.sample(n, seed, out=out, counts=counts))
     counts = torch.zeros(init.n_meas, dtype=torch.int64, device="cuda") if a.counts else None
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     for i in range(3):
-        s.sample(n, i, out=out, counts=counts)
+        run(i)
     ts = []
     for i in range(a.reps):
         flush.zero_()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        s.sample(n, 100 + i, out=out, counts=counts)
+        run(100 + i)
         e1.record()
         torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1))
@@ -49,9 +53,11 @@ def main():
     ms = ts[len(ts) // 2]
     bytes_ = init.n_meas * n / 8
     env = {k: v for k, v in os.environ.items() if k.startswith("SP_")}
-    print(json.dumps({"config": a.config, "shots": n, "T": T, "env": env, "ms_median": ms,
+    print(json.dumps({"config": a.config, "tiled": a.tiled, "shots": n, "T": T, "env": env,
+                      "ms_median": ms,
                       "ms_min": ts[0], "GBps": bytes_ / ms / 1e6,
-                      "bits_per_s": init.n_meas * n / ms * 1e3, "timers": timers}))
+                      "bits_per_s": init.n_meas * n / ms * 1e3, "timers": timers,
+                      "plan": s.plan_info()}))
 
 
 if __name__ == "__main__":
