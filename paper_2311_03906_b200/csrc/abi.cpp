@@ -96,8 +96,8 @@ struct sp_ctx {
   DevPlan dp;
   // plan buffers
   DBuf b_row_ptr, b_sym_idx, b_col_ptr, b_col_rows, b_dense, b_first, b_arity, b_dist, b_param,
-      b_row_const_compat, b_ones, b_dense_sym, b_drow_ptr, b_drow_slot, b_cls, b_cls_groups,
-      b_desc, b_colrow, b_live_groups, b_path_rows, b_path_ptr, b_path_par, b_round_ptr, b_plist, b_pslot_ptr, b_pslots, b_keep_rows, b_timers;
+      b_row_const_compat, b_ones, b_dense_sym, b_coin_ptr, b_coin_rows, b_cls, b_cls_groups,
+      b_desc, b_colrow, b_live_groups, b_path_rows, b_path_ptr, b_path_par, b_round_ptr, b_plist, b_keep_rows, b_timers;
   uint64_t dnnz = 0;  // nnz of D (chain transform), for reports
   // K2's own copy of the rows (independent of the group table)
   bool prod_ready = false;
@@ -314,22 +314,21 @@ void build_plan(sp_ctx* c) {
     cls[it->second].groups.push_back(static_cast<uint32_t>(g));
   }
 
-  // Dense slots (live first) and per-row slot lists; slot n_dense_live is the
-  // all-ones slot standing for the constant term.
+  // Dense slots (live first). The fused kernel XORs each live slot's coin
+  // words into its D column; the extra slot n_dense_live is the constant
+  // term (all-ones words into the rows of row_const).
   const uint64_t n_dense_live = dense_live.size();
-  if (n_dense_live + 1 >= 65535) throw std::invalid_argument("too many fair-coin symbols");
   std::vector<uint32_t> dense_sym = dense_live;
   dense_sym.insert(dense_sym.end(), dense_dead.begin(), dense_dead.end());
-  std::vector<uint32_t> slot_of(n_sym, UINT32_MAX);
-  for (uint32_t i = 0; i < n_dense_live; ++i) slot_of[dense_live[i]] = i;
-  std::vector<uint32_t> drow_ptr(n_meas + 1, 0);
-  std::vector<uint16_t> drow_slot;
-  for (uint64_t k = 0; k < n_meas; ++k) {
-    if ((row_const[k >> 5] >> (k & 31)) & 1u) drow_slot.push_back(static_cast<uint16_t>(n_dense_live));
-    for (uint64_t i = X.rp[k]; i < X.rp[k + 1]; ++i)
-      if (slot_of[X.si[i]] != UINT32_MAX) drow_slot.push_back(static_cast<uint16_t>(slot_of[X.si[i]]));
-    drow_ptr[k + 1] = static_cast<uint32_t>(drow_slot.size());
+  std::vector<uint32_t> coin_ptr{0};
+  std::vector<uint32_t> coin_rows_k;  // D rows; scaled by tw once T is known
+  for (uint32_t sym : dense_live) {
+    for (uint64_t i = dcol_ptr[sym]; i < dcol_ptr[sym + 1]; ++i) coin_rows_k.push_back(dcol_rows[i]);
+    coin_ptr.push_back(static_cast<uint32_t>(coin_rows_k.size()));
   }
+  for (uint64_t k = 0; k < n_meas; ++k)
+    if ((row_const[k >> 5] >> (k & 31)) & 1u) coin_rows_k.push_back(static_cast<uint32_t>(k));
+  coin_ptr.push_back(static_cast<uint32_t>(coin_rows_k.size()));
   uint64_t live_positions = 0, live_colrow = 0;
   for (const Cls& cl : live_cls)
     for (uint32_t g : cl.groups) {
@@ -344,7 +343,6 @@ void build_plan(sp_ctx* c) {
   d.n_groups = static_cast<uint32_t>(G);
   d.n_dense_live = static_cast<uint32_t>(n_dense_live);
   d.n_dense_all = static_cast<uint32_t>(dense_sym.size());
-  d.n_drow = static_cast<uint32_t>(drow_slot.size());
   d.n_cls_live = static_cast<uint32_t>(live_cls.size());
   d.n_desc_live = static_cast<uint32_t>(live_positions);
   d.n_colrow = live_colrow;
@@ -389,11 +387,13 @@ void build_plan(sp_ctx* c) {
     d.cta_per_sm = static_cast<uint32_t>(std::max<long>(
         1, std::min<long>(env_long("SP_CTAS", 2), static_cast<long>((228 * 1024) / (smem + 1024)))));
     const double ev = events_per_shot * T, flips = flips_per_shot * T;
-    // Generator warps also make the coin words; drain warps only rebuild and
-    // store rows (~40 instructions per 128-shot row word).
-    const double gen = ev * 60.0 + flips * 4.0 + n_dense_live * (T / 128.0) * 60.0;
+    // Generator warps also make the coin words and XOR them into their D
+    // columns; drain warps only rebuild and store rows (~20 instructions per
+    // 128-shot row word).
+    const double gen = ev * 60.0 + flips * 4.0 + n_dense_live * (T / 128.0) * 60.0 +
+                       coin_rows_k.size() * (T / 32.0) * 3.0;
     const double items = static_cast<double>(n_meas) * (T / 128);
-    const double drain = items * (40.0 + 3.0 * drow_slot.size() / std::max<uint64_t>(n_meas, 1));
+    const double drain = items * 20.0;
     d.cta_threads = static_cast<uint32_t>(env_long("SP_CTA_THREADS", kFusedThreads));
     const long n_warps = d.cta_threads / 32;
     // measured on B200: the drain's latency chains want ~15% more warps than
@@ -506,8 +506,13 @@ void build_plan(sp_ctx* c) {
   d.n_ones = static_cast<uint32_t>(ones.size());
   d.ones_syms = c->b_ones.upload(ones, s);
   d.dense_sym = c->b_dense_sym.upload(dense_sym, s);
-  d.drow_ptr = c->b_drow_ptr.upload(drow_ptr, s);
-  d.drow_slot = c->b_drow_slot.upload(drow_slot, s);
+  {
+    std::vector<uint16_t> coin_rows(coin_rows_k.size() + 1, 0);
+    for (size_t i = 0; i < coin_rows_k.size(); ++i)
+      coin_rows[i] = static_cast<uint16_t>(coin_rows_k[i] * d.tw);
+    d.coin_ptr = c->b_coin_ptr.upload(coin_ptr, s);
+    d.coin_rows = c->b_coin_rows.upload(coin_rows, s);
+  }
   d.n_cls_all = static_cast<uint32_t>(cls_info.size());
   d.n_seg_live = static_cast<uint32_t>(n_chains_live);
   d.n_seg_all = static_cast<uint32_t>(n_chains);
@@ -572,16 +577,12 @@ void build_plan(sp_ctx* c) {
       if (pa >= 0 && heavy[pa] != static_cast<int32_t>(k)) keep[pa] = 1;  // light child
     }
     std::vector<uint32_t> path_rows;
-    std::vector<uint32_t> path_ptr{0}, round_ptr(n_rounds + 1, 0), pslot_ptr;
-    std::vector<uint16_t> pslots, keep_rows;
+    std::vector<uint32_t> path_ptr{0}, round_ptr(n_rounds + 1, 0);
+    std::vector<uint16_t> keep_rows;
     std::vector<int32_t> path_par;
     for (uint32_t id : order) {
-      pslot_ptr.push_back(static_cast<uint32_t>(pslots.size()));
       for (uint16_t r : paths[id]) {
-        const uint32_t ns = drow_ptr[r + 1] - drow_ptr[r];
-        if (ns > 0x7FFF) throw std::invalid_argument("too many dense symbols in one row");
-        path_rows.push_back(r | (ns << 16) | (keep[r] ? 0x80000000u : 0u));
-        pslots.insert(pslots.end(), drow_slot.begin() + drow_ptr[r], drow_slot.begin() + drow_ptr[r + 1]);
+        path_rows.push_back(r | (keep[r] ? 0x80000000u : 0u));
         if (keep[r]) keep_rows.push_back(r);
       }
       path_ptr.push_back(static_cast<uint32_t>(path_rows.size()));
@@ -589,15 +590,13 @@ void build_plan(sp_ctx* c) {
       round_ptr[round_of_path[id] + 1]++;
     }
     for (uint32_t r = 0; r < n_rounds; ++r) round_ptr[r + 1] += round_ptr[r];
-    if (path_rows.empty()) path_rows.push_back(0);
+    path_rows.push_back(0);  // prefetch padding: the walk reads one entry past a path
     d.n_paths = static_cast<uint32_t>(paths.size());
     d.n_rounds = n_rounds;
     d.n_keep = static_cast<uint32_t>(keep_rows.size());
     d.path_rows = c->b_path_rows.upload(path_rows, s);
     d.path_ptr = c->b_path_ptr.upload(path_ptr, s);
     d.path_par = c->b_path_par.upload(path_par, s);
-    d.pslot_ptr = c->b_pslot_ptr.upload(pslot_ptr, s);
-    d.pslots = c->b_pslots.upload(pslots, s);
     d.keep_rows = c->b_keep_rows.upload(keep_rows, s);
     d.round_ptr = c->b_round_ptr.upload(round_ptr, s);
   }

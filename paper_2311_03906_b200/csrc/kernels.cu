@@ -247,6 +247,17 @@ __device__ __forceinline__ void named_arrive(uint32_t id, uint32_t n) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
+// 16-byte shared store of v (keep != 0) or of zeros, as two predicated
+// stores instead of four selects.
+__device__ __forceinline__ void sts_or_zero(uint32_t a, uint4 v, uint32_t keep) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %5, 0;\n\t"
+      "@p st.shared.v4.u32 [%0], {%1, %2, %3, %4};\n\t"
+      "@!p st.shared.v4.u32 [%0], {%6, %6, %6, %6};\n\t}" ::"r"(a),
+      "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "r"(keep), "r"(0u)
+      : "memory");
+}
+
 __device__ __forceinline__ uint4 xor4(uint4 a, uint4 b) {
   return make_uint4(a.x ^ b.x, a.y ^ b.y, a.z ^ b.z, a.w ^ b.w);
 }
@@ -277,11 +288,9 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
   const uint32_t tw = P.tw, tw4_log2 = P.t_log2 - 7, tw4 = 1u << tw4_log2;
   // One spare row absorbs the XORs of padded flip-list entries (never read).
   const uint32_t tile_words = (P.n_meas + 1) * tw;
-  const uint32_t n_slots = P.n_dense_live + 1;  // + the all-ones constant slot
   const bool with_counts = counts != nullptr;
   uint32_t* tiles = reinterpret_cast<uint32_t*>(smem);
-  uint32_t* coins = tiles + 2 * tile_words;
-  uint8_t* p = reinterpret_cast<uint8_t*>(coins + 2 * n_slots * tw);
+  uint8_t* p = reinterpret_cast<uint8_t*>(tiles + 2 * tile_words);
   uint32_t* cnt = reinterpret_cast<uint32_t*>(p);
   p += align16(4ull * P.n_meas);
   uint32_t* segctr = reinterpret_cast<uint32_t*>(p);  // per-buffer segment dispensers
@@ -294,35 +303,23 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
   const uint32_t* PROWS = P.path_rows;
   const uint32_t* PPTR = P.path_ptr;
   const int32_t* PPAR = P.path_par;
-  const uint32_t* PSLP = P.pslot_ptr;
-  const uint16_t* PSL = P.pslots;
   const uint16_t* KEEP = P.keep_rows;
   if (kRowStaged) {
     uint32_t* s_prows = reinterpret_cast<uint32_t*>(p);
-    p += align16(4ull * P.n_meas);
+    p += align16(4ull * (P.n_meas + 1));
     uint32_t* s_pptr = reinterpret_cast<uint32_t*>(p);
     p += align16(4ull * (P.n_paths + 1));
     int32_t* s_ppar = reinterpret_cast<int32_t*>(p);
     p += align16(4ull * P.n_paths);
-    uint32_t* s_pslp = reinterpret_cast<uint32_t*>(p);
-    p += align16(4ull * P.n_paths);
-    uint16_t* s_psl = reinterpret_cast<uint16_t*>(p);
-    p += align16(2ull * P.n_drow);
     uint16_t* s_keep = reinterpret_cast<uint16_t*>(p);
     p += align16(2ull * P.n_keep);
-    for (uint32_t i = threadIdx.x; i < P.n_meas; i += blockDim.x) s_prows[i] = P.path_rows[i];
+    for (uint32_t i = threadIdx.x; i <= P.n_meas; i += blockDim.x) s_prows[i] = P.path_rows[i];
     for (uint32_t i = threadIdx.x; i <= P.n_paths; i += blockDim.x) s_pptr[i] = P.path_ptr[i];
-    for (uint32_t i = threadIdx.x; i < P.n_paths; i += blockDim.x) {
-      s_ppar[i] = P.path_par[i];
-      s_pslp[i] = P.pslot_ptr[i];
-    }
-    for (uint32_t i = threadIdx.x; i < P.n_drow; i += blockDim.x) s_psl[i] = P.pslots[i];
+    for (uint32_t i = threadIdx.x; i < P.n_paths; i += blockDim.x) s_ppar[i] = P.path_par[i];
     for (uint32_t i = threadIdx.x; i < P.n_keep; i += blockDim.x) s_keep[i] = P.keep_rows[i];
     PROWS = s_prows;
     PPTR = s_pptr;
     PPAR = s_ppar;
-    PSLP = s_pslp;
-    PSL = s_psl;
     KEEP = s_keep;
   }
   if (kStaged) {
@@ -347,11 +344,6 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
     uint4* t4 = reinterpret_cast<uint4*>(tiles);
     for (uint32_t i = threadIdx.x; i < (2 * tile_words) / 4; i += blockDim.x)
       t4[i] = make_uint4(0, 0, 0, 0);
-    uint4* c4 = reinterpret_cast<uint4*>(coins);
-    for (uint32_t i = threadIdx.x; i < 2 * tw4; i += blockDim.x) {
-      const uint32_t b = i >> tw4_log2, q = i & (tw4 - 1);
-      c4[((b * n_slots + P.n_dense_live) << tw4_log2) + q] = make_uint4(kFull, kFull, kFull, kFull);
-    }
     if (with_counts)
       for (uint32_t i = threadIdx.x; i < P.n_meas; i += blockDim.x) cnt[i] = 0;
     if (threadIdx.x < 2) segctr[threadIdx.x] = 0;
@@ -372,19 +364,34 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
       if (i >= 2) named_sync(kBarEmpty0 + b, blockDim.x);
       long long tw1 = clock64();
       uint32_t* tile = tiles + b * tile_words;
-      {  // fair-coin words of this tile (dense symbols), keyed by (symbol, 128-shot quad)
-        uint4* c4 = reinterpret_cast<uint4*>(coins + b * n_slots * tw);
-        for (uint32_t j = threadIdx.x; j < (P.n_dense_live << tw4_log2); j += n_gen * 32) {
-          const uint32_t slot = j >> tw4_log2, q = j & (tw4 - 1);
+      const uint32_t tile_s = static_cast<uint32_t>(__cvta_generic_to_shared(tile));
+      // Fair-coin words of this tile (dense symbols), keyed by (symbol,
+      // 128-shot quad), XORed word-wise into the D rows of the symbol's
+      // column; the last slot is the constant term (all ones).
+      for (uint32_t j = threadIdx.x; j < ((P.n_dense_live + 1) << tw4_log2); j += n_gen * 32) {
+        const uint32_t slot = j >> tw4_log2, q = j & (tw4 - 1);
+        uint32_t e = __ldg(P.coin_ptr + slot);
+        const uint32_t e1 = __ldg(P.coin_ptr + slot + 1);
+        if (e == e1) continue;
+        uint4 c = make_uint4(kFull, kFull, kFull, kFull);
+        if (slot < P.n_dense_live) {
           const uint64_t gq = (gtile << tw4_log2) + q;
-          c4[j] = philox10(make_uint4(P.dense_sym[slot], static_cast<uint32_t>(gq),
-                                      (static_cast<uint32_t>(gq >> 32) & 0xFFFFFFu) |
-                                          (kDomCoin << 24),
-                                      0u),
-                           K);
+          c = philox10(make_uint4(P.dense_sym[slot], static_cast<uint32_t>(gq),
+                                  (static_cast<uint32_t>(gq >> 32) & 0xFFFFFFu) | (kDomCoin << 24),
+                                  0u),
+                       K);
+        }
+        for (; e < e1; ++e) {
+          const uint32_t a = tile_s + ((static_cast<uint32_t>(__ldg(P.coin_rows + e)) + 4 * q) << 2);
+          asm volatile(
+              "red.shared.xor.b32 [%0], %1;\n\t"
+              "red.shared.xor.b32 [%0+4], %2;\n\t"
+              "red.shared.xor.b32 [%0+8], %3;\n\t"
+              "red.shared.xor.b32 [%0+12], %4;" ::"r"(a),
+              "r"(c.x), "r"(c.y), "r"(c.z), "r"(c.w)
+              : "memory");
         }
       }
-      const uint32_t tile_s = static_cast<uint32_t>(__cvta_generic_to_shared(tile));
       const uint32_t spare = P.n_meas * tw;
       const uint32_t spare2 = spare * 0x10001u;  // two u16 spare-row offsets
       uint32_t seg = 0;
@@ -474,21 +481,21 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
   } else {
     // ---------------- drain warps ----------------
     const uint32_t ct = threadIdx.x - n_gen * 32, nct = blockDim.x - n_gen * 32;
+    const uint32_t ld_lo = static_cast<uint32_t>(ld), ld_hi = static_cast<uint32_t>(ld >> 32);
     for (uint32_t i = 0; i < n_my; ++i) {
       const uint32_t b = i & 1;
       const uint64_t t_local = blockIdx.x + static_cast<uint64_t>(i) * gridDim.x;
-      const uint64_t gtile = tile0 + t_local;
-      const uint4* c4 = reinterpret_cast<const uint4*>(coins + b * n_slots * tw);
       long long td0 = clock64();
       named_sync(kBarFull0 + b, blockDim.x);
       long long td1 = clock64();
 
       uint4* t4 = reinterpret_cast<uint4*>(tiles + b * tile_words);
+      const uint32_t t4_s = static_cast<uint32_t>(__cvta_generic_to_shared(t4));
       const uint64_t first = t_local << P.t_log2;
       const uint64_t valid = min(static_cast<uint64_t>(1) << P.t_log2, n_shots - first);
       const uint32_t vq = static_cast<uint32_t>((valid + 127) >> 7);
       const uint32_t rem = static_cast<uint32_t>(valid & 127);
-      const bool fast = vec && !with_counts && (valid == (static_cast<uint64_t>(1) << P.t_log2));
+      const bool fast = vec && (valid == (static_cast<uint64_t>(1) << P.t_log2));
       // Rows along parent paths (heavy-path decomposition of the L forest):
       // one thread walks a path top-down for one 128-shot column, carrying
       // the running row value; a path's head waits only for its parent's
@@ -504,37 +511,35 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
           const int32_t par = act ? PPAR[pth] : -1;
           uint4 prev = par >= 0 ? t4[(static_cast<uint32_t>(par) << tw4_log2) + q]
                                 : make_uint4(0, 0, 0, 0);
-          uint32_t sl = act ? PSLP[pth] : 0;
           const uint32_t xe = act ? PPTR[pth + 1] : 0;
           uint32_t x = act ? PPTR[pth] : 0;
           uint64_t* obase = out + t_local * tile_stride + 2 * q;
-          // Walks the path: rebuild row (tile ^ dense terms ^ parent), keep or
-          // clear the tile word, store 16 bytes to HBM, optionally count.
+          // Walks the path: row = tile word ^ parent row; keep or clear the
+          // tile word, store 16 bytes to HBM, optionally count.
           auto walk = [&](auto fast_tag) {
-            constexpr bool kFast = decltype(fast_tag)::value;  // full tile, aligned, no counts
-            uint32_t e = x < xe ? PROWS[x] : 0u;
-            uint4 cur = x < xe ? t4[((e & 0xFFFFu) << tw4_log2) + q] : make_uint4(0, 0, 0, 0);
+            constexpr bool kFast = decltype(fast_tag)::value;  // full tile, 16-byte aligned
+            // path_rows is padded by one entry, so the next row can always
+            // be prefetched (past a path's end the value is discarded).
+            uint32_t e = PROWS[x];
+            uint4 cur = t4[((e & 0xFFFFu) << tw4_log2) + q];
             for (; x < xe; ++x) {
-              // e = row | n_slots << 16 | keep << 31; prefetch the next row's word
-              const bool has_next = x + 1 < xe;
-              const uint32_t en = has_next ? PROWS[x + 1] : 0u;
-              const uint4 nxt =
-                  has_next ? t4[((en & 0xFFFFu) << tw4_log2) + q] : make_uint4(0, 0, 0, 0);
+              const uint32_t en = PROWS[x + 1];
+              const uint4 nxt = t4[((en & 0xFFFFu) << tw4_log2) + q];
               const uint32_t k = e & 0xFFFFu;
               uint4 v = xor4(cur, prev);
-              for (const uint32_t se = sl + ((e >> 16) & 0x7FFFu); sl < se; ++sl)
-                v = xor4(v, c4[(static_cast<uint32_t>(PSL[sl]) << tw4_log2) + q]);
               // Rows with light children keep their final value for a later
               // round; all others are cleared for tile i+2 right away.
-              t4[(k << tw4_log2) + q] = (e >> 31) ? v : make_uint4(0, 0, 0, 0);
+              sts_or_zero(t4_s + (((k << tw4_log2) + q) << 4), v, e >> 31);
               prev = v;
               e = en;
               cur = nxt;
-              uint64_t* o = obase + static_cast<uint64_t>(k) * ld;
+              uint64_t* o = obase + (static_cast<uint64_t>(k) * ld_lo +
+                                     (static_cast<uint64_t>(k * ld_hi) << 32));
+              uint32_t pc = 0;
               if constexpr (kFast) {
                 *reinterpret_cast<uint4*>(o) = v;
+                if (with_counts) pc = __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
               } else {
-                uint32_t pc = 0;
                 if (q < vq) {
                   bool two = true;  // whether the item's second u64 word is inside the tile
                   if (q == vq - 1 && rem) {
@@ -556,13 +561,13 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
                   }
                   if (with_counts) pc = __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
                 }
-                if (with_counts) {
-                  if (tw4 >= 32) {  // the whole warp walks this path: one atomic per row
-                    pc = __reduce_add_sync(kFull, pc);
-                    if (lane == 0 && pc) atomicAdd(&cnt[k], pc);
-                  } else if (pc) {
-                    atomicAdd(&cnt[k], pc);
-                  }
+              }
+              if (with_counts) {
+                if (tw4 >= 32) {  // the whole warp walks this path: one atomic per row
+                  pc = __reduce_add_sync(kFull, pc);
+                  if (lane == 0 && pc) atomicAdd(&cnt[k], pc);
+                } else if (pc) {
+                  atomicAdd(&cnt[k], pc);
                 }
               }
             }
@@ -943,13 +948,11 @@ int launch_k1(const DevPlan& P, const LaunchCfg& L, const RoundKeys& K, uint64_t
 size_t fused_smem_bytes(const DevPlan& P, uint32_t t_log2, bool staged, bool row_staged) {
   const size_t tw = size_t{1} << (t_log2 - 5);
   size_t b = 2 * static_cast<size_t>(P.n_meas + 1) * tw * 4;       // tiles (+ spare row)
-  b += 2 * static_cast<size_t>(P.n_dense_live + 1) * tw * 4;        // coin words + ones slot
   b += align16(4ull * P.n_meas) + 16;                               // counts, dispensers
   if (row_staged) {
-    b += align16(4ull * P.n_meas);
+    b += align16(4ull * (P.n_meas + 1));
     b += align16(4ull * (P.n_paths + 1));
-    b += 2 * align16(4ull * P.n_paths);
-    b += align16(2ull * P.n_drow);
+    b += align16(4ull * P.n_paths);
     b += align16(2ull * P.n_keep);
   }
   if (staged) {

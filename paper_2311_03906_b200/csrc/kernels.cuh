@@ -55,13 +55,13 @@ struct DevPlan {
   const uint32_t* ones_syms = nullptr;
 
   // Dense (bit-sliced) symbols: fair coins and Bernoulli(1/2). Live slots
-  // first; slot n_dense_live of the fused kernel's coin buffer is all ones
-  // and stands for the constant term.
+  // first. The fused kernel XORs each live slot's coin words into the D rows
+  // of its column coin_rows[coin_ptr[slot] .. coin_ptr[slot+1]) (entries =
+  // row * tw); slot n_dense_live stands for the constant term (all ones).
   uint32_t n_dense_live = 0, n_dense_all = 0;
   const uint32_t* dense_sym = nullptr;  // slot -> symbol id
-  const uint32_t* drow_ptr = nullptr;   // [n_meas+1] -> drow_slot
-  const uint16_t* drow_slot = nullptr;  // dense slots (and the ones slot) per row
-  uint32_t n_drow = 0;
+  const uint32_t* coin_ptr = nullptr;   // [n_dense_live + 2]
+  const uint16_t* coin_rows = nullptr;
 
   // Sparse channels (see ClassInfo). Live classes first.
   uint32_t n_cls_live = 0, n_cls_all = 0;
@@ -85,15 +85,13 @@ struct DevPlan {
   // heavy-path decomposition of the parent forest: path p lists rows
   // path_rows[path_ptr[p] .. path_ptr[p+1]) top-down; path_par[p] is the head's
   // parent (or -1), which lies on a path of an earlier round (round_ptr).
-  // Entry = row | n_dense_slots << 16 | keep << 31 (keep: row has light
-  // children, so its final value stays in the tile until the tile ends);
-  // each path's dense slots (coins, the ones slot) follow in pslots from
-  // pslot_ptr[path] in row order; keep_rows lists the rows to clear at the end.
+  // Entry = row | keep << 31 (keep: row has light children, so its final
+  // value stays in the tile until the tile ends); path_rows has one padding
+  // entry at the end so the walk can always prefetch x + 1. keep_rows lists
+  // the rows to clear at the end.
   const uint32_t* path_rows = nullptr;
   const uint32_t* path_ptr = nullptr;
   const int32_t* path_par = nullptr;
-  const uint32_t* pslot_ptr = nullptr;
-  const uint16_t* pslots = nullptr;
   const uint16_t* keep_rows = nullptr;
   const uint32_t* round_ptr = nullptr;  // [n_rounds + 1] over paths
   uint32_t n_paths = 0, n_rounds = 1, n_keep = 0;
