@@ -405,12 +405,87 @@ void build_plan(sp_ctx* c) {
   }
 
   // Segments: each class's flattened (group, shot) space of a tile is cut
-  // into slices of ~E expected firings (<= 2^24 trials), one warp walk each;
-  // E is chosen so each generator warp takes a few segments per tile.
+  // into slices (<= 2^22 trials, >= 32), one warp walk each. A walk over a
+  // slice holding N firings takes floor(N / S) + 1 steps of S slots (S =
+  // 32 lanes x 8 skips, or x 6 for DEPOLARIZE), so the slice count per class
+  // minimises expected steps + a fixed per-slice cost (init, first Philox
+  // latency), subject to enough slices per tile to keep every generator warp
+  // busy with two tiles in flight. SP_SEG_EVENTS=E forces ~E firings/slice.
   const double ev_tile = events_per_shot * T;
-  double E = ev_tile / d.gen_warps;
-  E = std::min(std::max(E, 32.0), 2048.0);
-  if (const long fe = env_long("SP_SEG_EVENTS", 0)) E = static_cast<double>(fe);
+  auto exp_steps = [](double lam, double S) {  // E[floor(N/S)] + 1, N ~ Poisson(lam)
+    double e = 1.0;
+    const double sd = std::sqrt(std::max(lam, 1e-9));
+    for (int j = 1;; ++j) {
+      const double tail = 0.5 * std::erfc((j * S - 0.5 - lam) / (sd * std::sqrt(2.0)));
+      e += tail;
+      if (j * S > lam && tail < 1e-7) break;
+    }
+    return e;
+  };
+  const double seg_cost = env_long("SP_SEG_COST_PCT", 35) / 100.0;
+  std::vector<uint64_t> live_nseg(live_cls.size(), 1);
+  {
+    const long fe = env_long("SP_SEG_EVENTS", 0);
+    std::vector<double> lam(live_cls.size()), S(live_cls.size());
+    std::vector<uint64_t> nmin(live_cls.size()), nmax(live_cls.size());
+    auto cost = [&](size_t c, uint64_t n) {
+      return n * (exp_steps(lam[c] / n, S[c]) + seg_cost);
+    };
+    uint64_t total = 0;
+    for (size_t c = 0; c < live_cls.size(); ++c) {
+      const uint64_t trials = live_cls[c].groups.size() * T;
+      lam[c] = trials * live_cls[c].p;
+      S[c] = 32.0 * (live_cls[c].dist == SP_DIST_BERNOULLI ? 8 : 6);
+      nmin[c] = std::max<uint64_t>(1, (trials + 4194303) / 4194304);
+      nmax[c] = std::max<uint64_t>(nmin[c], trials / 32);
+      uint64_t best = nmin[c];
+      if (fe > 0) {
+        best = static_cast<uint64_t>(std::ceil(lam[c] / fe));
+      } else {
+        double bc = cost(c, best);
+        const uint64_t hi = std::min<uint64_t>(nmax[c], static_cast<uint64_t>(2 * lam[c] / S[c]) + 2);
+        for (uint64_t n = nmin[c] + 1; n <= hi; ++n) {
+          const double cn = cost(c, n);
+          if (cn < bc) { bc = cn; best = n; }
+        }
+      }
+      live_nseg[c] = std::min(std::max(best, nmin[c]), nmax[c]);
+      total += live_nseg[c];
+    }
+    const uint64_t min_total =
+        fe > 0 ? 0 : static_cast<uint64_t>(env_long("SP_SEG_MIN", d.gen_warps));
+    while (total < min_total) {  // split where it costs the fewest extra steps
+      size_t arg = live_cls.size();
+      double dmin = 0;
+      for (size_t c = 0; c < live_cls.size(); ++c) {
+        if (live_nseg[c] >= nmax[c]) continue;
+        const double dc = cost(c, live_nseg[c] + 1) - cost(c, live_nseg[c]);
+        if (arg == live_cls.size() || dc < dmin) { dmin = dc; arg = c; }
+      }
+      if (arg == live_cls.size()) break;
+      ++live_nseg[arg];
+      ++total;
+    }
+    // Longest slices first: warps take slices in id order, so a warp that
+    // finishes early picks up a short one.
+    std::vector<size_t> ord(live_cls.size());
+    std::vector<double> steps(live_cls.size());
+    for (size_t c = 0; c < ord.size(); ++c) {
+      ord[c] = c;
+      steps[c] = exp_steps(lam[c] / live_nseg[c], S[c]);
+    }
+    std::stable_sort(ord.begin(), ord.end(), [&](size_t a, size_t b) { return steps[a] > steps[b]; });
+    std::vector<Cls> cls2;
+    std::vector<uint64_t> nseg2;
+    for (size_t c : ord) {
+      cls2.push_back(std::move(live_cls[c]));
+      nseg2.push_back(live_nseg[c]);
+    }
+    live_cls.swap(cls2);
+    live_nseg.swap(nseg2);
+  }
+  // Dead classes are only walked by the standalone draw kernel.
+  const double E = std::min(std::max(ev_tile / d.gen_warps, 32.0), 2048.0);
   std::vector<ClassInfo> cls_info;
   std::vector<uint32_t> cls_groups;
   std::vector<uint4> desc;
@@ -421,16 +496,23 @@ void build_plan(sp_ctx* c) {
   size_t max_plist = 0;
   uint64_t n_chains = 0, n_chains_live = 0;
   auto add_classes = [&](const std::vector<Cls>& cls, bool live) {
-    for (const Cls& cl : cls) {
+    for (size_t c = 0; c < cls.size(); ++c) {
+      const Cls& cl = cls[c];
       ClassInfo ci{};
       ci.dist = cl.dist;
-      ci.inv = static_cast<float>(1.0 / -std::log1p(-cl.p));  // p == 1 -> 0: fire every trial
+      // p == 1 -> -0: every trial fires
+      ci.clg = static_cast<float>(0.69314718055994531 / std::log1p(-cl.p));
       ci.goff = static_cast<uint32_t>(cls_groups.size());
       ci.trials = cl.groups.size() * T;
-      double len = std::ceil(E / cl.p);
-      len = std::min(std::max(len, 32.0), 16777216.0);
-      uint64_t n_seg = std::max<uint64_t>((ci.trials + static_cast<uint64_t>(len) - 1) /
-                                              static_cast<uint64_t>(len), 1);
+      uint64_t n_seg = 0;
+      if (live) {
+        n_seg = live_nseg[c];
+      } else {
+        double len = std::ceil(E / cl.p);
+        len = std::min(std::max(len, 32.0), 4194304.0);  // kernel skips clamp at 2^22
+        n_seg = std::max<uint64_t>((ci.trials + static_cast<uint64_t>(len) - 1) /
+                                       static_cast<uint64_t>(len), 1);
+      }
       ci.L = (ci.trials + n_seg - 1) / n_seg;
       ci.n_seg = static_cast<uint32_t>(n_seg);
       ci.seg_off = static_cast<uint32_t>(n_chains);
@@ -531,7 +613,9 @@ void build_plan(sp_ctx* c) {
     if (const long fp = env_long("SP_PAD_PRED", -1); fp >= 0) d.pad_pred = fp != 0;
     if (d.lp) {
       // padding = the spare tile row (row n_meas), absorbed and never read
-      std::vector<uint16_t> flat(plists.size() * d.lp, static_cast<uint16_t>(n_meas * d.tw));
+      // one extra all-padding list (index plists.size()) for invalid slots
+      d.plist_dummy = static_cast<uint32_t>(plists.size());
+      std::vector<uint16_t> flat((plists.size() + 1) * d.lp, static_cast<uint16_t>(n_meas * d.tw));
       for (size_t i = 0; i < plists.size(); ++i)
         std::copy(plists[i].begin(), plists[i].end(), flat.begin() + i * d.lp);
       std::vector<uint4> packed(std::max<size_t>(flat.size() / 8, 1));

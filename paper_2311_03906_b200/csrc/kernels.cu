@@ -56,16 +56,22 @@ __device__ __forceinline__ uint4 philox10(uint4 c, const RoundKeys& K) {
   return c;
 }
 
-// Exponential(1) variate -ln(u), u = k * 2^-24 with k = (r >> 8) + 1 in
-// [1, 2^24] (so P(u <= x) is exact to 2^-24). Near u = 1 the series of
-// -ln(1 - x) keeps full relative precision where lg2.approx would not.
-__device__ __forceinline__ float exp1_from_bits(uint32_t r) {
-  const uint32_t k = (r >> 8) + 1u;
-  const float ux = static_cast<float>(0x1000000u - k) * 0x1.0p-24f;  // 1 - u, exact
-  const float series = ux * (1.f + ux * (0.5f + ux * (0.33333334f + ux * 0.25f)));
+// Geometric skip floor(-ln(u) / -ln(1-p)) from 24 random bits: u = k * 2^-24
+// with k = (r >> 8) + 1 in [1, 2^24] (so P(u <= x) is exact to 2^-24).
+// Computed as lg2(u) * clg with clg = ln2 / ln(1-p) < 0. Near u = 1 the
+// series of log2(1 - x) keeps full relative precision where lg2.approx would
+// not. Clamped to 2^22 (segments are at most 2^22 trials, so a clamped skip
+// still lands past the segment end, and 256 of them cannot overflow u32).
+__device__ __forceinline__ uint32_t geo_skip(uint32_t r, float clg) {
+  constexpr float kL = 1.4426950408889634f;  // 1 / ln 2
+  const float u = static_cast<float>((r >> 8) + 1u) * 0x1.0p-24f;
+  const float ux = 1.f - u;  // exact: both are multiples of 2^-24 in [0, 1]
+  // log2(1 - x) = -(x + x^2/2 + x^3/3 + x^4/4 + ...) / ln 2
+  const float series = ux * (-kL + ux * (-0.5f * kL + ux * (-kL / 3.f + ux * (-0.25f * kL))));
   float lg;  // u >= 2^-24 is a normal float, so the flush-to-zero form is exact
-  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(lg) : "f"(static_cast<float>(k) * 0x1.0p-24f));
-  return ux < 0.03125f ? series : -lg * 0.6931471806f;  // branch-free select
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(lg) : "f"(u));
+  const float sf = (ux < 0.03125f ? series : lg) * clg;  // branch-free select
+  return __float2uint_rz(fminf(sf, 4194304.f));
 }
 
 // SplitMix64 finalizer and keyed draw — sampler.hpp:14-26.
@@ -104,18 +110,18 @@ __device__ __forceinline__ uint32_t group_bits_compat(uint32_t dist, double p, u
 //
 // A class's flattened (group, shot) trial space of one tile is cut into
 // segments; each segment is one Bernoulli(p) process walked by ONE warp in
-// lockstep. Every lane draws one Philox block per step: 4 Exp(1) skips
-// (Bernoulli) or 3 skips + one word whose three base-n digits pick the
+// lockstep. Every lane draws kBlocks Philox blocks per step: 4 skips per
+// block (Bernoulli) or 3 skips + one word whose three base-n digits pick the
 // non-identity Pauli of each firing (n = 3 for DEPOLARIZE1 -> X, Z, Y;
 // n = 15 for DEPOLARIZE2) — the joint channel pmf of fill_group
 // (sampler.cpp:24-42). Geometric gaps floor(Exp/-ln(1-p)) + 1 are laid
 // end to end in lane order with a warp prefix sum, so one step yields up to
-// 96-128 firing positions with no divergence. Streams are keyed by
+// 192-256 firing positions with no divergence. Streams are keyed by
 // (segment, global tile), independent of which warp, CTA or GPU runs them.
 struct Segment {
-  uint64_t lo;
+  uint32_t g0, s0;  // first trial = (class position g0, shot s0 in the tile)
   uint32_t len, seg, goff, dist, pbase, npat;
-  float inv;
+  float clg;
 };
 
 // Philox blocks each lane draws per walk step (independent counters, so the
@@ -126,40 +132,43 @@ constexpr int kSlots = 4 * kBlocks;
 // Firings of one walk step on one lane (slot k valid iff v & (1<<k)).
 struct Fired {
   uint32_t v;
-  uint32_t g[kSlots], shot[kSlots], pat[kSlots];  // group position, shot in tile, pattern
+  uint32_t g[kSlots], shot[kSlots], pat[kSlots];  // class position, shot in tile, pattern
 };
 
 __device__ __forceinline__ void segment_init(Segment& sg, const ClassInfo* cls, uint32_t n_cls,
-                                             uint32_t seg) {
+                                             uint32_t seg, uint32_t t_log2) {
   uint32_t lo = 0, hi = n_cls;  // largest k with cls[k].seg_off <= seg
   while (hi - lo > 1) {
     const uint32_t mid = (lo + hi) >> 1;
     if (cls[mid].seg_off <= seg) lo = mid; else hi = mid;
   }
   const ClassInfo& ci = cls[lo];
-  sg.lo = static_cast<uint64_t>(seg - ci.seg_off) * ci.L;
-  sg.len = static_cast<uint32_t>(min(sg.lo + ci.L, ci.trials) - sg.lo);
+  const uint64_t first = static_cast<uint64_t>(seg - ci.seg_off) * ci.L;
+  sg.g0 = static_cast<uint32_t>(first >> t_log2);
+  sg.s0 = static_cast<uint32_t>(first) & ((1u << t_log2) - 1u);
+  sg.len = static_cast<uint32_t>(min(first + ci.L, ci.trials) - first);
   sg.seg = seg;
   sg.goff = ci.goff;
   sg.dist = ci.dist;
   sg.pbase = ci.pbase;
   sg.npat = ci.npat;
-  sg.inv = ci.inv;
+  sg.clg = ci.clg;
 }
 
-// Walks one segment with the whole warp; emit(const Fired&) runs on every
-// lane after each step (lanes may have no valid firing).
-template <bool kBern, class Emit>
+// Walks one segment with the whole warp. After each step's positions are
+// known, pre(tag, f) runs (issue table loads), then the next step's Philox
+// blocks are computed — independent work that hides those loads — and then
+// emit(tag, f) runs on every lane (lanes may have no valid firing).
+template <bool kBern, class Pre, class Emit>
 __device__ __forceinline__ void segment_walk_t(const Segment& sg, const RoundKeys& K,
                                                uint64_t gtile, uint32_t t_log2, uint32_t lane,
-                                               Emit&& emit) {
+                                               Pre&& pre, Emit&& emit) {
   constexpr bool bern = kBern;
-  const uint32_t nk = bern ? 4u : 3u;  // skips per Philox block
   const uint32_t n = sg.dist == 3 ? 3u : 15u;
   const uint32_t magic = n == 3 ? 0x5556u : 0x1112u;  // exact /n for values < n^3
   const uint32_t tmask = (1u << t_log2) - 1u;
   const uint32_t c3 = (static_cast<uint32_t>(gtile >> 32) & 0xFFFFFFu) | (kDomChain << 24);
-  uint32_t pos = 0;  // trials consumed (warp-uniform), < len <= 2^24
+  uint32_t pos = 0;  // trials consumed (warp-uniform), < len <= 2^22
   uint4 r[kBlocks];
 #pragma unroll
   for (int b = 0; b < kBlocks; ++b)
@@ -172,10 +181,8 @@ __device__ __forceinline__ void segment_walk_t(const Segment& sg, const RoundKey
       const uint32_t w[4] = {r[b].x, r[b].y, r[b].z, r[b].w};
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        incl[4 * b + k] = acc;
-        if (k == 3 && !bern) continue;
-        const float sf = exp1_from_bits(w[k]) * sg.inv;
-        acc += (sf < 16777216.f ? static_cast<uint32_t>(sf) : 16777216u) + 1u;  // gap to next firing
+        if (k == 3 && !bern) { incl[4 * b + k] = acc; continue; }
+        acc += geo_skip(w[k], sg.clg) + 1u;  // gap to the next firing
         incl[4 * b + k] = acc;
       }
     }
@@ -186,7 +193,9 @@ __device__ __forceinline__ void segment_walk_t(const Segment& sg, const RoundKey
       if (lane >= static_cast<uint32_t>(o)) scan += t;
     }
     const uint32_t total = __shfl_sync(kFull, scan, 31);
+    // trial index (relative to the segment) of this lane's firings, minus 1
     const uint32_t base = pos + scan - acc - 1;
+    const uint32_t sbase = sg.s0 + base;
     Fired f;
     f.v = 0;
 #pragma unroll
@@ -204,16 +213,15 @@ __device__ __forceinline__ void segment_walk_t(const Segment& sg, const RoundKey
           f.pat[sl] = 1u + digits - q * n;
           digits = q;
         }
-        const uint32_t rel = base + incl[sl];
-        const uint64_t fl = sg.lo + rel;
-        f.g[sl] = static_cast<uint32_t>(fl >> t_log2);
-        f.shot[sl] = static_cast<uint32_t>(fl) & tmask;
-        f.v |= (rel < sg.len ? 1u : 0u) << sl;
+        const uint32_t t = sbase + incl[sl];  // < 2^12 + 2^31: no overflow
+        f.g[sl] = sg.g0 + (t >> t_log2);
+        f.shot[sl] = t & tmask;
+        f.v |= (base + incl[sl] < sg.len ? 1u : 0u) << sl;
       }
     }
-    (void)nk;
     pos += total;
     const bool more = pos < sg.len;
+    pre(std::integral_constant<bool, kBern>{}, f);
     // The next step's Philox blocks are independent of this step's table
     // loads and atomics: computing them first lets the two overlap.
     if (more) {
@@ -231,13 +239,14 @@ __device__ __forceinline__ void segment_walk_t(const Segment& sg, const RoundKey
 // Bernoulli classes use all four words of a block as skips; DEPOLARIZE
 // classes use three and draw patterns from the fourth. The two shapes are
 // separate instantiations so neither pays for the other's slots.
-template <class Emit>
+template <class Pre, class Emit>
 __device__ __forceinline__ void segment_walk(const Segment& sg, const RoundKeys& K, uint64_t gtile,
-                                             uint32_t t_log2, uint32_t lane, Emit&& emit) {
+                                             uint32_t t_log2, uint32_t lane, Pre&& pre,
+                                             Emit&& emit) {
   if (sg.dist == 1)
-    segment_walk_t<true>(sg, K, gtile, t_log2, lane, emit);
+    segment_walk_t<true>(sg, K, gtile, t_log2, lane, pre, emit);
   else
-    segment_walk_t<false>(sg, K, gtile, t_log2, lane, emit);
+    segment_walk_t<false>(sg, K, gtile, t_log2, lane, pre, emit);
 }
 
 __device__ __forceinline__ void named_sync(uint32_t id, uint32_t n) {
@@ -393,9 +402,32 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
         }
       }
       const uint32_t spare = P.n_meas * tw;
-      const uint32_t spare2 = spare * 0x10001u;  // two u16 spare-row offsets
       uint32_t seg = 0;
       Segment sg;
+      // Exact flip list of (class position, pattern): kLp u16 tile-word
+      // offsets padded with the spare row's. With kLp == 8 all of a step's
+      // lists are loaded before the next Philox blocks are computed (pre),
+      // so the L1/L2 latency hides under that arithmetic. Invalid slots load
+      // the all-padding list.
+      constexpr bool kPreload = kLp == 8 && !kPadPred;
+      constexpr int kLw = kLp > 0 ? kLp / 8 : 1;
+      uint4 lst[kSlots][kLw];
+      auto load_lists = [&](auto bern_tag, const Fired& f, int k0, int k1) {
+        constexpr bool kB = decltype(bern_tag)::value;
+#pragma unroll
+        for (int k = 0; k < kSlots; ++k) {
+          if (k < k0 || k >= k1 || (!kB && (k & 3) == 3)) continue;
+          const uint32_t li =
+              ((f.v >> k) & 1u) ? sg.pbase + f.g[k] * sg.npat + f.pat[k] - 1 : P.plist_dummy;
+#pragma unroll
+          for (int h = 0; h < kLw; ++h) lst[k][h] = __ldg(PLIST + static_cast<size_t>(li) * kLw + h);
+        }
+      };
+      auto pre = [&](auto bern_tag, const Fired& f) {
+        if constexpr (kLp > 0 && kPreload) {
+          if (!(P.debug_mode & 1u)) load_lists(bern_tag, f, 0, kSlots);
+        }
+      };
       auto emit = [&](auto bern_tag, const Fired& f) {
         constexpr bool kB = decltype(bern_tag)::value;
         if (P.debug_mode & 1u) {
@@ -403,33 +435,16 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
           return;
         }
         if constexpr (kLp > 0) {
-          // Exact flip list of (group, pattern), padded to kLp u16 rows with
-          // 0xFFFF; one or two 16-byte loads, then predicated shared atomics.
 #pragma unroll
           for (int half = 0; half < kSlots; half += 4) {
-            // Padding entries point at the spare row, so every entry is an
-            // unconditional shared XOR; an invalid slot XORs bit 0 of the
-            // spare row's first word.
-            uint4 lst[4][kLp / 8];
+            if constexpr (!kPreload) load_lists(bern_tag, f, half, half + 4);
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              if (!kB && k == 3) continue;
+            for (int k = half; k < half + 4; ++k) {
+              if (!kB && (k & 3) == 3) continue;
+              const uint32_t wb = tile_s + ((f.shot[k] >> 5) << 2);
+              const uint32_t bit = ((f.v >> k) & 1u) << (f.shot[k] & 31);
 #pragma unroll
-              for (int h = 0; h < kLp / 8; ++h)
-                lst[k][h] = ((f.v >> (half + k)) & 1u)
-                                ? __ldg(PLIST + (static_cast<uint64_t>(sg.pbase +
-                                                                       f.g[half + k] * sg.npat +
-                                                                       f.pat[half + k] - 1) *
-                                                     (kLp / 8) + h))
-                                : make_uint4(spare2, spare2, spare2, spare2);
-            }
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              if (!kB && k == 3) continue;
-              const uint32_t wb = tile_s + ((f.shot[half + k] >> 5) << 2);
-              const uint32_t bit = ((f.v >> (half + k)) & 1u) << (f.shot[half + k] & 31);
-#pragma unroll
-              for (int h = 0; h < kLp / 8; ++h) {
+              for (int h = 0; h < kLw; ++h) {
                 const uint32_t ww[4] = {lst[k][h].x, lst[k][h].y, lst[k][h].z, lst[k][h].w};
 #pragma unroll
                 for (int e = 0; e < 8; ++e) {
@@ -437,8 +452,9 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
                   if (kPadPred) {
                     // many firings per shot: skip padding so the ATOMS pipe
                     // only carries real flips
-                    if (row != spare) atomicXor(tile + (f.shot[half + k] >> 5) + row, bit);
+                    if (row != spare) atomicXor(tile + (f.shot[k] >> 5) + row, bit);
                   } else {
+                    // padding XORs the spare row (never read)
                     asm volatile("red.shared.xor.b32 [%0], %1;" ::"r"(wb + (row << 2)), "r"(bit)
                                  : "memory");
                   }
@@ -469,8 +485,8 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
         if (lane == 0) seg = atomicAdd(&segctr[b], 1u);
         seg = __shfl_sync(kFull, seg, 0);
         if (seg >= P.n_seg_live || (P.debug_mode & 2u)) break;
-        segment_init(sg, CLS, P.n_cls_live, seg);
-        segment_walk(sg, K, gtile, P.t_log2, lane, emit);
+        segment_init(sg, CLS, P.n_cls_live, seg, P.t_log2);
+        segment_walk(sg, K, gtile, P.t_log2, lane, pre, emit);
       }
       if (P.timers && lane == 0) {  // gen: [0] waiting EMPTY, [1] working
         atomicAdd(reinterpret_cast<unsigned long long*>(P.timers) + 0, tw1 - tw0);
@@ -698,8 +714,8 @@ __global__ void d_segments(const DevPlan P, const RoundKeys K, uint64_t tile0, u
     const uint32_t seg = static_cast<uint32_t>(i - static_cast<uint64_t>(t) * P.n_seg_all);
     const uint64_t base = static_cast<uint64_t>(t) << P.t_log2;
     Segment sg;
-    segment_init(sg, P.cls, P.n_cls_all, seg);
-    segment_walk(sg, K, tile0 + t, P.t_log2, lane, [&](auto, const Fired& f) {
+    segment_init(sg, P.cls, P.n_cls_all, seg, P.t_log2);
+    segment_walk(sg, K, tile0 + t, P.t_log2, lane, [](auto, const Fired&) {}, [&](auto, const Fired& f) {
       for (int k = 0; k < kSlots; ++k) {
         if (!((f.v >> k) & 1u)) continue;
         const uint64_t j = base + f.shot[k];

@@ -14,12 +14,12 @@ constexpr uint32_t kDomCoin = 2u;   // bit-sliced fair-coin words
 // for one shot tile is the flattened (group, shot) grid, group-major, cut into
 // n_seg segments of L trials (the last one shorter), one warp walk each.
 struct ClassInfo {
-  uint64_t L = 0;        // trials per segment (<= 2^24)
+  uint64_t L = 0;        // trials per segment (<= 2^22)
   uint64_t trials = 0;   // groups * T
   uint32_t seg_off = 0;  // first segment id of the class
   uint32_t n_seg = 0;
   uint32_t goff = 0;    // first class position (index into desc / cls_groups)
-  float inv = 0.f;      // 1 / -ln(1 - p): Exp(1) -> geometric skip
+  float clg = 0.f;      // ln 2 / ln(1 - p) (<= 0): log2(u) -> geometric skip
   uint32_t dist = 0;    // 1 Bernoulli, 3 DEPOLARIZE1, 4 DEPOLARIZE2
   uint32_t pbase = 0;   // first flip list of the class (lists in plist)
   uint32_t npat = 1;    // non-identity patterns per group: 1, 3 or 15
@@ -80,6 +80,7 @@ struct DevPlan {
   // List of (class position g, pattern pi) = plist[(pbase + g*npat + pi-1)].
   uint32_t lp = 0;
   uint32_t pad_pred = 0;  // skip padding entries (many firings per shot) vs XOR the spare row
+  uint32_t plist_dummy = 0;  // index of an all-padding list (invalid slots load it)
   const uint4* plist = nullptr;
   // Row reconstruction out[k] = d[k] ^ out[parent[k]] along the paths of a
   // heavy-path decomposition of the parent forest: path p lists rows

@@ -108,3 +108,19 @@ def test_seeds_differ_and_repeat(gpu_sampler_factory):
     a = host(s.sample(100_000, 1))
     assert np.array_equal(a, host(s.sample(100_000, 1)))
     assert not np.array_equal(a, host(s.sample(100_000, 2)))
+
+
+@pytest.mark.parametrize("p,expect", [(1e-9, 0.1), (1e-6, 100.0), (1e-4, 10_000.0)])
+def test_tiny_rates_no_spurious_firings(gpu_sampler_factory, p, expect):
+    """Skips far longer than a segment must not wrap the warp's position scan
+    (kernels.cu geo_skip clamps at 2^22): flip totals follow the rate."""
+    import torch
+    n_q, shots = 100, 1_000_000
+    text = f"X_ERROR({p!r}) " + " ".join(map(str, range(n_q))) + "\nM " + \
+        " ".join(map(str, range(n_q))) + "\n"
+    init = run_initialization(text)
+    s = gpu_sampler_factory(init)
+    counts = torch.zeros(init.n_meas, dtype=torch.int64, device="cuda")
+    s.sample(shots, 3, counts=counts)
+    total = int(counts.sum().item())
+    assert abs(total - expect) <= 5 * max(expect, 1.0) ** 0.5 + 3, (p, total, expect)
