@@ -604,7 +604,7 @@ void build_plan(sp_ctx* c) {
   d.colrow = c->b_colrow.upload(colrow16, s);
   {
     const long force_lp = env_long("SP_LP", -1);
-    d.lp = max_plist <= 8 ? 8 : max_plist <= 16 ? 16 : 0;
+    d.lp = max_plist <= 4 ? 4 : max_plist <= 8 ? 8 : max_plist <= 16 ? 16 : 0;
     if (force_lp >= 0) d.lp = static_cast<uint32_t>(force_lp);
     if (d.lp && d.lp < max_plist) d.lp = 0;
     // Unconditional padded XORs cost ATOMS throughput (~12 lanes/clk/SM on
@@ -612,14 +612,28 @@ void build_plan(sp_ctx* c) {
     d.pad_pred = events_per_shot * d.lp > 32.0;
     if (const long fp = env_long("SP_PAD_PRED", -1); fp >= 0) d.pad_pred = fp != 0;
     if (d.lp) {
-      // padding = the spare tile row (row n_meas), absorbed and never read
-      // one extra all-padding list (index plists.size()) for invalid slots
+      // Entries: u8 row indices when the tile has <= 256 rows (a list is
+      // 4-16 bytes, so the table stays in L1), else byte offsets into the
+      // tile (row * tw * 4: a flip is one add + one shared XOR). Padding =
+      // the spare tile row (row n_meas), absorbed and never read; one extra
+      // all-padding list (index plists.size()) stands in for invalid slots.
       d.plist_dummy = static_cast<uint32_t>(plists.size());
-      std::vector<uint16_t> flat((plists.size() + 1) * d.lp, static_cast<uint16_t>(n_meas * d.tw));
-      for (size_t i = 0; i < plists.size(); ++i)
-        std::copy(plists[i].begin(), plists[i].end(), flat.begin() + i * d.lp);
-      std::vector<uint4> packed(std::max<size_t>(flat.size() / 8, 1));
-      std::memcpy(packed.data(), flat.data(), flat.size() * 2);
+      d.u8 = n_meas + 1 <= 256 && env_long("SP_U8", 1) != 0;
+      std::vector<uint4> packed;
+      if (d.u8) {
+        std::vector<uint8_t> flat((plists.size() + 1) * d.lp, static_cast<uint8_t>(n_meas));
+        for (size_t i = 0; i < plists.size(); ++i)
+          for (size_t j = 0; j < plists[i].size(); ++j)
+            flat[i * d.lp + j] = static_cast<uint8_t>(plists[i][j] / d.tw);
+        packed.resize((flat.size() + 15) / 16);
+        std::memcpy(packed.data(), flat.data(), flat.size());
+      } else {
+        std::vector<uint32_t> flat((plists.size() + 1) * d.lp, static_cast<uint32_t>(n_meas * d.tw * 4));
+        for (size_t i = 0; i < plists.size(); ++i)
+          for (size_t j = 0; j < plists[i].size(); ++j) flat[i * d.lp + j] = 4u * plists[i][j];
+        packed.resize(flat.size() / 4);
+        std::memcpy(packed.data(), flat.data(), flat.size() * 4);
+      }
       d.plist = c->b_plist.upload(packed, s);
     }
   }

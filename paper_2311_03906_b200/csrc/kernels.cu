@@ -155,24 +155,33 @@ __device__ __forceinline__ void segment_init(Segment& sg, const ClassInfo* cls, 
   sg.clg = ci.clg;
 }
 
-// Walks one segment with the whole warp. After each step's positions are
-// known, pre(tag, f) runs (issue table loads), then the next step's Philox
-// blocks are computed — independent work that hides those loads — and then
-// emit(tag, f) runs on every lane (lanes may have no valid firing).
-template <bool kBern, class Pre, class Emit>
-__device__ __forceinline__ void segment_walk_t(const Segment& sg, const RoundKeys& K,
-                                               uint64_t gtile, uint32_t t_log2, uint32_t lane,
-                                               Pre&& pre, Emit&& emit) {
+__device__ __forceinline__ uint4 segment_philox(const Segment& sg, const RoundKeys& K,
+                                                uint64_t gtile, uint32_t step, int b,
+                                                uint32_t lane) {
+  const uint32_t c3 = (static_cast<uint32_t>(gtile >> 32) & 0xFFFFFFu) | (kDomChain << 24);
+  return philox10(make_uint4(sg.seg, (step * kBlocks + b) * 32 + lane,
+                             static_cast<uint32_t>(gtile), c3),
+                  K);
+}
+
+// Walks one segment with the whole warp; r holds the Philox blocks of its
+// first step. After each step's positions are known, pre(tag, f) runs
+// (issue table loads), then the next step's Philox blocks are computed —
+// independent work that hides those loads — and then emit(tag, f) runs on
+// every lane (lanes may have no valid firing). On the last step next(sn)
+// fetches the following segment, whose first blocks are computed in place
+// of the next step's, so segment boundaries cost no exposed Philox latency.
+// Returns whether sg/r now describe a following segment.
+template <bool kBern, class Pre, class Emit, class Next>
+__device__ __forceinline__ bool segment_walk_t(Segment& sg, uint4 (&r)[kBlocks],
+                                               const RoundKeys& K, uint64_t gtile,
+                                               uint32_t t_log2, uint32_t lane, Pre&& pre,
+                                               Emit&& emit, Next&& next) {
   constexpr bool bern = kBern;
   const uint32_t n = sg.dist == 3 ? 3u : 15u;
   const uint32_t magic = n == 3 ? 0x5556u : 0x1112u;  // exact /n for values < n^3
   const uint32_t tmask = (1u << t_log2) - 1u;
-  const uint32_t c3 = (static_cast<uint32_t>(gtile >> 32) & 0xFFFFFFu) | (kDomChain << 24);
   uint32_t pos = 0;  // trials consumed (warp-uniform), < len <= 2^22
-  uint4 r[kBlocks];
-#pragma unroll
-  for (int b = 0; b < kBlocks; ++b)
-    r[b] = philox10(make_uint4(sg.seg, b * 32 + lane, static_cast<uint32_t>(gtile), c3), K);
   for (uint32_t draw = 0;; ++draw) {
     uint32_t incl[kSlots];
     uint32_t acc = 0;
@@ -222,31 +231,49 @@ __device__ __forceinline__ void segment_walk_t(const Segment& sg, const RoundKey
     pos += total;
     const bool more = pos < sg.len;
     pre(std::integral_constant<bool, kBern>{}, f);
-    // The next step's Philox blocks are independent of this step's table
-    // loads and atomics: computing them first lets the two overlap.
+    // The next step's (or segment's) Philox blocks are independent of this
+    // step's table loads and atomics: computing them first overlaps the two.
+    Segment sn;
+    bool have_next = false;
     if (more) {
 #pragma unroll
-      for (int b = 0; b < kBlocks; ++b)
-        r[b] = philox10(make_uint4(sg.seg, ((draw + 1) * kBlocks + b) * 32 + lane,
-                                   static_cast<uint32_t>(gtile), c3),
-                        K);
+      for (int b = 0; b < kBlocks; ++b) r[b] = segment_philox(sg, K, gtile, draw + 1, b, lane);
+    } else {
+      have_next = next(sn);
+      if (have_next) {
+#pragma unroll
+        for (int b = 0; b < kBlocks; ++b) r[b] = segment_philox(sn, K, gtile, 0, b, lane);
+      }
     }
     emit(std::integral_constant<bool, kBern>{}, f);
-    if (!more) return;
+    if (!more) {
+      if (have_next) sg = sn;
+      return have_next;
+    }
   }
 }
 
 // Bernoulli classes use all four words of a block as skips; DEPOLARIZE
 // classes use three and draw patterns from the fourth. The two shapes are
 // separate instantiations so neither pays for the other's slots.
-template <class Pre, class Emit>
-__device__ __forceinline__ void segment_walk(const Segment& sg, const RoundKeys& K, uint64_t gtile,
-                                             uint32_t t_log2, uint32_t lane, Pre&& pre,
-                                             Emit&& emit) {
-  if (sg.dist == 1)
-    segment_walk_t<true>(sg, K, gtile, t_log2, lane, pre, emit);
-  else
-    segment_walk_t<false>(sg, K, gtile, t_log2, lane, pre, emit);
+template <class Pre, class Emit, class Next>
+__device__ __forceinline__ bool segment_walk_chain(Segment& sg, uint4 (&r)[kBlocks],
+                                                   const RoundKeys& K, uint64_t gtile,
+                                                   uint32_t t_log2, uint32_t lane, Pre&& pre,
+                                                   Emit&& emit, Next&& next) {
+  if (sg.dist == 1) return segment_walk_t<true>(sg, r, K, gtile, t_log2, lane, pre, emit, next);
+  return segment_walk_t<false>(sg, r, K, gtile, t_log2, lane, pre, emit, next);
+}
+
+// One segment on its own (the standalone draw kernel).
+template <class Emit>
+__device__ __forceinline__ void segment_walk(Segment sg, const RoundKeys& K, uint64_t gtile,
+                                             uint32_t t_log2, uint32_t lane, Emit&& emit) {
+  uint4 r[kBlocks];
+#pragma unroll
+  for (int b = 0; b < kBlocks; ++b) r[b] = segment_philox(sg, K, gtile, 0, b, lane);
+  segment_walk_chain(sg, r, K, gtile, t_log2, lane, [](auto, const Fired&) {}, emit,
+                     [](Segment&) { return false; });
 }
 
 __device__ __forceinline__ void named_sync(uint32_t id, uint32_t n) {
@@ -288,7 +315,7 @@ __device__ __forceinline__ uint4 xor4(uint4 a, uint4 b) {
 // with 16-byte stores and zero the buffer for tile i+2. Named barriers
 // FULL[b] / EMPTY[b] hand the buffers back and forth. Event tables and row
 // tables are staged in shared memory when they fit.
-template <bool kStaged, bool kRowStaged, int kLp, bool kPadPred>
+template <bool kStaged, bool kRowStaged, int kLp, bool kPadPred, bool kU8>
 __global__ void __launch_bounds__(kFusedThreads, 1)
 k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, uint64_t n_shots,
          uint64_t* __restrict__ out, uint64_t ld, uint64_t tile_stride,
@@ -300,8 +327,12 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
   const bool with_counts = counts != nullptr;
   uint32_t* tiles = reinterpret_cast<uint32_t*>(smem);
   uint8_t* p = reinterpret_cast<uint8_t*>(tiles + 2 * tile_words);
+  // Flip counts: per (row, lane) partials when a warp walks one path per
+  // 128-shot column group (T = 4096: no cross-lane reduction per row),
+  // else one counter per row.
+  const uint32_t cnt_lanes = tw4 >= 32 ? 32u : 1u;
   uint32_t* cnt = reinterpret_cast<uint32_t*>(p);
-  p += align16(4ull * P.n_meas);
+  p += align16(4ull * P.n_meas * cnt_lanes);
   uint32_t* segctr = reinterpret_cast<uint32_t*>(p);  // per-buffer segment dispensers
   p += 16;
 
@@ -354,7 +385,7 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
     for (uint32_t i = threadIdx.x; i < (2 * tile_words) / 4; i += blockDim.x)
       t4[i] = make_uint4(0, 0, 0, 0);
     if (with_counts)
-      for (uint32_t i = threadIdx.x; i < P.n_meas; i += blockDim.x) cnt[i] = 0;
+      for (uint32_t i = threadIdx.x; i < P.n_meas * cnt_lanes; i += blockDim.x) cnt[i] = 0;
     if (threadIdx.x < 2) segctr[threadIdx.x] = 0;
   }
   __syncthreads();
@@ -404,14 +435,19 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
       const uint32_t spare = P.n_meas * tw;
       uint32_t seg = 0;
       Segment sg;
-      // Exact flip list of (class position, pattern): kLp u16 tile-word
-      // offsets padded with the spare row's. With kLp == 8 all of a step's
-      // lists are loaded before the next Philox blocks are computed (pre),
-      // so the L1/L2 latency hides under that arithmetic. Invalid slots load
-      // the all-padding list.
-      constexpr bool kPreload = kLp == 8 && !kPadPred;
-      constexpr int kLw = kLp > 0 ? kLp / 8 : 1;
-      uint4 lst[kSlots][kLw];
+      // Exact flip list of (class position, pattern): kLp entries padded
+      // with the spare row — u8 row indices when the tile has <= 256 rows
+      // (kU8: a list is 4-16 bytes, so the table stays in L1), else u32
+      // tile byte offsets (a flip is then one add + one shared XOR). Lists
+      // are loaded before the next Philox blocks are computed (pre) where
+      // registers allow, so the L1/L2 latency hides under that arithmetic;
+      // the rest are issued at the start of emit. Invalid slots load the
+      // all-padding list.
+      constexpr int kWords = kLp > 0 ? (kU8 ? kLp / 4 : kLp) : 1;  // u32 words per list
+      constexpr int kPre = kWords * kSlots <= 32 ? kSlots : (kWords <= 8 && !kPadPred) ? 4 : 0;
+      const uint32_t spare_b = spare * 4u;
+      const uint32_t row_b = tw * 4u;
+      uint32_t lst[kSlots][kWords];
       auto load_lists = [&](auto bern_tag, const Fired& f, int k0, int k1) {
         constexpr bool kB = decltype(bern_tag)::value;
 #pragma unroll
@@ -419,13 +455,28 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
           if (k < k0 || k >= k1 || (!kB && (k & 3) == 3)) continue;
           const uint32_t li =
               ((f.v >> k) & 1u) ? sg.pbase + f.g[k] * sg.npat + f.pat[k] - 1 : P.plist_dummy;
+          const uint32_t* src = reinterpret_cast<const uint32_t*>(PLIST) + static_cast<size_t>(li) * kWords;
+          if constexpr (kWords == 1) {
+            lst[k][0] = __ldg(src);
+          } else if constexpr (kWords == 2) {
+            const uint2 v = __ldg(reinterpret_cast<const uint2*>(src));
+            lst[k][0] = v.x;
+            lst[k][1] = v.y;
+          } else {
 #pragma unroll
-          for (int h = 0; h < kLw; ++h) lst[k][h] = __ldg(PLIST + static_cast<size_t>(li) * kLw + h);
+            for (int h = 0; h < kWords / 4; ++h) {
+              const uint4 v = __ldg(reinterpret_cast<const uint4*>(src) + h);
+              lst[k][4 * h] = v.x;
+              lst[k][4 * h + 1] = v.y;
+              lst[k][4 * h + 2] = v.z;
+              lst[k][4 * h + 3] = v.w;
+            }
+          }
         }
       };
       auto pre = [&](auto bern_tag, const Fired& f) {
-        if constexpr (kLp > 0 && kPreload) {
-          if (!(P.debug_mode & 1u)) load_lists(bern_tag, f, 0, kSlots);
+        if constexpr (kLp > 0 && kPre > 0) {
+          if (!(P.debug_mode & 1u)) load_lists(bern_tag, f, 0, kPre);
         }
       };
       auto emit = [&](auto bern_tag, const Fired& f) {
@@ -435,30 +486,32 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
           return;
         }
         if constexpr (kLp > 0) {
+          if constexpr (kPre > 0 && kPre < kSlots) load_lists(bern_tag, f, kPre, kSlots);
 #pragma unroll
           for (int half = 0; half < kSlots; half += 4) {
-            if constexpr (!kPreload) load_lists(bern_tag, f, half, half + 4);
+            if constexpr (kPre == 0) load_lists(bern_tag, f, half, half + 4);
 #pragma unroll
             for (int k = half; k < half + 4; ++k) {
               if (!kB && (k & 3) == 3) continue;
               const uint32_t wb = tile_s + ((f.shot[k] >> 5) << 2);
               const uint32_t bit = ((f.v >> k) & 1u) << (f.shot[k] & 31);
 #pragma unroll
-              for (int h = 0; h < kLw; ++h) {
-                const uint32_t ww[4] = {lst[k][h].x, lst[k][h].y, lst[k][h].z, lst[k][h].w};
-#pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                  const uint32_t row = (ww[e >> 1] >> (16 * (e & 1))) & 0xFFFFu;
-                  if (kPadPred) {
-                    // many firings per shot: skip padding so the ATOMS pipe
-                    // only carries real flips
-                    if (row != spare) atomicXor(tile + (f.shot[k] >> 5) + row, bit);
-                  } else {
-                    // padding XORs the spare row (never read)
-                    asm volatile("red.shared.xor.b32 [%0], %1;" ::"r"(wb + (row << 2)), "r"(bit)
-                                 : "memory");
-                  }
+              for (int e = 0; e < kLp; ++e) {
+                uint32_t a;
+                bool real;
+                if constexpr (kU8) {
+                  const uint32_t row = __byte_perm(lst[k][e >> 2], 0u, 0x4440u | (e & 3));
+                  a = wb + row * row_b;
+                  real = row != P.n_meas;
+                } else {
+                  a = wb + lst[k][e];
+                  real = lst[k][e] != spare_b;
                 }
+                // kPadPred (many firings per shot): skip padding so the ATOMS
+                // pipe only carries real flips; else padding XORs the spare
+                // row (never read).
+                if (!kPadPred || real)
+                  asm volatile("red.shared.xor.b32 [%0], %1;" ::"r"(a), "r"(bit) : "memory");
               }
             }
           }
@@ -481,13 +534,22 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
           }
         }
       };
-      for (;;) {
+      // Segments of this tile, taken from the tile's dispenser one after
+      // another; each walk hands over to the next on its last step.
+      auto next = [&](Segment& sn) {
         if (lane == 0) seg = atomicAdd(&segctr[b], 1u);
         seg = __shfl_sync(kFull, seg, 0);
-        if (seg >= P.n_seg_live || (P.debug_mode & 2u)) break;
-        segment_init(sg, CLS, P.n_cls_live, seg, P.t_log2);
-        segment_walk(sg, K, gtile, P.t_log2, lane, pre, emit);
+        if (seg >= P.n_seg_live || (P.debug_mode & 2u)) return false;
+        segment_init(sn, CLS, P.n_cls_live, seg, P.t_log2);
+        return true;
+      };
+      uint4 r[kBlocks];
+      bool have = next(sg);
+      if (have) {
+#pragma unroll
+        for (int bb = 0; bb < kBlocks; ++bb) r[bb] = segment_philox(sg, K, gtile, 0, bb, lane);
       }
+      while (have) have = segment_walk_chain(sg, r, K, gtile, P.t_log2, lane, pre, emit, next);
       if (P.timers && lane == 0) {  // gen: [0] waiting EMPTY, [1] working
         atomicAdd(reinterpret_cast<unsigned long long*>(P.timers) + 0, tw1 - tw0);
         atomicAdd(reinterpret_cast<unsigned long long*>(P.timers) + 1, clock64() - tw1);
@@ -497,6 +559,7 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
   } else {
     // ---------------- drain warps ----------------
     const uint32_t ct = threadIdx.x - n_gen * 32, nct = blockDim.x - n_gen * 32;
+    const uint32_t cnt_s = static_cast<uint32_t>(__cvta_generic_to_shared(cnt));
     const uint32_t ld_lo = static_cast<uint32_t>(ld), ld_hi = static_cast<uint32_t>(ld >> 32);
     for (uint32_t i = 0; i < n_my; ++i) {
       const uint32_t b = i & 1;
@@ -579,9 +642,10 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
                 }
               }
               if (with_counts) {
-                if (tw4 >= 32) {  // the whole warp walks this path: one atomic per row
-                  pc = __reduce_add_sync(kFull, pc);
-                  if (lane == 0 && pc) atomicAdd(&cnt[k], pc);
+                if (tw4 >= 32) {  // the whole warp walks this path: per-lane partials
+                  asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(cnt_s + ((k * 32 + lane) << 2)),
+                               "r"(pc)
+                               : "memory");
                 } else if (pc) {
                   atomicAdd(&cnt[k], pc);
                 }
@@ -613,8 +677,15 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
   }
   if (with_counts) {
     __syncthreads();
-    for (uint32_t i = threadIdx.x; i < P.n_meas; i += blockDim.x)
-      if (cnt[i]) atomicAdd(&counts[i], static_cast<unsigned long long>(cnt[i]));
+    if (cnt_lanes == 32) {  // one warp per row: sum the lane partials
+      for (uint32_t k = threadIdx.x >> 5; k < P.n_meas; k += blockDim.x >> 5) {
+        const uint32_t c = __reduce_add_sync(kFull, cnt[k * 32 + lane]);
+        if (lane == 0 && c) atomicAdd(&counts[k], static_cast<unsigned long long>(c));
+      }
+    } else {
+      for (uint32_t i = threadIdx.x; i < P.n_meas; i += blockDim.x)
+        if (cnt[i]) atomicAdd(&counts[i], static_cast<unsigned long long>(cnt[i]));
+    }
   }
 }
 
@@ -715,7 +786,7 @@ __global__ void d_segments(const DevPlan P, const RoundKeys K, uint64_t tile0, u
     const uint64_t base = static_cast<uint64_t>(t) << P.t_log2;
     Segment sg;
     segment_init(sg, P.cls, P.n_cls_all, seg, P.t_log2);
-    segment_walk(sg, K, tile0 + t, P.t_log2, lane, [](auto, const Fired&) {}, [&](auto, const Fired& f) {
+    segment_walk(sg, K, tile0 + t, P.t_log2, lane, [&](auto, const Fired& f) {
       for (int k = 0; k < kSlots; ++k) {
         if (!((f.v >> k) & 1u)) continue;
         const uint64_t j = base + f.shot[k];
@@ -944,11 +1015,11 @@ int persistent_grid(Kern kernel, const LaunchCfg& L, size_t smem, uint32_t n_til
   return 0;
 }
 
-template <bool kStaged, bool kRowStaged, int kLp, bool kPadPred = false>
+template <bool kStaged, bool kRowStaged, int kLp, bool kPadPred = false, bool kU8 = false>
 int launch_k1(const DevPlan& P, const LaunchCfg& L, const RoundKeys& K, uint64_t tile0,
               uint32_t n_tiles, uint64_t n_shots, uint64_t* out, uint64_t ld, uint64_t tstride,
               unsigned long long* cnt) {
-  auto kern = k1_fused<kStaged, kRowStaged, kLp, kPadPred>;
+  auto kern = k1_fused<kStaged, kRowStaged, kLp, kPadPred, kU8>;
   const size_t smem = fused_smem_bytes(P, P.t_log2, kStaged, kRowStaged);
   int grid = 0;
   const int threads = static_cast<int>(P.cta_threads);
@@ -964,7 +1035,7 @@ int launch_k1(const DevPlan& P, const LaunchCfg& L, const RoundKeys& K, uint64_t
 size_t fused_smem_bytes(const DevPlan& P, uint32_t t_log2, bool staged, bool row_staged) {
   const size_t tw = size_t{1} << (t_log2 - 5);
   size_t b = 2 * static_cast<size_t>(P.n_meas + 1) * tw * 4;       // tiles (+ spare row)
-  b += align16(4ull * P.n_meas) + 16;                               // counts, dispensers
+  b += align16(4ull * P.n_meas * (t_log2 >= 12 ? 32 : 1)) + 16;   // counts, dispensers
   if (row_staged) {
     b += align16(4ull * (P.n_meas + 1));
     b += align16(4ull * (P.n_paths + 1));
@@ -988,19 +1059,21 @@ int launch_fused_sample(const DevPlan& P, const LaunchCfg& L, uint64_t seed, uin
   const uint32_t n_tiles = static_cast<uint32_t>((n_shots + T - 1) / T);
   const RoundKeys K = expand_keys(seed);
   auto* cnt = reinterpret_cast<unsigned long long*>(counts);
-#define SP_K1(st, rs, lp) \
-  launch_k1<st, rs, lp>(P, L, K, tile0, n_tiles, n_shots, out, ld, tstride, cnt)
-#define SP_K1P(st, rs, lp) \
-  launch_k1<st, rs, lp, true>(P, L, K, tile0, n_tiles, n_shots, out, ld, tstride, cnt)
-  if (P.lp == 8 && P.pad_pred) return P.row_staged ? SP_K1P(false, true, 8) : SP_K1P(false, false, 8);
-  if (P.lp == 16 && P.pad_pred)
-    return P.row_staged ? SP_K1P(false, true, 16) : SP_K1P(false, false, 16);
-  if (P.lp == 8) return P.row_staged ? SP_K1(false, true, 8) : SP_K1(false, false, 8);
-  if (P.lp == 16) return P.row_staged ? SP_K1(false, true, 16) : SP_K1(false, false, 16);
-  if (P.staged) return P.row_staged ? SP_K1(true, true, 0) : SP_K1(true, false, 0);
-  return P.row_staged ? SP_K1(false, true, 0) : SP_K1(false, false, 0);
+#define SP_K1(st, rs, lp, pp, u8) \
+  launch_k1<st, rs, lp, pp, u8>(P, L, K, tile0, n_tiles, n_shots, out, ld, tstride, cnt)
+#define SP_K1R(lp, pp, u8) \
+  (P.row_staged ? SP_K1(false, true, lp, pp, u8) : SP_K1(false, false, lp, pp, u8))
+#define SP_K1L(lp) \
+  (P.pad_pred ? (P.u8 ? SP_K1R(lp, true, true) : SP_K1R(lp, true, false)) \
+              : (P.u8 ? SP_K1R(lp, false, true) : SP_K1R(lp, false, false)))
+  if (P.lp == 4) return SP_K1L(4);
+  if (P.lp == 8) return SP_K1L(8);
+  if (P.lp == 16) return SP_K1L(16);
+  if (P.staged) return P.row_staged ? SP_K1(true, true, 0, false, false) : SP_K1(true, false, 0, false, false);
+  return SP_K1R(0, false, false);
 #undef SP_K1
-#undef SP_K1P
+#undef SP_K1R
+#undef SP_K1L
 }
 
 int launch_fused_sample_compat(const DevPlan& P, const LaunchCfg& L, uint64_t seed,

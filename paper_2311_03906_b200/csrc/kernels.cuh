@@ -75,12 +75,15 @@ struct DevPlan {
   const uint4* desc = nullptr;
   const uint16_t* colrow = nullptr;
   uint64_t n_colrow = 0;
-  // Exact per-(group, pattern) flip lists in D space, padded with 0xFFFF to
-  // lp u16 rows (lp = 8 or 16; 0 = lists too long, use desc/colrow loops).
+  // Exact per-(group, pattern) flip lists in D space: lp entries padded
+  // with the spare row (lp = 4, 8 or 16; 0 = lists too long, use the
+  // desc/colrow loops). Entries are u8 row indices when n_meas < 256, else
+  // u32 tile byte offsets (row * tw * 4).
   // List of (class position g, pattern pi) = plist[(pbase + g*npat + pi-1)].
   uint32_t lp = 0;
   uint32_t pad_pred = 0;  // skip padding entries (many firings per shot) vs XOR the spare row
   uint32_t plist_dummy = 0;  // index of an all-padding list (invalid slots load it)
+  uint32_t u8 = 0;           // entries are u8 row indices (n_meas < 256), else u32 offsets
   const uint4* plist = nullptr;
   // Row reconstruction out[k] = d[k] ^ out[parent[k]] along the paths of a
   // heavy-path decomposition of the parent forest: path p lists rows
