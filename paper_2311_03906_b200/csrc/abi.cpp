@@ -423,56 +423,62 @@ void build_plan(sp_ctx* c) {
     return e;
   };
   const double seg_cost = env_long("SP_SEG_COST_PCT", 35) / 100.0;
-  std::vector<uint64_t> live_nseg(live_cls.size(), 1);
-  {
-    const long fe = env_long("SP_SEG_EVENTS", 0);
-    std::vector<double> lam(live_cls.size()), S(live_cls.size());
-    std::vector<uint64_t> nmin(live_cls.size()), nmax(live_cls.size());
+  const long seg_fe = env_long("SP_SEG_EVENTS", 0);
+  std::vector<double> seg_lam(live_cls.size()), seg_S(live_cls.size());
+  std::vector<uint64_t> seg_nmin(live_cls.size()), seg_nmax(live_cls.size());
+  // Slice counts of the live classes (in live_cls order) for gw generator warps.
+  auto plan_segments = [&](uint32_t gw) {
+    std::vector<uint64_t> nseg(live_cls.size(), 1);
     auto cost = [&](size_t c, uint64_t n) {
-      return n * (exp_steps(lam[c] / n, S[c]) + seg_cost);
+      return n * (exp_steps(seg_lam[c] / n, seg_S[c]) + seg_cost);
     };
     uint64_t total = 0;
     for (size_t c = 0; c < live_cls.size(); ++c) {
       const uint64_t trials = live_cls[c].groups.size() * T;
-      lam[c] = trials * live_cls[c].p;
-      S[c] = 32.0 * (live_cls[c].dist == SP_DIST_BERNOULLI ? 8 : 6);
-      nmin[c] = std::max<uint64_t>(1, (trials + 4194303) / 4194304);
-      nmax[c] = std::max<uint64_t>(nmin[c], trials / 32);
-      uint64_t best = nmin[c];
-      if (fe > 0) {
-        best = static_cast<uint64_t>(std::ceil(lam[c] / fe));
+      seg_lam[c] = trials * live_cls[c].p;
+      seg_S[c] = 32.0 * (live_cls[c].dist == SP_DIST_BERNOULLI ? 8 : 6);
+      seg_nmin[c] = std::max<uint64_t>(1, (trials + 4194303) / 4194304);
+      seg_nmax[c] = std::max<uint64_t>(seg_nmin[c], trials / 32);
+      uint64_t best = seg_nmin[c];
+      if (seg_fe > 0) {
+        best = static_cast<uint64_t>(std::ceil(seg_lam[c] / seg_fe));
       } else {
         double bc = cost(c, best);
-        const uint64_t hi = std::min<uint64_t>(nmax[c], static_cast<uint64_t>(2 * lam[c] / S[c]) + 2);
-        for (uint64_t n = nmin[c] + 1; n <= hi; ++n) {
+        const uint64_t hi =
+            std::min<uint64_t>(seg_nmax[c], static_cast<uint64_t>(2 * seg_lam[c] / seg_S[c]) + 2);
+        for (uint64_t n = seg_nmin[c] + 1; n <= hi; ++n) {
           const double cn = cost(c, n);
           if (cn < bc) { bc = cn; best = n; }
         }
       }
-      live_nseg[c] = std::min(std::max(best, nmin[c]), nmax[c]);
-      total += live_nseg[c];
+      nseg[c] = std::min(std::max(best, seg_nmin[c]), seg_nmax[c]);
+      total += nseg[c];
     }
-    const uint64_t min_total =
-        fe > 0 ? 0 : static_cast<uint64_t>(env_long("SP_SEG_MIN", d.gen_warps));
+    const uint64_t min_total = seg_fe > 0 ? 0 : static_cast<uint64_t>(env_long("SP_SEG_MIN", gw));
     while (total < min_total) {  // split where it costs the fewest extra steps
       size_t arg = live_cls.size();
       double dmin = 0;
       for (size_t c = 0; c < live_cls.size(); ++c) {
-        if (live_nseg[c] >= nmax[c]) continue;
-        const double dc = cost(c, live_nseg[c] + 1) - cost(c, live_nseg[c]);
+        if (nseg[c] >= seg_nmax[c]) continue;
+        const double dc = cost(c, nseg[c] + 1) - cost(c, nseg[c]);
         if (arg == live_cls.size() || dc < dmin) { dmin = dc; arg = c; }
       }
       if (arg == live_cls.size()) break;
-      ++live_nseg[arg];
+      ++nseg[arg];
       ++total;
     }
+    return nseg;
+  };
+  std::vector<uint64_t> live_nseg = plan_segments(d.gen_warps);
+  {
     // Longest slices first: warps take slices in id order, so a warp that
-    // finishes early picks up a short one.
+    // finishes early picks up a short one. (The order is fixed here; the
+    // launch autotune below only changes slice counts.)
     std::vector<size_t> ord(live_cls.size());
     std::vector<double> steps(live_cls.size());
     for (size_t c = 0; c < ord.size(); ++c) {
       ord[c] = c;
-      steps[c] = exp_steps(lam[c] / live_nseg[c], S[c]);
+      steps[c] = exp_steps(seg_lam[c] / live_nseg[c], seg_S[c]);
     }
     std::stable_sort(ord.begin(), ord.end(), [&](size_t a, size_t b) { return steps[a] > steps[b]; });
     std::vector<Cls> cls2;
@@ -494,7 +500,6 @@ void build_plan(sp_ctx* c) {
   // pattern's set symbols, as row * tw offsets.
   std::vector<std::vector<uint16_t>> plists;
   size_t max_plist = 0;
-  uint64_t n_chains = 0, n_chains_live = 0;
   auto add_classes = [&](const std::vector<Cls>& cls, bool live) {
     for (size_t c = 0; c < cls.size(); ++c) {
       const Cls& cl = cls[c];
@@ -504,19 +509,6 @@ void build_plan(sp_ctx* c) {
       ci.clg = static_cast<float>(0.69314718055994531 / std::log1p(-cl.p));
       ci.goff = static_cast<uint32_t>(cls_groups.size());
       ci.trials = cl.groups.size() * T;
-      uint64_t n_seg = 0;
-      if (live) {
-        n_seg = live_nseg[c];
-      } else {
-        double len = std::ceil(E / cl.p);
-        len = std::min(std::max(len, 32.0), 4194304.0);  // kernel skips clamp at 2^22
-        n_seg = std::max<uint64_t>((ci.trials + static_cast<uint64_t>(len) - 1) /
-                                       static_cast<uint64_t>(len), 1);
-      }
-      ci.L = (ci.trials + n_seg - 1) / n_seg;
-      ci.n_seg = static_cast<uint32_t>(n_seg);
-      ci.seg_off = static_cast<uint32_t>(n_chains);
-      n_chains += n_seg;
       ci.npat = cl.dist == SP_DIST_DEPOLARIZE2 ? 15 : cl.dist == SP_DIST_DEPOLARIZE1 ? 3 : 1;
       ci.pbase = static_cast<uint32_t>(plists.size());
       cls_info.push_back(ci);
@@ -558,9 +550,34 @@ void build_plan(sp_ctx* c) {
     }
   };
   add_classes(live_cls, true);
-  n_chains_live = n_chains;
   add_classes(dead_cls, false);
-  if (n_chains >= (1ull << 32)) throw std::invalid_argument("too many sampling chains");
+  // Segment table: live classes get the planned slice counts, dead ones
+  // (walked only by the standalone draw kernel) ~E firings per slice.
+  auto apply_segments = [&](const std::vector<uint64_t>& nseg_live) {
+    uint64_t n_chains = 0;
+    for (size_t c = 0; c < cls_info.size(); ++c) {
+      ClassInfo& ci = cls_info[c];
+      uint64_t n_seg = 0;
+      if (c < live_cls.size()) {
+        n_seg = nseg_live[c];
+      } else {
+        const double pc = dead_cls[c - live_cls.size()].p;
+        double len = std::ceil(E / pc);
+        len = std::min(std::max(len, 32.0), 4194304.0);  // kernel skips clamp at 2^22
+        n_seg = std::max<uint64_t>((ci.trials + static_cast<uint64_t>(len) - 1) /
+                                       static_cast<uint64_t>(len), 1);
+      }
+      ci.L = (ci.trials + n_seg - 1) / n_seg;
+      ci.n_seg = static_cast<uint32_t>(n_seg);
+      ci.seg_off = static_cast<uint32_t>(n_chains);
+      n_chains += n_seg;
+      if (c + 1 == live_cls.size()) d.n_seg_live = static_cast<uint32_t>(n_chains);
+    }
+    if (live_cls.empty()) d.n_seg_live = 0;
+    if (n_chains >= (1ull << 32)) throw std::invalid_argument("too many sampling chains");
+    d.n_seg_all = static_cast<uint32_t>(n_chains);
+    d.cls = c->b_cls.upload(cls_info, s);
+  };
 
   std::vector<uint32_t> g_first(G), g_arity(G);
   std::vector<uint8_t> g_dist(G);
@@ -596,9 +613,7 @@ void build_plan(sp_ctx* c) {
     d.coin_rows = c->b_coin_rows.upload(coin_rows, s);
   }
   d.n_cls_all = static_cast<uint32_t>(cls_info.size());
-  d.n_seg_live = static_cast<uint32_t>(n_chains_live);
-  d.n_seg_all = static_cast<uint32_t>(n_chains);
-  d.cls = c->b_cls.upload(cls_info, s);
+  apply_segments(live_nseg);
   d.cls_groups = c->b_cls_groups.upload(cls_groups, s);
   d.desc = c->b_desc.upload(desc, s);
   d.colrow = c->b_colrow.upload(colrow16, s);
@@ -706,6 +721,66 @@ void build_plan(sp_ctx* c) {
     d.timers = c->b_timers.upload(z, s);
   }
   ck(cudaStreamSynchronize(s), "plan upload");
+
+  // Launch autotune: the generator/drain warp split (and with it the slice
+  // counts) is measured, not modelled — a few short launches of the fused
+  // kernel over ~6 tiles per CTA for the candidates around the model's
+  // pick. SP_GEN_WARPS fixes the split; SP_AUTOTUNE=0 keeps the model's.
+  if (c->fused_ok && !live_cls.empty() && n_meas > 0 && env_long("SP_GEN_WARPS", 0) == 0 &&
+      env_long("SP_AUTOTUNE", 1) != 0) {
+    const long n_warps = d.cta_threads / 32;
+    const uint32_t gw0 = d.gen_warps;
+    std::vector<uint32_t> cand{gw0};
+    for (long dg : {-1L, 1L, -2L, 2L}) {
+      const long g = static_cast<long>(gw0) + dg;
+      if (g >= n_warps / 2 && g <= n_warps - 2) cand.push_back(static_cast<uint32_t>(g));
+    }
+    const uint64_t cal_shots = (static_cast<uint64_t>(c->L.num_sms) * d.cta_per_sm * 10) << d.t_log2;
+    const uint64_t ldw = cal_shots / 64;
+    uint64_t* buf = nullptr;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    ck(cudaMalloc(reinterpret_cast<void**>(&buf), n_meas * ldw * 8), "cudaMalloc (autotune)");
+    ck(cudaEventCreate(&e0), "cudaEventCreate");
+    ck(cudaEventCreate(&e1), "cudaEventCreate");
+    float best_ms = 0.f;
+    uint32_t best = gw0;
+    std::vector<uint64_t> best_nseg = live_nseg;
+    try {
+      for (uint32_t gw : cand) {
+        d.gen_warps = gw;
+        const std::vector<uint64_t> ns = plan_segments(gw);
+        apply_segments(ns);
+        float t = 0.f;
+        for (int rep = 0; rep < 4; ++rep) {
+          ck(cudaEventRecord(e0, s), "cudaEventRecord");
+          if (launch_fused_sample(d, c->L, 0x5EEDull + rep, 0, cal_shots, buf, ldw, nullptr) < 0)
+            throw CudaError("autotune launch failed");
+          ck(cudaEventRecord(e1, s), "cudaEventRecord");
+          ck(cudaEventSynchronize(e1), "cudaEventSynchronize");
+          float ms = 0.f;
+          ck(cudaEventElapsedTime(&ms, e0, e1), "cudaEventElapsedTime");
+          if (rep > 0) t = rep == 1 ? ms : std::min(t, ms);  // rep 0 warms up
+        }
+        if (gw == gw0 || t < best_ms * 0.99f) {
+          best_ms = t;
+          best = gw;
+          best_nseg = ns;
+        }
+      }
+    } catch (...) {
+      cudaFree(buf);
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+      throw;
+    }
+    cudaFree(buf);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    d.gen_warps = best;
+    apply_segments(best_nseg);
+    if (d.timers) d.timers = c->b_timers.upload(std::vector<long long>(4, 0), s);
+    ck(cudaStreamSynchronize(s), "plan upload");
+  }
   c->plan_ready = true;
 }
 

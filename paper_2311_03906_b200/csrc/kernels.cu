@@ -560,7 +560,8 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
     // ---------------- drain warps ----------------
     const uint32_t ct = threadIdx.x - n_gen * 32, nct = blockDim.x - n_gen * 32;
     const uint32_t cnt_s = static_cast<uint32_t>(__cvta_generic_to_shared(cnt));
-    const uint32_t ld_lo = static_cast<uint32_t>(ld), ld_hi = static_cast<uint32_t>(ld >> 32);
+    // row stride in bytes for the fast path's 32x32->64 address multiply
+    const uint32_t ldb = ld < (1ull << 29) ? static_cast<uint32_t>(ld * 8) : 0u;
     for (uint32_t i = 0; i < n_my; ++i) {
       const uint32_t b = i & 1;
       const uint64_t t_local = blockIdx.x + static_cast<uint64_t>(i) * gridDim.x;
@@ -574,7 +575,7 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
       const uint64_t valid = min(static_cast<uint64_t>(1) << P.t_log2, n_shots - first);
       const uint32_t vq = static_cast<uint32_t>((valid + 127) >> 7);
       const uint32_t rem = static_cast<uint32_t>(valid & 127);
-      const bool fast = vec && (valid == (static_cast<uint64_t>(1) << P.t_log2));
+      const bool fast = vec && ldb != 0 && (valid == (static_cast<uint64_t>(1) << P.t_log2));
       // Rows along parent paths (heavy-path decomposition of the L forest):
       // one thread walks a path top-down for one 128-shot column, carrying
       // the running row value; a path's head waits only for its parent's
@@ -593,69 +594,76 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
           const uint32_t xe = act ? PPTR[pth + 1] : 0;
           uint32_t x = act ? PPTR[pth] : 0;
           uint64_t* obase = out + t_local * tile_stride + 2 * q;
-          // Walks the path: row = tile word ^ parent row; keep or clear the
-          // tile word, store 16 bytes to HBM, optionally count.
-          auto walk = [&](auto fast_tag) {
-            constexpr bool kFast = decltype(fast_tag)::value;  // full tile, 16-byte aligned
-            // path_rows is padded by one entry, so the next row can always
-            // be prefetched (past a path's end the value is discarded).
-            uint32_t e = PROWS[x];
-            uint4 cur = t4[((e & 0xFFFFu) << tw4_log2) + q];
-            for (; x < xe; ++x) {
-              const uint32_t en = PROWS[x + 1];
-              const uint4 nxt = t4[((en & 0xFFFFu) << tw4_log2) + q];
-              const uint32_t k = e & 0xFFFFu;
-              uint4 v = xor4(cur, prev);
-              // Rows with light children keep their final value for a later
-              // round; all others are cleared for tile i+2 right away.
-              sts_or_zero(t4_s + (((k << tw4_log2) + q) << 4), v, e >> 31);
-              prev = v;
-              e = en;
-              cur = nxt;
-              uint64_t* o = obase + (static_cast<uint64_t>(k) * ld_lo +
-                                     (static_cast<uint64_t>(k * ld_hi) << 32));
-              uint32_t pc = 0;
-              if constexpr (kFast) {
-                *reinterpret_cast<uint4*>(o) = v;
-                if (with_counts) pc = __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
-              } else {
-                if (q < vq) {
-                  bool two = true;  // whether the item's second u64 word is inside the tile
-                  if (q == vq - 1 && rem) {
-                    const uint32_t m[4] = {
-                        rem >= 32 ? kFull : (1u << rem) - 1,
-                        rem >= 64 ? kFull : rem > 32 ? (1u << (rem - 32)) - 1 : 0u,
-                        rem >= 96 ? kFull : rem > 64 ? (1u << (rem - 64)) - 1 : 0u,
-                        rem > 96 ? (1u << (rem - 96)) - 1 : 0u};
-                    v.x &= m[0]; v.y &= m[1]; v.z &= m[2]; v.w &= m[3];
-                    two = rem > 64;
-                  }
-                  const uint64_t w0 = (static_cast<uint64_t>(v.y) << 32) | v.x;
-                  const uint64_t w1 = (static_cast<uint64_t>(v.w) << 32) | v.z;
-                  if (vec && two) {
-                    *reinterpret_cast<ulonglong2*>(o) = make_ulonglong2(w0, w1);
-                  } else {
-                    o[0] = w0;
-                    if (two) o[1] = w1;
-                  }
-                  if (with_counts) pc = __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
-                }
+          uint8_t* obase_b = reinterpret_cast<uint8_t*>(obase);
+          // One row of the path: row = tile word ^ parent row; keep or clear
+          // the tile word, store 16 bytes to HBM, optionally count.
+          auto row_step = [&](auto fast_tag, auto wp_tag, uint32_t e, uint4 c) {
+            constexpr bool kFast = decltype(fast_tag)::value;  // full tile, aligned, ldb < 2^32
+            constexpr bool kWarpPath = decltype(wp_tag)::value;  // a warp per path (T = 4096)
+            const uint32_t k = e & 0xFFFFu;
+            uint4 v = xor4(c, prev);
+            // Rows with light children keep their final value for a later
+            // round; all others are cleared for tile i+2 right away.
+            sts_or_zero(t4_s + (((k << tw4_log2) + q) << 4), v, e >> 31);
+            prev = v;
+            uint32_t pc = 0;
+            if constexpr (kFast) {
+              *reinterpret_cast<uint4*>(obase_b + static_cast<uint64_t>(k) * ldb) = v;
+              if (with_counts) pc = __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
+            } else if (q < vq) {
+              uint64_t* o = obase + static_cast<uint64_t>(k) * ld;
+              bool two = true;  // whether the item's second u64 word is inside the tile
+              if (q == vq - 1 && rem) {
+                const uint32_t m[4] = {
+                    rem >= 32 ? kFull : (1u << rem) - 1,
+                    rem >= 64 ? kFull : rem > 32 ? (1u << (rem - 32)) - 1 : 0u,
+                    rem >= 96 ? kFull : rem > 64 ? (1u << (rem - 64)) - 1 : 0u,
+                    rem > 96 ? (1u << (rem - 96)) - 1 : 0u};
+                v.x &= m[0]; v.y &= m[1]; v.z &= m[2]; v.w &= m[3];
+                two = rem > 64;
               }
-              if (with_counts) {
-                if (tw4 >= 32) {  // the whole warp walks this path: per-lane partials
-                  asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(cnt_s + ((k * 32 + lane) << 2)),
-                               "r"(pc)
-                               : "memory");
-                } else if (pc) {
-                  atomicAdd(&cnt[k], pc);
-                }
+              const uint64_t w0 = (static_cast<uint64_t>(v.y) << 32) | v.x;
+              const uint64_t w1 = (static_cast<uint64_t>(v.w) << 32) | v.z;
+              if (vec && two) {
+                *reinterpret_cast<ulonglong2*>(o) = make_ulonglong2(w0, w1);
+              } else {
+                o[0] = w0;
+                if (two) o[1] = w1;
+              }
+              if (with_counts) pc = __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
+            }
+            if (with_counts) {
+              if constexpr (kWarpPath) {  // per-lane partials, no reduction here
+                asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(cnt_s + ((k * 32 + lane) << 2)),
+                             "r"(pc)
+                             : "memory");
+              } else {
+                if (pc) atomicAdd(&cnt[k], pc);
               }
             }
           };
-          if (fast)
-            walk(std::true_type{});
-          else
-            walk(std::false_type{});
+          // Two rows per iteration with the next row's entry and tile word
+          // prefetched (path_rows is padded, so x + 2 <= n_meas is readable).
+          auto walk = [&](auto fast_tag, auto wp_tag) {
+            uint32_t ea = PROWS[x];
+            uint4 ca = t4[((ea & 0xFFFFu) << tw4_log2) + q];
+            for (; x + 2 <= xe; x += 2) {
+              const uint32_t eb = PROWS[x + 1];
+              const uint4 cb = t4[((eb & 0xFFFFu) << tw4_log2) + q];
+              row_step(fast_tag, wp_tag, ea, ca);
+              ea = PROWS[x + 2];
+              ca = t4[((ea & 0xFFFFu) << tw4_log2) + q];
+              row_step(fast_tag, wp_tag, eb, cb);
+            }
+            if (x < xe) row_step(fast_tag, wp_tag, ea, ca);
+          };
+          if (tw4 >= 32) {
+            if (fast) walk(std::true_type{}, std::true_type{});
+            else walk(std::false_type{}, std::true_type{});
+          } else {
+            if (fast) walk(std::true_type{}, std::false_type{});
+            else walk(std::false_type{}, std::false_type{});
+          }
         }
         // A later round must not start before every row a light child
         // reads is final.

@@ -12,7 +12,7 @@ import json
 for l in open("gpurun_out/sweep2.jsonl"):
     d = json.loads(l)
     p = d["plan"]
-    print(f'{d["config"]:5s} tiled={int(d["tiled"])} {d["env"]} ms={d["ms_median"]:.4f} GBps={d["GBps"]:.0f} '
+    print(f'{d["config"]:5s} tiled={int(d["tiled"])} counts={int(d.get("counts", 0))} {d["env"]} ms={d["ms_median"]:.4f} GBps={d["GBps"]:.0f} '
           f'T={p["shot_tile"]} gw={p["gen_warps"]} seg={p["n_segments"]} lp={p["lp"]} pp={p["pad_pred"]}'
           + (f' timers={d["timers"]}' if d.get("timers") else ''))
 PY

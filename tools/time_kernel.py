@@ -53,7 +53,7 @@ def main():
     ms = ts[len(ts) // 2]
     bytes_ = init.n_meas * n / 8
     env = {k: v for k, v in os.environ.items() if k.startswith("SP_")}
-    print(json.dumps({"config": a.config, "tiled": a.tiled, "shots": n, "T": T, "env": env,
+    print(json.dumps({"config": a.config, "tiled": a.tiled, "counts": a.counts, "shots": n, "T": T, "env": env,
                       "ms_median": ms,
                       "ms_min": ts[0], "GBps": bytes_ / ms / 1e6,
                       "bits_per_s": init.n_meas * n / ms * 1e3, "timers": timers,
