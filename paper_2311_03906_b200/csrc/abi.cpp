@@ -407,7 +407,7 @@ void build_plan(sp_ctx* c) {
   // Segments: each class's flattened (group, shot) space of a tile is cut
   // into slices (<= 2^22 trials, >= 32), one warp walk each. A walk over a
   // slice holding N firings takes floor(N / S) + 1 steps of S slots (S =
-  // 32 lanes x 8 skips, or x 6 for DEPOLARIZE), so the slice count per class
+  // 32 lanes x 8 skips), so the slice count per class
   // minimises expected steps + a fixed per-slice cost (init, first Philox
   // latency), subject to enough slices per tile to keep every generator warp
   // busy with two tiles in flight. SP_SEG_EVENTS=E forces ~E firings/slice.
@@ -436,7 +436,7 @@ void build_plan(sp_ctx* c) {
     for (size_t c = 0; c < live_cls.size(); ++c) {
       const uint64_t trials = live_cls[c].groups.size() * T;
       seg_lam[c] = trials * live_cls[c].p;
-      seg_S[c] = 32.0 * (live_cls[c].dist == SP_DIST_BERNOULLI ? 8 : 6);
+      seg_S[c] = 32.0 * 8;
       seg_nmin[c] = std::max<uint64_t>(1, (trials + 4194303) / 4194304);
       seg_nmax[c] = std::max<uint64_t>(seg_nmin[c], trials / 32);
       uint64_t best = seg_nmin[c];
@@ -633,22 +633,27 @@ void build_plan(sp_ctx* c) {
       // the spare tile row (row n_meas), absorbed and never read; one extra
       // all-padding list (index plists.size()) stands in for invalid slots.
       d.plist_dummy = static_cast<uint32_t>(plists.size());
-      d.u8 = n_meas + 1 <= 256 && env_long("SP_U8", 1) != 0;
-      std::vector<uint4> packed;
-      if (d.u8) {
-        std::vector<uint8_t> flat((plists.size() + 1) * d.lp, static_cast<uint8_t>(n_meas));
-        for (size_t i = 0; i < plists.size(); ++i)
-          for (size_t j = 0; j < plists[i].size(); ++j)
-            flat[i * d.lp + j] = static_cast<uint8_t>(plists[i][j] / d.tw);
-        packed.resize((flat.size() + 15) / 16);
-        std::memcpy(packed.data(), flat.data(), flat.size());
-      } else {
-        std::vector<uint32_t> flat((plists.size() + 1) * d.lp, static_cast<uint32_t>(n_meas * d.tw * 4));
-        for (size_t i = 0; i < plists.size(); ++i)
-          for (size_t j = 0; j < plists[i].size(); ++j) flat[i * d.lp + j] = 4u * plists[i][j];
-        packed.resize(flat.size() / 4);
-        std::memcpy(packed.data(), flat.data(), flat.size() * 4);
-      }
+      const uint64_t tile_bytes = (n_meas * d.tw + spare_words(d.tw)) * 4;
+      d.entry_bytes = n_meas < 256 ? 1 : tile_bytes <= 65536 ? 2 : 4;
+      if (const long fe = env_long("SP_ENTRY_BYTES", 0); fe == 2 || fe == 4) d.entry_bytes = fe;
+      if (d.entry_bytes == 2 && tile_bytes > 65536) d.entry_bytes = 4;
+      // padding: spare-region offsets varied per list and entry, so the
+      // padding XORs of a warp spread over the banks (u8: the spare row)
+      auto entry = [&](size_t i, size_t j) -> uint32_t {
+        if (i < plists.size() && j < plists[i].size())
+          return d.entry_bytes == 1 ? plists[i][j] / d.tw : 4u * plists[i][j];
+        if (d.entry_bytes == 1) return static_cast<uint32_t>(n_meas);
+        return 4u * static_cast<uint32_t>(n_meas * d.tw + ((i * 7 + j * 13) & 31));
+      };
+      const size_t n_ent = (plists.size() + 1) * d.lp;
+      std::vector<uint8_t> bytes(((n_ent * d.entry_bytes) + 15) & ~size_t{15}, 0);
+      for (size_t i = 0; i <= plists.size(); ++i)
+        for (size_t j = 0; j < d.lp; ++j) {
+          const uint32_t v = entry(i, j);
+          std::memcpy(bytes.data() + (i * d.lp + j) * d.entry_bytes, &v, d.entry_bytes);  // little-endian
+        }
+      std::vector<uint4> packed(bytes.size() / 16);
+      std::memcpy(packed.data(), bytes.data(), bytes.size());
       d.plist = c->b_plist.upload(packed, s);
     }
   }
@@ -723,49 +728,68 @@ void build_plan(sp_ctx* c) {
   ck(cudaStreamSynchronize(s), "plan upload");
 
   // Launch autotune: the generator/drain warp split (and with it the slice
-  // counts) is measured, not modelled — a few short launches of the fused
-  // kernel over ~6 tiles per CTA for the candidates around the model's
-  // pick. SP_GEN_WARPS fixes the split; SP_AUTOTUNE=0 keeps the model's.
-  if (c->fused_ok && !live_cls.empty() && n_meas > 0 && env_long("SP_GEN_WARPS", 0) == 0 &&
+  // counts) and the padded-XOR mode are measured, not modelled — a few short
+  // launches of the fused kernel over ~16 tiles per CTA: first the padding
+  // mode at the model's split, then the splits around it. SP_GEN_WARPS /
+  // SP_PAD_PRED fix a choice; SP_AUTOTUNE=0 keeps the model's.
+  const bool fix_gw = env_long("SP_GEN_WARPS", 0) != 0;
+  const bool fix_pp = env_long("SP_PAD_PRED", -1) >= 0 || d.lp == 0;
+  if (c->fused_ok && !live_cls.empty() && n_meas > 0 && !(fix_gw && fix_pp) &&
       env_long("SP_AUTOTUNE", 1) != 0) {
     const long n_warps = d.cta_threads / 32;
-    const uint32_t gw0 = d.gen_warps;
-    std::vector<uint32_t> cand{gw0};
-    for (long dg : {-1L, 1L, -2L, 2L}) {
-      const long g = static_cast<long>(gw0) + dg;
-      if (g >= n_warps / 2 && g <= n_warps - 2) cand.push_back(static_cast<uint32_t>(g));
-    }
-    const uint64_t cal_shots = (static_cast<uint64_t>(c->L.num_sms) * d.cta_per_sm * 10) << d.t_log2;
+    const uint64_t cal_shots = (static_cast<uint64_t>(c->L.num_sms) * d.cta_per_sm * 16) << d.t_log2;
     const uint64_t ldw = cal_shots / 64;
     uint64_t* buf = nullptr;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     ck(cudaMalloc(reinterpret_cast<void**>(&buf), n_meas * ldw * 8), "cudaMalloc (autotune)");
     ck(cudaEventCreate(&e0), "cudaEventCreate");
     ck(cudaEventCreate(&e1), "cudaEventCreate");
-    float best_ms = 0.f;
-    uint32_t best = gw0;
-    std::vector<uint64_t> best_nseg = live_nseg;
+    auto time_launch = [&]() {
+      float t = 0.f;
+      for (int rep = 0; rep < 4; ++rep) {
+        ck(cudaEventRecord(e0, s), "cudaEventRecord");
+        // tiled layout: contiguous stores, so the kernel's own balance decides
+        if (launch_fused_sample(d, c->L, 0x5EEDull + rep, 0, cal_shots, buf, ldw, nullptr, true) < 0)
+          throw CudaError("autotune launch failed");
+        ck(cudaEventRecord(e1, s), "cudaEventRecord");
+        ck(cudaEventSynchronize(e1), "cudaEventSynchronize");
+        float ms = 0.f;
+        ck(cudaEventElapsedTime(&ms, e0, e1), "cudaEventElapsedTime");
+        if (rep > 0) t = rep == 1 ? ms : std::min(t, ms);  // rep 0 warms up
+      }
+      return t;
+    };
     try {
-      for (uint32_t gw : cand) {
-        d.gen_warps = gw;
-        const std::vector<uint64_t> ns = plan_segments(gw);
-        apply_segments(ns);
-        float t = 0.f;
-        for (int rep = 0; rep < 4; ++rep) {
-          ck(cudaEventRecord(e0, s), "cudaEventRecord");
-          if (launch_fused_sample(d, c->L, 0x5EEDull + rep, 0, cal_shots, buf, ldw, nullptr) < 0)
-            throw CudaError("autotune launch failed");
-          ck(cudaEventRecord(e1, s), "cudaEventRecord");
-          ck(cudaEventSynchronize(e1), "cudaEventSynchronize");
-          float ms = 0.f;
-          ck(cudaEventElapsedTime(&ms, e0, e1), "cudaEventElapsedTime");
-          if (rep > 0) t = rep == 1 ? ms : std::min(t, ms);  // rep 0 warms up
+      if (!fix_pp) {
+        const uint32_t pp0 = d.pad_pred;
+        const float t0 = time_launch();
+        d.pad_pred = !pp0;
+        const float t1 = time_launch();
+        if (!(t1 < t0 * 0.99f)) d.pad_pred = pp0;
+      }
+      if (!fix_gw) {
+        const uint32_t gw0 = d.gen_warps;
+        std::vector<uint32_t> cand{gw0};
+        for (long dg : {-1L, 1L, -2L, 2L}) {
+          const long g = static_cast<long>(gw0) + dg;
+          if (g >= n_warps / 2 && g <= n_warps - 2) cand.push_back(static_cast<uint32_t>(g));
         }
-        if (gw == gw0 || t < best_ms * 0.99f) {
-          best_ms = t;
-          best = gw;
-          best_nseg = ns;
+        float best_ms = 0.f;
+        uint32_t best = gw0;
+        std::vector<uint64_t> best_nseg = live_nseg;
+        for (uint32_t gw : cand) {
+          d.gen_warps = gw;
+          const std::vector<uint64_t> ns = plan_segments(gw);
+          apply_segments(ns);
+          const float t = time_launch();
+          if (gw == gw0 || t < best_ms * 0.99f) {
+            best_ms = t;
+            best = gw;
+            best_nseg = ns;
+          }
         }
+        d.gen_warps = best;
+        apply_segments(best_nseg);
       }
     } catch (...) {
       cudaFree(buf);
@@ -776,8 +800,6 @@ void build_plan(sp_ctx* c) {
     cudaFree(buf);
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
-    d.gen_warps = best;
-    apply_segments(best_nseg);
     if (d.timers) d.timers = c->b_timers.upload(std::vector<long long>(4, 0), s);
     ck(cudaStreamSynchronize(s), "plan upload");
   }

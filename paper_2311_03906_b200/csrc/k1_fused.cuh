@@ -1,0 +1,444 @@
+// K1, the fused warp-specialised Philox sampler, as a template over its
+// launch shape. Instantiated per (flip-list length, entry width) in separate
+// units (k1_inst.cu, built once per variant) so the variants compile in
+// parallel; kernels.cu dispatches to them through launch_k1.
+#pragma once
+
+#include "device_common.cuh"
+
+namespace symphase {
+namespace {
+
+// ---- K1: fused, warp-specialised Philox sampler ---------------------------
+//
+// The planner rewrites M_sym = L·D (abi.cpp, chain transform): each row k has
+// at most one earlier parent row p(k) and D row k = row k XOR row p(k), which
+// for syndrome-extraction circuits is the detector-like difference of
+// consecutive rounds — far fewer symbols per column. The kernel samples in
+// D space and rebuilds M rows level by level (out[k] = d[k] ^ out[p(k)]).
+//
+// Per CTA: two shared-memory accumulation tiles [n_meas][T/32] u32 (double
+// buffer) and two coin buffers [n_dense+1][T/32]. Generator warps walk the
+// geometric-skip segments of tile i (warp-cooperative) and XOR each fired
+// symbol's D column into tile[i&1] with shared atomics; drain warps
+// meanwhile make tile i's fair-coin words, then — once the tile is complete
+// — add dense terms and parents level by level, stream the records to HBM
+// with 16-byte stores and zero the buffer for tile i+2. Named barriers
+// FULL[b] / EMPTY[b] hand the buffers back and forth. Event tables and row
+// tables are staged in shared memory when they fit.
+template <bool kStaged, bool kRowStaged, int kLp, bool kPadPred, int kEB>
+__global__ void __launch_bounds__(kFusedThreads, 1)
+k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, uint64_t n_shots,
+         uint64_t* __restrict__ out, uint64_t ld, uint64_t tile_stride,
+         unsigned long long* __restrict__ counts, bool vec) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const uint32_t tw = P.tw, tw4_log2 = P.t_log2 - 7, tw4 = 1u << tw4_log2;
+  // One spare row absorbs the XORs of padded flip-list entries (never read).
+  // Tile rows, then a spare region (never read) that absorbs the XORs of
+  // padded flip-list entries, spread over 32 banks.
+  const uint32_t tile_words = P.n_meas * tw + spare_words(tw);
+  const bool with_counts = counts != nullptr;
+  uint32_t* tiles = reinterpret_cast<uint32_t*>(smem);
+  uint8_t* p = reinterpret_cast<uint8_t*>(tiles + 2 * tile_words);
+  // Flip counts: per (row, lane) partials when a warp walks one path per
+  // 128-shot column group (T = 4096: no cross-lane reduction per row),
+  // else one counter per row.
+  const uint32_t cnt_lanes = tw4 >= 32 ? 32u : 1u;
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(p);
+  p += align16(4ull * P.n_meas * cnt_lanes);
+  uint32_t* segctr = reinterpret_cast<uint32_t*>(p);  // per-buffer segment dispensers
+  p += 16;
+
+  const ClassInfo* CLS = P.cls;
+  const uint4* DESC = P.desc;
+  const uint16_t* COLROW = P.colrow;
+  const uint4* PLIST = P.plist;
+  const uint32_t* PROWS = P.path_rows;
+  const uint32_t* PPTR = P.path_ptr;
+  const int32_t* PPAR = P.path_par;
+  const uint16_t* KEEP = P.keep_rows;
+  if (kRowStaged) {
+    uint32_t* s_prows = reinterpret_cast<uint32_t*>(p);
+    p += align16(4ull * (P.n_meas + 1));
+    uint32_t* s_pptr = reinterpret_cast<uint32_t*>(p);
+    p += align16(4ull * (P.n_paths + 1));
+    int32_t* s_ppar = reinterpret_cast<int32_t*>(p);
+    p += align16(4ull * P.n_paths);
+    uint16_t* s_keep = reinterpret_cast<uint16_t*>(p);
+    p += align16(2ull * P.n_keep);
+    for (uint32_t i = threadIdx.x; i <= P.n_meas; i += blockDim.x) s_prows[i] = P.path_rows[i];
+    for (uint32_t i = threadIdx.x; i <= P.n_paths; i += blockDim.x) s_pptr[i] = P.path_ptr[i];
+    for (uint32_t i = threadIdx.x; i < P.n_paths; i += blockDim.x) s_ppar[i] = P.path_par[i];
+    for (uint32_t i = threadIdx.x; i < P.n_keep; i += blockDim.x) s_keep[i] = P.keep_rows[i];
+    PROWS = s_prows;
+    PPTR = s_pptr;
+    PPAR = s_ppar;
+    KEEP = s_keep;
+  }
+  if (kStaged) {
+    ClassInfo* s_cls = reinterpret_cast<ClassInfo*>(p);
+    p += align16(sizeof(ClassInfo) * P.n_cls_live);
+    uint4* s_desc = reinterpret_cast<uint4*>(p);
+    p += 16ull * P.n_desc_live;
+    uint16_t* s_col = reinterpret_cast<uint16_t*>(p);
+    {
+      const uint32_t* src = reinterpret_cast<const uint32_t*>(P.cls);
+      uint32_t* dst = reinterpret_cast<uint32_t*>(s_cls);
+      for (uint32_t i = threadIdx.x; i < P.n_cls_live * (sizeof(ClassInfo) / 4); i += blockDim.x)
+        dst[i] = src[i];
+    }
+    for (uint32_t i = threadIdx.x; i < P.n_desc_live; i += blockDim.x) s_desc[i] = P.desc[i];
+    for (uint64_t i = threadIdx.x; i < P.n_colrow; i += blockDim.x) s_col[i] = P.colrow[i];
+    CLS = s_cls;
+    DESC = s_desc;
+    COLROW = s_col;
+  }
+  {
+    uint4* t4 = reinterpret_cast<uint4*>(tiles);
+    for (uint32_t i = threadIdx.x; i < (2 * tile_words) / 4; i += blockDim.x)
+      t4[i] = make_uint4(0, 0, 0, 0);
+    if (with_counts)
+      for (uint32_t i = threadIdx.x; i < P.n_meas * cnt_lanes; i += blockDim.x) cnt[i] = 0;
+    if (threadIdx.x < 2) segctr[threadIdx.x] = 0;
+  }
+  __syncthreads();
+
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t n_gen = P.gen_warps;
+  const uint32_t n_my =
+      n_tiles > blockIdx.x ? (n_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0u;
+
+  if (warp < n_gen) {
+    // ---------------- event generators ----------------
+    for (uint32_t i = 0; i < n_my; ++i) {
+      const uint32_t b = i & 1;
+      const uint64_t gtile = tile0 + blockIdx.x + static_cast<uint64_t>(i) * gridDim.x;
+      long long tw0 = clock64();
+      if (i >= 2) named_sync(kBarEmpty0 + b, blockDim.x);
+      long long tw1 = clock64();
+      uint32_t* tile = tiles + b * tile_words;
+      const uint32_t tile_s = static_cast<uint32_t>(__cvta_generic_to_shared(tile));
+      // Fair-coin words of this tile (dense symbols), keyed by (symbol,
+      // 128-shot quad), XORed word-wise into the D rows of the symbol's
+      // column; the last slot is the constant term (all ones).
+      for (uint32_t j = threadIdx.x; j < ((P.n_dense_live + 1) << tw4_log2); j += n_gen * 32) {
+        const uint32_t slot = j >> tw4_log2, q = j & (tw4 - 1);
+        uint32_t e = __ldg(P.coin_ptr + slot);
+        const uint32_t e1 = __ldg(P.coin_ptr + slot + 1);
+        if (e == e1) continue;
+        uint4 c = make_uint4(kFull, kFull, kFull, kFull);
+        if (slot < P.n_dense_live) {
+          const uint64_t gq = (gtile << tw4_log2) + q;
+          c = philox10(make_uint4(P.dense_sym[slot], static_cast<uint32_t>(gq),
+                                  (static_cast<uint32_t>(gq >> 32) & 0xFFFFFFu) | (kDomCoin << 24),
+                                  0u),
+                       K);
+        }
+        for (; e < e1; ++e) {
+          const uint32_t a = tile_s + ((static_cast<uint32_t>(__ldg(P.coin_rows + e)) + 4 * q) << 2);
+          asm volatile(
+              "red.shared.xor.b32 [%0], %1;\n\t"
+              "red.shared.xor.b32 [%0+4], %2;\n\t"
+              "red.shared.xor.b32 [%0+8], %3;\n\t"
+              "red.shared.xor.b32 [%0+12], %4;" ::"r"(a),
+              "r"(c.x), "r"(c.y), "r"(c.z), "r"(c.w)
+              : "memory");
+        }
+      }
+      const uint32_t spare = P.n_meas * tw;
+      uint32_t seg = 0;
+      Segment sg;
+      // Exact flip list of (class position, pattern): kLp entries of kEB
+      // bytes padded with spare-region entries — u8 row indices when the
+      // tile has < 256 rows, u16 tile byte offsets when the tile is under
+      // 64 KB, else u32 byte offsets — so the table is as small as possible
+      // (L1/L2-resident) and a flip costs at most one extract, one add and
+      // one shared XOR. Lists are loaded before the next Philox blocks are
+      // computed (pre) where registers allow, so the L1/L2 latency hides
+      // under that arithmetic; the rest are issued at the start of emit.
+      // Invalid slots load the all-padding list.
+      constexpr int kWords = kLp > 0 ? kLp * kEB / 4 : 1;  // u32 words per list
+      constexpr int kPre = kWords * kSlots <= 32 ? kSlots : (kWords <= 8 && !kPadPred) ? 4 : 0;
+      const uint32_t spare_b = spare * 4u;  // u16/u32 entries >= spare_b are padding
+      const uint32_t row_b = tw * 4u;
+      uint32_t lst[kSlots][kWords];
+      auto load_lists = [&](auto, const Fired& f, int k0, int k1) {
+#pragma unroll
+        for (int k = 0; k < kSlots; ++k) {
+          if (k < k0 || k >= k1) continue;
+          const uint32_t li =
+              ((f.v >> k) & 1u) ? sg.pbase + f.g[k] * sg.npat + f.pat[k] - 1 : P.plist_dummy;
+          const uint32_t* src = reinterpret_cast<const uint32_t*>(PLIST) + static_cast<size_t>(li) * kWords;
+          if constexpr (kWords == 1) {
+            lst[k][0] = __ldg(src);
+          } else if constexpr (kWords == 2) {
+            const uint2 v = __ldg(reinterpret_cast<const uint2*>(src));
+            lst[k][0] = v.x;
+            lst[k][1] = v.y;
+          } else {
+#pragma unroll
+            for (int h = 0; h < kWords / 4; ++h) {
+              const uint4 v = __ldg(reinterpret_cast<const uint4*>(src) + h);
+              lst[k][4 * h] = v.x;
+              lst[k][4 * h + 1] = v.y;
+              lst[k][4 * h + 2] = v.z;
+              lst[k][4 * h + 3] = v.w;
+            }
+          }
+        }
+      };
+      auto pre = [&](auto bern_tag, const Fired& f) {
+        if constexpr (kLp > 0 && kPre > 0) {
+          if (!(P.debug_mode & 1u)) load_lists(bern_tag, f, 0, kPre);
+        }
+      };
+      auto emit = [&](auto bern_tag, const Fired& f) {
+        constexpr bool kB = decltype(bern_tag)::value;
+        if (P.debug_mode & 1u) {
+          if (f.v == 0xFFFFFFFFu) tile[0] = f.g[0] ^ f.shot[1] ^ f.pat[2];  // keep the walk alive
+          return;
+        }
+        if constexpr (kLp > 0) {
+          if constexpr (kPre > 0 && kPre < kSlots) load_lists(bern_tag, f, kPre, kSlots);
+#pragma unroll
+          for (int half = 0; half < kSlots; half += 4) {
+            if constexpr (kPre == 0) load_lists(bern_tag, f, half, half + 4);
+#pragma unroll
+            for (int k = half; k < half + 4; ++k) {
+              const uint32_t wb = tile_s + ((f.shot[k] >> 5) << 2);
+              const uint32_t bit = ((f.v >> k) & 1u) << (f.shot[k] & 31);
+#pragma unroll
+              for (int e = 0; e < kLp; ++e) {
+                uint32_t a;
+                bool real;
+                if constexpr (kEB == 1) {
+                  const uint32_t row = __byte_perm(lst[k][e >> 2], 0u, 0x4440u | (e & 3));
+                  a = wb + row * row_b;
+                  real = row != P.n_meas;
+                } else if constexpr (kEB == 2) {
+                  const uint32_t w = lst[k][e >> 1];
+                  const uint32_t x = (e & 1) ? (w >> 16) : (w & 0xFFFFu);
+                  a = wb + x;
+                  real = x < spare_b;
+                } else {
+                  a = wb + lst[k][e];
+                  real = lst[k][e] < spare_b;
+                }
+                // kPadPred (many firings per shot): skip padding so the ATOMS
+                // pipe only carries real flips; else padding XORs the spare
+                // row (never read).
+                if constexpr (kPadPred) {
+                  // predicated in PTX: an asm statement under a C++ branch
+                  // would compile to a divergent branch per entry
+                  asm volatile(
+                      "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t"
+                      "@p red.shared.xor.b32 [%0], %1;\n\t}" ::"r"(a),
+                      "r"(bit), "r"(real ? 1u : 0u)
+                      : "memory");
+                } else {
+                  asm volatile("red.shared.xor.b32 [%0], %1;" ::"r"(a), "r"(bit) : "memory");
+                }
+              }
+            }
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < kSlots; ++k) {
+            if (!((f.v >> k) & 1u)) continue;
+            const uint4 d = DESC[sg.goff + f.g[k]];
+            const uint32_t bit = 1u << (f.shot[k] & 31);
+            uint32_t* wb = tile + (f.shot[k] >> 5);
+            uint32_t off = d.x;
+            const uint32_t lens[4] = {d.y & 0xFFFFu, d.y >> 16, d.z & 0xFFFFu, d.z >> 16};
+#pragma unroll
+            for (int s = 0; s < 4; ++s) {
+              if ((f.pat[k] >> s) & 1u)
+                for (uint32_t j = 0; j < lens[s]; ++j) atomicXor(wb + COLROW[off + j], bit);
+              off += lens[s];
+            }
+          }
+        }
+      };
+      // Segments of this tile, taken from the tile's dispenser one after
+      // another; each walk hands over to the next on its last step.
+      auto next = [&](Segment& sn) {
+        if (lane == 0) seg = atomicAdd(&segctr[b], 1u);
+        seg = __shfl_sync(kFull, seg, 0);
+        if (seg >= P.n_seg_live || (P.debug_mode & 2u)) return false;
+        segment_init(sn, CLS, P.n_cls_live, seg, P.t_log2);
+        return true;
+      };
+      uint4 r[kBlocks];
+      bool have = next(sg);
+      if (have) {
+#pragma unroll
+        for (int bb = 0; bb < kBlocks; ++bb) r[bb] = segment_philox(sg, K, gtile, 0, bb, lane);
+      }
+      while (have) have = segment_walk_chain(sg, r, K, gtile, P.t_log2, lane, pre, emit, next);
+      if (P.timers && lane == 0) {  // gen: [0] waiting EMPTY, [1] working
+        atomicAdd(reinterpret_cast<unsigned long long*>(P.timers) + 0, tw1 - tw0);
+        atomicAdd(reinterpret_cast<unsigned long long*>(P.timers) + 1, clock64() - tw1);
+      }
+      named_arrive(kBarFull0 + b, blockDim.x);
+    }
+  } else {
+    // ---------------- drain warps ----------------
+    const uint32_t ct = threadIdx.x - n_gen * 32, nct = blockDim.x - n_gen * 32;
+    const uint32_t cnt_s = static_cast<uint32_t>(__cvta_generic_to_shared(cnt));
+    // row stride in bytes for the fast path's 32x32->64 address multiply
+    const uint32_t ldb = ld < (1ull << 29) ? static_cast<uint32_t>(ld * 8) : 0u;
+    for (uint32_t i = 0; i < n_my; ++i) {
+      const uint32_t b = i & 1;
+      const uint64_t t_local = blockIdx.x + static_cast<uint64_t>(i) * gridDim.x;
+      long long td0 = clock64();
+      named_sync(kBarFull0 + b, blockDim.x);
+      long long td1 = clock64();
+
+      uint4* t4 = reinterpret_cast<uint4*>(tiles + b * tile_words);
+      const uint32_t t4_s = static_cast<uint32_t>(__cvta_generic_to_shared(t4));
+      const uint64_t first = t_local << P.t_log2;
+      const uint64_t valid = min(static_cast<uint64_t>(1) << P.t_log2, n_shots - first);
+      const uint32_t vq = static_cast<uint32_t>((valid + 127) >> 7);
+      const uint32_t rem = static_cast<uint32_t>(valid & 127);
+      const bool fast = vec && ldb != 0 && (valid == (static_cast<uint64_t>(1) << P.t_log2));
+      // Rows along parent paths (heavy-path decomposition of the L forest):
+      // one thread walks a path top-down for one 128-shot column, carrying
+      // the running row value; a path's head waits only for its parent's
+      // path, which ran in an earlier round.
+      for (uint32_t rd = 0; rd < ((P.debug_mode & 8u) ? 0u : P.n_rounds); ++rd) {
+        const uint32_t p0 = P.round_ptr[rd], p1 = P.round_ptr[rd + 1];
+        const uint32_t tasks = (p1 - p0) << tw4_log2;
+        const uint32_t tasks_rounded = (tasks + 31) & ~31u;
+        for (uint32_t j = ct; j < tasks_rounded; j += nct) {
+          const bool act = j < tasks;
+          const uint32_t pth = act ? p0 + (j >> tw4_log2) : p0;
+          const uint32_t q = j & (tw4 - 1);
+          const int32_t par = act ? PPAR[pth] : -1;
+          uint4 prev = par >= 0 ? t4[(static_cast<uint32_t>(par) << tw4_log2) + q]
+                                : make_uint4(0, 0, 0, 0);
+          const uint32_t xe = act ? PPTR[pth + 1] : 0;
+          uint32_t x = act ? PPTR[pth] : 0;
+          uint64_t* obase = out + t_local * tile_stride + 2 * q;
+          uint8_t* obase_b = reinterpret_cast<uint8_t*>(obase);
+          // One row of the path: row = tile word ^ parent row; keep or clear
+          // the tile word, store 16 bytes to HBM, optionally count.
+          auto row_step = [&](auto fast_tag, auto wp_tag, uint32_t e, uint4 c) {
+            constexpr bool kFast = decltype(fast_tag)::value;  // full tile, aligned, ldb < 2^32
+            constexpr bool kWarpPath = decltype(wp_tag)::value;  // a warp per path (T = 4096)
+            const uint32_t k = e & 0xFFFFu;
+            uint4 v = xor4(c, prev);
+            // Rows with light children keep their final value for a later
+            // round; all others are cleared for tile i+2 right away.
+            sts_or_zero(t4_s + (((k << tw4_log2) + q) << 4), v, e >> 31);
+            prev = v;
+            uint32_t pc = 0;
+            if constexpr (kFast) {
+              *reinterpret_cast<uint4*>(obase_b + static_cast<uint64_t>(k) * ldb) = v;
+              if (with_counts) pc = __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
+            } else if (q < vq) {
+              uint64_t* o = obase + static_cast<uint64_t>(k) * ld;
+              bool two = true;  // whether the item's second u64 word is inside the tile
+              if (q == vq - 1 && rem) {
+                const uint32_t m[4] = {
+                    rem >= 32 ? kFull : (1u << rem) - 1,
+                    rem >= 64 ? kFull : rem > 32 ? (1u << (rem - 32)) - 1 : 0u,
+                    rem >= 96 ? kFull : rem > 64 ? (1u << (rem - 64)) - 1 : 0u,
+                    rem > 96 ? (1u << (rem - 96)) - 1 : 0u};
+                v.x &= m[0]; v.y &= m[1]; v.z &= m[2]; v.w &= m[3];
+                two = rem > 64;
+              }
+              const uint64_t w0 = (static_cast<uint64_t>(v.y) << 32) | v.x;
+              const uint64_t w1 = (static_cast<uint64_t>(v.w) << 32) | v.z;
+              if (vec && two) {
+                *reinterpret_cast<ulonglong2*>(o) = make_ulonglong2(w0, w1);
+              } else {
+                o[0] = w0;
+                if (two) o[1] = w1;
+              }
+              if (with_counts) pc = __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
+            }
+            if (with_counts) {
+              if constexpr (kWarpPath) {  // per-lane partials, no reduction here
+                asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(cnt_s + ((k * 32 + lane) << 2)),
+                             "r"(pc)
+                             : "memory");
+              } else {
+                if (pc) atomicAdd(&cnt[k], pc);
+              }
+            }
+          };
+          // Two rows per iteration with the next row's entry and tile word
+          // prefetched (path_rows is padded, so x + 2 <= n_meas is readable).
+          auto walk = [&](auto fast_tag, auto wp_tag) {
+            uint32_t ea = PROWS[x];
+            uint4 ca = t4[((ea & 0xFFFFu) << tw4_log2) + q];
+            for (; x + 2 <= xe; x += 2) {
+              const uint32_t eb = PROWS[x + 1];
+              const uint4 cb = t4[((eb & 0xFFFFu) << tw4_log2) + q];
+              row_step(fast_tag, wp_tag, ea, ca);
+              ea = PROWS[x + 2];
+              ca = t4[((ea & 0xFFFFu) << tw4_log2) + q];
+              row_step(fast_tag, wp_tag, eb, cb);
+            }
+            if (x < xe) row_step(fast_tag, wp_tag, ea, ca);
+          };
+          if (tw4 >= 32) {
+            if (fast) walk(std::true_type{}, std::true_type{});
+            else walk(std::false_type{}, std::true_type{});
+          } else {
+            if (fast) walk(std::true_type{}, std::false_type{});
+            else walk(std::false_type{}, std::false_type{});
+          }
+        }
+        // A later round must not start before every row a light child
+        // reads is final.
+        if (rd + 1 < P.n_rounds) named_sync(kBarDrain, nct);
+      }
+      if (P.n_keep) {
+        named_sync(kBarDrain, nct);  // all light children have read their parents
+        for (uint32_t j = ct; j < (P.n_keep << tw4_log2); j += nct)
+          t4[(static_cast<uint32_t>(KEEP[j >> tw4_log2]) << tw4_log2) + (j & (tw4 - 1))] =
+              make_uint4(0, 0, 0, 0);
+      }
+      if (ct == 0) segctr[b] = 0;  // all generators are past tile i (FULL[b] completed)
+      if (P.timers && lane == 0) {  // drain: [2] waiting FULL, [3] working
+        atomicAdd(reinterpret_cast<unsigned long long*>(P.timers) + 2, td1 - td0);
+        atomicAdd(reinterpret_cast<unsigned long long*>(P.timers) + 3, clock64() - td1);
+      }
+      if (i + 2 < n_my) named_arrive(kBarEmpty0 + b, blockDim.x);
+    }
+  }
+  if (with_counts) {
+    __syncthreads();
+    if (cnt_lanes == 32) {  // one warp per row: sum the lane partials
+      for (uint32_t k = threadIdx.x >> 5; k < P.n_meas; k += blockDim.x >> 5) {
+        const uint32_t c = __reduce_add_sync(kFull, cnt[k * 32 + lane]);
+        if (lane == 0 && c) atomicAdd(&counts[k], static_cast<unsigned long long>(c));
+      }
+    } else {
+      for (uint32_t i = threadIdx.x; i < P.n_meas; i += blockDim.x)
+        if (cnt[i]) atomicAdd(&counts[i], static_cast<unsigned long long>(cnt[i]));
+    }
+  }
+}
+
+}  // namespace
+
+namespace k1 {
+template <bool kStaged, bool kRowStaged, int kLp, bool kPadPred, int kEB>
+int launch_k1(const DevPlan& P, const LaunchCfg& L, const RoundKeys& K, uint64_t tile0,
+              uint32_t n_tiles, uint64_t n_shots, uint64_t* out, uint64_t ld, uint64_t tstride,
+              unsigned long long* cnt) {
+  auto kern = k1_fused<kStaged, kRowStaged, kLp, kPadPred, kEB>;
+  const size_t smem = fused_smem_bytes(P, P.t_log2, kStaged, kRowStaged);
+  int grid = 0;
+  const int threads = static_cast<int>(P.cta_threads);
+  if (persistent_grid(kern, L, smem, n_tiles, P.cta_per_sm, &grid, threads)) return -1;
+  const bool vec = (ld % 2 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0);
+  kern<<<grid, threads, smem, L.stream>>>(P, K, tile0, n_tiles, n_shots, out, ld, tstride, cnt,
+                                          vec);
+  return check_launch() ? -1 : 1;
+}
+
+}  // namespace k1
+}  // namespace symphase

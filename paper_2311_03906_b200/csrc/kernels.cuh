@@ -76,14 +76,14 @@ struct DevPlan {
   const uint16_t* colrow = nullptr;
   uint64_t n_colrow = 0;
   // Exact per-(group, pattern) flip lists in D space: lp entries padded
-  // with the spare row (lp = 4, 8 or 16; 0 = lists too long, use the
-  // desc/colrow loops). Entries are u8 row indices when n_meas < 256, else
-  // u32 tile byte offsets (row * tw * 4).
+  // with spare-region entries (lp = 4, 8 or 16; 0 = lists too long, use the
+  // desc/colrow loops). Entries are u8 row indices when n_meas < 256, u16
+  // tile byte offsets (row * tw * 4) when the tile is under 64 KB, else u32.
   // List of (class position g, pattern pi) = plist[(pbase + g*npat + pi-1)].
   uint32_t lp = 0;
   uint32_t pad_pred = 0;  // skip padding entries (many firings per shot) vs XOR the spare row
   uint32_t plist_dummy = 0;  // index of an all-padding list (invalid slots load it)
-  uint32_t u8 = 0;           // entries are u8 row indices (n_meas < 256), else u32 offsets
+  uint32_t entry_bytes = 4;  // 1: u8 row indices, 2: u16 / 4: u32 tile byte offsets
   const uint4* plist = nullptr;
   // Row reconstruction out[k] = d[k] ^ out[parent[k]] along the paths of a
   // heavy-path decomposition of the parent forest: path p lists rows
@@ -135,6 +135,11 @@ struct LaunchCfg {
 // 16 warps per CTA, one CTA per SM (a 32-warp variant with 64 registers per
 // thread measured slower on both cfg2 and cfg3).
 constexpr int kFusedThreads = 512;
+
+// Words of the fused kernel's spare tile region (after the n_meas rows):
+// padded flip-list entries point into it, spread over 32 banks (u32 lists:
+// offset n_meas*tw + r, r < 32, plus the firing's word < tw).
+__host__ __device__ constexpr uint32_t spare_words(uint32_t tw) { return ((tw + 32) + 3) & ~3u; }
 
 // Shared-memory bytes of the fused kernel for a plan shape.
 size_t fused_smem_bytes(const DevPlan& P, uint32_t t_log2, bool staged, bool row_staged);
