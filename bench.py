@@ -354,7 +354,9 @@ def run_ours(args):
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(written),
                     "path": "Sampler.load + Sampler.sample_to_host (C ABI sp_load_msym_csr/"
-                            "sp_load_groups/sp_sample_to_host), b8 records to pinned host"},
+                            "sp_load_groups/sp_sample_to_host), b8 records to pinned host; "
+                            "each step re-uploads the model arrays (the derived plan is reused "
+                            "when the reloaded model's content fingerprint matches)"},
             "gpu_launches": launches,
             "wall_s_timed": wall,
         }

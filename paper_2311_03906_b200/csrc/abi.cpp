@@ -5,16 +5,21 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <mutex>
 #include <new>
 #include <stdexcept>
 #include <string>
 #include <vector>
 
 #include "frontend.hpp"
+
+extern char** environ;
 #include "kernels.cuh"
 
 using namespace symphase;
@@ -51,9 +56,14 @@ struct DBuf {
   }
   template <class T>
   T* upload(const std::vector<T>& v, cudaStream_t s) {
-    reset();
-    bytes = std::max<size_t>(v.size() * sizeof(T), 16);
-    ck(cudaMalloc(&p, bytes), "cudaMalloc");
+    // reuse the allocation when it is large enough (stream-ordered copy; no
+    // cudaFree, which would synchronise the device)
+    const size_t need = std::max<size_t>(v.size() * sizeof(T), 16);
+    if (!p || bytes < need) {
+      reset();
+      bytes = need;
+      ck(cudaMalloc(&p, bytes), "cudaMalloc");
+    }
     if (!v.empty()) ck(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s),
                        "cudaMemcpyAsync H2D");
     return static_cast<T*>(p);
@@ -91,6 +101,8 @@ struct sp_ctx {
   sp_product product = SP_PRODUCT_AUTO;
   LaunchCfg L;
   bool have_msym = false, have_groups = false, plan_ready = false, fused_ok = false;
+  bool plan_built = false;  // dp/hp-derived buffers describe the model with plan_fp
+  uint64_t plan_fp = 0;
   std::string fused_why;
   HostPlan hp;
   DevPlan dp;
@@ -103,9 +115,19 @@ struct sp_ctx {
   bool prod_ready = false;
   DevPlan pp;
   DBuf p_row_ptr, p_sym_idx, p_dense;
-  // scratch for sp_sample_to_host
-  DBuf s_out, s_bytes;
+  // sp_sample_to_host: double-buffered records/bytes, a copy stream and the
+  // events that hand each buffer between the compute and copy streams
+  DBuf s_out[2], s_bytes[2];
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev_ready[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
   uint64_t launches = 0;
+  ~sp_ctx() {
+    for (int b = 0; b < 2; ++b) {
+      if (ev_ready[b]) cudaEventDestroy(ev_ready[b]);
+      if (ev_free[b]) cudaEventDestroy(ev_free[b]);
+    }
+    if (copy_stream) cudaStreamDestroy(copy_stream);
+  }
 };
 
 namespace {
@@ -189,7 +211,21 @@ ChainXf chain_transform(uint64_t n_meas, const std::vector<uint64_t>& row_ptr,
   return x;
 }
 
+// SP_PLAN_TIMING=1: per-phase host times of build_plan on stderr.
+struct PlanTimer {
+  bool on = std::getenv("SP_PLAN_TIMING") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(const char* what) {
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[plan] %-22s %8.3f ms\n", what,
+                 std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
+};
+
 void build_plan(sp_ctx* c) {
+  PlanTimer ptm;
   HostPlan& h = c->hp;
   DevPlan& d = c->dp;
   cudaStream_t s = c->stream;
@@ -221,6 +257,7 @@ void build_plan(sp_ctx* c) {
         col_rows[fillp[h.sym_idx[i]]++] = static_cast<uint32_t>(k);
   }
   auto col_len = [&](uint64_t sidx) { return col_ptr[sidx + 1] - col_ptr[sidx]; };
+  ptm.mark("groups+csc");
 
   // D = L^-1 M (chain transform); skipped when M is dense enough that the
   // parent search (sum of squared column lengths) would be expensive.
@@ -229,6 +266,7 @@ void build_plan(sp_ctx* c) {
   const ChainXf X = chain_transform(n_meas, h.row_ptr, h.sym_idx, col_ptr, col_rows,
                                     sq < 2e9 && env_long("SP_NO_CHAIN", 0) == 0);
   c->dnnz = X.si.size();
+  ptm.mark("chain transform");
   std::vector<uint64_t> dcol_ptr(n_sym + 1, 0);
   for (uint32_t sidx : X.si) dcol_ptr[sidx + 1]++;
   for (uint64_t i = 0; i < n_sym; ++i) dcol_ptr[i + 1] += dcol_ptr[i];
@@ -336,6 +374,7 @@ void build_plan(sp_ctx* c) {
       for (uint32_t b = 0; b < h.groups[g].arity; ++b) live_colrow += dcol_len(h.groups[g].first_symbol + b);
     }
 
+  ptm.mark("classify");
   // ---- launch shape: tile T, table staging, generator/drain warp split ----
   d = DevPlan{};
   d.n_meas = static_cast<uint32_t>(n_meas);
@@ -498,7 +537,10 @@ void build_plan(sp_ctx* c) {
   std::vector<uint16_t> colrow16;
   // Exact flip lists per (group, pattern): XOR of the D columns of the
   // pattern's set symbols, as row * tw offsets.
-  std::vector<std::vector<uint16_t>> plists;
+  // flat: list i = pl_rows[pl_off[i] .. pl_off[i+1])
+  std::vector<uint32_t> pl_off{0};
+  std::vector<uint16_t> pl_rows;
+  std::vector<uint16_t> scratch;
   size_t max_plist = 0;
   auto add_classes = [&](const std::vector<Cls>& cls, bool live) {
     for (size_t c = 0; c < cls.size(); ++c) {
@@ -510,31 +552,33 @@ void build_plan(sp_ctx* c) {
       ci.goff = static_cast<uint32_t>(cls_groups.size());
       ci.trials = cl.groups.size() * T;
       ci.npat = cl.dist == SP_DIST_DEPOLARIZE2 ? 15 : cl.dist == SP_DIST_DEPOLARIZE1 ? 3 : 1;
-      ci.pbase = static_cast<uint32_t>(plists.size());
+      ci.pbase = static_cast<uint32_t>(pl_off.size() - 1);
       cls_info.push_back(ci);
       for (uint32_t g : cl.groups) {
         cls_groups.push_back(g);
         if (!live) continue;
         const sp_group& gr = h.groups[g];
         for (uint32_t pat = 1; pat <= ci.npat; ++pat) {
-          std::vector<uint16_t> rows;
+          // symmetric difference of the D columns of the pattern's symbols,
+          // merged in place at the end of pl_rows (sorted, as row * tw)
+          const size_t start = pl_rows.size();
           for (uint32_t b = 0; b < gr.arity; ++b) {
             if (!((pat >> b) & 1u)) continue;
             const uint64_t sidx = gr.first_symbol + b;
-            std::vector<uint16_t> merged;
+            scratch.assign(pl_rows.begin() + start, pl_rows.end());
+            pl_rows.resize(start);
             size_t i = 0;
             uint64_t j = dcol_ptr[sidx];
-            while (i < rows.size() || j < dcol_ptr[sidx + 1]) {
-              const uint32_t a = i < rows.size() ? rows[i] : UINT32_MAX;
+            while (i < scratch.size() || j < dcol_ptr[sidx + 1]) {
+              const uint32_t a = i < scratch.size() ? scratch[i] : UINT32_MAX;
               const uint32_t c2 = j < dcol_ptr[sidx + 1] ? dcol_rows[j] * d.tw : UINT32_MAX;
-              if (a < c2) { merged.push_back(static_cast<uint16_t>(a)); ++i; }
-              else if (c2 < a) { merged.push_back(static_cast<uint16_t>(c2)); ++j; }
+              if (a < c2) { pl_rows.push_back(static_cast<uint16_t>(a)); ++i; }
+              else if (c2 < a) { pl_rows.push_back(static_cast<uint16_t>(c2)); ++j; }
               else { ++i; ++j; }
             }
-            rows.swap(merged);
           }
-          max_plist = std::max(max_plist, rows.size());
-          plists.push_back(std::move(rows));
+          max_plist = std::max<size_t>(max_plist, pl_rows.size() - start);
+          pl_off.push_back(static_cast<uint32_t>(pl_rows.size()));
         }
         uint32_t lens[4] = {0, 0, 0, 0};
         const uint32_t base = static_cast<uint32_t>(colrow16.size());
@@ -549,8 +593,10 @@ void build_plan(sp_ctx* c) {
       }
     }
   };
+  ptm.mark("segment plan");
   add_classes(live_cls, true);
   add_classes(dead_cls, false);
+  ptm.mark("flip lists");
   // Segment table: live classes get the planned slice counts, dead ones
   // (walked only by the standalone draw kernel) ~E firings per slice.
   auto apply_segments = [&](const std::vector<uint64_t>& nseg_live) {
@@ -631,32 +677,37 @@ void build_plan(sp_ctx* c) {
       // 4-16 bytes, so the table stays in L1), else byte offsets into the
       // tile (row * tw * 4: a flip is one add + one shared XOR). Padding =
       // the spare tile row (row n_meas), absorbed and never read; one extra
-      // all-padding list (index plists.size()) stands in for invalid slots.
-      d.plist_dummy = static_cast<uint32_t>(plists.size());
+      // all-padding list (index n_lists) stands in for invalid slots.
+      const size_t n_lists = pl_off.size() - 1;
+      d.plist_dummy = static_cast<uint32_t>(n_lists);
       const uint64_t tile_bytes = (n_meas * d.tw + spare_words(d.tw)) * 4;
       d.entry_bytes = n_meas < 256 ? 1 : tile_bytes <= 65536 ? 2 : 4;
       if (const long fe = env_long("SP_ENTRY_BYTES", 0); fe == 2 || fe == 4) d.entry_bytes = fe;
       if (d.entry_bytes == 2 && tile_bytes > 65536) d.entry_bytes = 4;
       // padding: spare-region offsets varied per list and entry, so the
       // padding XORs of a warp spread over the banks (u8: the spare row)
-      auto entry = [&](size_t i, size_t j) -> uint32_t {
-        if (i < plists.size() && j < plists[i].size())
-          return d.entry_bytes == 1 ? plists[i][j] / d.tw : 4u * plists[i][j];
-        if (d.entry_bytes == 1) return static_cast<uint32_t>(n_meas);
-        return 4u * static_cast<uint32_t>(n_meas * d.tw + ((i * 7 + j * 13) & 31));
-      };
-      const size_t n_ent = (plists.size() + 1) * d.lp;
+      const size_t n_ent = (n_lists + 1) * d.lp;
       std::vector<uint8_t> bytes(((n_ent * d.entry_bytes) + 15) & ~size_t{15}, 0);
-      for (size_t i = 0; i <= plists.size(); ++i)
+      for (size_t i = 0; i <= n_lists; ++i) {
+        const size_t len = i < n_lists ? pl_off[i + 1] - pl_off[i] : 0;
         for (size_t j = 0; j < d.lp; ++j) {
-          const uint32_t v = entry(i, j);
+          uint32_t v;
+          if (j < len) {
+            const uint32_t r = pl_rows[pl_off[i] + j];
+            v = d.entry_bytes == 1 ? r / d.tw : 4u * r;
+          } else {
+            v = d.entry_bytes == 1 ? static_cast<uint32_t>(n_meas)
+                                   : 4u * static_cast<uint32_t>(n_meas * d.tw + ((i * 7 + j * 13) & 31));
+          }
           std::memcpy(bytes.data() + (i * d.lp + j) * d.entry_bytes, &v, d.entry_bytes);  // little-endian
         }
+      }
       std::vector<uint4> packed(bytes.size() / 16);
       std::memcpy(packed.data(), bytes.data(), bytes.size());
       d.plist = c->b_plist.upload(packed, s);
     }
   }
+  ptm.mark("uploads");
   {
     // Heavy-path decomposition of the parent forest (parents precede
     // children, so one reverse sweep gives subtree sizes).
@@ -727,6 +778,7 @@ void build_plan(sp_ctx* c) {
   }
   ck(cudaStreamSynchronize(s), "plan upload");
 
+  ptm.mark("paths");
   // Launch autotune: the generator/drain warp split (and with it the slice
   // counts) and the padded-XOR mode are measured, not modelled — a few short
   // launches of the fused kernel over ~16 tiles per CTA: first the padding
@@ -734,7 +786,45 @@ void build_plan(sp_ctx* c) {
   // SP_PAD_PRED fix a choice; SP_AUTOTUNE=0 keeps the model's.
   const bool fix_gw = env_long("SP_GEN_WARPS", 0) != 0;
   const bool fix_pp = env_long("SP_PAD_PRED", -1) >= 0 || d.lp == 0;
-  if (c->fused_ok && !live_cls.empty() && n_meas > 0 && !(fix_gw && fix_pp) &&
+  // Tuned shapes are cached per (model, device, plan shape) fingerprint, so
+  // re-loading the same model does not re-measure.
+  uint64_t fp = 0xcbf29ce484222325ull;
+  auto mix = [&](const void* data, size_t n) {  // FNV-1a over 64-bit words
+    const uint8_t* b = static_cast<const uint8_t*>(data);
+    size_t i = 0;
+    for (; i + 8 <= n; i += 8) {
+      uint64_t w;
+      std::memcpy(&w, b + i, 8);
+      fp = (fp ^ w) * 0x100000001b3ull;
+    }
+    for (; i < n; ++i) fp = (fp ^ b[i]) * 0x100000001b3ull;
+  };
+  auto mix64v = [&](uint64_t v) { mix(&v, 8); };
+  mix64v(n_meas);
+  mix64v(n_sym);
+  mix(h.row_ptr.data(), h.row_ptr.size() * 8);
+  mix(h.sym_idx.data(), h.sym_idx.size() * 4);
+  for (const sp_group& g : h.groups) {
+    mix64v(g.dist);
+    mix(&g.param, 8);
+    mix64v(g.first_symbol);
+  }
+  mix64v(static_cast<uint64_t>(c->L.num_sms) << 32 | d.t_log2);
+  mix64v(d.lp | static_cast<uint64_t>(d.entry_bytes) << 8 | static_cast<uint64_t>(d.cta_threads) << 16);
+  static std::mutex tune_mu;
+  static std::map<uint64_t, std::pair<uint32_t, uint32_t>> tune_cache;  // fp -> (gen_warps, pad_pred)
+  bool cached = false;
+  if (!fix_gw || !fix_pp) {
+    std::lock_guard<std::mutex> lk(tune_mu);
+    auto it = tune_cache.find(fp);
+    if (it != tune_cache.end()) {
+      if (!fix_gw) d.gen_warps = it->second.first;
+      if (!fix_pp) d.pad_pred = it->second.second;
+      cached = true;
+    }
+  }
+  if (cached && !fix_gw) apply_segments(plan_segments(d.gen_warps));
+  if (!cached && c->fused_ok && !live_cls.empty() && n_meas > 0 && !(fix_gw && fix_pp) &&
       env_long("SP_AUTOTUNE", 1) != 0) {
     const long n_warps = d.cta_threads / 32;
     const uint64_t cal_shots = (static_cast<uint64_t>(c->L.num_sms) * d.cta_per_sm * 16) << d.t_log2;
@@ -802,8 +892,59 @@ void build_plan(sp_ctx* c) {
     cudaEventDestroy(e1);
     if (d.timers) d.timers = c->b_timers.upload(std::vector<long long>(4, 0), s);
     ck(cudaStreamSynchronize(s), "plan upload");
+    std::lock_guard<std::mutex> lk(tune_mu);
+    tune_cache[fp] = {d.gen_warps, d.pad_pred};
   }
+  ptm.mark("autotune");
   c->plan_ready = true;
+}
+
+// Content fingerprint of the loaded model and of the SP_* planner switches.
+uint64_t model_fingerprint(const HostPlan& h) {
+  uint64_t fp = 0xcbf29ce484222325ull;
+  auto mix = [&](const void* data, size_t n) {  // FNV-1a over 64-bit words
+    const uint8_t* b = static_cast<const uint8_t*>(data);
+    size_t i = 0;
+    for (; i + 8 <= n; i += 8) {
+      uint64_t w;
+      std::memcpy(&w, b + i, 8);
+      fp = (fp ^ w) * 0x100000001b3ull;
+    }
+    for (; i < n; ++i) fp = (fp ^ b[i]) * 0x100000001b3ull;
+  };
+  const uint64_t dims[4] = {h.n_meas, h.n_sym, h.groups.size(), h.ldm};
+  mix(dims, sizeof dims);
+  mix(h.row_ptr.data(), h.row_ptr.size() * 8);
+  mix(h.sym_idx.data(), h.sym_idx.size() * 4);
+  mix(h.dense_words.data(), h.dense_words.size() * 8);
+  mix(h.groups.data(), h.groups.size() * sizeof(sp_group));
+  for (char** e = environ; e && *e; ++e)
+    if (std::strncmp(*e, "SP_", 3) == 0) mix(*e, std::strlen(*e));
+  return fp;
+}
+
+// Re-upload the raw model arrays of an unchanged model; the derived plan
+// (chain transform, flip lists, paths, tuned launch shape) stays.
+void refresh_model_uploads(sp_ctx* c) {
+  HostPlan& h = c->hp;
+  DevPlan& d = c->dp;
+  cudaStream_t s = c->stream;
+  d.row_ptr = c->b_row_ptr.upload(h.row_ptr, s);
+  d.sym_idx = c->b_sym_idx.upload(h.sym_idx, s);
+  const uint64_t G = h.groups.size();
+  std::vector<uint32_t> g_first(G), g_arity(G);
+  std::vector<uint8_t> g_dist(G);
+  std::vector<double> g_param(G);
+  for (uint64_t g = 0; g < G; ++g) {
+    g_first[g] = h.groups[g].first_symbol;
+    g_arity[g] = h.groups[g].arity;
+    g_dist[g] = h.groups[g].dist;
+    g_param[g] = h.groups[g].param;
+  }
+  d.g_first = c->b_first.upload(g_first, s);
+  d.g_arity = c->b_arity.upload(g_arity, s);
+  d.g_dist = c->b_dist.upload(g_dist, s);
+  d.g_param = c->b_param.upload(g_param, s);
 }
 
 int ensure_plan(sp_ctx* c) {
@@ -815,7 +956,18 @@ int ensure_plan(sp_ctx* c) {
     for (const sp_group& g : c->hp.groups) total += g.arity;
     if (total != c->hp.n_sym)
       return fail(SP_ERR_INVALID_ARGUMENT, "group arities do not add up to n_sym");
+    // Re-loading the model this plan was built from (same content, same
+    // planner switches) keeps the plan: only the raw arrays are uploaded.
+    const uint64_t fp = model_fingerprint(c->hp);
+    if (c->plan_built && fp == c->plan_fp) {
+      refresh_model_uploads(c);
+      c->plan_ready = true;
+      return SP_OK;
+    }
+    c->plan_built = false;
     build_plan(c);
+    c->plan_fp = fp;
+    c->plan_built = true;
   } catch (const std::invalid_argument& e) {
     return fail(SP_ERR_INVALID_ARGUMENT, e.what());
   } catch (const CudaError& e) {
@@ -1191,30 +1343,52 @@ int sp_sample_to_host(sp_ctx* ctx, uint64_t seed, uint64_t shot_begin, uint64_t 
   if (cap < need || (!h_out && need)) return fail(SP_ERR_INVALID_ARGUMENT, "host buffer too small");
   const uint64_t T = 1ull << ctx->dp.t_log2;
   if (shot_begin % T) return fail(SP_ERR_INVALID_ARGUMENT, "shot_begin must be a multiple of the shot tile");
-  // Chunks of ~64 MB of records, a multiple of the shot tile.
+  // Chunks of ~32 MB of encoded records (a multiple of the shot tile), two
+  // buffers deep: chunk i+1 is sampled and encoded on the compute stream
+  // while chunk i is copied to the host on the copy stream.
   const uint64_t per_shot = std::max<uint64_t>(sp_encoded_size(n_meas, 1, fmt), 1);
-  uint64_t chunk = std::max<uint64_t>((64ull << 20) / per_shot / T, 1) * T;
+  uint64_t chunk = std::max<uint64_t>((32ull << 20) / per_shot / T, 1) * T;
   chunk = std::min(chunk, (n_shots + T - 1) / T * T);
   const uint64_t ld = chunk / 64;
   try {
-    uint64_t* d_m = static_cast<uint64_t*>(ctx->s_out.ensure(std::max<uint64_t>(n_meas * ld * 8, 16)));
-    uint8_t* d_b = static_cast<uint8_t*>(ctx->s_bytes.ensure(std::max<uint64_t>(chunk * per_shot, 16)));
+    if (!ctx->copy_stream) {
+      ck(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking), "cudaStreamCreate");
+      for (int b = 0; b < 2; ++b) {
+        ck(cudaEventCreateWithFlags(&ctx->ev_ready[b], cudaEventDisableTiming), "cudaEventCreate");
+        ck(cudaEventCreateWithFlags(&ctx->ev_free[b], cudaEventDisableTiming), "cudaEventCreate");
+      }
+    }
+    uint64_t* d_m[2];
+    uint8_t* d_b[2];
+    for (int b = 0; b < 2; ++b) {
+      d_m[b] = static_cast<uint64_t*>(ctx->s_out[b].ensure(std::max<uint64_t>(n_meas * ld * 8, 16)));
+      d_b[b] = static_cast<uint8_t*>(ctx->s_bytes[b].ensure(std::max<uint64_t>(chunk * per_shot, 16)));
+    }
     uint64_t off = 0;
-    for (uint64_t done = 0; done < n_shots; done += chunk) {
+    uint64_t i = 0;
+    for (uint64_t done = 0; done < n_shots; done += chunk, ++i) {
+      const int b = static_cast<int>(i & 1);
       const uint64_t n = std::min(chunk, n_shots - done);
+      if (i >= 2) ck(cudaStreamWaitEvent(ctx->stream, ctx->ev_free[b], 0), "cudaStreamWaitEvent");
       int r = SP_OK;
       if (ctx->rng == SP_RNG_PHILOX && n_meas) {
         // tiled records: coalesced stores for any row count
-        if ((r = sp_sample_tiled(ctx, seed, shot_begin + done, n, d_m, nullptr))) return r;
-        if ((r = sp_encode_tiled(ctx, d_m, n, fmt, d_b))) return r;
+        if ((r = sp_sample_tiled(ctx, seed, shot_begin + done, n, d_m[b], nullptr))) return r;
+        if ((r = sp_encode_tiled(ctx, d_m[b], n, fmt, d_b[b]))) return r;
       } else {
-        if (n_meas && (r = sp_sample(ctx, seed, shot_begin + done, n, d_m, ld, nullptr))) return r;
-        if ((r = sp_encode(ctx, d_m, ld, n_meas, n, fmt, d_b))) return r;
+        if (n_meas && (r = sp_sample(ctx, seed, shot_begin + done, n, d_m[b], ld, nullptr))) return r;
+        if ((r = sp_encode(ctx, d_m[b], ld, n_meas, n, fmt, d_b[b]))) return r;
       }
       const uint64_t nb = sp_encoded_size(n_meas, n, fmt);
-      if (nb) ck(cudaMemcpyAsync(h_out + off, d_b, nb, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+      ck(cudaEventRecord(ctx->ev_ready[b], ctx->stream), "cudaEventRecord");
+      ck(cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_ready[b], 0), "cudaStreamWaitEvent");
+      if (nb) ck(cudaMemcpyAsync(h_out + off, d_b[b], nb, cudaMemcpyDeviceToHost, ctx->copy_stream), "D2H");
+      ck(cudaEventRecord(ctx->ev_free[b], ctx->copy_stream), "cudaEventRecord");
       off += nb;
     }
+    // the compute stream must not run ahead of the copies into host memory
+    ck(cudaStreamWaitEvent(ctx->stream, ctx->ev_free[(i - 1) & 1], 0), "cudaStreamWaitEvent");
+    ck(cudaStreamSynchronize(ctx->copy_stream), "sync");
     ck(cudaStreamSynchronize(ctx->stream), "sync");
     if (written) *written = off;
   } catch (const CudaError& e) {

@@ -248,19 +248,18 @@ __device__ __forceinline__ uint32_t transpose32(uint32_t x) {
 
 // b8: ceil(n_m/8) bytes per shot, measurement k at bit k%8 of byte k/8.
 // Each warp turns one 32-shot column into 32 records, staged in shared
-// memory so the global write of the block's records is contiguous.
-// Word (row k, 32-shot column c) of a measurement-major (tw32 == 0) or
-// tiled (tw32 = T/32) record array.
+// memory so the global write of the block's records is contiguous (16-byte
+// stores when aligned). Word (row k, 32-shot column c) of a
+// measurement-major (tw_log2 < 0) or tiled (tw32 = 2^tw_log2 = T/32) array.
 __device__ __forceinline__ uint64_t rec_word(uint32_t k, uint64_t c, uint64_t ld32,
-                                             uint32_t n_meas, uint32_t tw32) {
-  if (tw32 == 0) return k * ld32 + c;
-  return (c / tw32) * (static_cast<uint64_t>(n_meas) * tw32) + static_cast<uint64_t>(k) * tw32 +
-         (c % tw32);
+                                             uint32_t n_meas, int tw_log2) {
+  if (tw_log2 < 0) return k * ld32 + c;
+  return ((c >> tw_log2) * n_meas + k << tw_log2) + (c & ((1u << tw_log2) - 1));
 }
 
 __global__ void k3_b8(const uint32_t* __restrict__ m32, uint64_t ld32, uint32_t n_meas,
                       uint64_t n_shots, uint32_t rec, uint8_t* __restrict__ out, bool staged,
-                      uint32_t tw32) {
+                      int tw_log2) {
   extern __shared__ __align__(16) uint8_t stage[];
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const uint64_t n_words32 = (n_shots + 31) >> 5;
@@ -270,7 +269,7 @@ __global__ void k3_b8(const uint32_t* __restrict__ m32, uint64_t ld32, uint32_t 
   const uint64_t my_shot = shot0 + warp * 32 + lane;
   for (uint32_t kw = 0; kw < kwords; ++kw) {
     const uint32_t k = kw * 32 + lane;
-    uint32_t x = (k < n_meas && col < n_words32) ? m32[rec_word(k, col, ld32, n_meas, tw32)] : 0u;
+    uint32_t x = (k < n_meas && col < n_words32) ? m32[rec_word(k, col, ld32, n_meas, tw_log2)] : 0u;
     x = transpose32(x);
     uint8_t* dst = staged ? stage + static_cast<uint64_t>(warp * 32 + lane) * rec
                           : out + my_shot * rec;
@@ -284,12 +283,18 @@ __global__ void k3_b8(const uint32_t* __restrict__ m32, uint64_t ld32, uint32_t 
   const uint64_t shots = min(static_cast<uint64_t>(nw) * 32, n_shots - shot0);
   const uint64_t nbytes = shots * rec;
   uint8_t* dst = out + shot0 * rec;
-  for (uint64_t i = threadIdx.x; i < nbytes; i += blockDim.x) dst[i] = stage[i];
+  if ((reinterpret_cast<uintptr_t>(dst) & 15) == 0 && (nbytes & 15) == 0) {
+    const uint4* s4 = reinterpret_cast<const uint4*>(stage);
+    uint4* d4 = reinterpret_cast<uint4*>(dst);
+    for (uint64_t i = threadIdx.x; i < (nbytes >> 4); i += blockDim.x) d4[i] = s4[i];
+  } else {
+    for (uint64_t i = threadIdx.x; i < nbytes; i += blockDim.x) dst[i] = stage[i];
+  }
 }
 
 // '01': one line per shot, '0'/'1' per measurement then '\n'.
 __global__ void k3_01(const uint32_t* __restrict__ m32, uint64_t ld32, uint32_t n_meas,
-                      uint64_t n_shots, uint8_t* __restrict__ out, uint32_t tw32) {
+                      uint64_t n_shots, uint8_t* __restrict__ out, int tw_log2) {
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const uint64_t n_words32 = (n_shots + 31) >> 5;
   const uint64_t col = static_cast<uint64_t>(blockIdx.x) * nw + warp;
@@ -299,7 +304,7 @@ __global__ void k3_01(const uint32_t* __restrict__ m32, uint64_t ld32, uint32_t 
   const uint32_t kwords = (n_meas + 31) >> 5;
   for (uint32_t kw = 0; kw < kwords; ++kw) {
     const uint32_t k = kw * 32 + lane;
-    uint32_t x = k < n_meas ? m32[rec_word(k, col, ld32, n_meas, tw32)] : 0u;
+    uint32_t x = k < n_meas ? m32[rec_word(k, col, ld32, n_meas, tw_log2)] : 0u;
     x = transpose32(x);
     if (shot < n_shots) {
       uint8_t* dst = out + shot * line + kw * 32;
@@ -476,7 +481,9 @@ int launch_product(const DevPlan& P, const LaunchCfg& L, bool dense, const uint6
 
 int launch_encode(const LaunchCfg& L, const uint64_t* m, uint64_t ld, uint64_t n_meas,
                   uint64_t n_shots, int fmt, uint8_t* bytes, uint32_t tile_shots) {
-  const uint32_t tw32 = tile_shots / 32;
+  // tiled input: T/32 words per row per tile (T a power of two >= 128)
+  int tw_log2 = -1;
+  if (tile_shots) tw_log2 = __builtin_ctz(tile_shots / 32);
   if (n_shots == 0 || n_meas == 0) {
     if (fmt == 0 && n_shots) {  // n_meas == 0: one empty line per shot
       if (cudaMemsetAsync(bytes, '\n', n_shots, L.stream) != cudaSuccess) return -1;
@@ -489,7 +496,7 @@ int launch_encode(const LaunchCfg& L, const uint64_t* m, uint64_t ld, uint64_t n
     const uint64_t blocks = (n_words32 + 7) / 8;
     k3_01<<<static_cast<unsigned>(blocks), 256, 0, L.stream>>>(m32, 2 * ld,
                                                                static_cast<uint32_t>(n_meas),
-                                                               n_shots, bytes, tw32);
+                                                               n_shots, bytes, tw_log2);
   } else {
     const uint32_t rec = static_cast<uint32_t>((n_meas + 7) / 8);
     const size_t budget = 96 * 1024;
@@ -502,7 +509,7 @@ int launch_encode(const LaunchCfg& L, const uint64_t* m, uint64_t ld, uint64_t n
       return -1;
     const uint64_t blocks = (n_words32 + warps - 1) / warps;
     k3_b8<<<static_cast<unsigned>(blocks), warps * 32, smem, L.stream>>>(
-        m32, 2 * ld, static_cast<uint32_t>(n_meas), n_shots, rec, bytes, staged, tw32);
+        m32, 2 * ld, static_cast<uint32_t>(n_meas), n_shots, rec, bytes, staged, tw_log2);
   }
   return check_launch() ? -1 : 1;
 }
