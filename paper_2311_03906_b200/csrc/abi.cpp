@@ -211,6 +211,30 @@ ChainXf chain_transform(uint64_t n_meas, const std::vector<uint64_t>& row_ptr,
   return x;
 }
 
+// Content fingerprint of the loaded model and of the SP_* planner switches.
+uint64_t model_fingerprint(const HostPlan& h) {
+  uint64_t fp = 0xcbf29ce484222325ull;
+  auto mix = [&](const void* data, size_t n) {  // FNV-1a over 64-bit words
+    const uint8_t* b = static_cast<const uint8_t*>(data);
+    size_t i = 0;
+    for (; i + 8 <= n; i += 8) {
+      uint64_t w;
+      std::memcpy(&w, b + i, 8);
+      fp = (fp ^ w) * 0x100000001b3ull;
+    }
+    for (; i < n; ++i) fp = (fp ^ b[i]) * 0x100000001b3ull;
+  };
+  const uint64_t dims[4] = {h.n_meas, h.n_sym, h.groups.size(), h.ldm};
+  mix(dims, sizeof dims);
+  mix(h.row_ptr.data(), h.row_ptr.size() * 8);
+  mix(h.sym_idx.data(), h.sym_idx.size() * 4);
+  mix(h.dense_words.data(), h.dense_words.size() * 8);
+  mix(h.groups.data(), h.groups.size() * sizeof(sp_group));
+  for (char** e = environ; e && *e; ++e)
+    if (std::strncmp(*e, "SP_", 3) == 0) mix(*e, std::strlen(*e));
+  return fp;
+}
+
 // SP_PLAN_TIMING=1: per-phase host times of build_plan on stderr.
 struct PlanTimer {
   bool on = std::getenv("SP_PLAN_TIMING") != nullptr;
@@ -392,23 +416,21 @@ void build_plan(sp_ctx* c) {
   bool staged = false, row_staged = false;
   const long force_lg = env_long("SP_TLOG2", 0), force_st = env_long("SP_STAGED", -1),
              force_rs = env_long("SP_ROWSTAGED", -1);
-  // Preference: event + row tables on chip (T >= 512), row tables only, none.
-  const bool cand[3][2] = {{true, true}, {false, true}, {false, false}};
-  for (int ci = 0; ci < 3 && lg < 0; ++ci) {
-    const bool st = cand[ci][0], rs = cand[ci][1];
-    if (force_st >= 0 && st != (force_st != 0)) continue;
-    if (force_rs >= 0 && rs != (force_rs != 0)) continue;
-    for (int t = 12; t >= 7; --t) {
-      if (force_lg && t != force_lg) continue;
-      if (static_cast<uint64_t>(n_meas + 1) * (1u << (t - 5)) >= 65536) continue;  // u16 row offsets
-      if (st && t < 9 && !force_lg) break;
-      if (fused_smem_bytes(d, t, st, rs) <= optin) {
-        lg = t;
-        staged = st;
-        row_staged = rs;
-        break;
-      }
-    }
+  // The shot tile T is part of the random-stream structure (streams are
+  // keyed by global tile), so it depends only on the model and the device's
+  // shared memory: the largest T whose tiles fit with no tables staged.
+  // Staging then takes what is left: row tables, then (T >= 512) the event
+  // tables of the table-walk variant.
+  for (int t = 12; t >= 7 && lg < 0; --t) {
+    if (force_lg && t != force_lg) continue;
+    if (static_cast<uint64_t>(n_meas + 1) * (1u << (t - 5)) >= 65536) continue;  // u16 row offsets
+    if (fused_smem_bytes(d, t, false, false) <= optin) lg = t;
+  }
+  if (lg >= 0) {
+    row_staged = force_rs >= 0 ? force_rs != 0 : fused_smem_bytes(d, lg, false, true) <= optin;
+    staged = force_st >= 0 ? force_st != 0
+                           : lg >= 9 && fused_smem_bytes(d, lg, true, row_staged) <= optin;
+    if (fused_smem_bytes(d, lg, staged, row_staged) > optin) lg = -1;  // forced staging does not fit
   }
   c->fused_ok = lg >= 0;
   if (lg < 0) {
@@ -465,8 +487,11 @@ void build_plan(sp_ctx* c) {
   const long seg_fe = env_long("SP_SEG_EVENTS", 0);
   std::vector<double> seg_lam(live_cls.size()), seg_S(live_cls.size());
   std::vector<uint64_t> seg_nmin(live_cls.size()), seg_nmax(live_cls.size());
-  // Slice counts of the live classes (in live_cls order) for gw generator warps.
-  auto plan_segments = [&](uint32_t gw) {
+  // Slice counts of the live classes (in live_cls order). The slices are the
+  // random streams (keyed by slice id and global tile), so they depend only
+  // on the model and the tile size — never on the launch shape — and a seed
+  // gives the same records on any GPU count and any tuned warp split.
+  auto plan_segments = [&](uint32_t min_slices) {
     std::vector<uint64_t> nseg(live_cls.size(), 1);
     auto cost = [&](size_t c, uint64_t n) {
       return n * (exp_steps(seg_lam[c] / n, seg_S[c]) + seg_cost);
@@ -493,7 +518,7 @@ void build_plan(sp_ctx* c) {
       nseg[c] = std::min(std::max(best, seg_nmin[c]), seg_nmax[c]);
       total += nseg[c];
     }
-    const uint64_t min_total = seg_fe > 0 ? 0 : static_cast<uint64_t>(env_long("SP_SEG_MIN", gw));
+    const uint64_t min_total = seg_fe > 0 ? 0 : min_slices;
     while (total < min_total) {  // split where it costs the fewest extra steps
       size_t arg = live_cls.size();
       double dmin = 0;
@@ -508,7 +533,9 @@ void build_plan(sp_ctx* c) {
     }
     return nseg;
   };
-  std::vector<uint64_t> live_nseg = plan_segments(d.gen_warps);
+  // at least 12 slices per tile: enough for ~12 generator warps with two
+  // tiles in flight
+  std::vector<uint64_t> live_nseg = plan_segments(static_cast<uint32_t>(env_long("SP_SEG_MIN", 12)));
   {
     // Longest slices first: warps take slices in id order, so a warp that
     // finishes early picks up a short one. (The order is fixed here; the
@@ -779,8 +806,9 @@ void build_plan(sp_ctx* c) {
   ck(cudaStreamSynchronize(s), "plan upload");
 
   ptm.mark("paths");
-  // Launch autotune: the generator/drain warp split (and with it the slice
-  // counts) and the padded-XOR mode are measured, not modelled — a few short
+  // Launch autotune: the generator/drain warp split and the padded-XOR mode
+  // (launch parameters only: results do not depend on them) are measured,
+  // not modelled — a few short
   // launches of the fused kernel over ~16 tiles per CTA: first the padding
   // mode at the model's split, then the splits around it. SP_GEN_WARPS /
   // SP_PAD_PRED fix a choice; SP_AUTOTUNE=0 keeps the model's.
@@ -788,29 +816,10 @@ void build_plan(sp_ctx* c) {
   const bool fix_pp = env_long("SP_PAD_PRED", -1) >= 0 || d.lp == 0;
   // Tuned shapes are cached per (model, device, plan shape) fingerprint, so
   // re-loading the same model does not re-measure.
-  uint64_t fp = 0xcbf29ce484222325ull;
-  auto mix = [&](const void* data, size_t n) {  // FNV-1a over 64-bit words
-    const uint8_t* b = static_cast<const uint8_t*>(data);
-    size_t i = 0;
-    for (; i + 8 <= n; i += 8) {
-      uint64_t w;
-      std::memcpy(&w, b + i, 8);
-      fp = (fp ^ w) * 0x100000001b3ull;
-    }
-    for (; i < n; ++i) fp = (fp ^ b[i]) * 0x100000001b3ull;
-  };
-  auto mix64v = [&](uint64_t v) { mix(&v, 8); };
-  mix64v(n_meas);
-  mix64v(n_sym);
-  mix(h.row_ptr.data(), h.row_ptr.size() * 8);
-  mix(h.sym_idx.data(), h.sym_idx.size() * 4);
-  for (const sp_group& g : h.groups) {
-    mix64v(g.dist);
-    mix(&g.param, 8);
-    mix64v(g.first_symbol);
-  }
-  mix64v(static_cast<uint64_t>(c->L.num_sms) << 32 | d.t_log2);
-  mix64v(d.lp | static_cast<uint64_t>(d.entry_bytes) << 8 | static_cast<uint64_t>(d.cta_threads) << 16);
+  const uint64_t fp =
+      ((model_fingerprint(h) ^ (static_cast<uint64_t>(c->L.num_sms) << 32 | d.t_log2)) *
+       0x100000001b3ull) ^
+      (d.lp | static_cast<uint64_t>(d.entry_bytes) << 8 | static_cast<uint64_t>(d.cta_threads) << 16);
   static std::mutex tune_mu;
   static std::map<uint64_t, std::pair<uint32_t, uint32_t>> tune_cache;  // fp -> (gen_warps, pad_pred)
   bool cached = false;
@@ -823,7 +832,6 @@ void build_plan(sp_ctx* c) {
       cached = true;
     }
   }
-  if (cached && !fix_gw) apply_segments(plan_segments(d.gen_warps));
   if (!cached && c->fused_ok && !live_cls.empty() && n_meas > 0 && !(fix_gw && fix_pp) &&
       env_long("SP_AUTOTUNE", 1) != 0) {
     const long n_warps = d.cta_threads / 32;
@@ -866,20 +874,15 @@ void build_plan(sp_ctx* c) {
         }
         float best_ms = 0.f;
         uint32_t best = gw0;
-        std::vector<uint64_t> best_nseg = live_nseg;
         for (uint32_t gw : cand) {
           d.gen_warps = gw;
-          const std::vector<uint64_t> ns = plan_segments(gw);
-          apply_segments(ns);
           const float t = time_launch();
           if (gw == gw0 || t < best_ms * 0.99f) {
             best_ms = t;
             best = gw;
-            best_nseg = ns;
           }
         }
         d.gen_warps = best;
-        apply_segments(best_nseg);
       }
     } catch (...) {
       cudaFree(buf);
@@ -897,30 +900,6 @@ void build_plan(sp_ctx* c) {
   }
   ptm.mark("autotune");
   c->plan_ready = true;
-}
-
-// Content fingerprint of the loaded model and of the SP_* planner switches.
-uint64_t model_fingerprint(const HostPlan& h) {
-  uint64_t fp = 0xcbf29ce484222325ull;
-  auto mix = [&](const void* data, size_t n) {  // FNV-1a over 64-bit words
-    const uint8_t* b = static_cast<const uint8_t*>(data);
-    size_t i = 0;
-    for (; i + 8 <= n; i += 8) {
-      uint64_t w;
-      std::memcpy(&w, b + i, 8);
-      fp = (fp ^ w) * 0x100000001b3ull;
-    }
-    for (; i < n; ++i) fp = (fp ^ b[i]) * 0x100000001b3ull;
-  };
-  const uint64_t dims[4] = {h.n_meas, h.n_sym, h.groups.size(), h.ldm};
-  mix(dims, sizeof dims);
-  mix(h.row_ptr.data(), h.row_ptr.size() * 8);
-  mix(h.sym_idx.data(), h.sym_idx.size() * 4);
-  mix(h.dense_words.data(), h.dense_words.size() * 8);
-  mix(h.groups.data(), h.groups.size() * sizeof(sp_group));
-  for (char** e = environ; e && *e; ++e)
-    if (std::strncmp(*e, "SP_", 3) == 0) mix(*e, std::strlen(*e));
-  return fp;
 }
 
 // Re-upload the raw model arrays of an unchanged model; the derived plan

@@ -224,3 +224,44 @@ def test_tiled_layout_equals_measurement_major(gpu_sampler_factory, cfg):
         assert torch.equal(c1, c2)
         for fmt in ("b8", "01"):
             assert torch.equal(s.encode_tiled(tl, n, fmt), s.encode(mm, n, fmt))
+
+
+@pytest.mark.parametrize("env", [{"SP_GEN_WARPS": "9"}, {"SP_GEN_WARPS": "14"},
+                                 {"SP_PAD_PRED": "1"}, {"SP_PAD_PRED": "0"},
+                                 {"SP_AUTOTUNE": "0"}, {"SP_ROWSTAGED": "0"}])
+def test_launch_shape_does_not_change_records(gpu_sampler_factory, monkeypatch, env):
+    """Random streams are keyed by (slice, global tile) only: the warp split,
+    padded-XOR mode, autotune and staging choices change speed, not bits."""
+    import torch
+    for name, text in [("surf5", CI.surface_code(5, 5, 1e-3)), ("surf9", CI.surface_code(9, 3, 1e-3))]:
+        init = run_initialization(text)
+        base = gpu_sampler_factory(init)
+        n = 5 * base.shot_tile + 11
+        c0 = torch.zeros(init.n_meas, dtype=torch.int64, device="cuda")
+        want = base.sample(n, 77, counts=c0)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        s = gpu_sampler_factory(init)
+        c1 = torch.zeros(init.n_meas, dtype=torch.int64, device="cuda")
+        assert torch.equal(s.sample(n, 77, counts=c1), want), (name, env, s.plan_info())
+        assert torch.equal(c0, c1)
+        for k in env:
+            monkeypatch.delenv(k)
+
+
+def test_reload_same_and_other_model(gpu_sampler_factory, port):
+    """Re-loading an identical model keeps the plan and the records; loading
+    a different one rebuilds it (checked against the oracle)."""
+    a = run_initialization(CI.surface_code(5, 5, 1e-3))
+    b = run_initialization(CI.repetition_code(5, 5, 0.01))
+    s = gpu_sampler_factory(a)
+    n = 3 * s.shot_tile
+    first = host(s.sample(n, 5))
+    s.load(a)
+    assert np.array_equal(host(s.sample(n, 5)), first)
+    s.load(b)
+    nb = 3 * s.shot_tile
+    S = s.draw_assignments(nb, 5)
+    assert np.array_equal(host(s.sample(nb, 5)), port.sample(b.row_ptr, b.sym_idx, host(S), nb))
+    s.load(a)
+    assert np.array_equal(host(s.sample(n, 5)), first)
