@@ -229,13 +229,19 @@ def run_ours(args):
     T = smp.shot_tile
     shots = (shots + T - 1) // T * T
     shot_begin = rank * shots  # disjoint global shot ranges, tile-aligned
-    out = smp.empty_bits(init.n_meas, shots)
+    tiled = args.layout == "tiled"
+    if tiled:  # [tile][row][T/64] records: contiguous stores for any row count
+        out = torch.empty(smp.tiled_words(shots), dtype=torch.int64, device=dev)
+    else:
+        out = smp.empty_bits(init.n_meas, shots)
+    run = ((lambda n, seed, **kw: smp.sample_tiled(n, seed, out=out, **kw)) if tiled else
+           (lambda n, seed, **kw: smp.sample(n, seed, out=out, **kw)))
     counts = torch.zeros(init.n_meas, dtype=torch.int64, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
     stream = torch.cuda.current_stream()
 
     def step(i):
-        smp.sample(shots, 1000 + i, shot_begin=shot_begin, out=out, counts=counts)
+        run(shots, 1000 + i, shot_begin=shot_begin, counts=counts)
         if world > 1:
             dist.all_reduce(counts)
 
@@ -288,7 +294,7 @@ def run_ours(args):
     for i, (a, b) in enumerate(kev):
         flush.zero_()
         a.record(stream)
-        smp.sample(shots, 5000 + i, shot_begin=shot_begin, out=out)
+        run(shots, 5000 + i, shot_begin=shot_begin)
         b.record(stream)
     torch.cuda.synchronize()
     k_ms = statistics.mean(a.elapsed_time(b) for a, b in kev)
@@ -336,7 +342,8 @@ def run_ours(args):
                 "n_sym": init.n_sym, "nnz": init.nnz, "shot_tile": T,
                 "parallelism": f"shot-range sharding x{world}" + (", NCCL all_reduce of "
                                "per-measurement counts" if world > 1 else ""),
-                "output": "measurement-major u64 bit-sliced records in HBM + per-row counts",
+                "output": ("tiled [tile][row][T/64]" if tiled else "measurement-major") +
+                          " u64 bit-sliced records in HBM + per-row counts",
                 "l2": "flushed between timed steps (256 MiB memset outside the events); "
                       "output per step > L2",
                 "init_seconds": round(init_s, 4),
@@ -378,6 +385,9 @@ def main():
     ap.add_argument("--shots", type=int, default=0, help="override shots per GPU")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--layout", default="mm", choices=["mm", "tiled"],
+                    help="record layout in HBM: measurement-major (the reference's SampleMatrix "
+                         "orientation) or tiled (sp_sample_tiled)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -219,11 +219,14 @@ class Sampler:
                                   _ptr(counts)))
         return out
 
+    def tiled_words(self, n_shots: int) -> int:
+        """u64 words of the tiled record array for n_shots."""
+        return int(self._L.sp_tiled_words(self._h, n_shots))
+
     def sample_tiled(self, n_shots: int, seed: int, shot_begin: int = 0, out=None, counts=None):
         """Fused sampler with tiled records: blocks [n_meas][T/64] per T shots."""
         if out is None:
-            nw = int(self._L.sp_tiled_words(self._h, n_shots))
-            out = self._torch.empty(max(nw, 1), dtype=self._torch.int64,
+            out = self._torch.empty(max(self.tiled_words(n_shots), 1), dtype=self._torch.int64,
                                     device=f"cuda:{self.device}")
         N.check(self._L.sp_sample_tiled(self._h, seed, shot_begin, n_shots, _ptr(out),
                                         _ptr(counts)))
