@@ -237,3 +237,65 @@ CONFIGS = {
     "cfg4": dict(name="random Clifford n=1000, 100 layers",
                  text=lambda: random_clifford(1000, 100, 1e-3, 1), shots=10**6),
 }
+
+
+# ---- cfg5: raw GF(2) sampling sweep (BASELINE.json configs[4]) -------------
+#
+# Not a circuit: M_sym itself is drawn, m rows x v fault variables with
+# i.i.d. Bernoulli(dens) entries (geometric gaps for dens <
+# 0.05, else per-entry bits; seed 7), and each variable is its own
+# Bernoulli(p) fault group. Symbol 0 is the constant s0 (unused by the rows),
+# symbols 1..v the faults, as the reference registry would number them
+# (symbols.hpp:49-71).
+CFG5_DENSITIES = (0.001, 0.01, 0.5)
+CFG5_RATES = (1e-4, 1e-3, 1e-2)
+
+
+def random_msym_rows(m: int, v: int, dens: float, seed: int = 7):
+    """CSR rows (row_ptr u64 [m+1], sym_idx u32 ascending in [1, v])."""
+    import numpy as np
+
+    rng = np.random.default_rng(seed)
+    rows = []
+    if dens < 0.05:
+        # geometric gaps: positions of successes in a Bernoulli(dens) row
+        for _ in range(m):
+            need = int(v * dens + 8 * (v * dens) ** 0.5 + 16)
+            pos = np.cumsum(rng.geometric(dens, size=need)) - 1
+            while pos[-1] < v:  # rare: extend
+                more = np.cumsum(rng.geometric(dens, size=need)) + pos[-1]
+                pos = np.concatenate([pos, more])
+            rows.append((pos[pos < v] + 1).astype(np.uint32))
+    else:
+        for _ in range(m):
+            bits = rng.random(v) < dens
+            rows.append((np.flatnonzero(bits) + 1).astype(np.uint32))
+    row_ptr = np.zeros(m + 1, dtype=np.uint64)
+    row_ptr[1:] = np.cumsum([len(r) for r in rows])
+    sym_idx = np.concatenate(rows) if rows else np.zeros(0, np.uint32)
+    return row_ptr, sym_idx
+
+
+def random_msym_model(m: int = 10**4, v: int = 10**5, dens: float = 0.001, p: float = 1e-3,
+                      seed: int = 7):
+    """cfg5 model as an InitResult: random rows + v Bernoulli(p) groups."""
+    import numpy as np
+
+    from .sampler import GROUP_DTYPE, InitResult
+
+    row_ptr, sym_idx = random_msym_rows(m, v, dens, seed)
+    return InitResult(0, v + 1, row_ptr, sym_idx, bernoulli_groups(v, p))
+
+
+def bernoulli_groups(v: int, p: float):
+    """Group table: s0 (constant) + v single-symbol Bernoulli(p) groups."""
+    import numpy as np
+
+    from .sampler import GROUP_DTYPE
+
+    groups = np.zeros(v + 1, dtype=GROUP_DTYPE)
+    groups["dist"][1:] = 1  # Bernoulli
+    groups["param"][1:] = p
+    groups["first_symbol"] = np.arange(v + 1, dtype=np.uint32)
+    groups["arity"] = 1
+    return groups

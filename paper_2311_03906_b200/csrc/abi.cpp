@@ -418,19 +418,26 @@ void build_plan(sp_ctx* c) {
              force_rs = env_long("SP_ROWSTAGED", -1);
   // The shot tile T is part of the random-stream structure (streams are
   // keyed by global tile), so it depends only on the model and the device's
-  // shared memory: the largest T whose tiles fit with no tables staged.
-  // Staging then takes what is left: row tables, then (T >= 512) the event
-  // tables of the table-walk variant.
-  for (int t = 12; t >= 7 && lg < 0; --t) {
-    if (force_lg && t != force_lg) continue;
-    if (static_cast<uint64_t>(n_meas + 1) * (1u << (t - 5)) >= 65536) continue;  // u16 row offsets
-    if (fused_smem_bytes(d, t, false, false) <= optin) lg = t;
+  // shared memory: the largest T whose tiles fit double-buffered with no
+  // tables staged — else single-buffered (very many rows). Staging then
+  // takes what is left: row tables, then (T >= 512) the event tables of the
+  // table-walk variant.
+  uint32_t n_buf = 2;
+  for (uint32_t nb = 2; nb >= 1 && lg < 0; --nb) {
+    for (int t = 12; t >= 7 && lg < 0; --t) {
+      if (force_lg && t != force_lg) continue;
+      if (static_cast<uint64_t>(n_meas + 1) * (1u << (t - 5)) >= 65536) continue;  // u16 row offsets
+      if (fused_smem_bytes(d, t, false, false, nb) <= optin) {
+        lg = t;
+        n_buf = nb;
+      }
+    }
   }
   if (lg >= 0) {
-    row_staged = force_rs >= 0 ? force_rs != 0 : fused_smem_bytes(d, lg, false, true) <= optin;
+    row_staged = force_rs >= 0 ? force_rs != 0 : fused_smem_bytes(d, lg, false, true, n_buf) <= optin;
     staged = force_st >= 0 ? force_st != 0
-                           : lg >= 9 && fused_smem_bytes(d, lg, true, row_staged) <= optin;
-    if (fused_smem_bytes(d, lg, staged, row_staged) > optin) lg = -1;  // forced staging does not fit
+                           : lg >= 9 && fused_smem_bytes(d, lg, true, row_staged, n_buf) <= optin;
+    if (fused_smem_bytes(d, lg, staged, row_staged, n_buf) > optin) lg = -1;  // forced staging does not fit
   }
   c->fused_ok = lg >= 0;
   if (lg < 0) {
@@ -443,8 +450,9 @@ void build_plan(sp_ctx* c) {
   d.tw = static_cast<uint32_t>(T / 32);
   d.staged = staged;
   d.row_staged = row_staged;
+  d.n_buf = n_buf;
   {
-    const size_t smem = fused_smem_bytes(d, d.t_log2, staged, row_staged);
+    const size_t smem = fused_smem_bytes(d, d.t_log2, staged, row_staged, n_buf);
     d.cta_per_sm = static_cast<uint32_t>(std::max<long>(
         1, std::min<long>(env_long("SP_CTAS", 2), static_cast<long>((228 * 1024) / (smem + 1024)))));
     const double ev = events_per_shot * T, flips = flips_per_shot * T;
@@ -1397,7 +1405,7 @@ int sp_plan_info(sp_ctx* ctx, uint64_t* out16) {
   const uint64_t v[16] = {1ull << d.t_log2, d.gen_warps, d.cta_threads, d.staged, d.row_staged,
                           d.lp, d.pad_pred, d.n_paths, d.n_rounds, d.n_keep, d.n_seg_live,
                           d.n_cls_live, d.n_dense_live, ctx->dnnz,
-                          fused_smem_bytes(d, d.t_log2, d.staged, d.row_staged), ctx->fused_ok};
+                          fused_smem_bytes(d, d.t_log2, d.staged, d.row_staged, d.n_buf), ctx->fused_ok};
   std::memcpy(out16, v, sizeof(v));
   return SP_OK;
 }

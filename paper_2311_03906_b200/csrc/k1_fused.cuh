@@ -39,7 +39,10 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
   const uint32_t tile_words = P.n_meas * tw + spare_words(tw);
   const bool with_counts = counts != nullptr;
   uint32_t* tiles = reinterpret_cast<uint32_t*>(smem);
-  uint8_t* p = reinterpret_cast<uint8_t*>(tiles + 2 * tile_words);
+  // n_buf tile buffers: 2 (generators fill tile i+1 while drains empty tile
+  // i) or, when two do not fit (very many rows), 1 (the roles alternate)
+  const uint32_t n_buf = P.n_buf;
+  uint8_t* p = reinterpret_cast<uint8_t*>(tiles + n_buf * tile_words);
   // Flip counts: per (row, lane) partials when a warp walks one path per
   // 128-shot column group (T = 4096: no cross-lane reduction per row),
   // else one counter per row.
@@ -95,7 +98,7 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
   }
   {
     uint4* t4 = reinterpret_cast<uint4*>(tiles);
-    for (uint32_t i = threadIdx.x; i < (2 * tile_words) / 4; i += blockDim.x)
+    for (uint32_t i = threadIdx.x; i < (n_buf * tile_words) / 4; i += blockDim.x)
       t4[i] = make_uint4(0, 0, 0, 0);
     if (with_counts)
       for (uint32_t i = threadIdx.x; i < P.n_meas * cnt_lanes; i += blockDim.x) cnt[i] = 0;
@@ -111,10 +114,10 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
   if (warp < n_gen) {
     // ---------------- event generators ----------------
     for (uint32_t i = 0; i < n_my; ++i) {
-      const uint32_t b = i & 1;
+      const uint32_t b = i & (n_buf - 1);
       const uint64_t gtile = tile0 + blockIdx.x + static_cast<uint64_t>(i) * gridDim.x;
       long long tw0 = clock64();
-      if (i >= 2) named_sync(kBarEmpty0 + b, blockDim.x);
+      if (i >= n_buf) named_sync(kBarEmpty0 + b, blockDim.x);
       long long tw1 = clock64();
       uint32_t* tile = tiles + b * tile_words;
       const uint32_t tile_s = static_cast<uint32_t>(__cvta_generic_to_shared(tile));
@@ -288,7 +291,7 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
     // row stride in bytes for the fast path's 32x32->64 address multiply
     const uint32_t ldb = ld < (1ull << 29) ? static_cast<uint32_t>(ld * 8) : 0u;
     for (uint32_t i = 0; i < n_my; ++i) {
-      const uint32_t b = i & 1;
+      const uint32_t b = i & (n_buf - 1);
       const uint64_t t_local = blockIdx.x + static_cast<uint64_t>(i) * gridDim.x;
       long long td0 = clock64();
       named_sync(kBarFull0 + b, blockDim.x);
@@ -405,7 +408,7 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
         atomicAdd(reinterpret_cast<unsigned long long*>(P.timers) + 2, td1 - td0);
         atomicAdd(reinterpret_cast<unsigned long long*>(P.timers) + 3, clock64() - td1);
       }
-      if (i + 2 < n_my) named_arrive(kBarEmpty0 + b, blockDim.x);
+      if (i + n_buf < n_my) named_arrive(kBarEmpty0 + b, blockDim.x);
     }
   }
   if (with_counts) {
@@ -430,7 +433,7 @@ int launch_k1(const DevPlan& P, const LaunchCfg& L, const RoundKeys& K, uint64_t
               uint32_t n_tiles, uint64_t n_shots, uint64_t* out, uint64_t ld, uint64_t tstride,
               unsigned long long* cnt) {
   auto kern = k1_fused<kStaged, kRowStaged, kLp, kPadPred, kEB>;
-  const size_t smem = fused_smem_bytes(P, P.t_log2, kStaged, kRowStaged);
+  const size_t smem = fused_smem_bytes(P, P.t_log2, kStaged, kRowStaged, P.n_buf);
   int grid = 0;
   const int threads = static_cast<int>(P.cta_threads);
   if (persistent_grid(kern, L, smem, n_tiles, P.cta_per_sm, &grid, threads)) return -1;

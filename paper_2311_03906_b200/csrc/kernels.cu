@@ -352,9 +352,10 @@ int launch_k1(const DevPlan& P, const LaunchCfg& L, const RoundKeys& K, uint64_t
               unsigned long long* cnt);
 }  // namespace k1
 
-size_t fused_smem_bytes(const DevPlan& P, uint32_t t_log2, bool staged, bool row_staged) {
+size_t fused_smem_bytes(const DevPlan& P, uint32_t t_log2, bool staged, bool row_staged,
+                        uint32_t n_buf) {
   const size_t tw = size_t{1} << (t_log2 - 5);
-  size_t b = 2 * (static_cast<size_t>(P.n_meas) * tw + spare_words(tw)) * 4;  // tiles + spare
+  size_t b = n_buf * (static_cast<size_t>(P.n_meas) * tw + spare_words(tw)) * 4;  // tiles + spare
   b += align16(4ull * P.n_meas * (t_log2 >= 12 ? 32 : 1)) + 16;   // counts, dispensers
   if (row_staged) {
     b += align16(4ull * (P.n_meas + 1));

@@ -106,6 +106,7 @@ struct DevPlan {
   uint32_t gen_warps = 12;   // event-generator warps; the rest drain tiles
   uint32_t cta_per_sm = 1;
   uint32_t cta_threads = 512;
+  uint32_t n_buf = 2;        // shot-tile buffers in shared memory (1 or 2)
   // Profiling switches (SP_DEBUG_MODE): bit 0 skips the firing XORs, bit 1
   // skips the segment walks, bit 2 skips the HBM stores, bit 3 skips the row
   // rebuild. Results are wrong when set.
@@ -142,7 +143,8 @@ constexpr int kFusedThreads = 512;
 __host__ __device__ constexpr uint32_t spare_words(uint32_t tw) { return ((tw + 32) + 3) & ~3u; }
 
 // Shared-memory bytes of the fused kernel for a plan shape.
-size_t fused_smem_bytes(const DevPlan& P, uint32_t t_log2, bool staged, bool row_staged);
+size_t fused_smem_bytes(const DevPlan& P, uint32_t t_log2, bool staged, bool row_staged,
+                        uint32_t n_buf = 2);
 
 // K1 fused sampler (Philox). Returns number of launches issued, <0 on error.
 int launch_fused_sample(const DevPlan& P, const LaunchCfg& L, uint64_t seed, uint64_t tile0,

@@ -120,3 +120,19 @@ def test_port_vs_live_reference_random(port, ref):
 def test_golden_fixture_index(golden):
     names = json.loads(str(golden["frontend"]["names"]))
     assert "worked" in names and "surf3" in names
+
+
+def test_cfg5_generator_shapes():
+    """cfg5 rows: ascending symbol ids in [1, v], density within 5 sigma."""
+    from paper_2311_03906_b200 import circuits as CI
+    for dens in CI.CFG5_DENSITIES:
+        m, v = 200, 4000
+        rp, si = CI.random_msym_rows(m, v, dens, seed=7)
+        assert rp[0] == 0 and len(rp) == m + 1
+        for k in range(m):
+            r = si[rp[k]:rp[k + 1]]
+            assert np.all(np.diff(r.astype(np.int64)) > 0) and (len(r) == 0 or (r[0] >= 1 and r[-1] <= v))
+        n = m * v
+        assert abs(int(rp[-1]) - n * dens) <= 5 * (n * dens * (1 - dens)) ** 0.5 + 1
+        rp2, si2 = CI.random_msym_rows(m, v, dens, seed=7)
+        assert np.array_equal(rp, rp2) and np.array_equal(si, si2)
