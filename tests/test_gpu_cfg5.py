@@ -56,3 +56,21 @@ def test_cfg5_full_size_csr_equals_dense(gpu_sampler_factory, port, dens):
     assert np.array_equal(host(a[:, :64].contiguous()), want)
     del S, a, b
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("dens", [0.0005, 0.002])
+def test_fused_many_rows_single_buffer(gpu_sampler_factory, port, dens):
+    """8000 rows do not fit two shot tiles on chip: the fused sampler runs
+    single-buffered, and its records still equal M_sym . S for the S its
+    streams draw (and the oracle)."""
+    model = CI.random_msym_model(8000, 20000, dens, 2e-3, seed=11)
+    s = gpu_sampler_factory(model)
+    T = s.shot_tile
+    for n in (T, 5 * T + 9):
+        out = s.sample(n, 3)
+        S = s.draw_assignments(n, 3)
+        assert np.array_equal(host(out), host(s.sample_given(S, n)))
+    n = 2 * T
+    S = s.draw_assignments(n, 4)
+    assert np.array_equal(host(s.sample(n, 4)),
+                          port.sample(model.row_ptr, model.sym_idx, host(S), n))
