@@ -10,11 +10,13 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <iterator>
 #include <map>
 #include <mutex>
 #include <new>
 #include <stdexcept>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "frontend.hpp"
@@ -319,10 +321,32 @@ void build_plan(sp_ctx* c) {
   struct Cls {
     uint8_t dist;
     double p;
+    uint32_t lpc;  // flip-list length class (live): every pattern's D list has <= lpc rows
     std::vector<uint32_t> groups;
   };
   std::vector<Cls> live_cls, dead_cls;
-  std::map<std::pair<uint8_t, uint64_t>, size_t> live_key, dead_key;
+  std::map<std::tuple<uint8_t, uint64_t, uint32_t>, size_t> live_key, dead_key;
+  // Longest flip list over a group's patterns (symmetric differences of the
+  // D columns of the pattern's symbols), rounded up to 2, 4, 8, 16 (0: longer).
+  std::vector<uint32_t> mrg_a, mrg_b;
+  const bool split_lists = env_long("SP_LIST_CLASSES", 1) != 0;
+  auto list_class = [&](const sp_group& gr) -> uint32_t {
+    const uint32_t npat = (1u << gr.arity) - 1;
+    size_t mx = 0;
+    for (uint32_t pat = 1; pat <= npat; ++pat) {
+      mrg_a.clear();
+      for (uint32_t b = 0; b < gr.arity; ++b) {
+        if (!((pat >> b) & 1u)) continue;
+        const uint64_t sidx = gr.first_symbol + b;
+        mrg_b.clear();
+        std::set_symmetric_difference(mrg_a.begin(), mrg_a.end(), dcol_rows.begin() + dcol_ptr[sidx],
+                                      dcol_rows.begin() + dcol_ptr[sidx + 1], std::back_inserter(mrg_b));
+        mrg_a.swap(mrg_b);
+      }
+      mx = std::max(mx, mrg_a.size());
+    }
+    return mx <= 2 ? 2u : mx <= 4 ? 4u : mx <= 8 ? 8u : mx <= 16 ? 16u : 0u;
+  };
   std::vector<uint32_t> live_groups;
   double events_per_shot = 0, flips_per_shot = 0;
   for (uint64_t g = 1; g < G; ++g) {
@@ -365,15 +389,59 @@ void build_plan(sp_ctx* c) {
     }
     uint64_t pbits;
     std::memcpy(&pbits, &p, 8);
-    auto key = std::make_pair(gr.dist, pbits);
+    // Live classes are split by flip-list length, so a slice's warp only
+    // runs as many list entries as its class needs.
+    const uint32_t lpc = live && split_lists ? list_class(gr) : 0u;
+    auto key = std::make_tuple(gr.dist, pbits, lpc);
     auto& keymap = live ? live_key : dead_key;
     auto& cls = live ? live_cls : dead_cls;
     auto it = keymap.find(key);
     if (it == keymap.end()) {
       it = keymap.emplace(key, cls.size()).first;
-      cls.push_back(Cls{gr.dist, std::min(p, 1.0), {}});
+      cls.push_back(Cls{gr.dist, std::min(p, 1.0), lpc, {}});
     }
     cls[it->second].groups.push_back(static_cast<uint32_t>(g));
+  }
+  {
+    // Merge length classes holding < 5 % of their (dist, p) family's trials
+    // into the next longer class (or the longest one into its neighbour),
+    // so no class is too small to fill its slices. lpc 0 (lists > 16) is
+    // the longest.
+    auto rank = [](uint32_t l) { return l == 0 ? 99u : l; };
+    std::stable_sort(live_cls.begin(), live_cls.end(), [&](const Cls& a, const Cls& b) {
+      if (a.dist != b.dist) return a.dist < b.dist;
+      if (a.p != b.p) return a.p < b.p;
+      return rank(a.lpc) < rank(b.lpc);
+    });
+    std::vector<Cls> merged;
+    for (size_t i = 0; i < live_cls.size();) {
+      size_t j = i;
+      uint64_t fam = 0;
+      while (j < live_cls.size() && live_cls[j].dist == live_cls[i].dist && live_cls[j].p == live_cls[i].p)
+        fam += live_cls[j++].groups.size();
+      std::vector<Cls> f(std::make_move_iterator(live_cls.begin() + i),
+                         std::make_move_iterator(live_cls.begin() + j));
+      for (size_t k = 0; k + 1 < f.size();) {  // small ones flow upward
+        if (f[k].groups.size() * 20 < fam) {
+          f[k + 1].groups.insert(f[k + 1].groups.end(), f[k].groups.begin(), f[k].groups.end());
+          f.erase(f.begin() + k);
+        } else {
+          ++k;
+        }
+      }
+      if (f.size() > 1 && f.back().groups.size() * 20 < fam) {  // a small longest class
+        Cls& prev = f[f.size() - 2];
+        prev.groups.insert(prev.groups.end(), f.back().groups.begin(), f.back().groups.end());
+        prev.lpc = f.back().lpc;
+        f.pop_back();
+      }
+      for (Cls& c : f) {
+        std::sort(c.groups.begin(), c.groups.end());
+        merged.push_back(std::move(c));
+      }
+      i = j;
+    }
+    live_cls.swap(merged);
   }
 
   // Dense slots (live first). The fused kernel XORs each live slot's coin
@@ -423,7 +491,9 @@ void build_plan(sp_ctx* c) {
   // takes what is left: row tables, then (T >= 512) the event tables of the
   // table-walk variant.
   uint32_t n_buf = 2;
-  for (uint32_t nb = 2; nb >= 1 && lg < 0; --nb) {
+  const long force_nb = std::min<long>(env_long("SP_NBUF", 0), 4);
+  for (uint32_t nb = force_nb > 0 ? force_nb : 2; nb >= 1 && lg < 0; --nb) {
+    if (force_nb > 0 && nb != static_cast<uint32_t>(force_nb)) break;
     for (int t = 12; t >= 7 && lg < 0; --t) {
       if (force_lg && t != force_lg) continue;
       if (static_cast<uint64_t>(n_meas + 1) * (1u << (t - 5)) >= 65536) continue;  // u16 row offsets
@@ -541,9 +611,9 @@ void build_plan(sp_ctx* c) {
     }
     return nseg;
   };
-  // at least 12 slices per tile: enough for ~12 generator warps with two
-  // tiles in flight
-  std::vector<uint64_t> live_nseg = plan_segments(static_cast<uint32_t>(env_long("SP_SEG_MIN", 12)));
+  // at least 16 slices per tile: every generator warp takes one or two per
+  // tile (measured best for cfg2 and cfg3 among 8..32)
+  std::vector<uint64_t> live_nseg = plan_segments(static_cast<uint32_t>(env_long("SP_SEG_MIN", 16)));
   {
     // Longest slices first: warps take slices in id order, so a warp that
     // finishes early picks up a short one. (The order is fixed here; the
@@ -587,6 +657,7 @@ void build_plan(sp_ctx* c) {
       ci.goff = static_cast<uint32_t>(cls_groups.size());
       ci.trials = cl.groups.size() * T;
       ci.npat = cl.dist == SP_DIST_DEPOLARIZE2 ? 15 : cl.dist == SP_DIST_DEPOLARIZE1 ? 3 : 1;
+      ci.lp = cl.lpc;  // the kernel runs min(lp, plan lp) list entries for this class
       ci.pbase = static_cast<uint32_t>(pl_off.size() - 1);
       cls_info.push_back(ci);
       for (uint32_t g : cl.groups) {

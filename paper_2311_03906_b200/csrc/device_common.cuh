@@ -14,7 +14,8 @@ namespace {
 constexpr unsigned kFull = 0xFFFFFFFFu;
 
 // Named barriers of the fused kernel (0 is __syncthreads).
-constexpr uint32_t kBarFull0 = 1, kBarEmpty0 = 3, kBarDrain = 5;
+constexpr uint32_t kMaxBuf = 4;  // shot-tile buffers of the fused kernel
+constexpr uint32_t kBarFull0 = 1, kBarEmpty0 = 1 + kMaxBuf, kBarDrain = 1 + 2 * kMaxBuf;
 
 __host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) & ~size_t{15}; }
 
@@ -98,6 +99,7 @@ __device__ __forceinline__ uint32_t group_bits_compat(uint32_t dist, double p, u
 struct Segment {
   uint32_t g0, s0;  // first trial = (class position g0, shot s0 in the tile)
   uint32_t len, seg, goff, dist, pbase, npat;
+  uint32_t lp;      // list entries the class needs (ClassInfo::lp)
   float clg;
 };
 
@@ -129,6 +131,7 @@ __device__ __forceinline__ void segment_init(Segment& sg, const ClassInfo* cls, 
   sg.dist = ci.dist;
   sg.pbase = ci.pbase;
   sg.npat = ci.npat;
+  sg.lp = ci.lp;
   sg.clg = ci.clg;
 }
 

@@ -39,14 +39,14 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
   const uint32_t tile_words = P.n_meas * tw + spare_words(tw);
   const bool with_counts = counts != nullptr;
   uint32_t* tiles = reinterpret_cast<uint32_t*>(smem);
-  // n_buf tile buffers: 2 (generators fill tile i+1 while drains empty tile
-  // i) or, when two do not fit (very many rows), 1 (the roles alternate)
+  // n_buf tile buffers (1..4): with 2+ the generators fill tiles ahead while
+  // the drains empty tile i; 1 when two do not fit (very many rows)
   const uint32_t n_buf = P.n_buf;
   uint8_t* p = reinterpret_cast<uint8_t*>(tiles + n_buf * tile_words);
   // Flip counts: per (row, lane) partials when a warp walks one path per
   // 128-shot column group (T = 4096: no cross-lane reduction per row),
   // else one counter per row.
-  const uint32_t cnt_lanes = tw4 >= 32 ? 32u : 1u;
+  const uint32_t cnt_lanes = count_lanes(P.t_log2, P.n_buf);
   uint32_t* cnt = reinterpret_cast<uint32_t*>(p);
   p += align16(4ull * P.n_meas * cnt_lanes);
   uint32_t* segctr = reinterpret_cast<uint32_t*>(p);  // per-buffer segment dispensers
@@ -102,7 +102,7 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
       t4[i] = make_uint4(0, 0, 0, 0);
     if (with_counts)
       for (uint32_t i = threadIdx.x; i < P.n_meas * cnt_lanes; i += blockDim.x) cnt[i] = 0;
-    if (threadIdx.x < 2) segctr[threadIdx.x] = 0;
+    if (threadIdx.x < kMaxBuf) segctr[threadIdx.x] = 0;
   }
   __syncthreads();
 
@@ -114,7 +114,7 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
   if (warp < n_gen) {
     // ---------------- event generators ----------------
     for (uint32_t i = 0; i < n_my; ++i) {
-      const uint32_t b = i & (n_buf - 1);
+      const uint32_t b = i % n_buf;
       const uint64_t gtile = tile0 + blockIdx.x + static_cast<uint64_t>(i) * gridDim.x;
       long long tw0 = clock64();
       if (i >= n_buf) named_sync(kBarEmpty0 + b, blockDim.x);
@@ -202,6 +202,7 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
           return;
         }
         if constexpr (kLp > 0) {
+          const uint32_t lpu = sg.lp == 0 ? static_cast<uint32_t>(kLp) : sg.lp;
           if constexpr (kPre > 0 && kPre < kSlots) load_lists(bern_tag, f, kPre, kSlots);
 #pragma unroll
           for (int half = 0; half < kSlots; half += 4) {
@@ -212,6 +213,9 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
               const uint32_t bit = ((f.v >> k) & 1u) << (f.shot[k] & 31);
 #pragma unroll
               for (int e = 0; e < kLp; ++e) {
+                // the class's lists end by entry lpu (warp-uniform): skip the
+                // padding in power-of-two blocks
+                if (e >= 2 && (e & (e - 1)) == 0 && lpu <= static_cast<uint32_t>(e)) break;
                 uint32_t a;
                 bool real;
                 if constexpr (kEB == 1) {
@@ -291,7 +295,7 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
     // row stride in bytes for the fast path's 32x32->64 address multiply
     const uint32_t ldb = ld < (1ull << 29) ? static_cast<uint32_t>(ld * 8) : 0u;
     for (uint32_t i = 0; i < n_my; ++i) {
-      const uint32_t b = i & (n_buf - 1);
+      const uint32_t b = i % n_buf;
       const uint64_t t_local = blockIdx.x + static_cast<uint64_t>(i) * gridDim.x;
       long long td0 = clock64();
       named_sync(kBarFull0 + b, blockDim.x);
@@ -304,6 +308,7 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
       const uint32_t vq = static_cast<uint32_t>((valid + 127) >> 7);
       const uint32_t rem = static_cast<uint32_t>(valid & 127);
       const bool fast = vec && ldb != 0 && (valid == (static_cast<uint64_t>(1) << P.t_log2));
+      uint64_t* const tbase = out + t_local * tile_stride;  // this tile's records
       // Rows along parent paths (heavy-path decomposition of the L forest):
       // one thread walks a path top-down for one 128-shot column, carrying
       // the running row value; a path's head waits only for its parent's
@@ -321,7 +326,7 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
                                 : make_uint4(0, 0, 0, 0);
           const uint32_t xe = act ? PPTR[pth + 1] : 0;
           uint32_t x = act ? PPTR[pth] : 0;
-          uint64_t* obase = out + t_local * tile_stride + 2 * q;
+          uint64_t* obase = tbase + 2 * q;
           uint8_t* obase_b = reinterpret_cast<uint8_t*>(obase);
           // One row of the path: row = tile word ^ parent row; keep or clear
           // the tile word, store 16 bytes to HBM, optionally count.
@@ -361,10 +366,15 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
               if (with_counts) pc = __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
             }
             if (with_counts) {
-              if constexpr (kWarpPath) {  // per-lane partials, no reduction here
-                asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(cnt_s + ((k * 32 + lane) << 2)),
-                             "r"(pc)
-                             : "memory");
+              if constexpr (kWarpPath) {
+                if (cnt_lanes == 32) {  // per-lane partials, no reduction here
+                  asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(cnt_s + ((k * 32 + lane) << 2)),
+                               "r"(pc)
+                               : "memory");
+                } else {  // the warp walks this path: one add per row
+                  pc = __reduce_add_sync(kFull, pc);
+                  if (lane == 0) atomicAdd(&cnt[k], pc);
+                }
               } else {
                 if (pc) atomicAdd(&cnt[k], pc);
               }

@@ -23,7 +23,7 @@ struct ClassInfo {
   uint32_t dist = 0;    // 1 Bernoulli, 3 DEPOLARIZE1, 4 DEPOLARIZE2
   uint32_t pbase = 0;   // first flip list of the class (lists in plist)
   uint32_t npat = 1;    // non-identity patterns per group: 1, 3 or 15
-  uint32_t pad = 0;
+  uint32_t lp = 0;      // longest flip list of the class (2/4/8/16; 0 = longer)
 };
 
 // Everything a kernel needs about the loaded model, all device pointers.
@@ -141,6 +141,13 @@ constexpr int kFusedThreads = 512;
 // padded flip-list entries point into it, spread over 32 banks (u32 lists:
 // offset n_meas*tw + r, r < 32, plus the firing's word < tw).
 __host__ __device__ constexpr uint32_t spare_words(uint32_t tw) { return ((tw + 32) + 3) & ~3u; }
+
+// Per-row flip-count slots of the fused kernel: 32 per-lane partials when a
+// warp walks one path per 4096-shot tile (no per-row reduction), unless
+// three or more tile buffers leave no room for them.
+__host__ __device__ constexpr uint32_t count_lanes(uint32_t t_log2, uint32_t n_buf) {
+  return t_log2 >= 12 && n_buf <= 2 ? 32u : 1u;
+}
 
 // Shared-memory bytes of the fused kernel for a plan shape.
 size_t fused_smem_bytes(const DevPlan& P, uint32_t t_log2, bool staged, bool row_staged,
