@@ -51,6 +51,14 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
   p += align16(4ull * P.n_meas * cnt_lanes);
   uint32_t* segctr = reinterpret_cast<uint32_t*>(p);  // per-buffer segment dispensers
   p += 16;
+  // Tile hand-off: full[b] completes when every generator thread finished
+  // its work on the tile in buffer b, empty[b] when every drain thread has
+  // emptied it. Each side waits on the other's phase without arriving, so a
+  // generator warp that runs out of slices moves on to the next tile
+  // without waiting for the other generators.
+  uint64_t* mbar_full = reinterpret_cast<uint64_t*>(p);
+  uint64_t* mbar_empty = mbar_full + kMaxBuf;
+  p += 16 * kMaxBuf;
 
   const ClassInfo* CLS = P.cls;
   const uint4* DESC = P.desc;
@@ -102,7 +110,11 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
       t4[i] = make_uint4(0, 0, 0, 0);
     if (with_counts)
       for (uint32_t i = threadIdx.x; i < P.n_meas * cnt_lanes; i += blockDim.x) cnt[i] = 0;
-    if (threadIdx.x < kMaxBuf) segctr[threadIdx.x] = 0;
+    if (threadIdx.x < kMaxBuf) {
+      segctr[threadIdx.x] = 0;
+      mbar_init(mbar_full + threadIdx.x, P.gen_warps * 32);
+      mbar_init(mbar_empty + threadIdx.x, blockDim.x - P.gen_warps * 32);
+    }
   }
   __syncthreads();
 
@@ -117,7 +129,7 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
       const uint32_t b = i % n_buf;
       const uint64_t gtile = tile0 + blockIdx.x + static_cast<uint64_t>(i) * gridDim.x;
       long long tw0 = clock64();
-      if (i >= n_buf) named_sync(kBarEmpty0 + b, blockDim.x);
+      if (i >= n_buf) mbar_wait(mbar_empty + b, ((i / n_buf) - 1) & 1);
       long long tw1 = clock64();
       uint32_t* tile = tiles + b * tile_words;
       const uint32_t tile_s = static_cast<uint32_t>(__cvta_generic_to_shared(tile));
@@ -286,7 +298,7 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
         atomicAdd(reinterpret_cast<unsigned long long*>(P.timers) + 0, tw1 - tw0);
         atomicAdd(reinterpret_cast<unsigned long long*>(P.timers) + 1, clock64() - tw1);
       }
-      named_arrive(kBarFull0 + b, blockDim.x);
+      mbar_arrive(mbar_full + b);
     }
   } else {
     // ---------------- drain warps ----------------
@@ -298,7 +310,7 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
       const uint32_t b = i % n_buf;
       const uint64_t t_local = blockIdx.x + static_cast<uint64_t>(i) * gridDim.x;
       long long td0 = clock64();
-      named_sync(kBarFull0 + b, blockDim.x);
+      mbar_wait(mbar_full + b, (i / n_buf) & 1);
       long long td1 = clock64();
 
       uint4* t4 = reinterpret_cast<uint4*>(tiles + b * tile_words);
@@ -418,7 +430,7 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
         atomicAdd(reinterpret_cast<unsigned long long*>(P.timers) + 2, td1 - td0);
         atomicAdd(reinterpret_cast<unsigned long long*>(P.timers) + 3, clock64() - td1);
       }
-      if (i + n_buf < n_my) named_arrive(kBarEmpty0 + b, blockDim.x);
+      if (i + n_buf < n_my) mbar_arrive(mbar_empty + b);
     }
   }
   if (with_counts) {

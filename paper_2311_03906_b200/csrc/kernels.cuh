@@ -142,6 +142,8 @@ constexpr int kFusedThreads = 512;
 // offset n_meas*tw + r, r < 32, plus the firing's word < tw).
 __host__ __device__ constexpr uint32_t spare_words(uint32_t tw) { return ((tw + 32) + 3) & ~3u; }
 
+constexpr uint32_t kMaxBufHost = 4;  // tile buffers of the fused kernel (device: kMaxBuf)
+
 // Per-row flip-count slots of the fused kernel: 32 per-lane partials when a
 // warp walks one path per 4096-shot tile (no per-row reduction), unless
 // three or more tile buffers leave no room for them.
