@@ -285,9 +285,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n"
       "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
       "@!p bra WAIT_%=;\n\t}" ::"r"(a),
-      "r"(parity)
+      "r"(parity), "r"(1000000u)  // suspend up to 1 ms per try: woken on completion, no spinning
       : "memory");
 }
 
