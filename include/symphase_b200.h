@@ -116,6 +116,20 @@ int sp_load_msym_dense(sp_ctx* ctx, uint64_t n_meas, uint64_t n_sym, const uint6
 int sp_load_groups(sp_ctx* ctx, uint64_t n_groups, const sp_group* h_groups);
 int sp_load_model(sp_ctx* ctx, const sp_model* m); /* = csr + groups */
 
+/* Plan. The first call that needs the model builds the sampling plan on the
+ * host and uploads it: the chain transform M = L*D, per-(group, pattern) flip
+ * lists, the sampling slices, and the heavy-path drain order. The first plan
+ * for a model also measures the fused kernel's generator/drain warp split and
+ * padded-XOR mode with a few short launches, cached per model fingerprint.
+ * Re-loading a model with identical content keeps the plan and only
+ * re-uploads the raw arrays.
+ *
+ * Results never depend on that tuning. Random streams are keyed by
+ * (seed, sampling slice, global T-shot tile), and the slices and T depend
+ * only on the model and the device's shared memory. The SP_* environment
+ * switches in DESIGN.md change speed, not bits, except SP_TLOG2, SP_SEG_MIN,
+ * SP_SEG_EVENTS and SP_LIST_CLASSES, which redefine the slices. */
+
 /* Shot-tile size T of the fused sampler for the loaded model. Random streams
  * are keyed by (seed, global T-shot tile), so any split of a shot range into
  * calls whose shot_begin is a multiple of T — one GPU or many — yields the
