@@ -224,6 +224,13 @@ def run_ours(args):
     text = circuit_text(args.config)
     t0 = time.perf_counter()
     init = run_initialization(text)
+    if args.records == "detectors":  # detector layer: D_sym = A . M_sym
+        from paper_2311_03906_b200 import circuits as CI
+        dd = {"cfg2": (5, 5), "cfg3": (15, 15)}.get(args.config)
+        if dd is None:
+            raise SystemExit("--records detectors needs a surface-code workload (cfg2, cfg3)")
+        dets, obs = CI.surface_code_detectors(*dd)
+        init = init.detector_model(dets + obs)
     init_s = time.perf_counter() - t0
     smp = Sampler(init, device=local)
     T = smp.shot_tile
@@ -332,16 +339,19 @@ def run_ours(args):
             tr = json.loads(tp.read_text()).get(args.config)
             if tr and tr.get("shots") == shots:
                 traffic = tr.get("dram_bytes")
+        metric = METRIC if args.records == "measurements" else \
+            "sampled detector bits/sec (detectors + logical observable)"
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "metric": metric, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
             "data": "synthetic (seeded circuit generators, SURVEY Appendix A; seeds 1000+i)",
             "config": {
                 "workload": desc, "shots_per_gpu": shots, "n_meas": init.n_meas,
                 "n_sym": init.n_sym, "nnz": init.nnz, "shot_tile": T,
-                "parallelism": f"shot-range sharding x{world}" + (", NCCL all_reduce of "
-                               "per-measurement counts" if world > 1 else ""),
+                "parallelism": f"shot-range sharding x{world}" + (
+                    f", NCCL all_reduce of per-{args.records[:-1]} counts" if world > 1 else ""),
+                "records": args.records,
                 "output": ("tiled [tile][row][T/64]" if tiled else "measurement-major") +
                           " u64 bit-sliced records in HBM + per-row counts",
                 "l2": "flushed between timed steps (256 MiB memset outside the events); "
@@ -367,7 +377,7 @@ def run_ours(args):
             "gpu_launches": launches,
             "wall_s_timed": wall,
         }
-        if world == 1 and not args.no_cpu_baseline:
+        if world == 1 and not args.no_cpu_baseline and args.records == "measurements":
             r, cores, kind, sample, t = cpu_reference_rate(text, init.n_meas, 10.0)
             line["cpu_baseline"] = {"value": r, "unit": UNIT, "cores": cores, "kind": kind,
                                     "sample": sample, "seconds": round(t, 3)}
@@ -385,6 +395,9 @@ def main():
     ap.add_argument("--shots", type=int, default=0, help="override shots per GPU")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--records", default="measurements", choices=["measurements", "detectors"],
+                    help="sample measurement records (the metric) or, for the surface-code "
+                         "workloads, detector + observable records (D_sym = A . M_sym)")
     ap.add_argument("--layout", default="mm", choices=["mm", "tiled"],
                     help="record layout in HBM: measurement-major (the reference's SampleMatrix "
                          "orientation) or tiled (sp_sample_tiled)")

@@ -94,6 +94,21 @@ int sp_model_dims(const sp_model* m, uint64_t* n_qubits, uint64_t* n_meas, uint6
 /* row_ptr[n_meas+1], sym_idx[nnz], groups[n_groups]; any may be NULL. */
 int sp_model_export(const sp_model* m, uint64_t* row_ptr, uint32_t* sym_idx, sp_group* groups);
 
+/* Detector layer (not in the reference: its parser has no DETECTOR,
+ * circuit.cpp:117-121). A detector is the XOR of a set of measurements;
+ * detector k = measurements det_meas[det_ptr[k] .. det_ptr[k+1]). Its symbolic
+ * row is the GF(2) sum of those M_sym rows (sorted symmetric difference), so
+ * D_sym = A * M_sym. Loading D_sym rows (with the same group table) into a
+ * context samples detector records and per-detector counts with the same
+ * kernels; for a supplied S, D_sym * S == A * (M_sym * S) bit for bit.
+ * Two-pass: call with out_sym_idx == NULL to get *nnz_out, then again with a
+ * buffer of that many entries. Measurement ids must be < n_meas
+ * (SP_ERR_OUT_OF_RANGE otherwise). */
+int sp_detector_rows(uint64_t n_meas, const uint64_t* row_ptr, const uint32_t* sym_idx,
+                     uint64_t n_det, const uint64_t* det_ptr, const uint32_t* det_meas,
+                     uint64_t* out_row_ptr, uint32_t* out_sym_idx, uint64_t cap,
+                     uint64_t* nnz_out);
+
 /* ---- device context ---------------------------------------------------- */
 int sp_ctx_create(int device, sp_ctx** out);
 void sp_ctx_destroy(sp_ctx* ctx);

@@ -45,6 +45,7 @@ SIGNATURES = [
     ("sp_model_destroy", None, [_p]),
     ("sp_model_dims", _i, [_p, _pu64, _pu64, _pu64, _pu64, _pu64]),
     ("sp_model_export", _i, [_p, _p, _p, _p]),
+    ("sp_detector_rows", _i, [_u64, _p, _p, _u64, _p, _p, _p, _p, _u64, _pu64]),
     ("sp_ctx_create", _i, [_i, C.POINTER(_p)]),
     ("sp_ctx_destroy", None, [_p]),
     ("sp_set_stream", _i, [_p, _p]),

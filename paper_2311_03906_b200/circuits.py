@@ -156,6 +156,38 @@ def surface_code(d: int = 5, rounds: int | None = None, p: float = 1e-3) -> str:
     return "\n".join(out) + "\n"
 
 
+def surface_code_detectors(d: int = 5, rounds: int | None = None):
+    """Detectors and the logical observable of `surface_code(d, rounds)`
+    (memory-Z), as lists of measurement indices (the
+    reference has no DETECTOR instruction, so these are builder-defined).
+
+    Record order per round is X ancillas then Z ancillas (`M anc`), then the
+    final data measurements. Z stabilizers: round 0 alone (deterministic),
+    then round r xor r-1, then the last round xor the data on the support.
+    X stabilizers: round r xor r-1 for r >= 1 (round 0 is random). The
+    observable is the data row y = 1 (a logical Z: it commutes with every X
+    stabilizer, so it is deterministic without noise)."""
+    rounds = d if rounds is None else rounds
+    L = surface_layout(d)
+    dset = set(L.data)
+    nx, nz = len(L.xanc), len(L.zanc)
+    na = nx + nz
+    data_pos = {c: k for k, c in enumerate(L.data)}
+    dets = []
+    for r in range(rounds):
+        for j in range(nx):
+            if r >= 1:
+                dets.append([r * na + j, (r - 1) * na + j])
+        for j in range(nz):
+            i = nx + j
+            dets.append([i] if r == 0 else [r * na + i, (r - 1) * na + i])
+    for j, (x, y) in enumerate(L.zanc):
+        sup = [(x + dx, y + dy) for dx in (-1, 1) for dy in (-1, 1) if (x + dx, y + dy) in dset]
+        dets.append([(rounds - 1) * na + nx + j] + [rounds * na + data_pos[c] for c in sup])
+    obs = [[rounds * na + data_pos[c] for c in L.data if c[1] == 1]]
+    return dets, obs
+
+
 def random_clifford(n: int = 1000, layers: int = 100, p: float = 1e-3, seed: int = 1,
                     measure_every: int = 10, measure_frac: float = 0.1) -> str:
     """BASELINE config 4: layered random Clifford circuit."""

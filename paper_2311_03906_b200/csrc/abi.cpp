@@ -289,8 +289,12 @@ void build_plan(sp_ctx* c) {
   // parent search (sum of squared column lengths) would be expensive.
   double sq = 0;
   for (uint64_t sidx = 0; sidx < n_sym; ++sidx) sq += static_cast<double>(col_len(sidx)) * col_len(sidx);
-  const ChainXf X = chain_transform(n_meas, h.row_ptr, h.sym_idx, col_ptr, col_rows,
-                                    sq < 2e9 && env_long("SP_NO_CHAIN", 0) == 0);
+  ChainXf X = chain_transform(n_meas, h.row_ptr, h.sym_idx, col_ptr, col_rows,
+                              sq < 2e9 && env_long("SP_NO_CHAIN", 0) == 0);
+  // A transform that saves < 5 % of the nonzeros is not worth the drain's
+  // parent walks: without any parent the drain is a flat pass.
+  if (static_cast<double>(X.si.size()) > 0.95 * static_cast<double>(h.nnz))
+    X = chain_transform(n_meas, h.row_ptr, h.sym_idx, col_ptr, col_rows, false);
   c->dnnz = X.si.size();
   ptm.mark("chain transform");
   std::vector<uint64_t> dcol_ptr(n_sym + 1, 0);
@@ -869,6 +873,7 @@ void build_plan(sp_ctx* c) {
     d.n_paths = static_cast<uint32_t>(paths.size());
     d.n_rounds = n_rounds;
     d.n_keep = static_cast<uint32_t>(keep_rows.size());
+    d.flat_rows = paths.size() == n_meas && keep_rows.empty();
     d.path_rows = c->b_path_rows.upload(path_rows, s);
     d.path_ptr = c->b_path_ptr.upload(path_ptr, s);
     d.path_par = c->b_path_par.upload(path_par, s);
@@ -1100,6 +1105,40 @@ int sp_model_export(const sp_model* m, uint64_t* row_ptr, uint32_t* sym_idx, sp_
       o.arity = m->m.groups[g].arity;
       groups[g] = o;
     }
+  }
+  return SP_OK;
+}
+
+int sp_detector_rows(uint64_t n_meas, const uint64_t* row_ptr, const uint32_t* sym_idx,
+                     uint64_t n_det, const uint64_t* det_ptr, const uint32_t* det_meas,
+                     uint64_t* out_row_ptr, uint32_t* out_sym_idx, uint64_t cap,
+                     uint64_t* nnz_out) {
+  if (!row_ptr || (n_det && (!det_ptr || (det_ptr[n_det] && !det_meas))) || !out_row_ptr || !nnz_out)
+    return fail(SP_ERR_INVALID_ARGUMENT, "null argument");
+  try {
+    std::vector<uint32_t> acc, tmp;
+    uint64_t nnz = 0;
+    out_row_ptr[0] = 0;
+    for (uint64_t k = 0; k < n_det; ++k) {
+      acc.clear();
+      for (uint64_t i = det_ptr[k]; i < det_ptr[k + 1]; ++i) {
+        const uint64_t m = det_meas[i];
+        if (m >= n_meas) return fail(SP_ERR_OUT_OF_RANGE, "detector measurement id out of range");
+        tmp.clear();
+        std::set_symmetric_difference(acc.begin(), acc.end(), sym_idx + row_ptr[m],
+                                      sym_idx + row_ptr[m + 1], std::back_inserter(tmp));
+        acc.swap(tmp);
+      }
+      if (out_sym_idx) {
+        if (nnz + acc.size() > cap) return fail(SP_ERR_INVALID_ARGUMENT, "out_sym_idx too small");
+        std::copy(acc.begin(), acc.end(), out_sym_idx + nnz);
+      }
+      nnz += acc.size();
+      out_row_ptr[k + 1] = nnz;
+    }
+    *nnz_out = nnz;
+  } catch (const std::bad_alloc&) {
+    return fail(SP_ERR_INVALID_ARGUMENT, "host allocation failed");
   }
   return SP_OK;
 }

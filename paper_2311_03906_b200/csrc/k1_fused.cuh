@@ -321,11 +321,77 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
       const uint32_t rem = static_cast<uint32_t>(valid & 127);
       const bool fast = vec && ldb != 0 && (valid == (static_cast<uint64_t>(1) << P.t_log2));
       uint64_t* const tbase = out + t_local * tile_stride;  // this tile's records
+      // Row k's 128-shot column q is final: store 16 bytes to HBM (masked in a
+      // partial tile), optionally count its ones.
+      auto store_row = [&](auto fast_tag, auto wp_tag, uint32_t k, uint32_t q, uint4 v) {
+        constexpr bool kFast = decltype(fast_tag)::value;  // full tile, aligned, ldb < 2^32
+        constexpr bool kWarpPath = decltype(wp_tag)::value;  // a warp per row (T = 4096)
+        uint64_t* obase = tbase + 2 * q;
+        uint32_t pc = 0;
+        if constexpr (kFast) {
+          *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(obase) +
+                                    static_cast<uint64_t>(k) * ldb) = v;
+          if (with_counts) pc = __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
+        } else if (q < vq) {
+          uint64_t* o = obase + static_cast<uint64_t>(k) * ld;
+          bool two = true;  // whether the item's second u64 word is inside the tile
+          if (q == vq - 1 && rem) {
+            const uint32_t m[4] = {
+                rem >= 32 ? kFull : (1u << rem) - 1,
+                rem >= 64 ? kFull : rem > 32 ? (1u << (rem - 32)) - 1 : 0u,
+                rem >= 96 ? kFull : rem > 64 ? (1u << (rem - 64)) - 1 : 0u,
+                rem > 96 ? (1u << (rem - 96)) - 1 : 0u};
+            v.x &= m[0]; v.y &= m[1]; v.z &= m[2]; v.w &= m[3];
+            two = rem > 64;
+          }
+          const uint64_t w0 = (static_cast<uint64_t>(v.y) << 32) | v.x;
+          const uint64_t w1 = (static_cast<uint64_t>(v.w) << 32) | v.z;
+          if (vec && two) {
+            *reinterpret_cast<ulonglong2*>(o) = make_ulonglong2(w0, w1);
+          } else {
+            o[0] = w0;
+            if (two) o[1] = w1;
+          }
+          if (with_counts) pc = __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
+        }
+        if (with_counts) {
+          if constexpr (kWarpPath) {
+            if (cnt_lanes == 32) {  // per-lane partials, no reduction here
+              asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(cnt_s + ((k * 32 + lane) << 2)),
+                           "r"(pc)
+                           : "memory");
+            } else {  // the warp holds this row: one add per row
+              pc = __reduce_add_sync(kFull, pc);
+              if (lane == 0) atomicAdd(&cnt[k], pc);
+            }
+          } else {
+            if (pc) atomicAdd(&cnt[k], pc);
+          }
+        }
+      };
+      if (P.flat_rows && !(P.debug_mode & 8u)) {
+        // No parents (every row its own path, nothing kept): one pass over
+        // the tile in row order, clearing as it goes.
+        auto flat = [&](auto fast_tag, auto wp_tag) {
+          for (uint32_t j = ct; j < (P.n_meas << tw4_log2); j += nct) {
+            const uint4 v = t4[j];
+            t4[j] = make_uint4(0, 0, 0, 0);
+            store_row(fast_tag, wp_tag, j >> tw4_log2, j & (tw4 - 1), v);
+          }
+        };
+        if (tw4 >= 32) {
+          if (fast) flat(std::true_type{}, std::true_type{});
+          else flat(std::false_type{}, std::true_type{});
+        } else {
+          if (fast) flat(std::true_type{}, std::false_type{});
+          else flat(std::false_type{}, std::false_type{});
+        }
+      }
       // Rows along parent paths (heavy-path decomposition of the L forest):
       // one thread walks a path top-down for one 128-shot column, carrying
       // the running row value; a path's head waits only for its parent's
       // path, which ran in an earlier round.
-      for (uint32_t rd = 0; rd < ((P.debug_mode & 8u) ? 0u : P.n_rounds); ++rd) {
+      for (uint32_t rd = 0; rd < ((P.debug_mode & 8u) || P.flat_rows ? 0u : P.n_rounds); ++rd) {
         const uint32_t p0 = P.round_ptr[rd], p1 = P.round_ptr[rd + 1];
         const uint32_t tasks = (p1 - p0) << tw4_log2;
         const uint32_t tasks_rounded = (tasks + 31) & ~31u;
@@ -338,59 +404,16 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
                                 : make_uint4(0, 0, 0, 0);
           const uint32_t xe = act ? PPTR[pth + 1] : 0;
           uint32_t x = act ? PPTR[pth] : 0;
-          uint64_t* obase = tbase + 2 * q;
-          uint8_t* obase_b = reinterpret_cast<uint8_t*>(obase);
           // One row of the path: row = tile word ^ parent row; keep or clear
-          // the tile word, store 16 bytes to HBM, optionally count.
+          // the tile word, then store it (and count it).
           auto row_step = [&](auto fast_tag, auto wp_tag, uint32_t e, uint4 c) {
-            constexpr bool kFast = decltype(fast_tag)::value;  // full tile, aligned, ldb < 2^32
-            constexpr bool kWarpPath = decltype(wp_tag)::value;  // a warp per path (T = 4096)
             const uint32_t k = e & 0xFFFFu;
-            uint4 v = xor4(c, prev);
+            const uint4 v = xor4(c, prev);
             // Rows with light children keep their final value for a later
             // round; all others are cleared for tile i+2 right away.
             sts_or_zero(t4_s + (((k << tw4_log2) + q) << 4), v, e >> 31);
             prev = v;
-            uint32_t pc = 0;
-            if constexpr (kFast) {
-              *reinterpret_cast<uint4*>(obase_b + static_cast<uint64_t>(k) * ldb) = v;
-              if (with_counts) pc = __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
-            } else if (q < vq) {
-              uint64_t* o = obase + static_cast<uint64_t>(k) * ld;
-              bool two = true;  // whether the item's second u64 word is inside the tile
-              if (q == vq - 1 && rem) {
-                const uint32_t m[4] = {
-                    rem >= 32 ? kFull : (1u << rem) - 1,
-                    rem >= 64 ? kFull : rem > 32 ? (1u << (rem - 32)) - 1 : 0u,
-                    rem >= 96 ? kFull : rem > 64 ? (1u << (rem - 64)) - 1 : 0u,
-                    rem > 96 ? (1u << (rem - 96)) - 1 : 0u};
-                v.x &= m[0]; v.y &= m[1]; v.z &= m[2]; v.w &= m[3];
-                two = rem > 64;
-              }
-              const uint64_t w0 = (static_cast<uint64_t>(v.y) << 32) | v.x;
-              const uint64_t w1 = (static_cast<uint64_t>(v.w) << 32) | v.z;
-              if (vec && two) {
-                *reinterpret_cast<ulonglong2*>(o) = make_ulonglong2(w0, w1);
-              } else {
-                o[0] = w0;
-                if (two) o[1] = w1;
-              }
-              if (with_counts) pc = __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
-            }
-            if (with_counts) {
-              if constexpr (kWarpPath) {
-                if (cnt_lanes == 32) {  // per-lane partials, no reduction here
-                  asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(cnt_s + ((k * 32 + lane) << 2)),
-                               "r"(pc)
-                               : "memory");
-                } else {  // the warp walks this path: one add per row
-                  pc = __reduce_add_sync(kFull, pc);
-                  if (lane == 0) atomicAdd(&cnt[k], pc);
-                }
-              } else {
-                if (pc) atomicAdd(&cnt[k], pc);
-              }
-            }
+            store_row(fast_tag, wp_tag, k, q, v);
           };
           // Two rows per iteration with the next row's entry and tile word
           // prefetched (path_rows is padded, so x + 2 <= n_meas is readable).

@@ -99,6 +99,7 @@ struct DevPlan {
   const uint16_t* keep_rows = nullptr;
   const uint32_t* round_ptr = nullptr;  // [n_rounds + 1] over paths
   uint32_t n_paths = 0, n_rounds = 1, n_keep = 0;
+  uint32_t flat_rows = 0;  // no parents at all: the drain is one pass in row order
 
   // Fused-kernel launch shape (chosen by the planner).
   uint32_t staged = 0;       // event tables copied into shared memory

@@ -81,6 +81,29 @@ class InitResult:
         return cls(int(z["n_qubits"][0]), int(z["n_sym"][0]), z["row_ptr"].astype(np.uint64),
                    z["sym_idx"].astype(np.uint32), groups)
 
+    def detector_model(self, detectors) -> "InitResult":
+        """Detector layer: rows = GF(2) sums of the listed measurements' rows
+        (D_sym = A . M_sym, sp_detector_rows), same symbols and groups. The
+        result samples like any model: detector records and counts."""
+        L = N.lib()
+        det_ptr = np.zeros(len(detectors) + 1, dtype=np.uint64)
+        det_ptr[1:] = np.cumsum([len(d) for d in detectors])
+        det_meas = np.ascontiguousarray(np.concatenate(
+            [np.asarray(d, dtype=np.uint32) for d in detectors]) if len(detectors) else
+            np.zeros(1, np.uint32), dtype=np.uint32)
+        if det_meas.size == 0:
+            det_meas = np.zeros(1, np.uint32)
+        rp = np.zeros(len(detectors) + 1, dtype=np.uint64)
+        nnz = C.c_uint64()
+        si = np.ascontiguousarray(self.sym_idx if self.sym_idx.size else np.zeros(1, np.uint32),
+                                  dtype=np.uint32)
+        args = (self.n_meas, self.row_ptr.ctypes.data, si.ctypes.data, len(detectors),
+                det_ptr.ctypes.data, det_meas.ctypes.data, rp.ctypes.data)
+        N.check(L.sp_detector_rows(*args, None, 0, C.byref(nnz)))
+        out = np.zeros(max(nnz.value, 1), dtype=np.uint32)
+        N.check(L.sp_detector_rows(*args, out.ctypes.data, out.size, C.byref(nnz)))
+        return InitResult(self.n_qubits, self.n_sym, rp, out[:nnz.value], self.groups)
+
     def dense_words(self) -> np.ndarray:
         """M_sym as dense row-major u64 words [n_meas][ceil(n_sym/64)]."""
         ldm = max((self.n_sym + 63) // 64, 1)
