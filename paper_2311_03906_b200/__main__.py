@@ -3,6 +3,7 @@
 
     python -m paper_2311_03906_b200 sample --in c.stim --shots N --seed S \
         [--format 01|b8] [--out FILE] [--rng philox|compat] [--dump-assignments FILE]
+        [--detectors FILE]
     python -m paper_2311_03906_b200 analyze --in c.stim [--out FILE]
 
 `sample` writes the records exactly as the reference encodes them
@@ -47,6 +48,10 @@ def cmd_sample(a) -> int:
     text = _read(a.input)
     t0 = time.perf_counter()
     init = run_initialization(text)
+    if a.detectors:  # detector layer: one detector per line, measurement ids
+        with open(a.detectors) as f:
+            dets = [[int(t) for t in line.split()] for line in f if line.strip()]
+        init = init.detector_model(dets)
     init_s = time.perf_counter() - t0
     t1 = time.perf_counter()
     smp = Sampler(init, device=a.device, rng=a.rng)
@@ -95,6 +100,8 @@ def main(argv=None) -> int:
     s.add_argument("--rng", choices=["philox", "compat"], default="philox")
     s.add_argument("--device", type=int, default=0)
     s.add_argument("--dump-assignments")
+    s.add_argument("--detectors", help="file with one detector per line (measurement ids, "
+                                       "0-based); records are detector outcomes instead")
     s.add_argument("--threads", type=int, default=1, help="accepted for compatibility; unused")
     an = sub.add_parser("analyze", help="print measurement outcomes as symbol expressions")
     an.add_argument("--in", dest="input")

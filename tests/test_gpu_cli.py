@@ -66,3 +66,24 @@ def test_analyze_on_dumped_assignments_matches_sample(tmp_path):
             for k, e in enumerate(exprs):
                 v = sum(rows[s][j] == "1" for s in e) % 2
                 assert str(v) == shot_line[k], (rng, j, k)
+
+
+def test_sample_detectors_file(tmp_path):
+    """--detectors: records are detector outcomes (XOR of the listed
+    measurements), here checked against the measurement records of the same
+    compat-RNG run."""
+    circ = "X_ERROR(0.3) 0 1 2\nM 0 1 2\n"
+    inp = tmp_path / "c.stim"
+    inp.write_text(circ)
+    det = tmp_path / "d.txt"
+    det.write_text("0 1\n1 2\n0 1 2\n\n2\n")
+    common = ["sample", "--in", str(inp), "--shots", "300", "--seed", "5", "--rng", "compat"]
+    m = run_cli(common)
+    d = run_cli(common + ["--detectors", str(det)])
+    assert m.returncode == 0 and d.returncode == 0, d.stderr
+    ml = m.stdout.decode().split()
+    dl = d.stdout.decode().split()
+    assert len(ml) == len(dl) == 300
+    for a, b in zip(ml, dl):
+        x = [int(c) for c in a]
+        assert b == f"{x[0] ^ x[1]}{x[1] ^ x[2]}{x[0] ^ x[1] ^ x[2]}{x[2]}"
