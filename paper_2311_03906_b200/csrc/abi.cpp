@@ -120,6 +120,7 @@ struct sp_ctx {
   // sp_sample_to_host: double-buffered records/bytes, a copy stream and the
   // events that hand each buffer between the compute and copy streams
   DBuf s_out[2], s_bytes[2];
+  DBuf s_S;  // sp_sample without an on-chip tile: the drawn assignments of one chunk
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t ev_ready[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
   uint64_t launches = 0;
@@ -1310,11 +1311,35 @@ int sp_sample(sp_ctx* ctx, uint64_t seed, uint64_t shot_begin, uint64_t n_shots,
   if (n_shots == 0) return fail(SP_ERR_INVALID_ARGUMENT, "need at least one shot");  // sampler.cpp:50
   if (int r = set_device(ctx)) return r;
   if (int r = ensure_plan(ctx)) return r;
-  if (!ctx->fused_ok) return fail(SP_ERR_UNSUPPORTED, ctx->fused_why);
   const uint64_t T = 1ull << ctx->dp.t_log2;
   if (shot_begin % T) return fail(SP_ERR_INVALID_ARGUMENT, "shot_begin must be a multiple of the shot tile");
   if (ctx->hp.n_meas == 0) return SP_OK;
   if (!d_out || ld < (n_shots + 63) / 64) return fail(SP_ERR_INVALID_ARGUMENT, "output too small");
+  if (!ctx->fused_ok) {
+    // Too many rows for an on-chip shot tile: the same streams through the
+    // unfused path, draw S (device) then the explicit-S product, in shot
+    // chunks that keep S under ~2 GB. Same records as the fused kernel.
+    const uint64_t per_shot = std::max<uint64_t>(ctx->hp.n_sym, 1) / 8 + 1;
+    uint64_t chunk = std::max<uint64_t>((2ull << 30) / per_shot / T, 1) * T;
+    chunk = std::min(chunk, (n_shots + T - 1) / T * T);
+    const uint64_t ldS = chunk / 64;
+    try {
+      uint64_t* d_S = static_cast<uint64_t*>(ctx->s_S.ensure(ctx->hp.n_sym * ldS * 8));
+      for (uint64_t done = 0; done < n_shots; done += chunk) {
+        const uint64_t n = std::min(chunk, n_shots - done);
+        if (int r = sp_draw_assignments(ctx, seed, shot_begin + done, n, d_S, ldS)) return r;
+        if (int r = sp_sample_given_S(ctx, d_S, ctx->hp.n_sym, ldS, n, d_out + done / 64, ld))
+          return r;
+        if (d_counts) {
+          const int r = launch_row_counts(ctx->L, d_out + done / 64, ld, ctx->hp.n_meas, n, d_counts);
+          if (int e = launched(ctx, r, "row counts launch")) return e;
+        }
+      }
+    } catch (const CudaError& e) {
+      return fail(SP_ERR_CUDA, e.what());
+    }
+    return SP_OK;
+  }
   const uint64_t tile0 = shot_begin / T;
   int r = ctx->rng == SP_RNG_PHILOX
               ? launch_fused_sample(ctx->dp, ctx->L, seed, tile0, n_shots, d_out, ld, d_counts)
@@ -1468,7 +1493,7 @@ int sp_sample_to_host(sp_ctx* ctx, uint64_t seed, uint64_t shot_begin, uint64_t 
       const uint64_t n = std::min(chunk, n_shots - done);
       if (i >= 2) ck(cudaStreamWaitEvent(ctx->stream, ctx->ev_free[b], 0), "cudaStreamWaitEvent");
       int r = SP_OK;
-      if (ctx->rng == SP_RNG_PHILOX && n_meas) {
+      if (ctx->rng == SP_RNG_PHILOX && n_meas && ctx->fused_ok) {
         // tiled records: coalesced stores for any row count
         if ((r = sp_sample_tiled(ctx, seed, shot_begin + done, n, d_m[b], nullptr))) return r;
         if ((r = sp_encode_tiled(ctx, d_m[b], n, fmt, d_b[b]))) return r;

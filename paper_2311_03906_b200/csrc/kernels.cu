@@ -315,6 +315,20 @@ __global__ void k3_01(const uint32_t* __restrict__ m32, uint64_t ld32, uint32_t 
   if (shot < n_shots) out[shot * line + n_meas] = '\n';
 }
 
+// counts[k] += popcount of row k's first n_shots bits (one warp per row).
+__global__ void k_row_counts(const uint64_t* __restrict__ m, uint64_t ld, uint32_t n_meas,
+                             uint64_t n_words, uint64_t tail, unsigned long long* counts) {
+  const uint32_t lane = threadIdx.x & 31;
+  for (uint64_t k = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5; k < n_meas;
+       k += (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5) {
+    unsigned long long c = 0;
+    for (uint64_t w = lane; w < n_words; w += 32)
+      c += __popcll(w == n_words - 1 ? (m[k * ld + w] & tail) : m[k * ld + w]);
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(kFull, c, o);
+    if (lane == 0 && c) atomicAdd(&counts[k], c);
+  }
+}
+
 // Tiled [tile][row][T/64] -> measurement-major [row][ld]; one thread per u64.
 __global__ void k_untile(const uint64_t* __restrict__ in, uint32_t n_meas, uint32_t tw2,
                          uint64_t n_words, uint64_t total, uint64_t* __restrict__ out,
@@ -525,6 +539,17 @@ int launch_untile(const LaunchCfg& L, const uint64_t* in, uint64_t n_meas, uint3
   const unsigned blocks = static_cast<unsigned>(std::min<uint64_t>((total + 255) / 256, 1u << 20));
   k_untile<<<blocks, 256, 0, L.stream>>>(in, static_cast<uint32_t>(n_meas), tile_shots / 64,
                                         n_words, total, out, ld);
+  return check_launch() ? -1 : 1;
+}
+
+int launch_row_counts(const LaunchCfg& L, const uint64_t* m, uint64_t ld, uint64_t n_meas,
+                      uint64_t n_shots, uint64_t* counts) {
+  const uint64_t n_words = (n_shots + 63) / 64;
+  if (!n_meas || !n_words) return 0;
+  const uint64_t tail = (n_shots & 63) ? ((1ull << (n_shots & 63)) - 1) : ~0ull;
+  const unsigned blocks = static_cast<unsigned>(std::min<uint64_t>((n_meas + 7) / 8, 65535));
+  k_row_counts<<<blocks, 256, 0, L.stream>>>(m, ld, static_cast<uint32_t>(n_meas), n_words, tail,
+                                            reinterpret_cast<unsigned long long*>(counts));
   return check_launch() ? -1 : 1;
 }
 

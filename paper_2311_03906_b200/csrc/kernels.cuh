@@ -177,6 +177,9 @@ int launch_encode(const LaunchCfg& L, const uint64_t* m, uint64_t ld, uint64_t n
 // Tiled records -> measurement-major.
 int launch_untile(const LaunchCfg& L, const uint64_t* in, uint64_t n_meas, uint32_t tile_shots,
                   uint64_t n_shots, uint64_t* out, uint64_t ld);
+// counts[k] += popcount of row k of measurement-major records (n_shots bits).
+int launch_row_counts(const LaunchCfg& L, const uint64_t* m, uint64_t ld, uint64_t n_meas,
+                      uint64_t n_shots, uint64_t* counts);
 // Known-answer hook for the Philox4x32-10 implementation.
 int launch_debug_philox(const LaunchCfg& L, const uint32_t* ctr_key_dev, uint32_t* out_dev);
 

@@ -74,3 +74,22 @@ def test_fused_many_rows_single_buffer(gpu_sampler_factory, port, dens):
     S = s.draw_assignments(n, 4)
     assert np.array_equal(host(s.sample(n, 4)),
                           port.sample(model.row_ptr, model.sym_idx, host(S), n))
+
+
+def test_sample_without_onchip_tile_uses_draw_and_product(gpu_sampler_factory, port):
+    """A model with too many rows for any on-chip tile still samples through
+    sp_sample (draw S + explicit product), with counts and host records."""
+    import torch
+    model = CI.random_msym_model(40000, 3000, 0.002, 0.01, seed=5)
+    s = gpu_sampler_factory(model)
+    assert not s.plan_info()["fused_ok"]
+    n = 3 * 4096 + 77
+    counts = torch.zeros(model.n_meas, dtype=torch.int64, device="cuda")
+    out = s.sample(n, 9, counts=counts)
+    S = s.draw_assignments(n, 9)
+    want = port.sample(model.row_ptr, model.sym_idx, host(S), n)
+    assert np.array_equal(host(out), want)
+    pc = np.unpackbits(want.view(np.uint8), axis=1).sum(axis=1)
+    assert np.array_equal(counts.cpu().numpy(), pc)
+    buf, w = s.sample_to_host(n, 9, "b8")
+    assert bytes(buf[:w]) == port.encode(want, model.n_meas, n, "b8")
