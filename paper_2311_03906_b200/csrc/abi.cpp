@@ -768,6 +768,12 @@ void build_plan(sp_ctx* c) {
       coin_rows[i] = static_cast<uint16_t>(coin_rows_k[i] * d.tw);
     d.coin_ptr = c->b_coin_ptr.upload(coin_ptr, s);
     d.coin_rows = c->b_coin_rows.upload(coin_rows, s);
+    d.n_coin_rows = static_cast<uint32_t>(coin_rows_k.size());
+    if (c->fused_ok && env_long("SP_COINS_SMEM", 1) != 0) {
+      DevPlan t = d;
+      t.coins_staged = 1;
+      if (fused_smem_bytes(t, t.t_log2, t.staged, t.row_staged, t.n_buf) <= optin) d.coins_staged = 1;
+    }
   }
   d.n_cls_all = static_cast<uint32_t>(cls_info.size());
   apply_segments(live_nseg);

@@ -68,6 +68,9 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
   const uint32_t* PPTR = P.path_ptr;
   const int32_t* PPAR = P.path_par;
   const uint16_t* KEEP = P.keep_rows;
+  const uint32_t* CPTR = P.coin_ptr;
+  const uint16_t* CROWS = P.coin_rows;
+  const uint32_t* CSYM = P.dense_sym;
   if (kRowStaged) {
     uint32_t* s_prows = reinterpret_cast<uint32_t*>(p);
     p += align16(4ull * (P.n_meas + 1));
@@ -104,6 +107,20 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
     DESC = s_desc;
     COLROW = s_col;
   }
+  if (P.coins_staged) {  // coin columns and symbols: small, read every tile
+    uint32_t* s_cptr = reinterpret_cast<uint32_t*>(p);
+    p += align16(4ull * (P.n_dense_live + 2));
+    uint32_t* s_csym = reinterpret_cast<uint32_t*>(p);
+    p += align16(4ull * P.n_dense_live);
+    uint16_t* s_crows = reinterpret_cast<uint16_t*>(p);
+    p += align16(2ull * P.n_coin_rows);
+    for (uint32_t i = threadIdx.x; i < P.n_dense_live + 2; i += blockDim.x) s_cptr[i] = P.coin_ptr[i];
+    for (uint32_t i = threadIdx.x; i < P.n_dense_live; i += blockDim.x) s_csym[i] = P.dense_sym[i];
+    for (uint32_t i = threadIdx.x; i < P.n_coin_rows; i += blockDim.x) s_crows[i] = P.coin_rows[i];
+    CPTR = s_cptr;
+    CSYM = s_csym;
+    CROWS = s_crows;
+  }
   {
     uint4* t4 = reinterpret_cast<uint4*>(tiles);
     for (uint32_t i = threadIdx.x; i < (n_buf * tile_words) / 4; i += blockDim.x)
@@ -135,30 +152,40 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
       const uint32_t tile_s = static_cast<uint32_t>(__cvta_generic_to_shared(tile));
       // Fair-coin words of this tile (dense symbols), keyed by (symbol,
       // 128-shot quad), XORed word-wise into the D rows of the symbol's
-      // column; the last slot is the constant term (all ones).
-      for (uint32_t j = threadIdx.x; j < ((P.n_dense_live + 1) << tw4_log2); j += n_gen * 32) {
-        const uint32_t slot = j >> tw4_log2, q = j & (tw4 - 1);
-        uint32_t e = __ldg(P.coin_ptr + slot);
-        const uint32_t e1 = __ldg(P.coin_ptr + slot + 1);
-        if (e == e1) continue;
-        uint4 c = make_uint4(kFull, kFull, kFull, kFull);
-        if (slot < P.n_dense_live) {
+      // column; the last slot is the constant term (all ones). Two tasks per
+      // iteration, so two Philox chains interleave.
+      {
+        const uint32_t n_tasks = (P.n_dense_live + 1) << tw4_log2;
+        auto coin_word = [&](uint32_t slot, uint32_t q) {
+          if (slot >= P.n_dense_live) return make_uint4(kFull, kFull, kFull, kFull);
           const uint64_t gq = (gtile << tw4_log2) + q;
-          c = philox10(make_uint4(P.dense_sym[slot], static_cast<uint32_t>(gq),
-                                  (static_cast<uint32_t>(gq >> 32) & 0xFFFFFFu) | (kDomCoin << 24),
-                                  0u),
-                       K);
+          return philox10(make_uint4(CSYM[slot], static_cast<uint32_t>(gq),
+                                     (static_cast<uint32_t>(gq >> 32) & 0xFFFFFFu) | (kDomCoin << 24),
+                                     0u),
+                          K);
+        };
+        auto coin_xor = [&](uint32_t slot, uint32_t q, uint4 c) {
+          for (uint32_t e = CPTR[slot]; e < CPTR[slot + 1]; ++e) {
+            const uint32_t a = tile_s + ((static_cast<uint32_t>(CROWS[e]) + 4 * q) << 2);
+            asm volatile(
+                "red.shared.xor.b32 [%0], %1;\n\t"
+                "red.shared.xor.b32 [%0+4], %2;\n\t"
+                "red.shared.xor.b32 [%0+8], %3;\n\t"
+                "red.shared.xor.b32 [%0+12], %4;" ::"r"(a),
+                "r"(c.x), "r"(c.y), "r"(c.z), "r"(c.w)
+                : "memory");
+          }
+        };
+        const uint32_t stride = n_gen * 32;
+        uint32_t j = threadIdx.x;
+        for (; j + stride < n_tasks; j += 2 * stride) {
+          const uint32_t j2 = j + stride;
+          const uint4 c0 = coin_word(j >> tw4_log2, j & (tw4 - 1));
+          const uint4 c1 = coin_word(j2 >> tw4_log2, j2 & (tw4 - 1));
+          coin_xor(j >> tw4_log2, j & (tw4 - 1), c0);
+          coin_xor(j2 >> tw4_log2, j2 & (tw4 - 1), c1);
         }
-        for (; e < e1; ++e) {
-          const uint32_t a = tile_s + ((static_cast<uint32_t>(__ldg(P.coin_rows + e)) + 4 * q) << 2);
-          asm volatile(
-              "red.shared.xor.b32 [%0], %1;\n\t"
-              "red.shared.xor.b32 [%0+4], %2;\n\t"
-              "red.shared.xor.b32 [%0+8], %3;\n\t"
-              "red.shared.xor.b32 [%0+12], %4;" ::"r"(a),
-              "r"(c.x), "r"(c.y), "r"(c.z), "r"(c.w)
-              : "memory");
-        }
+        if (j < n_tasks) coin_xor(j >> tw4_log2, j & (tw4 - 1), coin_word(j >> tw4_log2, j & (tw4 - 1)));
       }
       const uint32_t spare = P.n_meas * tw;
       uint32_t seg = 0;

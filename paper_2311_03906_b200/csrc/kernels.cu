@@ -372,6 +372,9 @@ size_t fused_smem_bytes(const DevPlan& P, uint32_t t_log2, bool staged, bool row
   size_t b = n_buf * (static_cast<size_t>(P.n_meas) * tw + spare_words(tw)) * 4;  // tiles + spare
   b += align16(4ull * P.n_meas * count_lanes(t_log2, n_buf)) + 16;  // counts, dispensers
   b += 16 * kMaxBufHost;                                               // tile mbarriers
+  if (P.coins_staged)
+    b += align16(4ull * (P.n_dense_live + 2)) + align16(4ull * P.n_dense_live) +
+         align16(2ull * P.n_coin_rows);                                 // coin tables
   if (row_staged) {
     b += align16(4ull * (P.n_meas + 1));
     b += align16(4ull * (P.n_paths + 1));

@@ -62,6 +62,8 @@ struct DevPlan {
   const uint32_t* dense_sym = nullptr;  // slot -> symbol id
   const uint32_t* coin_ptr = nullptr;   // [n_dense_live + 2]
   const uint16_t* coin_rows = nullptr;
+  uint32_t n_coin_rows = 0;
+  uint32_t coins_staged = 0;  // coin tables copied into shared memory
 
   // Sparse channels (see ClassInfo). Live classes first.
   uint32_t n_cls_live = 0, n_cls_all = 0;
