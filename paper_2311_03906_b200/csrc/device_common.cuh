@@ -15,7 +15,7 @@ constexpr unsigned kFull = 0xFFFFFFFFu;
 
 // Named barriers of the fused kernel (0 is __syncthreads).
 constexpr uint32_t kMaxBuf = 4;  // shot-tile buffers of the fused kernel
-constexpr uint32_t kBarFull0 = 1, kBarEmpty0 = 1 + kMaxBuf, kBarDrain = 1 + 2 * kMaxBuf;
+constexpr uint32_t kBarDrain = 1;  // named barrier among the drain warps (0 is __syncthreads)
 
 __host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) & ~size_t{15}; }
 
@@ -291,9 +291,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
-__device__ __forceinline__ void named_arrive(uint32_t id, uint32_t n) {
-  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
 
 // 16-byte shared store of v (keep != 0) or of zeros, as two predicated
 // stores instead of four selects.

@@ -15,17 +15,20 @@ namespace {
 // at most one earlier parent row p(k) and D row k = row k XOR row p(k), which
 // for syndrome-extraction circuits is the detector-like difference of
 // consecutive rounds — far fewer symbols per column. The kernel samples in
-// D space and rebuilds M rows level by level (out[k] = d[k] ^ out[p(k)]).
+// D space and rebuilds M rows along parent paths (out[k] = d[k] ^ out[p(k)]).
 //
-// Per CTA: two shared-memory accumulation tiles [n_meas][T/32] u32 (double
-// buffer) and two coin buffers [n_dense+1][T/32]. Generator warps walk the
-// geometric-skip segments of tile i (warp-cooperative) and XOR each fired
-// symbol's D column into tile[i&1] with shared atomics; drain warps
-// meanwhile make tile i's fair-coin words, then — once the tile is complete
-// — add dense terms and parents level by level, stream the records to HBM
-// with 16-byte stores and zero the buffer for tile i+2. Named barriers
-// FULL[b] / EMPTY[b] hand the buffers back and forth. Event tables and row
-// tables are staged in shared memory when they fit.
+// Per CTA (one per SM, 16 warps): n_buf shared-memory accumulation tiles
+// [n_meas][T/32] u32 plus a spare region. Generator warps make each tile's
+// fair-coin words and XOR them into the coins' D columns, then walk the
+// tile's sampling slices (warp-cooperative geometric skips) and XOR each
+// firing's flip list into the tile with shared atomics. Drain warps, once a
+// tile is complete, rebuild rows along the heavy paths of the parent forest
+// (or in one flat pass when there are no parents), stream the records to
+// HBM with 16-byte stores, count, and clear the tile for reuse. mbarriers
+// full[b] / empty[b] hand the buffers back and forth; each side waits
+// without arriving, so generator warps never wait for one another. Row,
+// coin and (table-walk variant) event tables are staged in shared memory
+// when they fit.
 template <bool kStaged, bool kRowStaged, int kLp, bool kPadPred, int kEB>
 __global__ void __launch_bounds__(kFusedThreads, 1)
 k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, uint64_t n_shots,
@@ -33,7 +36,6 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
          unsigned long long* __restrict__ counts, bool vec) {
   extern __shared__ __align__(16) uint8_t smem[];
   const uint32_t tw = P.tw, tw4_log2 = P.t_log2 - 7, tw4 = 1u << tw4_log2;
-  // One spare row absorbs the XORs of padded flip-list entries (never read).
   // Tile rows, then a spare region (never read) that absorbs the XORs of
   // padded flip-list entries, spread over 32 banks.
   const uint32_t tile_words = P.n_meas * tw + spare_words(tw);
@@ -475,7 +477,7 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
           t4[(static_cast<uint32_t>(KEEP[j >> tw4_log2]) << tw4_log2) + (j & (tw4 - 1))] =
               make_uint4(0, 0, 0, 0);
       }
-      if (ct == 0) segctr[b] = 0;  // all generators are past tile i (FULL[b] completed)
+      if (ct == 0) segctr[b] = 0;  // all generators are past tile i (full[b] completed)
       if (P.timers && lane == 0) {  // drain: [2] waiting FULL, [3] working
         atomicAdd(reinterpret_cast<unsigned long long*>(P.timers) + 2, td1 - td0);
         atomicAdd(reinterpret_cast<unsigned long long*>(P.timers) + 3, clock64() - td1);
