@@ -352,17 +352,86 @@ void build_plan(sp_ctx* c) {
     }
     return mx <= 2 ? 2u : mx <= 4 ? 4u : mx <= 8 ? 8u : mx <= 16 ? 16u : 0u;
   };
+  // Channel merging (exact). A sparse group whose non-empty flip lists are
+  // all one list L acts as Bernoulli(p_eff) on L (p_eff = p * #patterns with
+  // list L / #patterns). Independent such groups on the same L merge into one
+  // Bernoulli with the piling-up rate q = (1 - prod(1 - 2 p_eff)) / 2 — the
+  // same distribution of records with far fewer firings when many channels
+  // hit the same rows (cfg4: 72,723 groups, 73 firings per shot, on one row).
+  // The merged variable is a pseudo symbol (id >= n_sym) with D column L; the
+  // merged-away groups are still drawn by sp_draw_assignments (as dead
+  // classes), so S stays complete, but K1 records of a merged model are not
+  // M_sym . S of that S. Buckets of >= SP_MERGE_MIN (64) groups are merged.
+  const long merge_min = env_long("SP_MERGE_MIN", 64);
+  std::vector<uint8_t> merged(G, 0);
+  std::vector<sp_group> pseudo;  // group id G + j
+  {
+    std::map<std::vector<uint32_t>, std::pair<std::vector<uint32_t>, double>> buckets;
+    std::vector<uint32_t> la, lb, one;
+    for (uint64_t g = 1; g < G && merge_min > 0; ++g) {
+      const sp_group& gr = h.groups[g];
+      const double p = gr.param;
+      const bool sparse = (gr.dist == SP_DIST_BERNOULLI && p > 0.0 && p < 1.0 && p != 0.5) ||
+                          ((gr.dist == SP_DIST_DEPOLARIZE1 || gr.dist == SP_DIST_DEPOLARIZE2) && p > 0.0);
+      if (!sparse) continue;
+      bool live = false;
+      for (uint32_t b = 0; b < gr.arity; ++b) live |= col_len(gr.first_symbol + b) > 0;
+      if (!live) continue;
+      const uint32_t npat = (1u << gr.arity) - 1;
+      uint32_t k = 0;
+      bool single = true;
+      one.clear();
+      for (uint32_t pat = 1; pat <= npat && single; ++pat) {
+        la.clear();
+        for (uint32_t b = 0; b < gr.arity; ++b) {
+          if (!((pat >> b) & 1u)) continue;
+          const uint64_t sidx = gr.first_symbol + b;
+          lb.clear();
+          std::set_symmetric_difference(la.begin(), la.end(), dcol_rows.begin() + dcol_ptr[sidx],
+                                        dcol_rows.begin() + dcol_ptr[sidx + 1], std::back_inserter(lb));
+          la.swap(lb);
+        }
+        if (la.empty()) continue;
+        if (k == 0) one = la;
+        else if (la != one) single = false;
+        ++k;
+      }
+      if (!single || k == 0) continue;
+      const double p_eff = std::min(p, 1.0) * k / npat;
+      auto& bk = buckets[one];
+      if (bk.first.empty()) bk.second = 1.0;
+      bk.first.push_back(static_cast<uint32_t>(g));
+      bk.second *= 1.0 - 2.0 * p_eff;
+    }
+    for (auto& [rows, bk] : buckets) {
+      if (static_cast<long>(bk.first.size()) < merge_min) continue;
+      const uint64_t sym = dcol_ptr.size() - 1;  // next pseudo symbol id
+      for (uint32_t r : rows) dcol_rows.push_back(r);
+      dcol_ptr.push_back(dcol_rows.size());
+      sp_group pg{};
+      pg.dist = SP_DIST_BERNOULLI;
+      pg.param = 0.5 * (1.0 - bk.second);
+      pg.first_symbol = static_cast<uint32_t>(sym);
+      pg.arity = 1;
+      pseudo.push_back(pg);
+      for (uint32_t g : bk.first) merged[g] = 1;
+    }
+  }
+  auto grp = [&](uint64_t g) -> const sp_group& { return g < G ? h.groups[g] : pseudo[g - G]; };
+
   std::vector<uint32_t> live_groups;
   double events_per_shot = 0, flips_per_shot = 0;
-  for (uint64_t g = 1; g < G; ++g) {
-    const sp_group& gr = h.groups[g];
+  for (uint64_t g = 1; g < G + pseudo.size(); ++g) {
+    const sp_group& gr = grp(g);
+    const bool is_pseudo = g >= G;
     bool live = false;
     uint64_t flips = 0;
     for (uint32_t b = 0; b < gr.arity; ++b) {
-      live |= col_len(gr.first_symbol + b) > 0;
+      live |= is_pseudo || col_len(gr.first_symbol + b) > 0;
       flips += dcol_len(gr.first_symbol + b);
     }
-    if (live) live_groups.push_back(static_cast<uint32_t>(g));
+    if (live && !is_pseudo) live_groups.push_back(static_cast<uint32_t>(g));  // compat (M space)
+    if (!is_pseudo && merged[g]) live = false;  // sampled through its merged variable
     const double p = gr.param;
     switch (gr.dist) {
       case SP_DIST_CONSTANT:
@@ -468,7 +537,7 @@ void build_plan(sp_ctx* c) {
   for (const Cls& cl : live_cls)
     for (uint32_t g : cl.groups) {
       ++live_positions;
-      for (uint32_t b = 0; b < h.groups[g].arity; ++b) live_colrow += dcol_len(h.groups[g].first_symbol + b);
+      for (uint32_t b = 0; b < grp(g).arity; ++b) live_colrow += dcol_len(grp(g).first_symbol + b);
     }
 
   ptm.mark("classify");
@@ -668,7 +737,7 @@ void build_plan(sp_ctx* c) {
       for (uint32_t g : cl.groups) {
         cls_groups.push_back(g);
         if (!live) continue;
-        const sp_group& gr = h.groups[g];
+        const sp_group& gr = grp(g);
         for (uint32_t pat = 1; pat <= ci.npat; ++pat) {
           // symmetric difference of the D columns of the pattern's symbols,
           // merged in place at the end of pl_rows (sorted, as row * tw)

@@ -106,6 +106,7 @@ __global__ void d_coins(const DevPlan P, const RoundKeys K, uint64_t quad0, uint
     const uint64_t slot = i / n_quads, q = i - slot * n_quads;
     const uint64_t gq = quad0 + q;
     const uint32_t sym = P.dense_sym[slot];
+    if (sym >= P.n_sym) continue;  // a merged pseudo coin: not a symbol of S
     const uint4 r = philox10(make_uint4(sym, static_cast<uint32_t>(gq),
                                         (static_cast<uint32_t>(gq >> 32) & 0xFFFFFFu) |
                                             (kDomCoin << 24),
@@ -138,7 +139,9 @@ __global__ void d_segments(const DevPlan P, const RoundKeys K, uint64_t tile0, u
         if (!((f.v >> k) & 1u)) continue;
         const uint64_t j = base + f.shot[k];
         if (j >= n_shots) continue;
-        uint32_t s = P.g_first[P.cls_groups[sg.goff + f.g[k]]];
+        const uint32_t gid = P.cls_groups[sg.goff + f.g[k]];
+        if (gid >= P.n_groups) continue;  // a merged pseudo group: not a symbol of S
+        uint32_t s = P.g_first[gid];
         for (uint32_t pat = f.pat[k]; pat; pat >>= 1, ++s)
           if (pat & 1u) atomicXor(&S32[s * ld32 + (j >> 5)], 1u << (j & 31));
       }

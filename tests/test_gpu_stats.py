@@ -124,3 +124,30 @@ def test_tiny_rates_no_spurious_firings(gpu_sampler_factory, p, expect):
     s.sample(shots, 3, counts=counts)
     total = int(counts.sum().item())
     assert abs(total - expect) <= 5 * max(expect, 1.0) ** 0.5 + 3, (p, total, expect)
+
+
+def test_merged_channels_rates_10M(gpu_sampler_factory):
+    """Channels whose only effect is the same flip list merge into one
+    Bernoulli with the piling-up rate (abi.cpp, channel merging): the record
+    rates still match the analytic values, draw_assignments still draws every
+    original symbol, and SP_MERGE_MIN=0 (no merging) agrees in distribution."""
+    import os
+    import torch
+    text = "X_ERROR(0.001) 0\n" * 300 + "DEPOLARIZE1(0.002) 1\n" * 200 + \
+           "CX 0 2\nX_ERROR(0.01) 2\nM 0 1 2\n"
+    init = run_initialization(text)
+    want = oracle.flip_rates(init)
+    for env in ("64", "0"):
+        os.environ["SP_MERGE_MIN"] = env
+        try:
+            s = gpu_sampler_factory(init)
+            counts = torch.zeros(init.n_meas, dtype=torch.int64, device="cuda")
+            s.sample(N, 31, counts=counts)
+            got = counts.cpu().numpy()
+            for k in range(init.n_meas):
+                ok, detail = within(int(got[k]), N, float(want[k]))
+                assert ok, (env, k, detail)
+            S = host(s.draw_assignments(4096, 5))
+            assert S.shape[0] == init.n_sym
+        finally:
+            del os.environ["SP_MERGE_MIN"]
