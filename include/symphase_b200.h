@@ -176,8 +176,12 @@ int sp_encode_tiled(sp_ctx* ctx, const uint64_t* d_tiled, uint64_t n_shots, sp_f
 
 /* draw_assignments (sampler.hpp:51-52) on the device: the exact assignment
  * matrix S the fused sampler uses for these shots (row 0 = constant = all
- * ones). d_S: [n_sym][ldS]. With SP_RNG_COMPAT_SPLITMIX it is bit-identical
- * to the reference's draw_assignments(registry, n, seed) when shot_begin=0. */
+ * ones), so sp_sample == M_sym . S bit for bit. The exception is a model
+ * where the planner merged many channels with one common flip list into a
+ * single variable (SP_MERGE_MIN): there S is an independent draw of every
+ * original symbol, correct in distribution. d_S: [n_sym][ldS]. With
+ * SP_RNG_COMPAT_SPLITMIX it is bit-identical to the reference's
+ * draw_assignments(registry, n, seed) when shot_begin=0. */
 int sp_draw_assignments(sp_ctx* ctx, uint64_t seed, uint64_t shot_begin, uint64_t n_shots,
                         uint64_t* d_S, uint64_t ldS);
 
