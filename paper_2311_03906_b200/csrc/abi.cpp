@@ -104,6 +104,7 @@ struct sp_ctx {
   LaunchCfg L;
   bool have_msym = false, have_groups = false, plan_ready = false, fused_ok = false;
   bool plan_built = false;  // dp/hp-derived buffers describe the model with plan_fp
+  bool unfused = false;     // sp_sample draws S and runs the explicit-S product (faster here)
   uint64_t plan_fp = 0;
   std::string fused_why;
   HostPlan hp;
@@ -253,6 +254,7 @@ struct PlanTimer {
 
 void build_plan(sp_ctx* c) {
   PlanTimer ptm;
+  c->unfused = env_long("SP_UNFUSED", -1) > 0;
   HostPlan& h = c->hp;
   DevPlan& d = c->dp;
   cudaStream_t s = c->stream;
@@ -988,7 +990,8 @@ void build_plan(sp_ctx* c) {
     auto it = tune_cache.find(fp);
     if (it != tune_cache.end()) {
       if (!fix_gw) d.gen_warps = it->second.first;
-      if (!fix_pp) d.pad_pred = it->second.second;
+      if (!fix_pp) d.pad_pred = it->second.second & 1u;
+      c->unfused = (it->second.second & 2u) != 0;
       cached = true;
     }
   }
@@ -1044,6 +1047,35 @@ void build_plan(sp_ctx* c) {
         }
         d.gen_warps = best;
       }
+      // Fused vs unfused (device draw of S + explicit-S product): the same
+      // bits for an unmerged model (K1 == M_sym . S of its own draw), so the
+      // faster one serves sp_sample. Unfused wins when firings x list
+      // lengths per shot are very large (cfg5 density 0.01, p = 1e-2).
+      if (pseudo.empty() && env_long("SP_UNFUSED", -1) < 0) {
+        const float t_fused = time_launch() / static_cast<float>(cal_shots);
+        const uint64_t n_u = std::min<uint64_t>(
+            cal_shots, std::max<uint64_t>(1, (256ull << 20) / (n_sym / 8 + 1) / (1ull << d.t_log2)) << d.t_log2);
+        const uint64_t ldS = n_u / 64;
+        uint64_t* S = nullptr;
+        ck(cudaMalloc(reinterpret_cast<void**>(&S), n_sym * ldS * 8), "cudaMalloc (autotune S)");
+        float tu = 0.f;
+        for (int rep = 0; rep < 3; ++rep) {
+          ck(cudaEventRecord(e0, s), "cudaEventRecord");
+          const int r1 = launch_draw(d, c->L, false, 0x5EEDull + rep, 0, n_u, S, ldS);
+          const int r2 = launch_product(d, c->L, false, S, ldS, n_u, buf, ldS);
+          ck(cudaEventRecord(e1, s), "cudaEventRecord");
+          ck(cudaEventSynchronize(e1), "cudaEventSynchronize");
+          if (r1 < 0 || r2 < 0) {
+            cudaFree(S);
+            throw CudaError("autotune unfused launch failed");
+          }
+          float ms = 0.f;
+          ck(cudaEventElapsedTime(&ms, e0, e1), "cudaEventElapsedTime");
+          if (rep > 0) tu = rep == 1 ? ms : std::min(tu, ms);
+        }
+        cudaFree(S);
+        c->unfused = tu / static_cast<float>(n_u) < 0.8f * t_fused;
+      }
     } catch (...) {
       cudaFree(buf);
       cudaEventDestroy(e0);
@@ -1056,7 +1088,7 @@ void build_plan(sp_ctx* c) {
     if (d.timers) d.timers = c->b_timers.upload(std::vector<long long>(4, 0), s);
     ck(cudaStreamSynchronize(s), "plan upload");
     std::lock_guard<std::mutex> lk(tune_mu);
-    tune_cache[fp] = {d.gen_warps, d.pad_pred};
+    tune_cache[fp] = {d.gen_warps, d.pad_pred | (c->unfused ? 2u : 0u)};
   }
   ptm.mark("autotune");
   c->plan_ready = true;
@@ -1390,10 +1422,11 @@ int sp_sample(sp_ctx* ctx, uint64_t seed, uint64_t shot_begin, uint64_t n_shots,
   if (shot_begin % T) return fail(SP_ERR_INVALID_ARGUMENT, "shot_begin must be a multiple of the shot tile");
   if (ctx->hp.n_meas == 0) return SP_OK;
   if (!d_out || ld < (n_shots + 63) / 64) return fail(SP_ERR_INVALID_ARGUMENT, "output too small");
-  if (!ctx->fused_ok) {
-    // Too many rows for an on-chip shot tile: the same streams through the
-    // unfused path, draw S (device) then the explicit-S product, in shot
-    // chunks that keep S under ~2 GB. Same records as the fused kernel.
+  if (!ctx->fused_ok || (ctx->unfused && ctx->rng == SP_RNG_PHILOX)) {
+    // Too many rows for an on-chip shot tile, or measured faster: the same
+    // streams through the unfused path, draw S (device) then the explicit-S
+    // product, in shot chunks that keep S under ~2 GB. Same records as the
+    // fused kernel.
     const uint64_t per_shot = std::max<uint64_t>(ctx->hp.n_sym, 1) / 8 + 1;
     uint64_t chunk = std::max<uint64_t>((2ull << 30) / per_shot / T, 1) * T;
     chunk = std::min(chunk, (n_shots + T - 1) / T * T);
@@ -1568,7 +1601,7 @@ int sp_sample_to_host(sp_ctx* ctx, uint64_t seed, uint64_t shot_begin, uint64_t 
       const uint64_t n = std::min(chunk, n_shots - done);
       if (i >= 2) ck(cudaStreamWaitEvent(ctx->stream, ctx->ev_free[b], 0), "cudaStreamWaitEvent");
       int r = SP_OK;
-      if (ctx->rng == SP_RNG_PHILOX && n_meas && ctx->fused_ok) {
+      if (ctx->rng == SP_RNG_PHILOX && n_meas && ctx->fused_ok && !ctx->unfused) {
         // tiled records: coalesced stores for any row count
         if ((r = sp_sample_tiled(ctx, seed, shot_begin + done, n, d_m[b], nullptr))) return r;
         if ((r = sp_encode_tiled(ctx, d_m[b], n, fmt, d_b[b]))) return r;
