@@ -1048,7 +1048,9 @@ void build_plan(sp_ctx* c) {
         for (long dg : {0L, -1L, 1L, -2L, 2L}) {
           const long g = static_cast<long>(gw0) + dg;
           if (fix_gw && dg != 0) continue;
-          if (g < n_warps / 2 || g > n_warps - 2) continue;
+          // the model's own pick is always a candidate (a model with very
+          // few firings may want a single generator warp)
+          if (dg != 0 && (g < std::min<long>(n_warps / 2, gw0) || g > n_warps - 2 || g < 1)) continue;
           for (uint32_t pp : {pp0, pp0 ^ 1u}) {
             if (fix_pp && pp != pp0) continue;
             cand.emplace_back(static_cast<uint32_t>(g), pp);
