@@ -213,9 +213,10 @@ int sp_debug_philox(sp_ctx* ctx, const uint32_t* ctr_key, uint32_t* out);
 int sp_plan_info(sp_ctx* ctx, uint64_t* out16);
 
 /* Profiling hook: per-role cycle counters of the fused kernel (gen wait,
- * gen work, drain wait, drain work), enabled by SP_PHASE_TIMERS=1 at plan
- * build; copied out and cleared. */
-int sp_debug_timers(sp_ctx* ctx, long long* out4);
+ * gen work, drain wait, drain work), then walk steps, firings and two
+ * reserved slots, enabled by SP_PHASE_TIMERS=1 at plan build; copied out
+ * (8 values) and cleared. */
+int sp_debug_timers(sp_ctx* ctx, long long* out8);
 
 /* Number of kernel launches this context has issued so far. */
 uint64_t sp_launch_count(const sp_ctx* ctx);

@@ -11,7 +11,7 @@ import ctypes as C
 import os
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "libsymphase_b200.so"
+LIB_PATH = Path(os.environ.get("SP_LIB") or Path(__file__).resolve().parent / "libsymphase_b200.so")  # SP_LIB: A/B tools only
 
 SP_OK = 0
 STATUS = {

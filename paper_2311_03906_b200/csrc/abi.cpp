@@ -961,8 +961,9 @@ void build_plan(sp_ctx* c) {
   d.n_live_groups = static_cast<uint32_t>(live_groups.size());
   d.live_groups = c->b_live_groups.upload(live_groups, s);
   d.debug_mode = static_cast<uint32_t>(env_long("SP_DEBUG_MODE", 0));
+  d.wait_ns = static_cast<uint32_t>(std::max<long>(32, env_long("SP_WAIT_NS", 256)));
   if (env_long("SP_PHASE_TIMERS", 0)) {
-    std::vector<long long> z(4, 0);
+    std::vector<long long> z(8, 0);
     d.timers = c->b_timers.upload(z, s);
   }
   ck(cudaStreamSynchronize(s), "plan upload");
@@ -1107,7 +1108,7 @@ void build_plan(sp_ctx* c) {
     cudaFree(buf);
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
-    if (d.timers) d.timers = c->b_timers.upload(std::vector<long long>(4, 0), s);
+    if (d.timers) d.timers = c->b_timers.upload(std::vector<long long>(8, 0), s);
     ck(cudaStreamSynchronize(s), "plan upload");
     std::lock_guard<std::mutex> lk(tune_mu);
     tune_cache[fp] = {d.gen_warps, d.pad_pred | (c->unfused ? 2u : 0u)};
@@ -1676,12 +1677,14 @@ int sp_plan_info(sp_ctx* ctx, uint64_t* out16) {
 }
 
 // Test/profiling hook: copies (and clears) the fused kernel's per-role cycle
-// counters when the plan was built with SP_PHASE_TIMERS=1.
-int sp_debug_timers(sp_ctx* ctx, long long* out4) {
+// counters when the plan was built with SP_PHASE_TIMERS=1: out[0..3] cycles
+// (generators waiting / working, drains waiting / working), out[4] walk steps,
+// out[5] firings, out[6..7] reserved.
+int sp_debug_timers(sp_ctx* ctx, long long* out4) {  // 8 values
   if (!ctx || !out4) return fail(SP_ERR_INVALID_ARGUMENT, "null argument");
   if (!ctx->dp.timers) return fail(SP_ERR_NOT_LOADED, "timers not enabled (SP_PHASE_TIMERS=1)");
-  if (cudaMemcpy(out4, ctx->dp.timers, 32, cudaMemcpyDeviceToHost) != cudaSuccess ||
-      cudaMemset(ctx->dp.timers, 0, 32) != cudaSuccess)
+  if (cudaMemcpy(out4, ctx->dp.timers, 64, cudaMemcpyDeviceToHost) != cudaSuccess ||
+      cudaMemset(ctx->dp.timers, 0, 64) != cudaSuccess)
     return fail(SP_ERR_CUDA, "timer copy failed");
   return SP_OK;
 }

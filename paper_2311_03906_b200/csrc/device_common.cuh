@@ -280,15 +280,29 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(a)
                : "memory");
 }
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(bar));
+// One bounded try of the phase-parity wait (the hardware may suspend the
+// warp for a while before returning false).
+__device__ __forceinline__ bool mbar_try(uint32_t a, uint32_t parity) {
+  uint32_t ok;
   asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
-      "@!p bra WAIT_%=;\n\t}" ::"r"(a),
-      "r"(parity), "r"(1000000u)  // suspend up to 1 ms per try: woken on completion, no spinning
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(a), "r"(parity)
       : "memory");
+  return ok != 0;
+}
+// Wait for the phase with exponential back-off sleeps (32 ns doubling up to
+// max_ns): a waiting warp issues a handful of instructions per wait instead
+// of polling.
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity, uint32_t max_ns = 256) {
+  const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(bar));
+  uint32_t ns = 32;
+  while (!mbar_try(a, parity)) {
+    __nanosleep(ns);
+    ns = min(2 * ns, max_ns);
+  }
 }
 
 

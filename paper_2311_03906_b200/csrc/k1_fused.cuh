@@ -148,7 +148,7 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
       const uint32_t b = i % n_buf;
       const uint64_t gtile = tile0 + blockIdx.x + static_cast<uint64_t>(i) * gridDim.x;
       long long tw0 = clock64();
-      if (i >= n_buf) mbar_wait(mbar_empty + b, ((i / n_buf) - 1) & 1);
+      if (i >= n_buf) mbar_wait(mbar_empty + b, ((i / n_buf) - 1) & 1, P.wait_ns);
       long long tw1 = clock64();
       uint32_t* tile = tiles + b * tile_words;
       const uint32_t tile_s = static_cast<uint32_t>(__cvta_generic_to_shared(tile));
@@ -238,6 +238,14 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
       };
       auto emit = [&](auto bern_tag, const Fired& f) {
         constexpr bool kB = decltype(bern_tag)::value;
+        if (P.timers) {  // profiling counters: [4] walk steps, [5] firings
+          const uint32_t nv = __reduce_add_sync(kFull, __popc(f.v));
+          if (lane == 0) {
+            atomicAdd(reinterpret_cast<unsigned long long*>(P.timers) + 4, 1ull);
+            atomicAdd(reinterpret_cast<unsigned long long*>(P.timers) + 5,
+                      static_cast<unsigned long long>(nv));
+          }
+        }
         if (P.debug_mode & 1u) {
           if (f.v == 0xFFFFFFFFu) tile[0] = f.g[0] ^ f.shot[1] ^ f.pat[2];  // keep the walk alive
           return;
@@ -339,7 +347,7 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
       const uint32_t b = i % n_buf;
       const uint64_t t_local = blockIdx.x + static_cast<uint64_t>(i) * gridDim.x;
       long long td0 = clock64();
-      mbar_wait(mbar_full + b, (i / n_buf) & 1);
+      mbar_wait(mbar_full + b, (i / n_buf) & 1, P.wait_ns);
       long long td1 = clock64();
 
       uint4* t4 = reinterpret_cast<uint4*>(tiles + b * tile_words);

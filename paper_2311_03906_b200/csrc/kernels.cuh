@@ -114,6 +114,7 @@ struct DevPlan {
   // skips the segment walks, bit 2 skips the HBM stores, bit 3 skips the row
   // rebuild. Results are wrong when set.
   uint32_t debug_mode = 0;
+  uint32_t wait_ns = 256;  // longest back-off sleep of an mbarrier wait (ns)
   // Optional per-role cycle counters (SP_PHASE_TIMERS=1): gen wait/work,
   // drain wait/work, summed over warps and tiles (u64[4], device).
   long long* timers = nullptr;

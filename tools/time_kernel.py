@@ -47,7 +47,7 @@ def main():
     timers = None
     if os.environ.get("SP_PHASE_TIMERS"):
         import ctypes as C
-        buf = (C.c_longlong * 4)()
+        buf = (C.c_longlong * 8)()
         s._L.sp_debug_timers(s._h, C.cast(buf, C.c_void_p))
         timers = list(buf)
     ms = ts[len(ts) // 2]
