@@ -111,7 +111,7 @@ struct sp_ctx {
   DevPlan dp;
   // plan buffers
   DBuf b_row_ptr, b_sym_idx, b_col_ptr, b_col_rows, b_dense, b_first, b_arity, b_dist, b_param,
-      b_row_const_compat, b_ones, b_dense_sym, b_coin_ptr, b_coin_rows, b_cls, b_cls_groups,
+      b_row_const_compat, b_ones, b_dense_sym, b_coin_ptr, b_coin_rows, b_cls, b_cls_groups, b_thin_src, b_g_masks,
       b_desc, b_colrow, b_live_groups, b_path_rows, b_path_ptr, b_path_par, b_round_ptr, b_plist, b_keep_rows, b_timers;
   uint64_t dnnz = 0;  // nnz of D (chain transform), for reports
   // K2's own copy of the rows (independent of the group table)
@@ -331,8 +331,8 @@ void build_plan(sp_ctx* c) {
     uint32_t lpc;  // flip-list length class (live): every pattern's D list has <= lpc rows
     std::vector<uint32_t> groups;
   };
-  std::vector<Cls> live_cls, dead_cls;
-  std::map<std::tuple<uint8_t, uint64_t, uint32_t>, size_t> live_key, dead_key;
+  std::vector<Cls> live_cls, dead_cls, null_cls;
+  std::map<std::tuple<uint8_t, uint64_t, uint32_t>, size_t> live_key, dead_key, null_key;
   // Longest flip list over a group's patterns (symmetric differences of the
   // D columns of the pattern's symbols), rounded up to 2, 4, 8, 16 (0: longer).
   std::vector<uint32_t> mrg_a, mrg_b;
@@ -364,13 +364,27 @@ void build_plan(sp_ctx* c) {
   // merged-away groups are still drawn by sp_draw_assignments (as dead
   // classes), so S stays complete, but K1 records of a merged model are not
   // M_sym . S of that S. Buckets of >= SP_MERGE_MIN (64) groups are merged.
+  //
+  // Thinning (exact, keeps K1 == M_sym . S of its own draw). A single-list
+  // group that is not merged becomes its own pseudo variable: Bernoulli(p_eff)
+  // on L, so the patterns that flip nothing cost no firings. The draw kernel
+  // maps a firing of that pseudo group back to one of the group's non-null
+  // patterns (uniform, keyed hash) and draws the null patterns in a second
+  // pass: Bernoulli(p_null / (1 - p_eff)) over the trials where the group did
+  // not fire (a null event on a trial that fired is dropped), so every
+  // pattern keeps probability p / #patterns and S stays exact.
   const long merge_min = env_long("SP_MERGE_MIN", 64);
-  std::vector<uint8_t> merged(G, 0);
-  std::vector<sp_group> pseudo;  // group id G + j
+  const bool thin = env_long("SP_THIN", 1) != 0;
+  std::vector<uint8_t> merged(G, 0), thinned(G, 0);
+  std::vector<sp_group> pseudo;        // group id G + j
+  std::vector<uint32_t> thin_src;      // pseudo j -> thinned source group (UINT32_MAX: a merged bucket)
+  std::vector<uint32_t> g_masks(G, 0);  // thinned group: non-null pattern mask | null mask << 16
+  std::vector<double> null_p(G, 0.0);   // thinned group: rate of its null events given no firing
   {
     std::map<std::vector<uint32_t>, std::pair<std::vector<uint32_t>, double>> buckets;
+    std::map<uint32_t, std::pair<double, uint32_t>> singles;  // g -> (p_eff, non-null mask)
     std::vector<uint32_t> la, lb, one;
-    for (uint64_t g = 1; g < G && merge_min > 0; ++g) {
+    for (uint64_t g = 1; g < G && (merge_min > 0 || thin); ++g) {
       const sp_group& gr = h.groups[g];
       const double p = gr.param;
       const bool sparse = (gr.dist == SP_DIST_BERNOULLI && p > 0.0 && p < 1.0 && p != 0.5) ||
@@ -380,7 +394,7 @@ void build_plan(sp_ctx* c) {
       for (uint32_t b = 0; b < gr.arity; ++b) live |= col_len(gr.first_symbol + b) > 0;
       if (!live) continue;
       const uint32_t npat = (1u << gr.arity) - 1;
-      uint32_t k = 0;
+      uint32_t k = 0, nonnull = 0;
       bool single = true;
       one.clear();
       for (uint32_t pat = 1; pat <= npat && single; ++pat) {
@@ -396,6 +410,7 @@ void build_plan(sp_ctx* c) {
         if (la.empty()) continue;
         if (k == 0) one = la;
         else if (la != one) single = false;
+        nonnull |= 1u << (pat - 1);
         ++k;
       }
       if (!single || k == 0) continue;
@@ -404,9 +419,37 @@ void build_plan(sp_ctx* c) {
       if (bk.first.empty()) bk.second = 1.0;
       bk.first.push_back(static_cast<uint32_t>(g));
       bk.second *= 1.0 - 2.0 * p_eff;
+      // (p_eff = 1/2 would make the pseudo variable a fair coin: not thinned)
+      if (k < npat && p_eff < 0.5) singles.emplace(static_cast<uint32_t>(g), std::make_pair(p_eff, nonnull));
     }
     for (auto& [rows, bk] : buckets) {
-      if (static_cast<long>(bk.first.size()) < merge_min) continue;
+      if (merge_min <= 0 || static_cast<long>(bk.first.size()) < merge_min) {
+        if (!thin) continue;
+        for (uint32_t g : bk.first) {  // thin each of the bucket's groups on its own
+          auto it = singles.find(g);
+          if (it == singles.end()) continue;
+          const sp_group& gr = h.groups[g];
+          const uint32_t npat = (1u << gr.arity) - 1;
+          const double p_eff = it->second.first;
+          const uint32_t nonnull = it->second.second;
+          const uint64_t sym = dcol_ptr.size() - 1;
+          for (uint32_t r : rows) dcol_rows.push_back(r);
+          dcol_ptr.push_back(dcol_rows.size());
+          sp_group pg{};
+          pg.dist = SP_DIST_BERNOULLI;
+          pg.param = p_eff;
+          pg.first_symbol = static_cast<uint32_t>(sym);
+          pg.arity = 1;
+          pseudo.push_back(pg);
+          thin_src.push_back(g);
+          const uint32_t nullm = ((1u << npat) - 1) & ~nonnull;
+          g_masks[g] = nonnull | (nullm << 16);
+          null_p[g] = (gr.param * __builtin_popcount(nullm) / npat) / (1.0 - p_eff);
+          thinned[g] = 1;
+          merged[g] = 1;
+        }
+        continue;
+      }
       const uint64_t sym = dcol_ptr.size() - 1;  // next pseudo symbol id
       for (uint32_t r : rows) dcol_rows.push_back(r);
       dcol_ptr.push_back(dcol_rows.size());
@@ -416,9 +459,12 @@ void build_plan(sp_ctx* c) {
       pg.first_symbol = static_cast<uint32_t>(sym);
       pg.arity = 1;
       pseudo.push_back(pg);
+      thin_src.push_back(UINT32_MAX);
       for (uint32_t g : bk.first) merged[g] = 1;
     }
   }
+  const bool merged_any =
+      std::any_of(thin_src.begin(), thin_src.end(), [](uint32_t v) { return v == UINT32_MAX; });
   auto grp = [&](uint64_t g) -> const sp_group& { return g < G ? h.groups[g] : pseudo[g - G]; };
 
   std::vector<uint32_t> live_groups;
@@ -433,6 +479,20 @@ void build_plan(sp_ctx* c) {
       flips += dcol_len(gr.first_symbol + b);
     }
     if (live && !is_pseudo) live_groups.push_back(static_cast<uint32_t>(g));  // compat (M space)
+    if (!is_pseudo && thinned[g]) {
+      // fires through its pseudo variable; the draw kernel's second pass
+      // draws its null patterns (Bernoulli null_p over the trials it did not fire)
+      uint64_t pbits;
+      std::memcpy(&pbits, &null_p[g], 8);
+      auto key = std::make_tuple(static_cast<uint8_t>(SP_DIST_BERNOULLI), pbits, 0u);
+      auto it = null_key.find(key);
+      if (it == null_key.end()) {
+        it = null_key.emplace(key, null_cls.size()).first;
+        null_cls.push_back(Cls{SP_DIST_BERNOULLI, std::min(null_p[g], 1.0), 0u, {}});
+      }
+      null_cls[it->second].groups.push_back(static_cast<uint32_t>(g));
+      continue;
+    }
     if (!is_pseudo && merged[g]) live = false;  // sampled through its merged variable
     const double p = gr.param;
     switch (gr.dist) {
@@ -778,6 +838,8 @@ void build_plan(sp_ctx* c) {
   ptm.mark("segment plan");
   add_classes(live_cls, true);
   add_classes(dead_cls, false);
+  const size_t n_cls_ld = cls_info.size();  // live + dead; null classes follow
+  add_classes(null_cls, false);
   ptm.mark("flip lists");
   // Segment table: live classes get the planned slice counts, dead ones
   // (walked only by the standalone draw kernel) ~E firings per slice.
@@ -789,7 +851,7 @@ void build_plan(sp_ctx* c) {
       if (c < live_cls.size()) {
         n_seg = nseg_live[c];
       } else {
-        const double pc = dead_cls[c - live_cls.size()].p;
+        const double pc = c < n_cls_ld ? dead_cls[c - live_cls.size()].p : null_cls[c - n_cls_ld].p;
         double len = std::ceil(E / pc);
         len = std::min(std::max(len, 32.0), 4194304.0);  // kernel skips clamp at 2^22
         n_seg = std::max<uint64_t>((ci.trials + static_cast<uint64_t>(len) - 1) /
@@ -800,10 +862,12 @@ void build_plan(sp_ctx* c) {
       ci.seg_off = static_cast<uint32_t>(n_chains);
       n_chains += n_seg;
       if (c + 1 == live_cls.size()) d.n_seg_live = static_cast<uint32_t>(n_chains);
+      if (c + 1 == n_cls_ld) d.n_seg_all = static_cast<uint32_t>(n_chains);
     }
     if (live_cls.empty()) d.n_seg_live = 0;
+    if (n_cls_ld == 0) d.n_seg_all = 0;
     if (n_chains >= (1ull << 32)) throw std::invalid_argument("too many sampling chains");
-    d.n_seg_all = static_cast<uint32_t>(n_chains);
+    d.n_seg_null = static_cast<uint32_t>(n_chains) - d.n_seg_all;
     d.cls = c->b_cls.upload(cls_info, s);
   };
 
@@ -846,8 +910,12 @@ void build_plan(sp_ctx* c) {
       if (fused_smem_bytes(t, t.t_log2, t.staged, t.row_staged, t.n_buf) <= optin) d.coins_staged = 1;
     }
   }
-  d.n_cls_all = static_cast<uint32_t>(cls_info.size());
+  d.n_cls_all = static_cast<uint32_t>(n_cls_ld);
+  d.n_cls_null = static_cast<uint32_t>(cls_info.size() - n_cls_ld);
   apply_segments(live_nseg);
+  if (thin_src.empty()) thin_src.push_back(UINT32_MAX);  // never read; keeps the buffer non-null
+  d.thin_src = c->b_thin_src.upload(thin_src, s);
+  d.g_masks = c->b_g_masks.upload(g_masks, s);
   d.cls_groups = c->b_cls_groups.upload(cls_groups, s);
   d.desc = c->b_desc.upload(desc, s);
   d.colrow = c->b_colrow.upload(colrow16, s);
@@ -1074,7 +1142,7 @@ void build_plan(sp_ctx* c) {
       // bits for an unmerged model (K1 == M_sym . S of its own draw), so the
       // faster one serves sp_sample. Unfused wins when firings x list
       // lengths per shot are very large (cfg5 density 0.01, p = 1e-2).
-      if (pseudo.empty() && env_long("SP_UNFUSED", -1) < 0) {
+      if (!merged_any && env_long("SP_UNFUSED", -1) < 0) {
         const float t_fused = time_launch() / static_cast<float>(cal_shots);
         const uint64_t n_u = std::min<uint64_t>(
             cal_shots, std::max<uint64_t>(1, (256ull << 20) / (n_sym / 8 + 1) / (1ull << d.t_log2)) << d.t_log2);

@@ -122,27 +122,64 @@ __global__ void d_coins(const DevPlan P, const RoundKeys K, uint64_t quad0, uint
   }
 }
 
+// The j-th set bit (0-based) of a pattern mask, as a 1-based pattern.
+__device__ __forceinline__ uint32_t nth_pattern(uint32_t mask, uint32_t j) {
+  for (; j; --j) mask &= mask - 1;
+  return static_cast<uint32_t>(__ffs(mask));
+}
+
+// Sparse symbols of S: the same slices (streams) as the fused kernel. Pass 0
+// walks the live and dead classes; a firing of a thinned group's pseudo
+// variable sets one of the group's non-null patterns (uniform, keyed by
+// (group, global shot)). Pass 1 walks the null classes: a null event of a
+// thinned group on a shot where the group did not fire sets one of its null
+// patterns (the pass runs after pass 0, so the check sees every firing).
 __global__ void d_segments(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles,
-                           uint64_t n_shots, uint32_t* S32, uint64_t ld32) {
+                           uint64_t n_shots, uint32_t* S32, uint64_t ld32, uint32_t pass) {
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t warp = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5;
   const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
-  const uint64_t total = static_cast<uint64_t>(P.n_seg_all) * n_tiles;
+  const uint32_t seg0 = pass ? P.n_seg_all : 0u, n_seg = pass ? P.n_seg_null : P.n_seg_all;
+  const uint32_t n_cls = P.n_cls_all + (pass ? P.n_cls_null : 0u);
+  const uint64_t total = static_cast<uint64_t>(n_seg) * n_tiles;
+  const uint64_t shot0 = tile0 << P.t_log2;
   for (uint64_t i = warp; i < total; i += nwarps) {
-    const uint32_t t = static_cast<uint32_t>(i / P.n_seg_all);
-    const uint32_t seg = static_cast<uint32_t>(i - static_cast<uint64_t>(t) * P.n_seg_all);
+    const uint32_t t = static_cast<uint32_t>(i / n_seg);
+    const uint32_t seg = seg0 + static_cast<uint32_t>(i - static_cast<uint64_t>(t) * n_seg);
     const uint64_t base = static_cast<uint64_t>(t) << P.t_log2;
     Segment sg;
-    segment_init(sg, P.cls, P.n_cls_all, seg, P.t_log2);
+    segment_init(sg, P.cls, n_cls, seg, P.t_log2);
     segment_walk(sg, K, tile0 + t, P.t_log2, lane, [&](auto, const Fired& f) {
       for (int k = 0; k < kSlots; ++k) {
         if (!((f.v >> k) & 1u)) continue;
         const uint64_t j = base + f.shot[k];
         if (j >= n_shots) continue;
-        const uint32_t gid = P.cls_groups[sg.goff + f.g[k]];
-        if (gid >= P.n_groups) continue;  // a merged pseudo group: not a symbol of S
-        uint32_t s = P.g_first[gid];
-        for (uint32_t pat = f.pat[k]; pat; pat >>= 1, ++s)
+        uint32_t gid = P.cls_groups[sg.goff + f.g[k]];
+        uint32_t pat = f.pat[k];
+        if (pass == 0 && gid >= P.n_groups) {
+          gid = P.thin_src[gid - P.n_groups];
+          if (gid == UINT32_MAX) continue;  // a merged pseudo group: not a symbol of S
+        }
+        const uint32_t first = P.g_first[gid];
+        if (pass == 1 || P.g_masks[gid] != 0) {
+          const uint64_t gj = shot0 + j;
+          const uint32_t h = philox10(make_uint4(gid, static_cast<uint32_t>(gj),
+                                                 (static_cast<uint32_t>(gj >> 32) & 0xFFFFFFu) |
+                                                     (kDomThin << 24),
+                                                 0u),
+                                      K).x;
+          const uint32_t mask = pass == 0 ? (P.g_masks[gid] & 0xFFFFu) : (P.g_masks[gid] >> 16);
+          if (pass == 1) {
+            // dropped when the group fired on this shot in pass 0
+            bool fired = false;
+            for (uint32_t b = 0; b < P.g_arity[gid]; ++b)
+              fired |= (S32[(first + b) * ld32 + (j >> 5)] >> (j & 31)) & 1u;
+            if (fired) continue;
+          }
+          pat = nth_pattern(mask, __umulhi(h, __popc(mask)));
+        }
+        uint32_t s = first;
+        for (; pat; pat >>= 1, ++s)
           if (pat & 1u) atomicXor(&S32[s * ld32 + (j >> 5)], 1u << (j & 31));
       }
     });
@@ -475,7 +512,11 @@ int launch_draw(const DevPlan& P, const LaunchCfg& L, bool compat, uint64_t seed
     const uint64_t T = 1ull << P.t_log2;
     const uint32_t n_tiles = static_cast<uint32_t>((n_shots + T - 1) / T);
     if (P.n_seg_all) {
-      d_segments<<<grid, 256, 0, L.stream>>>(P, K, tile0, n_tiles, n_shots, S32, ld32);
+      d_segments<<<grid, 256, 0, L.stream>>>(P, K, tile0, n_tiles, n_shots, S32, ld32, 0u);
+      ++launches;
+    }
+    if (P.n_seg_null) {  // null patterns of thinned groups, after every firing is in S
+      d_segments<<<grid, 256, 0, L.stream>>>(P, K, tile0, n_tiles, n_shots, S32, ld32, 1u);
       ++launches;
     }
   }

@@ -9,6 +9,7 @@ namespace symphase {
 // Random-stream domains (top byte of Philox counter word 3).
 constexpr uint32_t kDomChain = 1u;  // geometric-skip event chains
 constexpr uint32_t kDomCoin = 2u;   // bit-sliced fair-coin words
+constexpr uint32_t kDomThin = 3u;   // pattern choice of thinned groups (draw kernel)
 
 // One class = all sparse channels sharing (distribution, p). Its trial space
 // for one shot tile is the flattened (group, shot) grid, group-major, cut into
@@ -70,6 +71,14 @@ struct DevPlan {
   uint32_t n_seg_live = 0, n_seg_all = 0;
   const ClassInfo* cls = nullptr;
   const uint32_t* cls_groups = nullptr;  // class position -> group id
+  // Thinned groups (abi.cpp): pseudo group j >= n_groups fires for source
+  // group thin_src[j] (UINT32_MAX: a merged bucket, not a symbol of S); per
+  // group g_masks = non-null pattern mask | null pattern mask << 16. The
+  // null classes (after live and dead) are walked by the draw kernel's
+  // second pass.
+  uint32_t n_cls_null = 0, n_seg_null = 0;
+  const uint32_t* thin_src = nullptr;
+  const uint32_t* g_masks = nullptr;
   // Fused-kernel event tables in D space (M_sym = L·D, see abi.cpp), class-
   // position order: desc = {colrow base, len0 | len1 << 16, len2 | len3 << 16,
   // group id}; colrow entries = D row * tw (u16: n_meas * tw < 65536).

@@ -107,12 +107,18 @@ def test_product_out_of_range_symbol(gpu_sampler_factory):
         s.sample_given(S, 8, n_sym_S=3)
 
 
-@pytest.mark.parametrize("cfg", ["rep", "surf5", "mixed"])
+@pytest.mark.parametrize("cfg", ["rep", "surf5", "mixed", "thin"])
 def test_philox_fused_equals_product_of_its_draws(gpu_sampler_factory, port, cfg):
-    """K1 output == M_sym . S for the S its streams draw (bit-exact), and K2(S) == oracle."""
+    """K1 output == M_sym . S for the S its streams draw (bit-exact), and K2(S) == oracle.
+    "thin": channels whose non-null patterns all flip one list (DEPOLARIZE1 before a Z
+    measurement, DEPOLARIZE2 with one qubit never measured) fire as thinned Bernoulli
+    variables in K1; the draw kernel maps each firing back to a pattern and draws the
+    null patterns in its second pass, so the identity still holds bit for bit."""
     text = {"rep": CI.repetition_code(5, 5, 0.01), "surf5": CI.surface_code(5, 5, 1e-3),
             "mixed": "H 0\nCX 0 1\nDEPOLARIZE1(0.2) 0\nX_ERROR(0.3) 1\nX_ERROR(1) 1\n"
-                     "X_ERROR(0.5) 0\nM 0\nR 1\nH 1\nDEPOLARIZE2(0.7) 0 1\nM 1 0\n"}[cfg]
+                     "X_ERROR(0.5) 0\nM 0\nR 1\nH 1\nDEPOLARIZE2(0.7) 0 1\nM 1 0\n",
+            "thin": "DEPOLARIZE1(0.3) 0 1 2\nDEPOLARIZE2(0.2) 3 4\nCX 0 3\n"
+                    "DEPOLARIZE1(0.01) 3 5\nDEPOLARIZE2(0.05) 5 6\nM 0 1 2 3 5\n"}[cfg]
     init = run_initialization(text)
     s = gpu_sampler_factory(init)
     T = s.shot_tile

@@ -102,6 +102,36 @@ def test_per_measurement_flip_rates_10M(gpu_sampler_factory, cfg):
         assert abs(want[0] - 0.5 * (1 - 0.9 * 0.6 * 0.1)) < 1e-12
 
 
+def test_thinned_pattern_marginals_10M(gpu_sampler_factory):
+    """Thinned channels (abi.cpp: single-list groups fire as Bernoulli(p_eff) in
+    K1): the draw kernel's pattern choice and its null-pattern pass keep every
+    pattern at p / #patterns — DEPOLARIZE1 measured in Z (Z is null) and
+    DEPOLARIZE2 with one qubit never measured (7 of 15 patterns null), at rates
+    where null events often coincide with firings and must be dropped."""
+    text = "DEPOLARIZE1(0.45) 0\nDEPOLARIZE2(0.6) 1 2\nDEPOLARIZE2(0.01) 3 4\nM 0 1 3\n"
+    init = run_initialization(text)
+    s = gpu_sampler_factory(init)
+    S = host(s.draw_assignments(N, 77))
+    g = init.groups
+    bad = []
+    for gi in range(1, len(g)):
+        d, p, f = int(g["dist"][gi]), float(g["param"][gi]), int(g["first_symbol"][gi])
+        arity = 2 if d == 3 else 4
+        n_pat = (1 << arity) - 1
+        rows = [S[f + b] for b in range(arity)]
+        for pat in range(n_pat + 1):
+            w = np.full(S.shape[1], ~np.uint64(0), dtype=np.uint64)
+            for b in range(arity):
+                w &= rows[b] if (pat >> b) & 1 else ~rows[b]
+            ok, info = within(int(np.bitwise_count(w).sum()), N, (1 - p) if pat == 0 else p / n_pat)
+            if not ok:
+                bad.append((gi, pat, info))
+    assert not bad, bad
+    # and the records K1 makes are the product of exactly these draws
+    out = s.sample(N, 77)
+    assert np.array_equal(host(out), host(s.sample_given(s.draw_assignments(N, 77), N)))
+
+
 def test_seeds_differ_and_repeat(gpu_sampler_factory):
     init = run_initialization(CI.surface_code(5, 5, 1e-3))
     s = gpu_sampler_factory(init)
