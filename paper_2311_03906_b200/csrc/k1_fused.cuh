@@ -157,7 +157,7 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
       // column; the last slot is the constant term (all ones). Two tasks per
       // iteration, so two Philox chains interleave.
       {
-        const uint32_t n_tasks = (P.n_dense_live + 1) << tw4_log2;
+        const uint32_t n_tasks = (P.debug_mode & 4u) ? 0u : (P.n_dense_live + 1) << tw4_log2;
         auto coin_word = [&](uint32_t slot, uint32_t q) {
           if (slot >= P.n_dense_live) return make_uint4(kFull, kFull, kFull, kFull);
           const uint64_t gq = (gtile << tw4_log2) + q;

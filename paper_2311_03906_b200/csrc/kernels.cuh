@@ -120,7 +120,7 @@ struct DevPlan {
   uint32_t cta_threads = 512;
   uint32_t n_buf = 2;        // shot-tile buffers in shared memory (1 or 2)
   // Profiling switches (SP_DEBUG_MODE): bit 0 skips the firing XORs, bit 1
-  // skips the segment walks, bit 2 skips the HBM stores, bit 3 skips the row
+  // skips the segment walks, bit 2 skips the coin words, bit 3 skips the row
   // rebuild. Results are wrong when set.
   uint32_t debug_mode = 0;
   uint32_t wait_ns = 256;  // longest back-off sleep of an mbarrier wait (ns)
