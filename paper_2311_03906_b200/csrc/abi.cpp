@@ -252,6 +252,26 @@ struct PlanTimer {
   }
 };
 
+// K2 variant: the Four-Russians dense product costs the same at any density
+// (n_meas x words x n_sym / 8 table lookups); the CSR walk costs nnz x words.
+// Measured on B200 at cfg5's shape the two cross at density ~0.17.
+constexpr double kDenseProductDensity = 0.17;
+bool dense_product(const sp_ctx* c) {
+  if (c->product == SP_PRODUCT_DENSE) return true;
+  if (c->product != SP_PRODUCT_AUTO) return false;
+  const double cells = static_cast<double>(c->hp.n_meas) * static_cast<double>(c->hp.n_sym);
+  return cells > 0 && static_cast<double>(c->hp.nnz) > kDenseProductDensity * cells;
+}
+// Dense row-major M_sym words from the CSR rows (first use only).
+void ensure_dense_words(HostPlan& h) {
+  if (!h.dense_words.empty()) return;
+  h.ldm = std::max<uint64_t>((h.n_sym + 63) / 64, 1);
+  h.dense_words.assign(h.n_meas * h.ldm, 0);
+  for (uint64_t k = 0; k < h.n_meas; ++k)
+    for (uint64_t i = h.row_ptr[k]; i < h.row_ptr[k + 1]; ++i)
+      h.dense_words[k * h.ldm + h.sym_idx[i] / 64] |= uint64_t{1} << (h.sym_idx[i] % 64);
+}
+
 void build_plan(sp_ctx* c) {
   PlanTimer ptm;
   c->unfused = env_long("SP_UNFUSED", -1) > 0;
@@ -259,6 +279,7 @@ void build_plan(sp_ctx* c) {
   DevPlan& d = c->dp;
   cudaStream_t s = c->stream;
   const uint64_t n_meas = h.n_meas, n_sym = h.n_sym, G = h.groups.size();
+  if (dense_product(c)) ensure_dense_words(h);  // the unfused path's product
 
   // Symbol -> group map; the registry tiles [0, n_sym) with its groups.
   std::vector<uint32_t> sym_group(n_sym, UINT32_MAX);
@@ -651,6 +672,15 @@ void build_plan(sp_ctx* c) {
                    "sp_draw_assignments + sp_sample_given_S";
     lg = 7;
   }
+  // Very many bit flips per shot (dense M_sym with frequent faults): one
+  // shared atomic per flip cannot compete with drawing S and running the
+  // explicit-S product (measured: cfg5 density 0.01, p = 1e-2 is 1e5 flips
+  // per shot, fused 401 ms vs 87 ms), so the fused plan is not built at all.
+  if (c->fused_ok && flips_per_shot > static_cast<double>(env_long("SP_FUSED_MAX_FLIPS", 50000))) {
+    c->fused_ok = false;
+    c->fused_why = "too many flips per shot for the fused sampler; sp_sample draws S and runs the "
+                   "explicit-S product";
+  }
   const uint64_t T = 1ull << lg;
   d.t_log2 = static_cast<uint32_t>(lg);
   d.tw = static_cast<uint32_t>(T / 32);
@@ -783,6 +813,7 @@ void build_plan(sp_ctx* c) {
   std::vector<uint16_t> pl_rows;
   std::vector<uint16_t> scratch;
   size_t max_plist = 0;
+  const bool fused_tables = c->fused_ok;
   auto add_classes = [&](const std::vector<Cls>& cls, bool live) {
     for (size_t c = 0; c < cls.size(); ++c) {
       const Cls& cl = cls[c];
@@ -798,7 +829,7 @@ void build_plan(sp_ctx* c) {
       cls_info.push_back(ci);
       for (uint32_t g : cl.groups) {
         cls_groups.push_back(g);
-        if (!live) continue;
+        if (!live || !fused_tables) continue;  // event tables serve the fused kernel only
         const sp_group& gr = grp(g);
         for (uint32_t pat = 1; pat <= ci.npat; ++pat) {
           // symmetric difference of the D columns of the pattern's symbols,
@@ -1153,7 +1184,7 @@ void build_plan(sp_ctx* c) {
         for (int rep = 0; rep < 3; ++rep) {
           ck(cudaEventRecord(e0, s), "cudaEventRecord");
           const int r1 = launch_draw(d, c->L, false, 0x5EEDull + rep, 0, n_u, S, ldS);
-          const int r2 = launch_product(d, c->L, false, S, ldS, n_u, buf, ldS);
+          const int r2 = launch_product(d, c->L, dense_product(c), S, ldS, n_u, buf, ldS);
           ck(cudaEventRecord(e1, s), "cudaEventRecord");
           ck(cudaEventSynchronize(e1), "cudaEventSynchronize");
           if (r1 < 0 || r2 < 0) {
@@ -1392,18 +1423,13 @@ int sp_set_product(sp_ctx* ctx, sp_product v) {
   if (!ctx) return fail(SP_ERR_INVALID_ARGUMENT, "null ctx");
   if (v != SP_PRODUCT_AUTO && v != SP_PRODUCT_SPARSE && v != SP_PRODUCT_DENSE)
     return fail(SP_ERR_INVALID_ARGUMENT, "unknown product variant");
-  if (v == SP_PRODUCT_DENSE && ctx->hp.dense_words.empty() && ctx->have_msym) {
+  ctx->product = v;
+  if (dense_product(ctx) && ctx->hp.dense_words.empty() && ctx->have_msym) {
     // Build the dense words from the CSR rows on first request.
-    HostPlan& h = ctx->hp;
-    h.ldm = std::max<uint64_t>((h.n_sym + 63) / 64, 1);
-    h.dense_words.assign(h.n_meas * h.ldm, 0);
-    for (uint64_t k = 0; k < h.n_meas; ++k)
-      for (uint64_t i = h.row_ptr[k]; i < h.row_ptr[k + 1]; ++i)
-        h.dense_words[k * h.ldm + h.sym_idx[i] / 64] |= uint64_t{1} << (h.sym_idx[i] % 64);
+    ensure_dense_words(ctx->hp);
     ctx->plan_ready = false;
     ctx->prod_ready = false;
   }
-  ctx->product = v;
   return SP_OK;
 }
 
@@ -1617,7 +1643,11 @@ int sp_sample_given_S(sp_ctx* ctx, const uint64_t* d_S, uint64_t n_sym_S, uint64
     return fail(SP_ERR_INVALID_ARGUMENT, "buffer too small");
   // K2 only needs the row lists (and dense words): it has its own device
   // copy, independent of the group table and of the fused sampler's plan.
-  bool dense = ctx->product == SP_PRODUCT_DENSE;
+  const bool dense = dense_product(ctx);
+  if (dense && ctx->hp.dense_words.empty()) {
+    ensure_dense_words(ctx->hp);
+    ctx->prod_ready = false;
+  }
   if (!ctx->prod_ready) {
     try {
       ctx->pp = DevPlan{};

@@ -243,31 +243,112 @@ k2_sparse(const uint64_t* __restrict__ row_ptr, const uint32_t* __restrict__ sym
   }
 }
 
-// Dense variant: the row is read as packed M_sym words; set bits select S rows.
-__global__ void __launch_bounds__(kK2Rows * 32)
-k2_dense(const uint64_t* __restrict__ M, uint64_t ldm, uint64_t m_words, uint32_t n_meas,
-         const uint64_t* __restrict__ S, uint64_t ldS, uint64_t n_words, uint64_t tail,
-         uint64_t* __restrict__ out, uint64_t ld) {
-  const uint32_t lane = threadIdx.x & 31;
-  const uint32_t k = blockIdx.x * kK2Rows + (threadIdx.x >> 5);
-  if (k >= n_meas) return;
-  const uint64_t* mrow = M + static_cast<uint64_t>(k) * ldm;
-  for (uint64_t win = blockIdx.y; win * 64 < n_words; win += gridDim.y) {
-    const uint64_t w0 = win * 64 + lane, w1 = w0 + 32;
-    const bool v0 = w0 < n_words, v1 = w1 < n_words;
-    uint64_t a0 = 0, a1 = 0;
-    for (uint64_t mw = 0; mw < m_words; ++mw) {
-      uint64_t m = __ldg(mrow + mw);
-      while (m) {
-        const uint64_t s = mw * 64 + __ffsll(static_cast<long long>(m)) - 1;
-        m &= m - 1;
-        const uint64_t* r = S + s * ldS;
-        if (v0) a0 ^= __ldg(r + w0);
-        if (v1) a1 ^= __ldg(r + w1);
+// Dense variant: Method of Four Russians over shared-memory tables. A CTA
+// owns 512 measurement rows x 32 shot words (lane = word, 32 rows per warp,
+// accumulators in registers). Symbols are taken 8 at a time: for group g the
+// CTA builds T_g[b][w] = XOR of S[8g + i][w] over the set bits i of b (256
+// entries, Gray-code order, one XOR each), then every row XORs in
+// T_g[byte g of its M_sym row] — one 8-byte shared load per row, group and
+// word instead of up to eight global S loads. S rows and M bytes are staged
+// 16 groups at a time with cp.async (double-buffered); two tables alternate,
+// so one barrier per group separates building T_g from reading it.
+// Work is n_meas x words x ceil(n_sym / 8) table lookups whatever the
+// density, so it wins over the CSR walk for dense M_sym (abi.cpp picks it).
+constexpr int kM4Rows = 512, kM4Words = 32, kM4Chunk = 16;
+constexpr size_t kM4Smem = (2ull * 256 * kM4Words + 2ull * kM4Chunk * 8 * kM4Words) * 8 +
+                           2ull * kM4Rows * kM4Chunk;
+
+__device__ __forceinline__ void cp_async8(uint32_t dst, const void* src, bool valid) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst), "l"(src),
+               "r"(valid ? 8 : 0)
+               : "memory");
+}
+
+__global__ void __launch_bounds__(kM4Rows, 1)
+k2_m4rm(const uint64_t* __restrict__ M, uint64_t ldm, uint32_t n_meas, uint32_t n_sym,
+        const uint64_t* __restrict__ S, uint64_t ldS, uint64_t n_words, uint64_t tail,
+        uint64_t* __restrict__ out, uint64_t ld) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  uint64_t* tab = reinterpret_cast<uint64_t*>(smem);             // [2][256][32]
+  uint64_t* ss = tab + 2 * 256 * kM4Words;                         // [2][128][32]
+  uint8_t* mb = reinterpret_cast<uint8_t*>(ss + 2 * kM4Chunk * 8 * kM4Words);  // [2][512][16]
+  const uint32_t t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const uint32_t r0 = blockIdx.y * kM4Rows;
+  const uint64_t w0 = static_cast<uint64_t>(blockIdx.x) * kM4Words;
+  const uint32_t n_g = (n_sym + 7) / 8;
+  const uint32_t n_chunks = (n_g + kM4Chunk - 1) / kM4Chunk;
+  // Stage chunk c (groups 16c .. 16c+15) into buffer c & 1: S rows
+  // [128c, 128c+128) x words [w0, w0+32), and bytes [16c, 16c+16) of each of
+  // the CTA's M rows (u64 words 2c, 2c+1). Out-of-range parts read as zero.
+  auto stage = [&](uint32_t c) {
+    const uint32_t buf = c & 1;
+    const uint32_t ss_s = static_cast<uint32_t>(__cvta_generic_to_shared(ss + buf * kM4Chunk * 8 * kM4Words));
+#pragma unroll
+    for (int i = 0; i < (kM4Chunk * 8 * kM4Words) / kM4Rows; ++i) {
+      const uint32_t e = t + i * kM4Rows;  // (row in chunk, word)
+      const uint64_t j = static_cast<uint64_t>(c) * kM4Chunk * 8 + (e >> 5);
+      const uint64_t w = w0 + (e & 31);
+      const bool ok = j < n_sym && w < n_words;
+      cp_async8(ss_s + e * 8, ok ? S + j * ldS + w : S, ok);
+    }
+    const uint32_t mb_s = static_cast<uint32_t>(__cvta_generic_to_shared(mb + buf * kM4Rows * kM4Chunk));
+    const uint32_t k = r0 + t;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const uint64_t mw = 2ull * c + h;
+      const bool ok = k < n_meas && mw < ldm;
+      cp_async8(mb_s + t * kM4Chunk + 8 * h, ok ? M + static_cast<uint64_t>(k) * ldm + mw : M, ok);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  uint64_t acc[32];
+#pragma unroll
+  for (int r = 0; r < 32; ++r) acc[r] = 0;
+  stage(0);
+  // Phase g: rows look up group g-1, the CTA builds the table of group g.
+  for (uint32_t g = 0; g <= n_g; ++g) {
+    const uint32_t c = g / kM4Chunk, gi = g % kM4Chunk;
+    if (gi == 0 && g < n_g) {  // chunk c must have landed
+      asm volatile("cp.async.wait_all;" ::: "memory");
+      __syncthreads();
+    }
+    if (gi == 1 && c + 1 < n_chunks) stage(c + 1);  // its buffer's last readers passed a barrier
+    if (g > 0) {
+      const uint32_t gp = g - 1;
+      const uint64_t* T = tab + (gp & 1) * 256 * kM4Words + lane;
+      const uint8_t* mrow = mb + ((gp / kM4Chunk) & 1) * kM4Rows * kM4Chunk + (warp * 32) * kM4Chunk +
+                            (gp % kM4Chunk);
+#pragma unroll
+      for (int r = 0; r < 32; ++r) acc[r] ^= T[static_cast<uint32_t>(mrow[r * kM4Chunk]) * kM4Words];
+    }
+    if (g < n_g) {
+      // entries b = 16h + l for this thread's word w and high nibble h:
+      // start from the XOR of the high rows, then walk l in Gray order
+      const uint32_t w = lane, h = warp;
+      const uint64_t* srow = ss + (c & 1) * kM4Chunk * 8 * kM4Words + gi * 8 * kM4Words + w;
+      uint64_t lo[4], e = 0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        lo[i] = srow[i * kM4Words];
+        if ((h >> i) & 1u) e ^= srow[(4 + i) * kM4Words];
+      }
+      uint64_t* T = tab + (g & 1) * 256 * kM4Words + (h * 16) * kM4Words + w;
+      T[0] = e;
+#pragma unroll
+      for (int l = 1; l < 16; ++l) {
+        e ^= lo[l & 1 ? 0 : l & 2 ? 1 : l & 4 ? 2 : 3];  // lowest set bit of l
+        T[(l ^ (l >> 1)) * kM4Words] = e;
       }
     }
-    if (v0) out[static_cast<uint64_t>(k) * ld + w0] = (w0 == n_words - 1) ? (a0 & tail) : a0;
-    if (v1) out[static_cast<uint64_t>(k) * ld + w1] = (w1 == n_words - 1) ? (a1 & tail) : a1;
+    __syncthreads();
+  }
+  const uint64_t w = w0 + lane;
+  if (w < n_words) {
+#pragma unroll
+    for (int r = 0; r < 32; ++r) {
+      const uint32_t k = r0 + warp * 32 + r;
+      if (k < n_meas) out[static_cast<uint64_t>(k) * ld + w] = (w == n_words - 1) ? (acc[r] & tail) : acc[r];
+    }
   }
 }
 
@@ -532,9 +613,18 @@ int launch_product(const DevPlan& P, const LaunchCfg& L, bool dense, const uint6
   dim3 grid((P.n_meas + kK2Rows - 1) / kK2Rows,
             static_cast<unsigned>(std::min<uint64_t>(windows, 65535)));
   if (dense) {
-    const uint64_t m_words = (P.n_sym + 63) / 64;
-    k2_dense<<<grid, kK2Rows * 32, 0, L.stream>>>(P.dense, P.ldm, m_words, P.n_meas, S, ldS,
-                                                  n_words, tail, out, ld);
+    static bool attr = false;
+    if (!attr) {
+      if (cudaFuncSetAttribute(k2_m4rm, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(kM4Smem)) != cudaSuccess)
+        return -1;
+      attr = true;
+    }
+    const uint64_t row_blocks = (P.n_meas + kM4Rows - 1) / kM4Rows;
+    if (row_blocks > 65535) return -1;
+    dim3 g4(static_cast<unsigned>((n_words + kM4Words - 1) / kM4Words), static_cast<unsigned>(row_blocks));
+    k2_m4rm<<<g4, kM4Rows, kM4Smem, L.stream>>>(P.dense, P.ldm, P.n_meas, P.n_sym, S, ldS, n_words,
+                                                tail, out, ld);
   } else {
     k2_sparse<<<grid, kK2Rows * 32, 0, L.stream>>>(P.row_ptr, P.sym_idx, P.n_meas, S, ldS,
                                                    n_words, tail, out, ld);

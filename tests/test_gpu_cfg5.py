@@ -93,3 +93,17 @@ def test_sample_without_onchip_tile_uses_draw_and_product(gpu_sampler_factory, p
     assert np.array_equal(counts.cpu().numpy(), pc)
     buf, w = s.sample_to_host(n, 9, "b8")
     assert bytes(buf[:w]) == port.encode(want, model.n_meas, n, "b8")
+
+
+def test_many_flips_per_shot_skips_fused_plan(gpu_sampler_factory, port):
+    """Dense M_sym with frequent faults (~9e4 bit flips per shot): the planner
+    does not build the fused kernel's tables (SP_FUSED_MAX_FLIPS); sp_sample
+    draws S and runs the explicit-S product (here the Four-Russians dense
+    variant, density 0.5) with the same records as the oracle on that S."""
+    model = CI.random_msym_model(300, 2000, 0.5, 0.3, seed=3)
+    s = gpu_sampler_factory(model)
+    assert not s.plan_info()["fused_ok"]
+    n = 5000
+    out = s.sample(n, 21)
+    S = s.draw_assignments(n, 21)
+    assert np.array_equal(host(out), port.sample(model.row_ptr, model.sym_idx, host(S), n))

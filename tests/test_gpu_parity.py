@@ -81,8 +81,10 @@ def test_product_on_supplied_batches_equals_reference(gpu_sampler_factory, golde
         assert np.array_equal(host(out), g[f"{i}.out"]), (variant, i)
 
 
-@pytest.mark.parametrize("variant", ["sparse", "dense"])
+@pytest.mark.parametrize("variant", ["sparse", "dense", "auto"])
 def test_product_random_vs_oracle(gpu_sampler_factory, port, variant):
+    """K2 on random M_sym / S vs the oracle: CSR walk, Four-Russians dense
+    product, and the density-based automatic choice (dense above ~0.17)."""
     rng = np.random.default_rng(5)
     s = gpu_sampler_factory()
     for n_m, n_s, n, dens in [(300, 500, 2048, 0.05), (1000, 3000, 100_000, 0.01),

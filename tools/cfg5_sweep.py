@@ -74,8 +74,6 @@ def main():
                               "bits_per_s": a.m * n / (ms / 1e3),
                               "alg_bytes": alg, "GBps": alg / (ms / 1e3) / 1e9,
                               "roofline_frac": alg / (ms / 1e3) / 1e9 / peak}), flush=True)
-        if dens >= 0.5:
-            continue
         for p in a.rates:
             s.load_groups(CI.bernoulli_groups(a.v, p))
             info = s.plan_info()
@@ -86,9 +84,12 @@ def main():
                                   "bits_per_s": a.m * n / (ms / 1e3),
                                   "GBps": out_bytes / (ms / 1e3) / 1e9,
                                   "roofline_frac": out_bytes / (ms / 1e3) / 1e9 / peak}), flush=True)
-            s.set_product("sparse")
+            s.set_product("auto")  # CSR walk, or Four-Russians above density ~0.17
             ms = timeit(lambda: (s.draw_assignments(n, 7, out=S), s.sample_given(S, n, out=out)))
-            print(json.dumps({**rec, "path": "draw + K2 sparse", "ms": ms,
+            print(json.dumps({**rec, "path": "draw + K2 auto", "ms": ms,
+                              "bits_per_s": a.m * n / (ms / 1e3)}), flush=True)
+            ms = timeit(lambda: s.sample(n, 7, out=out))  # what sp_sample picks
+            print(json.dumps({**rec, "path": "sp_sample", "ms": ms,
                               "bits_per_s": a.m * n / (ms / 1e3)}), flush=True)
         del s, out
         torch.cuda.empty_cache()
