@@ -73,7 +73,7 @@ typedef enum {
 typedef enum { SP_FMT_01 = 0, SP_FMT_B8 = 1 } sp_format; /* ShotFormat, sampler.hpp:60-63 */
 
 typedef enum {
-  SP_PRODUCT_AUTO = 0,
+  SP_PRODUCT_AUTO = 0,   /* DENSE when nnz(M_sym) > 0.17 n_meas n_sym (measured crossover), else SPARSE */
   SP_PRODUCT_SPARSE = 1, /* CSR over measurements (expression lists) */
   SP_PRODUCT_DENSE = 2   /* dense row-major M_sym words, Four-Russians tables */
 } sp_product;
@@ -176,10 +176,14 @@ int sp_encode_tiled(sp_ctx* ctx, const uint64_t* d_tiled, uint64_t n_shots, sp_f
 
 /* draw_assignments (sampler.hpp:51-52) on the device: the exact assignment
  * matrix S the fused sampler uses for these shots (row 0 = constant = all
- * ones), so sp_sample == M_sym . S bit for bit. The exception is a model
- * where the planner merged many channels with one common flip list into a
- * single variable (SP_MERGE_MIN): there S is an independent draw of every
- * original symbol, correct in distribution. d_S: [n_sym][ldS]. With
+ * ones), so sp_sample == M_sym . S bit for bit — also for thinned channels
+ * (a channel whose non-null patterns all flip one list fires as one
+ * Bernoulli variable; its firings map back to a uniform non-null pattern and
+ * its null patterns come from a second pass, so S keeps the channel's pmf).
+ * The exception is a model where the planner merged many channels with one
+ * common flip list into a single variable (SP_MERGE_MIN): there S is an
+ * independent draw of every original symbol, correct in distribution.
+ * d_S: [n_sym][ldS]. With
  * SP_RNG_COMPAT_SPLITMIX it is bit-identical to the reference's
  * draw_assignments(registry, n, seed) when shot_begin=0. */
 int sp_draw_assignments(sp_ctx* ctx, uint64_t seed, uint64_t shot_begin, uint64_t n_shots,
