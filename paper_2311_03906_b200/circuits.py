@@ -283,6 +283,49 @@ CFG5_DENSITIES = (0.001, 0.01, 0.5)
 CFG5_RATES = (1e-4, 1e-3, 1e-2)
 
 
+def gate_padding_pair(n: int = 32, rounds: int = 6, extra_gates: int = 100_000,
+                      seed: int = 0xC8) -> tuple[str, str]:
+    """The reference's acceptance criterion C8 workload (acceptance.cpp:437-533):
+    a noisy 32-qubit circuit (H on all, CX pairs q / q + n/2, X_ERROR(0.01),
+    DEPOLARIZE1(0.02), M all, six rounds), and the same circuit with
+    `extra_gates` gates inserted as adjacent self-inverse pairs (H H, CX CX,
+    S S_DAG), so every original instruction sees the same state and M_sym is
+    unchanged. Returns (base, padded) circuit texts."""
+    rng = MT19937_64(seed)
+    base = []
+    for _ in range(rounds):
+        base.append(_fmt("H", range(n)))
+        base.append(_fmt("CX", [t for q in range(n // 2) for t in (q, q + n // 2)]))
+        base.append(_fmt("X_ERROR", range(n), 0.01))
+        base.append(_fmt("DEPOLARIZE1", range(n), 0.02))
+        base.append(_fmt("M", range(n)))
+    padded, emitted = [], 0
+
+    def pair():
+        q = rng.below(n)
+        kind = rng.below(3)
+        if kind == 0:
+            padded.extend([f"H {q}", f"H {q}"])
+        elif kind == 1:
+            b = rng.below(n)
+            while b == q:
+                b = rng.below(n)
+            padded.extend([f"CX {q} {b}", f"CX {q} {b}"])
+        else:
+            padded.extend([f"S {q}", f"S_DAG {q}"])
+
+    per_slot = extra_gates // 2 // len(base)
+    for inst in base:
+        for _ in range(per_slot):
+            pair()
+            emitted += 1
+        padded.append(inst)
+    while 2 * emitted < extra_gates:
+        pair()
+        emitted += 1
+    return "\n".join(base) + "\n", "\n".join(padded) + "\n"
+
+
 def random_msym_rows(m: int, v: int, dens: float, seed: int = 7):
     """CSR rows (row_ptr u64 [m+1], sym_idx u32 ascending in [1, v])."""
     import numpy as np

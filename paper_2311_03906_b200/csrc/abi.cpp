@@ -744,7 +744,7 @@ void build_plan(sp_ctx* c) {
     for (size_t c = 0; c < live_cls.size(); ++c) {
       const uint64_t trials = live_cls[c].groups.size() * T;
       seg_lam[c] = trials * live_cls[c].p;
-      seg_S[c] = 32.0 * 8;
+      seg_S[c] = 32.0 * 4 * kWalkBlocks;
       seg_nmin[c] = std::max<uint64_t>(1, (trials + 4194303) / 4194304);
       seg_nmax[c] = std::max<uint64_t>(seg_nmin[c], trials / 32);
       uint64_t best = seg_nmin[c];

@@ -105,7 +105,7 @@ struct Segment {
 
 // Philox blocks each lane draws per walk step (independent counters, so the
 // two ten-round chains interleave), and the firings one step can yield.
-constexpr int kBlocks = 2;
+constexpr int kBlocks = kWalkBlocks;
 constexpr int kSlots = 4 * kBlocks;
 
 // Firings of one walk step on one lane (slot k valid iff v & (1<<k)).

@@ -7,6 +7,11 @@
 namespace symphase {
 
 // Random-stream domains (top byte of Philox counter word 3).
+#ifndef SP_KBLOCKS
+#define SP_KBLOCKS 2
+#endif
+// Philox blocks each lane draws per walk step (4 skip fields each).
+constexpr int kWalkBlocks = SP_KBLOCKS;
 constexpr uint32_t kDomChain = 1u;  // geometric-skip event chains
 constexpr uint32_t kDomCoin = 2u;   // bit-sliced fair-coin words
 constexpr uint32_t kDomThin = 3u;   // pattern choice of thinned groups (draw kernel)

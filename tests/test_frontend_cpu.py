@@ -103,3 +103,14 @@ def test_frontend_matches_live_reference_surface9(ref):
     c = ref.circuit(text)
     got = run_initialization(text)
     assert np.array_equal(got.row_ptr, c.row_ptr) and np.array_equal(got.sym_idx, c.sym_idx)
+
+
+def test_gate_padding_keeps_expressions(ref):
+    """Acceptance C8 (acceptance.cpp:437-533), first half: 100,000 extra gates
+    in self-inverse pairs leave M_sym and the registry unchanged — through
+    our front end, and equal to the reference library's own pass."""
+    base, padded = CI.gate_padding_pair()
+    ib, ip = run_initialization(base), run_initialization(padded)
+    assert _same(ib, ip)
+    c = ref.circuit(padded)
+    assert np.array_equal(ip.row_ptr, c.row_ptr) and np.array_equal(ip.sym_idx, c.sym_idx)
