@@ -105,6 +105,9 @@ struct sp_ctx {
   bool have_msym = false, have_groups = false, plan_ready = false, fused_ok = false;
   bool plan_built = false;  // dp/hp-derived buffers describe the model with plan_fp
   bool unfused = false;     // sp_sample draws S and runs the explicit-S product (faster here)
+  bool k5_ok = false;       // sp_sample / sp_draw_assignments use the K5 column sampler
+  K5Plan k5;
+  DBuf b_k5_cls, b_k5_groups, b_k5_sym, b_k5_cols, b_k5_rc;
   uint64_t plan_fp = 0;
   std::string fused_why;
   HostPlan hp;
@@ -270,6 +273,104 @@ void ensure_dense_words(HostPlan& h) {
   for (uint64_t k = 0; k < h.n_meas; ++k)
     for (uint64_t i = h.row_ptr[k]; i < h.row_ptr[k + 1]; ++i)
       h.dense_words[k * h.ldm + h.sym_idx[i] / 64] |= uint64_t{1} << (h.sym_idx[i] % 64);
+}
+
+// K5 column sampler plan (k5_columns.cu): for models the fused kernel does
+// not serve (too many flips per shot) whose firings x record words per shot
+// are far below the explicit product's work. Classes are built from the raw
+// group table (live first, then dead ones, which only the draw walks).
+void build_k5(sp_ctx* c, const std::vector<uint64_t>& col_ptr, const std::vector<uint32_t>& col_rows,
+              const std::vector<uint32_t>& ones, double events_per_shot, double flips_per_shot,
+              uint64_t n_dense_live) {
+  c->k5_ok = false;
+  const HostPlan& h = c->hp;
+  const long mode = env_long("SP_K5", -1);  // -1 auto, 0 never, 1 whenever eligible
+  if (mode == 0 || n_dense_live > 0 || h.n_meas == 0) return;
+  const uint64_t n_meas = h.n_meas, n_sym = h.n_sym, G = h.groups.size();
+  const uint32_t ncw = static_cast<uint32_t>(((n_meas + 31) / 32 + 3) & ~uint64_t{3});
+  int lg = -1;
+  for (int t = 7; t >= 5 && lg < 0; --t)
+    if (k5_smem_bytes(ncw, t, static_cast<uint32_t>(n_meas)) <= c->L.smem_optin) lg = t;
+  if (lg < 0) return;
+  // work per shot: firings x record words (K5) vs the explicit product's
+  // word operations per shot (CSR walk or Four-Russians lookups)
+  // (u32 words per shot: K5 XORs ncw words per firing; the CSR walk XORs nnz
+  // u64 words and the Four-Russians product n_meas * n_sym / 8 per 64 shots)
+  const double k5_work = events_per_shot * ncw;
+  const double k2_work = std::min(static_cast<double>(h.nnz),
+                                  static_cast<double>(n_meas) * ((n_sym + 7) / 8)) / 32.0;
+  if (mode < 0 && !(k5_work < 0.25 * k2_work)) return;
+  // vs the fused kernel, which pays per flipped bit: with exact flip lists
+  // (<= 16 entries) a flip costs about 0.35 K5 words (cfg3); on the
+  // table-walk path (long lists) about 6 (cfg5: K5 wins at 100 rows per
+  // column, K1 at 10, for 316-word records)
+  if (mode < 0 && c->fused_ok && !(k5_work < (c->dp.lp ? 0.35 : 6.0) * flips_per_shot)) return;
+  if (static_cast<double>(n_sym) * ncw * 4 > 8e9) return;  // columns must fit comfortably
+  struct KC { uint8_t dist; double p; std::vector<uint32_t> groups; };
+  std::vector<KC> live, dead;
+  std::map<std::pair<uint8_t, uint64_t>, size_t> lk, dk;
+  for (uint64_t g = 1; g < G; ++g) {
+    const sp_group& gr = h.groups[g];
+    const double p = gr.param;
+    const bool sparse = (gr.dist == SP_DIST_BERNOULLI && p > 0.0 && p < 1.0 && p != 0.5) ||
+                        ((gr.dist == SP_DIST_DEPOLARIZE1 || gr.dist == SP_DIST_DEPOLARIZE2) && p > 0.0);
+    if (!sparse) continue;
+    bool is_live = false;
+    for (uint32_t b = 0; b < gr.arity; ++b)
+      is_live |= col_ptr[gr.first_symbol + b + 1] > col_ptr[gr.first_symbol + b];
+    uint64_t pbits;
+    std::memcpy(&pbits, &p, 8);
+    auto& km = is_live ? lk : dk;
+    auto& v = is_live ? live : dead;
+    auto key = std::make_pair(gr.dist, pbits);
+    auto it = km.find(key);
+    // a walk covers <= 2^22 trials (the skip clamp): split larger classes
+    if (it == km.end() || v[it->second].groups.size() >= (1u << 22)) {
+      it = km.insert_or_assign(key, v.size()).first;
+      v.push_back(KC{gr.dist, std::min(p, 1.0), {}});
+    }
+    v[it->second].groups.push_back(static_cast<uint32_t>(g));
+  }
+  std::vector<ClassInfo> cls;
+  std::vector<uint32_t> cg;
+  for (auto* v : {&live, &dead})
+    for (const KC& k : *v) {
+      ClassInfo ci{};
+      ci.dist = k.dist;
+      ci.clg = static_cast<float>(0.69314718055994531 / std::log1p(-k.p));
+      ci.goff = static_cast<uint32_t>(cg.size());
+      ci.trials = k.groups.size();
+      ci.npat = k.dist == SP_DIST_DEPOLARIZE2 ? 15 : k.dist == SP_DIST_DEPOLARIZE1 ? 3 : 1;
+      cls.push_back(ci);
+      cg.insert(cg.end(), k.groups.begin(), k.groups.end());
+    }
+  // dense columns, and the rows that are one in every shot (s0, p >= 1)
+  std::vector<uint32_t> cols(static_cast<size_t>(n_sym) * ncw, 0), rc(ncw, 0);
+  for (uint64_t sidx = 0; sidx < n_sym; ++sidx)
+    for (uint64_t i = col_ptr[sidx]; i < col_ptr[sidx + 1]; ++i)
+      cols[sidx * ncw + col_rows[i] / 32] ^= 1u << (col_rows[i] % 32);
+  for (uint32_t sidx : ones)
+    for (uint32_t w = 0; w < ncw; ++w) rc[w] ^= cols[static_cast<size_t>(sidx) * ncw + w];
+  K5Plan& P = c->k5;
+  cudaStream_t s = c->stream;
+  P = K5Plan{};
+  P.n_meas = static_cast<uint32_t>(n_meas);
+  P.n_sym = static_cast<uint32_t>(n_sym);
+  P.ncw = ncw;
+  P.t_log2 = static_cast<uint32_t>(lg);
+  P.n_cls = static_cast<uint32_t>(cls.size());
+  P.n_cls_live = static_cast<uint32_t>(live.size());
+  if (cls.empty()) cls.push_back(ClassInfo{});
+  if (cg.empty()) cg.push_back(0);
+  P.cls = c->b_k5_cls.upload(cls, s);
+  P.cls_groups = c->b_k5_groups.upload(cg, s);
+  std::vector<uint32_t> csym(cg.size());
+  for (size_t i = 0; i < cg.size(); ++i) csym[i] = h.groups[cg[i]].first_symbol;
+  P.cls_sym = c->b_k5_sym.upload(csym, s);
+  P.cols = c->b_k5_cols.upload(cols, s);
+  P.row_const = c->b_k5_rc.upload(rc, s);
+  ck(cudaStreamSynchronize(s), "K5 plan upload");
+  c->k5_ok = true;
 }
 
 void build_plan(sp_ctx* c) {
@@ -1213,6 +1314,8 @@ void build_plan(sp_ctx* c) {
     tune_cache[fp] = {d.gen_warps, d.pad_pred | (c->unfused ? 2u : 0u)};
   }
   ptm.mark("autotune");
+  build_k5(c, col_ptr, col_rows, ones, events_per_shot, flips_per_shot, n_dense_live);
+  ptm.mark("k5");
   c->plan_ready = true;
 }
 
@@ -1539,6 +1642,10 @@ int sp_sample(sp_ctx* ctx, uint64_t seed, uint64_t shot_begin, uint64_t n_shots,
   if (shot_begin % T) return fail(SP_ERR_INVALID_ARGUMENT, "shot_begin must be a multiple of the shot tile");
   if (ctx->hp.n_meas == 0) return SP_OK;
   if (!d_out || ld < (n_shots + 63) / 64) return fail(SP_ERR_INVALID_ARGUMENT, "output too small");
+  if (ctx->k5_ok && ctx->rng == SP_RNG_PHILOX) {  // column sampler (dense M_sym)
+    const int r = launch_k5(ctx->k5, ctx->L, seed, shot_begin, n_shots, d_out, ld, d_counts);
+    return launched(ctx, r, "K5 column sampler launch");
+  }
   if (!ctx->fused_ok || (ctx->unfused && ctx->rng == SP_RNG_PHILOX)) {
     // Too many rows for an on-chip shot tile, or measured faster: the same
     // streams through the unfused path, draw S (device) then the explicit-S
@@ -1626,9 +1733,15 @@ int sp_draw_assignments(sp_ctx* ctx, uint64_t seed, uint64_t shot_begin, uint64_
   const uint64_t T = 1ull << ctx->dp.t_log2;
   if (shot_begin % T) return fail(SP_ERR_INVALID_ARGUMENT, "shot_begin must be a multiple of the shot tile");
   if (!d_S || ldS < (n_shots + 63) / 64) return fail(SP_ERR_INVALID_ARGUMENT, "output too small");
+  const bool k5 = ctx->k5_ok && ctx->rng == SP_RNG_PHILOX;
   int r = launch_draw(ctx->dp, ctx->L, ctx->rng == SP_RNG_COMPAT_SPLITMIX, seed, shot_begin / T,
-                      n_shots, d_S, ldS);
-  return launched(ctx, r, "draw launch");
+                      n_shots, d_S, ldS, !k5);
+  if (int e = launched(ctx, r, "draw launch")) return e;
+  if (k5) {  // the K5 streams: exactly the symbols the column sampler fires
+    r = launch_k5_draw(ctx->k5, ctx->L, seed, shot_begin, n_shots, d_S, ldS);
+    return launched(ctx, r, "K5 draw launch");
+  }
+  return SP_OK;
 }
 
 int sp_sample_given_S(sp_ctx* ctx, const uint64_t* d_S, uint64_t n_sym_S, uint64_t ldS,
@@ -1769,7 +1882,8 @@ int sp_plan_info(sp_ctx* ctx, uint64_t* out16) {
   const uint64_t v[16] = {1ull << d.t_log2, d.gen_warps, d.cta_threads, d.staged, d.row_staged,
                           d.lp, d.pad_pred, d.n_paths, d.n_rounds, d.n_keep, d.n_seg_live,
                           d.n_cls_live, d.n_dense_live, ctx->dnnz,
-                          fused_smem_bytes(d, d.t_log2, d.staged, d.row_staged, d.n_buf), ctx->fused_ok};
+                          fused_smem_bytes(d, d.t_log2, d.staged, d.row_staged, d.n_buf),
+                          ctx->k5_ok ? 2u : ctx->fused_ok ? 1u : 0u};
   std::memcpy(out16, v, sizeof(v));
   return SP_OK;
 }

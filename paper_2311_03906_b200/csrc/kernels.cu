@@ -559,7 +559,7 @@ int launch_fused_sample_compat(const DevPlan& P, const LaunchCfg& L, uint64_t se
 }
 
 int launch_draw(const DevPlan& P, const LaunchCfg& L, bool compat, uint64_t seed, uint64_t tile0,
-                uint64_t n_shots, uint64_t* S, uint64_t ldS) {
+                uint64_t n_shots, uint64_t* S, uint64_t ldS, bool segments) {
   int launches = 0;
   const uint64_t n_words = (n_shots + 63) / 64, n_words32 = (n_shots + 31) / 32;
   const uint64_t tail = (n_shots & 63) ? ((1ull << (n_shots & 63)) - 1) : ~0ull;
@@ -592,11 +592,11 @@ int launch_draw(const DevPlan& P, const LaunchCfg& L, bool compat, uint64_t seed
     }
     const uint64_t T = 1ull << P.t_log2;
     const uint32_t n_tiles = static_cast<uint32_t>((n_shots + T - 1) / T);
-    if (P.n_seg_all) {
+    if (P.n_seg_all && segments) {
       d_segments<<<grid, 256, 0, L.stream>>>(P, K, tile0, n_tiles, n_shots, S32, ld32, 0u);
       ++launches;
     }
-    if (P.n_seg_null) {  // null patterns of thinned groups, after every firing is in S
+    if (P.n_seg_null && segments) {  // null patterns of thinned groups, after every firing is in S
       d_segments<<<grid, 256, 0, L.stream>>>(P, K, tile0, n_tiles, n_shots, S32, ld32, 1u);
       ++launches;
     }

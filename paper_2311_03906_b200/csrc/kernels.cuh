@@ -138,6 +138,20 @@ struct DevPlan {
   const uint32_t* live_groups = nullptr;
 };
 
+// K5 column sampler (k5_columns.cu) for dense M_sym: shot-major records in
+// shared memory, each fired symbol's dense column XORed in by a warp.
+struct K5Plan {
+  uint32_t n_meas = 0, n_sym = 0;
+  uint32_t ncw = 0;        // u32 words per record / column (n_meas bits, padded to 4 words)
+  uint32_t t_log2 = 7;     // shots per CTA tile (32..128; not part of the streams)
+  uint32_t n_cls = 0, n_cls_live = 0;  // classes: live first (sampled), then dead (drawn only)
+  const ClassInfo* cls = nullptr;      // per class: trials = its groups, goff, dist, clg, npat
+  const uint32_t* cls_groups = nullptr;
+  const uint32_t* cls_sym = nullptr;    // class position -> first symbol of its group
+  const uint32_t* cols = nullptr;       // [n_sym][ncw] dense M_sym columns
+  const uint32_t* row_const = nullptr;  // [ncw] rows that are one in every shot
+};
+
 // Philox4x32-10 round keys for one seed (host-expanded, read from the
 // kernel-parameter bank).
 struct RoundKeys {
@@ -182,11 +196,19 @@ int launch_fused_sample_compat(const DevPlan& P, const LaunchCfg& L, uint64_t se
                                uint64_t tile0, uint64_t n_shots, uint64_t* out, uint64_t ld,
                                uint64_t* counts);
 // draw_assignments on device (same streams as the fused kernels).
+// segments = false: S rows of sparse channels are left zero (K5 draws them).
 int launch_draw(const DevPlan& P, const LaunchCfg& L, bool compat, uint64_t seed, uint64_t tile0,
-                uint64_t n_shots, uint64_t* S, uint64_t ldS);
+                uint64_t n_shots, uint64_t* S, uint64_t ldS, bool segments = true);
 // K2 explicit-S product: sparse (CSR rows) or dense (row-major words).
 int launch_product(const DevPlan& P, const LaunchCfg& L, bool dense, const uint64_t* S,
                    uint64_t ldS, uint64_t n_shots, uint64_t* out, uint64_t ld);
+// K5 column sampler (dense M_sym).
+size_t k5_smem_bytes(uint32_t ncw, uint32_t t_log2, uint32_t n_meas);
+int launch_k5(const K5Plan& P, const LaunchCfg& L, uint64_t seed, uint64_t shot_begin,
+              uint64_t n_shots, uint64_t* out, uint64_t ld, uint64_t* counts);
+// draw_assignments for the K5 streams (S must be zeroed, ones/coins filled).
+int launch_k5_draw(const K5Plan& P, const LaunchCfg& L, uint64_t seed, uint64_t shot_begin,
+                   uint64_t n_shots, uint64_t* S, uint64_t ldS);
 // K3 encode (fmt 0 = '01', 1 = 'b8').
 // tile_shots == 0: measurement-major input; else tiled blocks of tile_shots.
 int launch_encode(const LaunchCfg& L, const uint64_t* m, uint64_t ld, uint64_t n_meas,
