@@ -181,3 +181,25 @@ def test_merged_channels_rates_10M(gpu_sampler_factory):
             assert S.shape[0] == init.n_sym
         finally:
             del os.environ["SP_MERGE_MIN"]
+
+
+def test_coin_words_independent(gpu_sampler_factory):
+    """Fair coins (64 H-then-M qubits; Philox words per (symbol, 128-shot quad)) at 2^22 shots:
+    every coin, the agreement of neighbouring coins, of consecutive shots and
+    of shots across 128-shot quad boundaries are all 1/2 within 5 sigma."""
+    n_q, n = 64, 1 << 22
+    text = "H " + " ".join(map(str, range(n_q))) + "\nM " + " ".join(map(str, range(n_q))) + "\n"
+    init = run_initialization(text)
+    s = gpu_sampler_factory(init)
+    rec = host(s.sample(n, 2025))
+    bits = np.unpackbits(rec.view(np.uint8), axis=1, bitorder="little")[:, :n].astype(np.int8)
+
+    def half(hits, trials):
+        sd = np.sqrt(0.25 / trials)
+        return abs(hits / trials - 0.5) <= SIGMA * sd
+
+    assert all(half(int(bits[k].sum()), n) for k in range(n_q))
+    assert all(half(int((bits[k] == bits[k + 1]).sum()), n) for k in range(n_q - 1))
+    assert all(half(int((bits[k, :-1] == bits[k, 1:]).sum()), n - 1) for k in range(n_q))
+    b = bits[:, 127::128][:, :-1] == bits[:, 128::128]
+    assert half(int(b.sum()), b.size)
