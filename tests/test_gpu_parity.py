@@ -273,3 +273,37 @@ def test_reload_same_and_other_model(gpu_sampler_factory, port):
     assert np.array_equal(host(s.sample(nb, 5)), port.sample(b.row_ptr, b.sym_idx, host(S), nb))
     s.load(a)
     assert np.array_equal(host(s.sample(n, 5)), first)
+
+
+def test_tile_straddling_shot_counts(gpu_sampler_factory, port):
+    """Shot counts around word, tile and the reference's 512-shot tile sizes
+    (test_bit_matrix.cpp:328-349 uses 511/512/513/1024/1537): the compat
+    sampler equals the oracle's draw_assignments + sample, and the Philox
+    sampler equals the product of its own draws."""
+    init = run_initialization(CI.surface_code(3, 3, 0.02))
+    s = gpu_sampler_factory(init, rng="compat")
+    T = s.shot_tile
+    ns = sorted({1, 31, 32, 33, 63, 64, 65, 127, 128, 129, 511, 512, 513, 1024, 1537,
+                 T - 1, T, T + 1, 2 * T + 3})
+    for n in ns:
+        got = host(s.sample(n, 17))
+        S = port.draw_assignments(init, n, 17)
+        assert np.array_equal(got, port.sample(init.row_ptr, init.sym_idx, S, n)), n
+    s.set_rng("philox")
+    for n in ns:
+        out = s.sample(n, 17)
+        assert np.array_equal(host(out), host(s.sample_given(s.draw_assignments(n, 17), n))), n
+
+
+def test_no_measurements(gpu_sampler_factory):
+    """A circuit without measurements: empty records, '01' gives one empty
+    line per shot and 'b8' nothing (encode_shots, sampler.cpp:118-140)."""
+    init = run_initialization("H 0\nCX 0 1\nDEPOLARIZE1(0.1) 0\n")
+    assert init.n_meas == 0
+    s = gpu_sampler_factory(init)
+    out = s.sample(100, 1)
+    assert out.shape[0] == 0
+    assert s.encode(out, 100, "01", n_meas=0).cpu().numpy().tobytes() == b"\n" * 100
+    assert s.encode(out, 100, "b8", n_meas=0).numel() == 0
+    buf, w = s.sample_to_host(100, 1, "01")
+    assert bytes(buf[:w]) == b"\n" * 100
