@@ -26,6 +26,11 @@
 
 #include <algorithm>
 
+// column XORs flushed SP_K5Q at a time (their loads in flight together)
+#ifndef SP_K5Q
+#define SP_K5Q 4
+#endif
+
 namespace symphase {
 namespace {
 
@@ -94,28 +99,25 @@ k5_columns(const K5Plan P, const RoundKeys K, uint64_t shot_begin, uint64_t n_sh
 #pragma unroll
           for (int k = 0; k < kSlots; ++k)
             symk[k] = ((f.v >> k) & 1u) ? __ldg(P.cls_sym + sg.goff + f.g[k]) : 0u;
-          // pending column XOR: symbol (or ~0u for none)
-          uint32_t pend = ~0u;
-          auto flush = [&](uint32_t sym_a, uint32_t sym_b) {
-            // XOR up to two columns into the record; loads first
+          // pending column XORs (up to kQ symbols), flushed kQ at a time so
+          // kQ columns' loads are in flight together (the loads are the bound)
+          constexpr int kQ = SP_K5Q;
+          uint32_t pend[kQ];  // a shift register (static indices only)
+          int np = 0;
+          auto flush = [&](int cnt) {
             const uint32_t q = ncw / 4;
-            const uint4* ca = reinterpret_cast<const uint4*>(P.cols + static_cast<uint64_t>(sym_a) * ncw);
-            const uint4* cb = reinterpret_cast<const uint4*>(P.cols + static_cast<uint64_t>(sym_b) * ncw);
-            const bool hb = sym_b != ~0u;
-            for (uint32_t w4 = lane; w4 < q; w4 += 64) {
-              const bool two = w4 + 32 < q;
-              const uint4 a0 = __ldg(ca + w4);
-              const uint4 a1 = two ? __ldg(ca + w4 + 32) : make_uint4(0, 0, 0, 0);
-              const uint4 b0 = hb ? __ldg(cb + w4) : make_uint4(0, 0, 0, 0);
-              const uint4 b1 = hb && two ? __ldg(cb + w4 + 32) : make_uint4(0, 0, 0, 0);
-              uint4 r0 = r4[w4];
-              r0.x ^= a0.x ^ b0.x; r0.y ^= a0.y ^ b0.y; r0.z ^= a0.z ^ b0.z; r0.w ^= a0.w ^ b0.w;
-              r4[w4] = r0;
-              if (two) {
-                uint4 r1 = r4[w4 + 32];
-                r1.x ^= a1.x ^ b1.x; r1.y ^= a1.y ^ b1.y; r1.z ^= a1.z ^ b1.z; r1.w ^= a1.w ^ b1.w;
-                r4[w4 + 32] = r1;
+            for (uint32_t w4 = lane; w4 < q; w4 += 32) {
+              uint4 c[kQ];
+#pragma unroll
+              for (int t = 0; t < kQ; ++t)
+                c[t] = t < cnt ? __ldg(reinterpret_cast<const uint4*>(P.cols + static_cast<uint64_t>(pend[t]) * ncw) + w4)
+                               : make_uint4(0, 0, 0, 0);
+              uint4 r = r4[w4];
+#pragma unroll
+              for (int t = 0; t < kQ; ++t) {
+                r.x ^= c[t].x; r.y ^= c[t].y; r.z ^= c[t].z; r.w ^= c[t].w;
               }
+              r4[w4] = r;
             }
           };
 #pragma unroll
@@ -133,16 +135,19 @@ k5_columns(const K5Plan P, const RoundKeys K, uint64_t shot_begin, uint64_t n_sh
                     const uint64_t j = j0 + s;
                     atomicOr(&S32[sym * ld32 + (j >> 5)], 1u << (j & 31));
                   }
-                } else if (pend == ~0u) {
-                  pend = sym;
                 } else {
-                  flush(pend, sym);
-                  pend = ~0u;
+#pragma unroll
+                  for (int t = kQ - 1; t > 0; --t) pend[t] = pend[t - 1];
+                  pend[0] = sym;
+                  if (++np == kQ) {
+                    flush(kQ);
+                    np = 0;
+                  }
                 }
               }
             }
           }
-          if (!kDraw && pend != ~0u) flush(pend, ~0u);
+          if (!kDraw && np > 0) flush(np);
         });
       }
     }
