@@ -236,7 +236,11 @@ def run_ours(args):
     T = smp.shot_tile
     shots = (shots + T - 1) // T * T
     shot_begin = rank * shots  # disjoint global shot ranges, tile-aligned
-    tiled = args.layout == "tiled"
+    # auto: the tiled layout when a tile's rows are short (T < 1024: 16-128
+    # bytes per row per tile, scattered across measurement-major rows), like
+    # the reference's own 512 x 512 tiles; measurement-major otherwise
+    tiled = args.layout == "tiled" or (
+        args.layout == "auto" and T < 1024 and smp.plan_info()["fused_ok"] == 1)
     if tiled:  # [tile][row][T/64] records: contiguous stores for any row count
         out = torch.empty(smp.tiled_words(shots), dtype=torch.int64, device=dev)
     else:
@@ -413,9 +417,10 @@ def main():
     ap.add_argument("--records", default="measurements", choices=["measurements", "detectors"],
                     help="sample measurement records (the metric) or, for the surface-code "
                          "workloads, detector + observable records (D_sym = A . M_sym)")
-    ap.add_argument("--layout", default="mm", choices=["mm", "tiled"],
+    ap.add_argument("--layout", default="auto", choices=["auto", "mm", "tiled"],
                     help="record layout in HBM: measurement-major (the reference's SampleMatrix "
-                         "orientation) or tiled (sp_sample_tiled)")
+                         "orientation), tiled (sp_sample_tiled), or auto (tiled when the shot "
+                         "tile is under 1024 shots)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

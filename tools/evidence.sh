@@ -4,7 +4,7 @@
 tag=${1:-r}
 o=gpurun_out/ev_$tag; mkdir -p $o
 python bench.py > $o/bench_cfg2.json 2> $o/bench_cfg2.err
-python bench.py --config cfg3 --layout tiled --steps 3 --warmup 3 --no-cpu-baseline > $o/bench_cfg3.json 2> $o/bench_cfg3.err
+python bench.py --config cfg3 --steps 3 --warmup 3 --no-cpu-baseline > $o/bench_cfg3.json 2> $o/bench_cfg3.err
 python bench.py --config cfg1 --no-cpu-baseline > $o/bench_cfg1.json 2> $o/bench_cfg1.err
 python bench.py --config cfg4 --no-cpu-baseline > $o/bench_cfg4.json 2> $o/bench_cfg4.err
 python bench.py --impl reference --steps 3 --warmup 1 > $o/bench_ref_cfg2.json 2> $o/bench_ref_cfg2.err
