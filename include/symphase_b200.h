@@ -73,7 +73,7 @@ typedef enum {
 typedef enum { SP_FMT_01 = 0, SP_FMT_B8 = 1 } sp_format; /* ShotFormat, sampler.hpp:60-63 */
 
 typedef enum {
-  SP_PRODUCT_AUTO = 0,   /* DENSE when nnz(M_sym) > 0.17 n_meas n_sym (measured crossover), else SPARSE */
+  SP_PRODUCT_AUTO = 0,   /* DENSE when nnz(M_sym) > 0.15 n_meas n_sym (measured crossover), else SPARSE */
   SP_PRODUCT_SPARSE = 1, /* CSR over measurements (expression lists) */
   SP_PRODUCT_DENSE = 2   /* dense row-major M_sym words, Four-Russians tables */
 } sp_product;

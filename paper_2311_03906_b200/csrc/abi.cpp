@@ -113,14 +113,14 @@ struct sp_ctx {
   HostPlan hp;
   DevPlan dp;
   // plan buffers
-  DBuf b_row_ptr, b_sym_idx, b_col_ptr, b_col_rows, b_dense, b_first, b_arity, b_dist, b_param,
+  DBuf b_row_ptr, b_sym_idx, b_col_ptr, b_col_rows, b_dense, b_dense_gm, b_first, b_arity, b_dist, b_param,
       b_row_const_compat, b_ones, b_dense_sym, b_coin_ptr, b_coin_rows, b_cls, b_cls_groups, b_thin_src, b_g_masks,
       b_desc, b_colrow, b_live_groups, b_path_rows, b_path_ptr, b_path_par, b_round_ptr, b_plist, b_keep_rows, b_timers;
   uint64_t dnnz = 0;  // nnz of D (chain transform), for reports
   // K2's own copy of the rows (independent of the group table)
   bool prod_ready = false;
   DevPlan pp;
-  DBuf p_row_ptr, p_sym_idx, p_dense;
+  DBuf p_row_ptr, p_sym_idx, p_dense, p_dense_gm;
   // sp_sample_to_host: double-buffered records/bytes, a copy stream and the
   // events that hand each buffer between the compute and copy streams
   DBuf s_out[2], s_bytes[2];
@@ -257,8 +257,8 @@ struct PlanTimer {
 
 // K2 variant: the Four-Russians dense product costs the same at any density
 // (n_meas x words x n_sym / 8 table lookups); the CSR walk costs nnz x words.
-// Measured on B200 at cfg5's shape the two cross at density ~0.17.
-constexpr double kDenseProductDensity = 0.17;
+// Measured on B200 at cfg5's shape the two cross at density ~0.15.
+constexpr double kDenseProductDensity = 0.15;
 bool dense_product(const sp_ctx* c) {
   if (c->product == SP_PRODUCT_DENSE) return true;
   if (c->product != SP_PRODUCT_AUTO) return false;
@@ -371,6 +371,18 @@ void build_k5(sp_ctx* c, const std::vector<uint64_t>& col_ptr, const std::vector
   P.row_const = c->b_k5_rc.upload(rc, s);
   ck(cudaStreamSynchronize(s), "K5 plan upload");
   c->k5_ok = true;
+}
+
+// Group-major bytes of the dense words (k2_m4rm): byte g of row k at
+// [g * ld + k], ld = n_meas rounded up to 16.
+std::vector<uint8_t> group_major_bytes(const HostPlan& h, uint64_t* ld) {
+  const uint64_t n_g = (h.n_sym + 7) / 8;
+  *ld = (h.n_meas + 15) & ~uint64_t{15};
+  std::vector<uint8_t> gm(std::max<uint64_t>(n_g * *ld, 1), 0);
+  for (uint64_t k = 0; k < h.n_meas; ++k)
+    for (uint64_t g = 0; g < n_g; ++g)
+      gm[g * *ld + k] = static_cast<uint8_t>(h.dense_words[k * h.ldm + g / 8] >> (8 * (g % 8)));
+  return gm;
 }
 
 void build_plan(sp_ctx* c) {
@@ -1020,6 +1032,9 @@ void build_plan(sp_ctx* c) {
   if (!h.dense_words.empty()) {
     d.dense = c->b_dense.upload(h.dense_words, s);
     d.ldm = h.ldm;
+    const std::vector<uint8_t> gm = group_major_bytes(h, &d.gm_ld);
+    d.dense_gm = c->b_dense_gm.upload(gm, s);
+    ck(cudaStreamSynchronize(s), "dense upload");
   }
   d.g_first = c->b_first.upload(g_first, s);
   d.g_arity = c->b_arity.upload(g_arity, s);
@@ -1771,6 +1786,9 @@ int sp_sample_given_S(sp_ctx* ctx, const uint64_t* d_S, uint64_t n_sym_S, uint64
       if (!ctx->hp.dense_words.empty()) {
         ctx->pp.dense = ctx->p_dense.upload(ctx->hp.dense_words, ctx->stream);
         ctx->pp.ldm = ctx->hp.ldm;
+        const std::vector<uint8_t> gm = group_major_bytes(ctx->hp, &ctx->pp.gm_ld);
+        ctx->pp.dense_gm = ctx->p_dense_gm.upload(gm, ctx->stream);
+        ck(cudaStreamSynchronize(ctx->stream), "dense upload");
       }
       ctx->prod_ready = true;
     } catch (const CudaError& e) {

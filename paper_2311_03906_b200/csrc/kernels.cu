@@ -244,66 +244,74 @@ k2_sparse(const uint64_t* __restrict__ row_ptr, const uint32_t* __restrict__ sym
 }
 
 // Dense variant: Method of Four Russians over shared-memory tables. A CTA
-// owns 512 measurement rows x 32 shot words (lane = word, 32 rows per warp,
-// accumulators in registers). Symbols are taken 8 at a time: for group g the
-// CTA builds T_g[b][w] = XOR of S[8g + i][w] over the set bits i of b (256
-// entries, Gray-code order, one XOR each), then every row XORs in
-// T_g[byte g of its M_sym row] — one 8-byte shared load per row, group and
-// word instead of up to eight global S loads. S rows and M bytes are staged
-// 16 groups at a time with cp.async (double-buffered); two tables alternate,
-// so one barrier per group separates building T_g from reading it.
-// Work is n_meas x words x ceil(n_sym / 8) table lookups whatever the
-// density, so it wins over the CSR walk for dense M_sym (abi.cpp picks it).
-constexpr int kM4Rows = 512, kM4Words = 32, kM4Chunk = 16;
+// owns 512 measurement rows x 2048 shots (32 u64 words: lane = word, 32 row
+// accumulators per thread in registers). Symbols are taken 8 at a time: for
+// group g the CTA builds T_g[b][w] = XOR of S[8g + i][w] over the set bits i
+// of b (256 entries, Gray-code order, one XOR each), then every row XORs in
+// T_g[byte g of its M_sym row]. The row bytes come group-major (one 4-byte
+// shared broadcast serves four rows), S rows and bytes are staged 16 groups
+// at a time with cp.async (double-buffered), and two tables alternate, so
+// one barrier per group separates building T_g from reading it. Work is
+// n_meas x words x ceil(n_sym / 8) lookups whatever the density, so it wins
+// over the CSR walk for dense M_sym (abi.cpp picks it).
+constexpr int kM4Rows = 512, kM4Words = 32, kM4Chunk = 16, kM4Threads = 512;
+constexpr int kM4RowsPerWarp = kM4Rows / (kM4Threads / 32);  // 32
 constexpr size_t kM4Smem = (2ull * 256 * kM4Words + 2ull * kM4Chunk * 8 * kM4Words) * 8 +
-                           2ull * kM4Rows * kM4Chunk;
+                           2ull * kM4Chunk * kM4Rows;
 
 __device__ __forceinline__ void cp_async8(uint32_t dst, const void* src, bool valid) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst), "l"(src),
                "r"(valid ? 8 : 0)
                : "memory");
 }
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
+               "r"(valid ? 16 : 0)
+               : "memory");
+}
 
-__global__ void __launch_bounds__(kM4Rows, 1)
-k2_m4rm(const uint64_t* __restrict__ M, uint64_t ldm, uint32_t n_meas, uint32_t n_sym,
+__global__ void __launch_bounds__(kM4Threads, 1)
+k2_m4rm(const uint8_t* __restrict__ Mg, uint64_t gm_ld, uint32_t n_meas, uint32_t n_sym,
         const uint64_t* __restrict__ S, uint64_t ldS, uint64_t n_words, uint64_t tail,
         uint64_t* __restrict__ out, uint64_t ld) {
   extern __shared__ __align__(16) uint8_t smem[];
-  uint64_t* tab = reinterpret_cast<uint64_t*>(smem);             // [2][256][32]
-  uint64_t* ss = tab + 2 * 256 * kM4Words;                         // [2][128][32]
-  uint8_t* mb = reinterpret_cast<uint8_t*>(ss + 2 * kM4Chunk * 8 * kM4Words);  // [2][512][16]
+  uint64_t* tab = reinterpret_cast<uint64_t*>(smem);                   // [2][256][32]
+  uint64_t* ss = tab + 2 * 256 * kM4Words;                              // [2][128][32]
+  uint8_t* mb = reinterpret_cast<uint8_t*>(ss + 2 * kM4Chunk * 8 * kM4Words);  // [2][16][512]
   const uint32_t t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const uint32_t r0 = blockIdx.y * kM4Rows;
   const uint64_t w0 = static_cast<uint64_t>(blockIdx.x) * kM4Words;
   const uint32_t n_g = (n_sym + 7) / 8;
   const uint32_t n_chunks = (n_g + kM4Chunk - 1) / kM4Chunk;
   // Stage chunk c (groups 16c .. 16c+15) into buffer c & 1: S rows
-  // [128c, 128c+128) x words [w0, w0+32), and bytes [16c, 16c+16) of each of
-  // the CTA's M rows (u64 words 2c, 2c+1). Out-of-range parts read as zero.
+  // [128c, 128c+128) x words [w0, w0+32), and the bytes of those groups for
+  // the CTA's 512 rows. Out-of-range parts read as zero.
   auto stage = [&](uint32_t c) {
     const uint32_t buf = c & 1;
-    const uint32_t ss_s = static_cast<uint32_t>(__cvta_generic_to_shared(ss + buf * kM4Chunk * 8 * kM4Words));
+    const uint32_t ss_s =
+        static_cast<uint32_t>(__cvta_generic_to_shared(ss + buf * kM4Chunk * 8 * kM4Words));
 #pragma unroll
-    for (int i = 0; i < (kM4Chunk * 8 * kM4Words) / kM4Rows; ++i) {
-      const uint32_t e = t + i * kM4Rows;  // (row in chunk, word)
+    for (int i = 0; i < (kM4Chunk * 8 * kM4Words) / kM4Threads; ++i) {
+      const uint32_t e = t + i * kM4Threads;  // (row in chunk, word)
       const uint64_t j = static_cast<uint64_t>(c) * kM4Chunk * 8 + (e >> 5);
       const uint64_t w = w0 + (e & 31);
       const bool ok = j < n_sym && w < n_words;
       cp_async8(ss_s + e * 8, ok ? S + j * ldS + w : S, ok);
     }
-    const uint32_t mb_s = static_cast<uint32_t>(__cvta_generic_to_shared(mb + buf * kM4Rows * kM4Chunk));
-    const uint32_t k = r0 + t;
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const uint64_t mw = 2ull * c + h;
-      const bool ok = k < n_meas && mw < ldm;
-      cp_async8(mb_s + t * kM4Chunk + 8 * h, ok ? M + static_cast<uint64_t>(k) * ldm + mw : M, ok);
+    const uint32_t mb_s =
+        static_cast<uint32_t>(__cvta_generic_to_shared(mb + buf * kM4Chunk * kM4Rows));
+    {
+      const uint32_t e = t;  // 16-byte piece: (group in chunk, 16 rows)
+      const uint32_t gi = e / (kM4Rows / 16), rr = (e % (kM4Rows / 16)) * 16;
+      const uint64_t g = static_cast<uint64_t>(c) * kM4Chunk + gi;
+      const bool ok = g < n_g && r0 + rr < gm_ld;
+      cp_async16(mb_s + e * 16, ok ? Mg + g * gm_ld + r0 + rr : Mg, ok);
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
-  uint64_t acc[32];
+  uint64_t acc[kM4RowsPerWarp];
 #pragma unroll
-  for (int r = 0; r < 32; ++r) acc[r] = 0;
+  for (int r = 0; r < kM4RowsPerWarp; ++r) acc[r] = 0;
   stage(0);
   // Phase g: rows look up group g-1, the CTA builds the table of group g.
   for (uint32_t g = 0; g <= n_g; ++g) {
@@ -316,10 +324,15 @@ k2_m4rm(const uint64_t* __restrict__ M, uint64_t ldm, uint32_t n_meas, uint32_t 
     if (g > 0) {
       const uint32_t gp = g - 1;
       const uint64_t* T = tab + (gp & 1) * 256 * kM4Words + lane;
-      const uint8_t* mrow = mb + ((gp / kM4Chunk) & 1) * kM4Rows * kM4Chunk + (warp * 32) * kM4Chunk +
-                            (gp % kM4Chunk);
+      const uint32_t* bytes4 = reinterpret_cast<const uint32_t*>(
+          mb + ((gp / kM4Chunk) & 1) * kM4Chunk * kM4Rows + (gp % kM4Chunk) * kM4Rows +
+          warp * kM4RowsPerWarp);
 #pragma unroll
-      for (int r = 0; r < 32; ++r) acc[r] ^= T[static_cast<uint32_t>(mrow[r * kM4Chunk]) * kM4Words];
+      for (int q = 0; q < kM4RowsPerWarp / 4; ++q) {
+        const uint32_t v = bytes4[q];  // rows 4q .. 4q+3 of this warp (broadcast)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) acc[4 * q + r] ^= T[((v >> (8 * r)) & 0xFFu) * kM4Words];
+      }
     }
     if (g < n_g) {
       // entries b = 16h + l for this thread's word w and high nibble h:
@@ -345,8 +358,8 @@ k2_m4rm(const uint64_t* __restrict__ M, uint64_t ldm, uint32_t n_meas, uint32_t 
   const uint64_t w = w0 + lane;
   if (w < n_words) {
 #pragma unroll
-    for (int r = 0; r < 32; ++r) {
-      const uint32_t k = r0 + warp * 32 + r;
+    for (int r = 0; r < kM4RowsPerWarp; ++r) {
+      const uint32_t k = r0 + warp * kM4RowsPerWarp + r;
       if (k < n_meas) out[static_cast<uint64_t>(k) * ld + w] = (w == n_words - 1) ? (acc[r] & tail) : acc[r];
     }
   }
@@ -620,11 +633,13 @@ int launch_product(const DevPlan& P, const LaunchCfg& L, bool dense, const uint6
         return -1;
       attr = true;
     }
+    if (!P.dense_gm) return -1;
     const uint64_t row_blocks = (P.n_meas + kM4Rows - 1) / kM4Rows;
-    if (row_blocks > 65535) return -1;
-    dim3 g4(static_cast<unsigned>((n_words + kM4Words - 1) / kM4Words), static_cast<unsigned>(row_blocks));
-    k2_m4rm<<<g4, kM4Rows, kM4Smem, L.stream>>>(P.dense, P.ldm, P.n_meas, P.n_sym, S, ldS, n_words,
-                                                tail, out, ld);
+    const uint64_t slabs = (n_words + kM4Words - 1) / kM4Words;
+    if (row_blocks > 65535 || slabs > 0x7FFFFFFFull) return -1;
+    dim3 g4(static_cast<unsigned>(slabs), static_cast<unsigned>(row_blocks));
+    k2_m4rm<<<g4, kM4Threads, kM4Smem, L.stream>>>(P.dense_gm, P.gm_ld, P.n_meas, P.n_sym, S, ldS,
+                                                   n_words, tail, out, ld);
   } else {
     k2_sparse<<<grid, kK2Rows * 32, 0, L.stream>>>(P.row_ptr, P.sym_idx, P.n_meas, S, ldS,
                                                    n_words, tail, out, ld);

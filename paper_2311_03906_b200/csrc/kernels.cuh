@@ -46,6 +46,10 @@ struct DevPlan {
   // dense row-major M_sym words [n_meas][ldm] (only when requested)
   const uint64_t* dense = nullptr;
   uint64_t ldm = 0;
+  // the same bits group-major for the Four-Russians product: byte g of row k
+  // (symbols 8g .. 8g+7) at dense_gm[g * gm_ld + k], gm_ld = n_meas padded to 16
+  const uint8_t* dense_gm = nullptr;
+  uint64_t gm_ld = 0;
 
   // Group table (symbols.hpp:36-42).
   const uint32_t* g_first = nullptr;
