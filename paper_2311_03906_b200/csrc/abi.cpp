@@ -825,7 +825,7 @@ void build_plan(sp_ctx* c) {
   // Segments: each class's flattened (group, shot) space of a tile is cut
   // into slices (<= 2^22 trials, >= 32), one warp walk each. A walk over a
   // slice holding N firings takes floor(N / S) + 1 steps of S slots (S =
-  // 32 lanes x 8 skips), so the slice count per class
+  // 32 lanes x 4 skips per Philox block), so the slice count per class
   // minimises expected steps + a fixed per-slice cost (init, first Philox
   // latency), subject to enough slices per tile to keep every generator warp
   // busy with two tiles in flight. SP_SEG_EVENTS=E forces ~E firings/slice.

@@ -94,7 +94,7 @@ __device__ __forceinline__ uint32_t group_bits_compat(uint32_t dist, double p, u
 // -> X, Z, Y; n = 15 for DEPOLARIZE2): the joint channel pmf of fill_group
 // (sampler.cpp:24-42). Geometric gaps floor(Exp/-ln(1-p)) + 1 are laid
 // end to end in lane order with a warp prefix sum, so one step yields up to
-// 256 firing positions with no divergence. Streams are keyed by
+// 32 x kSlots firing positions with no divergence. Streams are keyed by
 // (segment, global tile), independent of which warp, CTA or GPU runs them.
 struct Segment {
   uint32_t g0, s0;  // first trial = (class position g0, shot s0 in the tile)

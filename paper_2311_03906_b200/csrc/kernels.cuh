@@ -8,7 +8,7 @@ namespace symphase {
 
 // Random-stream domains (top byte of Philox counter word 3).
 #ifndef SP_KBLOCKS
-#define SP_KBLOCKS 2
+#define SP_KBLOCKS 1
 #endif
 // Philox blocks each lane draws per walk step (4 skip fields each).
 constexpr int kWalkBlocks = SP_KBLOCKS;
@@ -171,7 +171,10 @@ struct LaunchCfg {
 
 // 16 warps per CTA, one CTA per SM (a 32-warp variant with 64 registers per
 // thread measured slower on both cfg2 and cfg3).
-constexpr int kFusedThreads = 512;
+#ifndef SP_FUSED_THREADS
+#define SP_FUSED_THREADS 512
+#endif
+constexpr int kFusedThreads = SP_FUSED_THREADS;
 
 // Words of the fused kernel's spare tile region (after the n_meas rows):
 // padded flip-list entries point into it, spread over 32 banks (u32 lists:
