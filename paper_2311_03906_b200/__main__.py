@@ -5,6 +5,7 @@
         [--format 01|b8] [--out FILE] [--rng philox|compat] [--dump-assignments FILE]
         [--detectors FILE]
     python -m paper_2311_03906_b200 analyze --in c.stim [--out FILE]
+    python -m paper_2311_03906_b200 bench [--n N ...] [--family a|b|c|all] [--shots N]
 
 `sample` writes the records exactly as the reference encodes them
 (sampler.cpp:118-140) and prints the reference's timing line
@@ -87,6 +88,34 @@ def cmd_analyze(a) -> int:
     return 0
 
 
+def cmd_bench(a) -> int:
+    """cmd_bench (cliffsym.cpp:243-278): the Fig. 3 families at each size,
+    CSV `family,n,init_seconds,sampling_seconds,shots`; the sampling time
+    covers draw + sample with the records left on the device, as in the
+    reference (whose timed region ends before encoding)."""
+    import torch
+
+    from . import Sampler, circuits, run_initialization
+    fams = ["a", "b", "c"] if a.family in ("all",) else [a.family]
+    print("family,n,init_seconds,sampling_seconds,shots")
+    for f in fams:
+        for n in a.sizes:
+            text = circuits.bench_family(f, n, a.seed)
+            t0 = time.perf_counter()
+            init = run_initialization(text)
+            init_s = time.perf_counter() - t0
+            smp = Sampler(init, device=a.device)
+            smp.sample(min(a.shots, 4096), a.seed)  # plan build + autotune, outside the timing
+            torch.cuda.synchronize(a.device)
+            t1 = time.perf_counter()
+            smp.sample(a.shots, a.seed)
+            torch.cuda.synchronize(a.device)
+            sampling_s = time.perf_counter() - t1
+            print(f"{circuits.BENCH_FAMILIES[f]},{n},{init_s:.6f},{sampling_s:.6f},{a.shots}",
+                  flush=True)
+    return 0
+
+
 def main(argv=None) -> int:
     ap = argparse.ArgumentParser(prog="python -m paper_2311_03906_b200",
                                  description="B200 stabilizer-circuit sampler (SymPhase)")
@@ -103,6 +132,14 @@ def main(argv=None) -> int:
     s.add_argument("--detectors", help="file with one detector per line (measurement ids, "
                                        "0-based); records are detector outcomes instead")
     s.add_argument("--threads", type=int, default=1, help="accepted for compatibility; unused")
+    b = sub.add_parser("bench", help="time the Fig. 3 circuit families (CSV)")
+    b.add_argument("--n", "--sizes", dest="sizes", type=int, nargs="+", default=[100],
+                   help="qubit counts to run")
+    b.add_argument("--family", choices=["a", "b", "c", "all"], default="all")
+    b.add_argument("--shots", type=int, default=1000)
+    b.add_argument("--seed", type=int, default=0)
+    b.add_argument("--device", type=int, default=0)
+    b.add_argument("--threads", type=int, default=1, help="accepted for compatibility; unused")
     an = sub.add_parser("analyze", help="print measurement outcomes as symbol expressions")
     an.add_argument("--in", dest="input")
     an.add_argument("--out")
@@ -117,6 +154,8 @@ def main(argv=None) -> int:
                 print("error: --shots must be positive", file=sys.stderr)
                 return 1
             return cmd_sample(a)
+        if a.cmd == "bench":
+            return cmd_bench(a)
         return cmd_analyze(a)
     except LogicError as e:
         print(f"internal error: {e}", file=sys.stderr)

@@ -283,6 +283,50 @@ CFG5_DENSITIES = (0.001, 0.01, 0.5)
 CFG5_RATES = (1e-4, 1e-3, 1e-2)
 
 
+BENCH_FAMILIES = {"a": "sparse_cnot", "b": "dense_cnot", "c": "dense_cnot_depolarize"}
+
+
+def bench_family(family: str, n: int, seed: int = 0, noise_p: float = 1e-3) -> str:
+    """The paper's Fig. 3 scaling families as `cliffsym bench` builds them
+    (circuit_gen.cpp:19-66): n qubits, n layers; each layer applies H or S or
+    nothing to every qubit (1/3 each), CX on 5 random pairs (sparse_cnot) or
+    on a random perfect matching of all qubits (dense_cnot*), DEPOLARIZE1(p)
+    on every qubit (dense_cnot_depolarize), and Z-measures max(1, n/20)
+    random qubits; all qubits are measured at the end. Seeded with our own
+    MT19937-64 and Fisher-Yates shuffles (same structure and distributions,
+    not the reference's exact gate list)."""
+    name = BENCH_FAMILIES.get(family, family)
+    rng = MT19937_64(seed)
+    qubits = list(range(n))
+
+    def shuffle():
+        for i in range(n - 1, 0, -1):
+            j = rng.below(i + 1)
+            qubits[i], qubits[j] = qubits[j], qubits[i]
+
+    pairs = min(5, n // 2) if name == "sparse_cnot" else n // 2
+    per_layer = max(1, n // 20)
+    lines = []
+    for _ in range(n):
+        h, s = [], []
+        for q in range(n):
+            r = rng.below(3)
+            (h if r == 0 else s if r == 1 else []).append(q)
+        if h:
+            lines.append(_fmt("H", h))
+        if s:
+            lines.append(_fmt("S", s))
+        shuffle()
+        if pairs:
+            lines.append(_fmt("CX", qubits[: 2 * pairs]))
+        if name == "dense_cnot_depolarize":
+            lines.append(_fmt("DEPOLARIZE1", range(n), noise_p))
+        shuffle()
+        lines.append(_fmt("M", sorted(qubits[:per_layer])))
+    lines.append(_fmt("M", range(n)))
+    return "\n".join(lines) + "\n"
+
+
 def gate_padding_pair(n: int = 32, rounds: int = 6, extra_gates: int = 100_000,
                       seed: int = 0xC8) -> tuple[str, str]:
     """The reference's acceptance criterion C8 workload (acceptance.cpp:437-533):

@@ -114,3 +114,16 @@ def test_gate_padding_keeps_expressions(ref):
     assert _same(ib, ip)
     c = ref.circuit(padded)
     assert np.array_equal(ip.row_ptr, c.row_ptr) and np.array_equal(ip.sym_idx, c.sym_idx)
+
+
+def test_bench_families_shape(ref):
+    """The Fig. 3 families (circuit_gen.cpp:19-66): n layers of single-qubit
+    gates, CX pairs, optional DEPOLARIZE1, max(1, n/20) measurements per layer
+    and n at the end; our front end agrees with the reference library."""
+    for fam, n in (("a", 40), ("b", 60), ("c", 30)):
+        text = CI.bench_family(fam, n, seed=3)
+        init = run_initialization(text)
+        assert init.n_meas == n * max(1, n // 20) + n
+        c = ref.circuit(text)
+        assert np.array_equal(init.row_ptr, c.row_ptr) and np.array_equal(init.sym_idx, c.sym_idx)
+    assert "DEPOLARIZE1" in CI.bench_family("c", 20) and "DEPOLARIZE1" not in CI.bench_family("b", 20)

@@ -87,3 +87,17 @@ def test_sample_detectors_file(tmp_path):
     for a, b in zip(ml, dl):
         x = [int(c) for c in a]
         assert b == f"{x[0] ^ x[1]}{x[1] ^ x[2]}{x[0] ^ x[1] ^ x[2]}{x[2]}"
+
+
+def test_bench_csv():
+    """cmd_bench (cliffsym.cpp:243-278): CSV header and one row per family
+    and size, in the reference's column order."""
+    r = run_cli(["bench", "--n", "40", "60", "--family", "all", "--shots", "5000"])
+    assert r.returncode == 0, r.stderr
+    lines = r.stdout.decode().splitlines()
+    assert lines[0] == "family,n,init_seconds,sampling_seconds,shots"
+    rows = [line.split(",") for line in lines[1:]]
+    assert [(f, n) for f, n, *_ in rows] == [(f, n) for f in ("sparse_cnot", "dense_cnot",
+                                                                "dense_cnot_depolarize")
+                                             for n in ("40", "60")]
+    assert all(float(r_[2]) >= 0 and float(r_[3]) > 0 and r_[4] == "5000" for r_ in rows)
