@@ -120,7 +120,7 @@ struct sp_ctx {
   // K2's own copy of the rows (independent of the group table)
   bool prod_ready = false;
   DevPlan pp;
-  DBuf p_row_ptr, p_sym_idx, p_dense, p_dense_gm;
+  DBuf p_row_ptr, p_sym_idx, p_dense, p_dense_gm, p_seg_ptr, p_seg_row, p_split_rows;
   // sp_sample_to_host: double-buffered records/bytes, a copy stream and the
   // events that hand each buffer between the compute and copy streams
   DBuf s_out[2], s_bytes[2];
@@ -1783,6 +1783,29 @@ int sp_sample_given_S(sp_ctx* ctx, const uint64_t* d_S, uint64_t n_sym_S, uint64
       ctx->pp.n_sym = static_cast<uint32_t>(ctx->hp.n_sym);
       ctx->pp.row_ptr = ctx->p_row_ptr.upload(ctx->hp.row_ptr, ctx->stream);
       ctx->pp.sym_idx = ctx->p_sym_idx.upload(ctx->hp.sym_idx, ctx->stream);
+      {
+        // segment work list: rows cut into pieces of <= kSegLen symbols
+        const uint64_t kSegLen = static_cast<uint64_t>(env_long("SP_K2_SEG", 1024));
+        std::vector<uint64_t> sp{0};
+        std::vector<uint32_t> sr, split;
+        for (uint64_t k = 0; k < ctx->hp.n_meas; ++k) {
+          const uint64_t b = ctx->hp.row_ptr[k], e = ctx->hp.row_ptr[k + 1];
+          const uint64_t pieces = e - b > kSegLen ? (e - b + kSegLen - 1) / kSegLen : 1;
+          if (pieces > 1) split.push_back(static_cast<uint32_t>(k));
+          for (uint64_t q = 0; q < pieces; ++q) {
+            sp.push_back(pieces > 1 ? std::min(e, b + (q + 1) * kSegLen) : e);
+            sr.push_back(static_cast<uint32_t>(k) | (pieces > 1 ? 0x80000000u : 0u));
+          }
+        }
+        if (!split.empty()) {  // only worth a work list when some row is cut
+          ctx->pp.k2_seg_ptr = ctx->p_seg_ptr.upload(sp, ctx->stream);
+          ctx->pp.k2_seg_row = ctx->p_seg_row.upload(sr, ctx->stream);
+          ctx->pp.k2_split_rows = ctx->p_split_rows.upload(split, ctx->stream);
+          ctx->pp.n_k2_seg = static_cast<uint32_t>(sr.size());
+          ctx->pp.n_k2_split = static_cast<uint32_t>(split.size());
+          ck(cudaStreamSynchronize(ctx->stream), "segment upload");
+        }
+      }
       if (!ctx->hp.dense_words.empty()) {
         ctx->pp.dense = ctx->p_dense.upload(ctx->hp.dense_words, ctx->stream);
         ctx->pp.ldm = ctx->hp.ldm;

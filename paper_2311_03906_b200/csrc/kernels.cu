@@ -243,6 +243,60 @@ k2_sparse(const uint64_t* __restrict__ row_ptr, const uint32_t* __restrict__ sym
   }
 }
 
+// CSR variant over a segment work list (long rows cut, see DevPlan): one
+// warp per segment; a cut row's segments XOR their partial words into the
+// (zeroed) output with 64-bit atomics.
+__global__ void __launch_bounds__(kK2Rows * 32)
+k2_sparse_seg(const uint64_t* __restrict__ seg_ptr, const uint32_t* __restrict__ seg_row,
+              uint32_t n_seg, const uint32_t* __restrict__ sym_idx, const uint64_t* __restrict__ S,
+              uint64_t ldS, uint64_t n_words, uint64_t tail, uint64_t* __restrict__ out,
+              uint64_t ld) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t sgi = blockIdx.x * kK2Rows + (threadIdx.x >> 5);
+  if (sgi >= n_seg) return;
+  const uint32_t rw = seg_row[sgi];
+  const uint32_t k = rw & 0x7FFFFFFFu;
+  const bool split = (rw >> 31) != 0;
+  const uint64_t b = seg_ptr[sgi], e = seg_ptr[sgi + 1];
+  for (uint64_t win = blockIdx.y; win * 64 < n_words; win += gridDim.y) {
+    const uint64_t w0 = win * 64 + lane, w1 = w0 + 32;
+    const bool v0 = w0 < n_words, v1 = w1 < n_words;
+    uint64_t a0 = 0, a1 = 0, c0 = 0, c1 = 0;
+    uint64_t i = b;
+    for (; i + 2 <= e; i += 2) {
+      const uint64_t* r0 = S + static_cast<uint64_t>(__ldg(sym_idx + i)) * ldS;
+      const uint64_t* r1 = S + static_cast<uint64_t>(__ldg(sym_idx + i + 1)) * ldS;
+      if (v0) { a0 ^= __ldg(r0 + w0); c0 ^= __ldg(r1 + w0); }
+      if (v1) { a1 ^= __ldg(r0 + w1); c1 ^= __ldg(r1 + w1); }
+    }
+    if (i < e) {
+      const uint64_t* r0 = S + static_cast<uint64_t>(__ldg(sym_idx + i)) * ldS;
+      if (v0) a0 ^= __ldg(r0 + w0);
+      if (v1) a1 ^= __ldg(r0 + w1);
+    }
+    a0 ^= c0;
+    a1 ^= c1;
+    if (w0 == n_words - 1) a0 &= tail;
+    if (w1 == n_words - 1) a1 &= tail;
+    uint64_t* o = out + static_cast<uint64_t>(k) * ld;
+    if (split) {
+      if (v0 && a0) atomicXor(reinterpret_cast<unsigned long long*>(o + w0), a0);
+      if (v1 && a1) atomicXor(reinterpret_cast<unsigned long long*>(o + w1), a1);
+    } else {
+      if (v0) o[w0] = a0;
+      if (v1) o[w1] = a1;
+    }
+  }
+}
+
+__global__ void k2_zero_rows(const uint32_t* __restrict__ rows, uint32_t n_rows, uint64_t n_words,
+                             uint64_t* __restrict__ out, uint64_t ld) {
+  const uint64_t total = static_cast<uint64_t>(n_rows) * n_words;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    out[static_cast<uint64_t>(rows[i / n_words]) * ld + i % n_words] = 0;
+}
+
 // Dense variant: Method of Four Russians over shared-memory tables. A CTA
 // owns 512 measurement rows x 2048 shots (32 u64 words: lane = word, 32 row
 // accumulators per thread in registers). Symbols are taken 8 at a time: for
@@ -640,6 +694,16 @@ int launch_product(const DevPlan& P, const LaunchCfg& L, bool dense, const uint6
     dim3 g4(static_cast<unsigned>(slabs), static_cast<unsigned>(row_blocks));
     k2_m4rm<<<g4, kM4Threads, kM4Smem, L.stream>>>(P.dense_gm, P.gm_ld, P.n_meas, P.n_sym, S, ldS,
                                                    n_words, tail, out, ld);
+  } else if (P.k2_seg_ptr) {
+    if (P.n_k2_split) {
+      const uint64_t total = static_cast<uint64_t>(P.n_k2_split) * n_words;
+      const int zb = static_cast<int>(std::min<uint64_t>((total + 255) / 256, 8ull * L.num_sms));
+      k2_zero_rows<<<zb, 256, 0, L.stream>>>(P.k2_split_rows, P.n_k2_split, n_words, out, ld);
+    }
+    dim3 gs((P.n_k2_seg + kK2Rows - 1) / kK2Rows,
+            static_cast<unsigned>(std::min<uint64_t>(windows, 65535)));
+    k2_sparse_seg<<<gs, kK2Rows * 32, 0, L.stream>>>(P.k2_seg_ptr, P.k2_seg_row, P.n_k2_seg,
+                                                     P.sym_idx, S, ldS, n_words, tail, out, ld);
   } else {
     k2_sparse<<<grid, kK2Rows * 32, 0, L.stream>>>(P.row_ptr, P.sym_idx, P.n_meas, S, ldS,
                                                    n_words, tail, out, ld);

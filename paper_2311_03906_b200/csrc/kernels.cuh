@@ -50,6 +50,16 @@ struct DevPlan {
   // (symbols 8g .. 8g+7) at dense_gm[g * gm_ld + k], gm_ld = n_meas padded to 16
   const uint8_t* dense_gm = nullptr;
   uint64_t gm_ld = 0;
+  // CSR product work list (K2): the rows cut into segments of <= ~1024
+  // symbols, so one very long row (the final measurements of a scrambled
+  // circuit can hold 10^5 symbols) is spread over many warps. Segment s
+  // covers sym_idx[k2_seg_ptr[s] .. k2_seg_ptr[s+1]) of row k2_seg_row[s] &
+  // 0x7FFFFFFF; bit 31 marks a row cut in several segments, whose partial
+  // XORs are combined with atomics into a zeroed row (k2_split_rows).
+  uint32_t n_k2_seg = 0, n_k2_split = 0;
+  const uint64_t* k2_seg_ptr = nullptr;
+  const uint32_t* k2_seg_row = nullptr;
+  const uint32_t* k2_split_rows = nullptr;
 
   // Group table (symbols.hpp:36-42).
   const uint32_t* g_first = nullptr;

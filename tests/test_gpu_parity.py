@@ -307,3 +307,24 @@ def test_no_measurements(gpu_sampler_factory):
     assert s.encode(out, 100, "b8", n_meas=0).numel() == 0
     buf, w = s.sample_to_host(100, 1, "01")
     assert bytes(buf[:w]) == b"\n" * 100
+
+
+def test_product_long_rows_split(gpu_sampler_factory, port, monkeypatch):
+    """K2 CSR with a few very long rows (a scrambled circuit's final
+    measurements can hold 10^5 symbols): the rows are cut into segments
+    combined with atomics, and the product still equals the oracle."""
+    monkeypatch.setenv("SP_K2_SEG", "64")
+    rng = np.random.default_rng(17)
+    n_m, n_s, n = 200, 3000, 5000 + 13
+    rows = []
+    for k in range(n_m):
+        length = int(rng.integers(2000, 3000)) if k % 37 == 5 else int(rng.integers(0, 20))
+        rows.append(np.sort(rng.choice(n_s, size=length, replace=False)).astype(np.uint32))
+    rp = np.concatenate([[0], np.cumsum([len(r) for r in rows])]).astype(np.uint64)
+    si = np.concatenate(rows).astype(np.uint32)
+    S = pack_bits(rng.integers(0, 2, size=(n_s, n), dtype=np.uint8))
+    s = gpu_sampler_factory()
+    s.load_csr(rp, si, n_s)
+    s.set_product("sparse")
+    got = host(s.sample_given(dev(S), n))
+    assert np.array_equal(got, port.sample(rp, si, S, n))
