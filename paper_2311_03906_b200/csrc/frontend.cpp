@@ -3,10 +3,12 @@
 // (circuit.cpp:188-226), decompose_noise (circuit.cpp:228-281) and the
 // one-pass symbolic tableau (tableau.cpp:17-198, 318-382).
 #include "frontend.hpp"
+#include "frontend_dev.hpp"
 
 #include <algorithm>
 #include <cctype>
 #include <charconv>
+#include <cstdlib>
 #include <cstring>
 #include <optional>
 
@@ -122,14 +124,20 @@ namespace {
 // Rows [0, n) destabilizers, [n, 2n) stabilizers; x/z row-major packed.
 class SymTableau {
  public:
-  SymTableau(size_t n, size_t capacity)
+  // dev: keep the phase matrix in device memory (frontend_dev.cu); row XORs
+  // of measurements run as kernels, single-bit flips are queued.
+  SymTableau(size_t n, size_t capacity, bool dev)
       : n_(n), wq_((n + 63) / 64), ws_((capacity + 63) / 64),
-        x_(2 * n * wq_, 0), z_(2 * n * wq_, 0), ph_(n * ws_, 0), hi_(n, 0) {
+        x_(2 * n * wq_, 0), z_(2 * n * wq_, 0), ph_(dev ? 0 : n * ws_, 0), hi_(n, 0) {
     for (size_t i = 0; i < n; ++i) {
       x_[i * wq_ + i / 64] |= bit(i);              // destabilizer X_i
       z_[(n + i) * wq_ + i / 64] |= bit(i);        // stabilizer Z_i
     }
+    if (dev) dev_ = phase_dev_create(n, ws_);
   }
+  ~SymTableau() { phase_dev_destroy(dev_); }
+  SymTableau(const SymTableau&) = delete;
+  SymTableau& operator=(const SymTableau&) = delete;
 
   // H, S, S_DAG, CX: tableau.cpp:38-78 (phase term into the constant symbol).
   void h(uint32_t a) {
@@ -190,9 +198,15 @@ class SymTableau {
       if (x_[r * wq_ + w] & m) { pivot = r; break; }
 
     if (pivot < 2 * n_) {
+      targets_.clear();
       for (size_t r = 0; r < 2 * n_; ++r) {
         if (r == pivot || r + n_ == pivot) continue;
         if (x_[r * wq_ + w] & m) rowsum(r, pivot);
+      }
+      if (dev_ && !targets_.empty()) {  // the phase XORs rowsum deferred, in one launch
+        flush_flips();
+        phase_dev_xor_rows(dev_, static_cast<uint32_t>(pivot - n_), targets_.data(), targets_.size(),
+                           hi_[pivot - n_]);
       }
       std::memcpy(&x_[(pivot - n_) * wq_], &x_[pivot * wq_], wq_ * 8);
       std::memcpy(&z_[(pivot - n_) * wq_], &z_[pivot * wq_], wq_ * 8);
@@ -200,7 +214,12 @@ class SymTableau {
       std::memset(&z_[pivot * wq_], 0, wq_ * 8);
       z_[pivot * wq_ + w] |= m;
       size_t i = pivot - n_;
-      std::memset(&ph_[i * ws_], 0, hi_[i] * 8);
+      if (dev_) {
+        flush_flips();
+        phase_dev_clear_row(dev_, static_cast<uint32_t>(i), hi_[i]);
+      } else {
+        std::memset(&ph_[i * ws_], 0, hi_[i] * 8);
+      }
       hi_[i] = 0;
       uint32_t sym = static_cast<uint32_t>(n_sym++);  // add_measurement_symbol, symbols.hpp:73-81
       groups.push_back(Group{kCoin, 0.5, sym, 1});
@@ -211,8 +230,11 @@ class SymTableau {
 
     // Determined: product of the stabilizers selected by destabilizers that
     // anticommute with Z_a is +/-Z_a; its symbolic phase is the outcome.
-    std::vector<uint64_t> sx(wq_, 0), sz(wq_, 0), sp(ws_, 0);
+    std::vector<uint64_t> sx(wq_, 0), sz(wq_, 0);
+    std::vector<uint64_t> sp(dev_ ? 0 : ws_, 0);
     size_t shi = 0;
+    uint64_t const_flip = 0;
+    targets_.clear();
     for (size_t i = 0; i < n_; ++i) {
       if (!(x_[i * wq_ + w] & m)) continue;
       const uint64_t* x1 = &x_[(n_ + i) * wq_];
@@ -220,10 +242,20 @@ class SymTableau {
       int res = phase_exponent(x1, z1, sx.data(), sz.data());
       if (res & 1) throw std::logic_error("non-hermitian generator product: tableau corrupt");
       for (size_t k = 0; k < wq_; ++k) { sx[k] ^= x1[k]; sz[k] ^= z1[k]; }
-      const uint64_t* p1 = &ph_[i * ws_];
-      for (size_t k = 0; k < hi_[i]; ++k) sp[k] ^= p1[k];
+      if (dev_) {
+        targets_.push_back(static_cast<uint32_t>(i));
+      } else {
+        const uint64_t* p1 = &ph_[i * ws_];
+        for (size_t k = 0; k < hi_[i]; ++k) sp[k] ^= p1[k];
+      }
       shi = std::max<size_t>(shi, hi_[i]);
-      if (res == 2) sp[0] ^= 1;
+      if (res == 2) const_flip ^= 1;
+    }
+    const uint64_t* spp = sp.data();
+    if (dev_) {
+      flush_flips();
+      spp = phase_dev_reduce(dev_, targets_.data(), targets_.size(),
+                             static_cast<uint32_t>(std::max<size_t>(shi, 1)));
     }
     bool ok = true;
     for (size_t k = 0; k < wq_; ++k) {
@@ -233,7 +265,7 @@ class SymTableau {
     if (!ok) throw std::logic_error("determined measurement did not reduce to Z_a");
     std::vector<uint32_t> e;
     for (size_t k = 0; k < std::max<size_t>(shi, 1); ++k) {
-      uint64_t v = sp[k];
+      uint64_t v = spp[k] ^ (k == 0 ? const_flip : 0);
       while (v) {
         e.push_back(static_cast<uint32_t>(k * 64 + __builtin_ctzll(v)));
         v &= v - 1;
@@ -246,8 +278,17 @@ class SymTableau {
   static uint64_t bit(size_t i) { return uint64_t{1} << (i & 63); }
 
   void flip_phase(size_t i, uint32_t sym) {
-    ph_[i * ws_ + sym / 64] ^= bit(sym);
+    if (dev_) {
+      flips_.push_back(static_cast<uint64_t>(i) << 32 | sym);
+    } else {
+      ph_[i * ws_ + sym / 64] ^= bit(sym);
+    }
     hi_[i] = std::max<uint32_t>(hi_[i], sym / 64 + 1);
+  }
+  // queued single-bit flips, applied before the next device row operation
+  void flush_flips() {
+    if (!flips_.empty()) phase_dev_flips(dev_, flips_.data(), flips_.size());
+    flips_.clear();
   }
 
   // i-exponent of (source * target), single_qubit_phase_exponent summed over
@@ -275,8 +316,12 @@ class SymTableau {
       int res = phase_exponent(xs, zs, xd, zd);
       if (res & 1) throw std::logic_error("non-hermitian generator product: tableau corrupt");
       size_t di = dst - n_, si = src - n_;
-      uint64_t* pd = &ph_[di * ws_]; const uint64_t* ps = &ph_[si * ws_];
-      for (size_t k = 0; k < hi_[si]; ++k) pd[k] ^= ps[k];
+      if (dev_) {
+        targets_.push_back(static_cast<uint32_t>(di));  // XORed by the caller in one launch
+      } else {
+        uint64_t* pd = &ph_[di * ws_]; const uint64_t* ps = &ph_[si * ws_];
+        for (size_t k = 0; k < hi_[si]; ++k) pd[k] ^= ps[k];
+      }
       hi_[di] = std::max(hi_[di], hi_[si]);
       if (res == 2) flip_phase(di, 0);
     }
@@ -286,6 +331,9 @@ class SymTableau {
   size_t n_, wq_, ws_;
   std::vector<uint64_t> x_, z_, ph_;
   std::vector<uint32_t> hi_;
+  PhaseDev* dev_ = nullptr;
+  std::vector<uint64_t> flips_;    // queued (row << 32 | symbol) flips (dev_)
+  std::vector<uint32_t> targets_;  // rows of the current device row operation
 };
 
 }  // namespace
@@ -308,7 +356,13 @@ Model run_initialization(const std::vector<Instr>& prog) {
   M.n_qubits = n;
   if (n == 0) return M;
 
-  SymTableau t(n, cap);
+  // The phase matrix goes to the device when it is large (n x capacity
+  // bits >= 2^28, 32 MB) and a GPU is present; SP_FRONTEND_DEV=0/1 forces.
+  const char* env = std::getenv("SP_FRONTEND_DEV");
+  const double bits = static_cast<double>(n) * static_cast<double>(cap);
+  bool dev = env ? std::atoi(env) != 0 : bits >= static_cast<double>(1ull << 28);
+  if (dev && !phase_dev_available()) dev = false;
+  SymTableau t(n, cap, dev);
   uint64_t& n_sym = M.n_sym;
   auto add_fault = [&](uint8_t dist, double p, uint32_t arity) {
     uint32_t first = static_cast<uint32_t>(n_sym);
