@@ -163,9 +163,11 @@ __device__ __forceinline__ bool segment_walk_t(Segment& sg, uint4 (&r)[kBlocks],
   const uint32_t magic = n == 3 ? 174763u : 34953u;
   const uint32_t tmask = (1u << t_log2) - 1u;
   uint32_t pos = 0;  // trials consumed (warp-uniform), < len <= 2^22
-  for (uint32_t draw = 0;; ++draw) {
-    uint32_t incl[kSlots];
-    uint32_t acc = 0;
+  uint32_t incl[kSlots];
+  uint32_t acc = 0;
+  // Gaps of one step's firings from its Philox blocks (inclusive sums).
+  auto skips = [&]() {
+    acc = 0;
 #pragma unroll
     for (int b = 0; b < kBlocks; ++b) {
       // Four 24-bit skip fields per block: the top bits of each word
@@ -186,6 +188,9 @@ __device__ __forceinline__ bool segment_walk_t(Segment& sg, uint4 (&r)[kBlocks],
         incl[4 * b + k] = acc;
       }
     }
+  };
+  skips();
+  for (uint32_t draw = 0;; ++draw) {
     uint32_t scan = acc;  // warp inclusive scan of the lanes' gap sums
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -228,6 +233,7 @@ __device__ __forceinline__ bool segment_walk_t(Segment& sg, uint4 (&r)[kBlocks],
     if (more) {
 #pragma unroll
       for (int b = 0; b < kBlocks; ++b) r[b] = segment_philox(sg, K, gtile, draw + 1, b, lane);
+      skips();  // the next step's gaps, independent of this step's XORs
     } else {
       have_next = next(sn);
       if (have_next) {
