@@ -128,6 +128,7 @@ class SymTableau {
   // of measurements run as kernels, single-bit flips are queued.
   SymTableau(size_t n, size_t capacity, bool dev)
       : n_(n), wq_((n + 63) / 64), ws_((capacity + 63) / 64),
+        rw_((2 * n + 63) / 64), xc_(n * ((2 * n + 63) / 64), 0), zc_(n * ((2 * n + 63) / 64), 0),
         x_(2 * n * wq_, 0), z_(2 * n * wq_, 0), ph_(dev ? 0 : n * ws_, 0), hi_(n, 0) {
     for (size_t i = 0; i < n; ++i) {
       x_[i * wq_ + i / 64] |= bit(i);              // destabilizer X_i
@@ -139,59 +140,60 @@ class SymTableau {
   SymTableau(const SymTableau&) = delete;
   SymTableau& operator=(const SymTableau&) = delete;
 
+  // Gates and symbol-conditioned Paulis work on a qubit-major copy of x/z
+  // (column q = one bit per row, 2n bits): every update is O(n/64) words,
+  // and the phase flips go to the rows of a bit mask. Measurements use the
+  // row-major form; the two are converted (64 x 64 block transposes) when
+  // the instruction kind switches.
   // H, S, S_DAG, CX: tableau.cpp:38-78 (phase term into the constant symbol).
   void h(uint32_t a) {
-    const size_t w = a / 64; const uint64_t m = bit(a);
-    for (size_t r = 0; r < 2 * n_; ++r) {
-      uint64_t& xr = x_[r * wq_ + w]; uint64_t& zr = z_[r * wq_ + w];
-      bool xa = xr & m, za = zr & m;
-      if (xa && za && r >= n_) flip_phase(r - n_, 0);
-      if (xa != za) { xr ^= m; zr ^= m; }
-    }
+    to_cols();
+    uint64_t* xa = &xc_[a * rw_]; uint64_t* za = &zc_[a * rw_];
+    flip_rows(0, [&](size_t w) { return xa[w] & za[w]; });
+    for (size_t w = 0; w < rw_; ++w) std::swap(xa[w], za[w]);
   }
   void s(uint32_t a) {
-    const size_t w = a / 64; const uint64_t m = bit(a);
-    for (size_t r = 0; r < 2 * n_; ++r) {
-      uint64_t& xr = x_[r * wq_ + w]; uint64_t& zr = z_[r * wq_ + w];
-      bool xa = xr & m, za = zr & m;
-      if (xa && za && r >= n_) flip_phase(r - n_, 0);
-      if (xa) zr ^= m;
-    }
+    to_cols();
+    uint64_t* xa = &xc_[a * rw_]; uint64_t* za = &zc_[a * rw_];
+    flip_rows(0, [&](size_t w) { return xa[w] & za[w]; });
+    for (size_t w = 0; w < rw_; ++w) za[w] ^= xa[w];
   }
   void s_dag(uint32_t a) {
-    const size_t w = a / 64; const uint64_t m = bit(a);
-    for (size_t r = 0; r < 2 * n_; ++r) {
-      uint64_t& xr = x_[r * wq_ + w]; uint64_t& zr = z_[r * wq_ + w];
-      bool xa = xr & m, za = zr & m;
-      if (xa && !za && r >= n_) flip_phase(r - n_, 0);
-      if (xa) zr ^= m;
-    }
+    to_cols();
+    uint64_t* xa = &xc_[a * rw_]; uint64_t* za = &zc_[a * rw_];
+    flip_rows(0, [&](size_t w) { return xa[w] & ~za[w]; });
+    for (size_t w = 0; w < rw_; ++w) za[w] ^= xa[w];
   }
   void cx(uint32_t a, uint32_t b) {
-    const size_t wa = a / 64, wb = b / 64; const uint64_t ma = bit(a), mb = bit(b);
-    for (size_t r = 0; r < 2 * n_; ++r) {
-      uint64_t* xr = &x_[r * wq_]; uint64_t* zr = &z_[r * wq_];
-      bool xa = xr[wa] & ma, za = zr[wa] & ma, xb = xr[wb] & mb, zb = zr[wb] & mb;
-      if (r >= n_ && xa && zb && !(xb ^ za)) flip_phase(r - n_, 0);
-      if (xa) xr[wb] ^= mb;
-      if (zb) zr[wa] ^= ma;
-    }
+    to_cols();
+    uint64_t* xa = &xc_[a * rw_]; uint64_t* za = &zc_[a * rw_];
+    uint64_t* xb = &xc_[b * rw_]; uint64_t* zb = &zc_[b * rw_];
+    flip_rows(0, [&](size_t w) { return xa[w] & zb[w] & ~(xb[w] ^ za[w]); });
+    for (size_t w = 0; w < rw_; ++w) { xb[w] ^= xa[w]; za[w] ^= zb[w]; }
   }
 
   // Symbol-conditioned Paulis (tableau.cpp:80-100): XOR symbol s into the
   // phase of every stabilizer row the Pauli anticommutes with.
+  // Works in whichever layout is current (a reset's conditional X follows
+  // its measurement, so no conversion).
   void pauli(uint32_t a, bool px, bool pz, uint32_t sym) {
-    const size_t w = a / 64; const uint64_t m = bit(a);
-    for (size_t i = 0; i < n_; ++i) {
-      size_t r = n_ + i;
-      bool xa = x_[r * wq_ + w] & m, za = z_[r * wq_ + w] & m;
-      bool anti = (px && za) ^ (pz && xa);
-      if (anti) flip_phase(i, sym);
+    if (!cols_) {
+      const size_t w = a / 64; const uint64_t m = bit(a);
+      for (size_t i = 0; i < n_; ++i) {
+        size_t r = n_ + i;
+        bool xa = x_[r * wq_ + w] & m, za = z_[r * wq_ + w] & m;
+        if ((px && za) ^ (pz && xa)) flip_phase(i, sym);
+      }
+      return;
     }
+    const uint64_t* xa = &xc_[a * rw_]; const uint64_t* za = &zc_[a * rw_];
+    const uint64_t mx = px ? ~0ull : 0ull, mz = pz ? ~0ull : 0ull;
+    flip_rows(sym, [&](size_t w) { return (mx & za[w]) ^ (mz & xa[w]); });
   }
 
   // Z-basis measurement (tableau.cpp:146-198). Returns sorted symbol ids.
   std::vector<uint32_t> measure(uint32_t a, uint64_t& n_sym, std::vector<Group>& groups) {
+    to_rows();
     const size_t w = a / 64; const uint64_t m = bit(a);
     size_t pivot = 2 * n_;
     for (size_t r = n_; r < 2 * n_; ++r)
@@ -277,6 +279,72 @@ class SymTableau {
  private:
   static uint64_t bit(size_t i) { return uint64_t{1} << (i & 63); }
 
+  // flip_phase(row - n, sym) for every stabilizer row whose bit is set in
+  // the column-form mask fn(word).
+  template <class F>
+  void flip_rows(uint32_t sym, F&& fn) {
+    for (size_t w = n_ / 64; w < rw_; ++w) {
+      uint64_t v = fn(w);
+      const size_t r0 = w * 64;
+      if (r0 < n_) v &= ~0ull << (n_ - r0);  // destabilizer rows carry no phase
+      if (r0 + 64 > 2 * n_) v &= (2 * n_ - r0 >= 64) ? ~0ull : ((1ull << (2 * n_ - r0)) - 1);
+      while (v) {
+        const size_t r = r0 + static_cast<size_t>(__builtin_ctzll(v));
+        v &= v - 1;
+        flip_phase(r - n_, sym);
+      }
+    }
+  }
+
+  // 64 x 64 bit transpose in place: bit j of word i <-> bit i of word j.
+  static void transpose64(uint64_t* a) {
+    uint64_t m = 0x00000000FFFFFFFFull;
+    for (int j = 32; j != 0; j >>= 1, m ^= m << j) {
+      for (int k = 0; k < 64; k = ((k | j) + 1) & ~j) {
+        const uint64_t t = ((a[k] >> j) ^ a[k | j]) & m;
+        a[k] ^= t << j;
+        a[k | j] ^= t;
+      }
+    }
+  }
+  // Row-major x_/z_ [2n][wq_] <-> qubit-major xc_/zc_ [n][rw_].
+  void to_cols() {
+    if (cols_) return;
+    convert(true);
+    cols_ = true;
+  }
+  void to_rows() {
+    if (!cols_) return;
+    convert(false);
+    cols_ = false;
+  }
+  void convert(bool to_c) {
+    uint64_t blk[64];
+    for (int pass = 0; pass < 2; ++pass) {
+      std::vector<uint64_t>& rm = pass ? z_ : x_;
+      std::vector<uint64_t>& cm = pass ? zc_ : xc_;
+      for (size_t R = 0; R < rw_; ++R) {      // 64-row block
+        for (size_t Q = 0; Q < wq_; ++Q) {    // 64-qubit block
+          if (to_c) {
+            for (size_t i = 0; i < 64; ++i) {
+              const size_t r = R * 64 + i;
+              blk[i] = r < 2 * n_ ? rm[r * wq_ + Q] : 0;
+            }
+            transpose64(blk);
+            for (size_t j = 0; j < 64 && Q * 64 + j < n_; ++j) cm[(Q * 64 + j) * rw_ + R] = blk[j];
+          } else {
+            for (size_t j = 0; j < 64; ++j) {
+              const size_t q = Q * 64 + j;
+              blk[j] = q < n_ ? cm[q * rw_ + R] : 0;
+            }
+            transpose64(blk);
+            for (size_t i = 0; i < 64 && R * 64 + i < 2 * n_; ++i) rm[(R * 64 + i) * wq_ + Q] = blk[i];
+          }
+        }
+      }
+    }
+  }
+
   void flip_phase(size_t i, uint32_t sym) {
     if (dev_) {
       flips_.push_back(static_cast<uint64_t>(i) << 32 | sym);
@@ -329,6 +397,9 @@ class SymTableau {
   }
 
   size_t n_, wq_, ws_;
+  size_t rw_ = 0;          // words per qubit column (2n rows)
+  bool cols_ = false;      // the qubit-major copy is current (row-major stale)
+  std::vector<uint64_t> xc_, zc_;
   std::vector<uint64_t> x_, z_, ph_;
   std::vector<uint32_t> hi_;
   PhaseDev* dev_ = nullptr;
