@@ -127,3 +127,17 @@ def test_bench_families_shape(ref):
         c = ref.circuit(text)
         assert np.array_equal(init.row_ptr, c.row_ptr) and np.array_equal(init.sym_idx, c.sym_idx)
     assert "DEPOLARIZE1" in CI.bench_family("c", 20) and "DEPOLARIZE1" not in CI.bench_family("b", 20)
+
+
+def test_frontend_matches_live_reference_wide_random(ref):
+    """Random circuits over 60-200 qubits (several 64-bit words per tableau
+    row and column, resets, noise, mid-circuit measurements): the qubit-major
+    gate path and its transposes agree with the reference's pass."""
+    rng = CI.MT19937_64(9090)
+    for _ in range(12):
+        n = 60 + rng.below(141)
+        text = CI.random_test_circuit(rng, n_qubits=n, n_instr=200 + rng.below(400))
+        c = ref.circuit(text)
+        got = run_initialization(text)
+        assert got.n_sym == c.n_sym
+        assert np.array_equal(got.row_ptr, c.row_ptr) and np.array_equal(got.sym_idx, c.sym_idx)
