@@ -120,7 +120,7 @@ def test_bench_families_shape(ref):
     """The Fig. 3 families (circuit_gen.cpp:19-66): n layers of single-qubit
     gates, CX pairs, optional DEPOLARIZE1, max(1, n/20) measurements per layer
     and n at the end; our front end agrees with the reference library."""
-    for fam, n in (("a", 40), ("b", 60), ("c", 30)):
+    for fam, n in (("a", 40), ("b", 60), ("c", 30), ("b", 130)):
         text = CI.bench_family(fam, n, seed=3)
         init = run_initialization(text)
         assert init.n_meas == n * max(1, n // 20) + n
