@@ -10,6 +10,7 @@
 #include <charconv>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <optional>
 
 namespace symphase {
@@ -433,7 +434,14 @@ Model run_initialization(const std::vector<Instr>& prog) {
   const double bits = static_cast<double>(n) * static_cast<double>(cap);
   bool dev = env ? std::atoi(env) != 0 : bits >= static_cast<double>(1ull << 28);
   if (dev && !phase_dev_available()) dev = false;
-  SymTableau t(n, cap, dev);
+  std::unique_ptr<SymTableau> tp;
+  try {
+    tp = std::make_unique<SymTableau>(n, cap, dev);
+  } catch (const std::runtime_error&) {  // no device memory for the phase matrix
+    if (!dev) throw;
+    tp = std::make_unique<SymTableau>(n, cap, false);
+  }
+  SymTableau& t = *tp;
   uint64_t& n_sym = M.n_sym;
   auto add_fault = [&](uint8_t dist, double p, uint32_t arity) {
     uint32_t first = static_cast<uint32_t>(n_sym);
