@@ -191,13 +191,19 @@ __device__ __forceinline__ bool segment_walk_t(Segment& sg, uint4 (&r)[kBlocks],
   };
   skips();
   for (uint32_t draw = 0;; ++draw) {
-    uint32_t scan = acc;  // warp inclusive scan of the lanes' gap sums
+    // warp total (REDUX, off the scan's dependency chain) and inclusive scan
+    // of the lanes' gap sums (the shuffle's own in-range predicate guards
+    // each add)
+    const uint32_t total = __reduce_add_sync(kFull, acc);
+    uint32_t scan = acc;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t t = __shfl_up_sync(kFull, scan, o);
-      if (lane >= static_cast<uint32_t>(o)) scan += t;
+      asm("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\t"
+          "shfl.sync.up.b32 t|p, %0, %1, 0, 0xffffffff;\n\t"
+          "@p add.u32 %0, %0, t;\n\t}"
+          : "+r"(scan)
+          : "r"(o));
     }
-    const uint32_t total = __shfl_sync(kFull, scan, 31);
     // trial index (relative to the segment) of this lane's firings, minus 1
     const uint32_t base = pos + scan - acc - 1;
     const uint32_t sbase = sg.s0 + base;
