@@ -1707,6 +1707,9 @@ int sp_sample_tiled(sp_ctx* ctx, uint64_t seed, uint64_t shot_begin, uint64_t n_
   if (int r = set_device(ctx)) return r;
   if (int r = ensure_plan(ctx)) return r;
   if (!ctx->fused_ok) return fail(SP_ERR_UNSUPPORTED, ctx->fused_why);
+  if (ctx->k5_ok)
+    return fail(SP_ERR_UNSUPPORTED, "this model is sampled by the column sampler (measurement-major "
+                                    "records only); use sp_sample");
   if (ctx->rng != SP_RNG_PHILOX)
     return fail(SP_ERR_UNSUPPORTED, "tiled output is produced by the Philox sampler only");
   const uint64_t T = 1ull << ctx->dp.t_log2;
@@ -1876,7 +1879,7 @@ int sp_sample_to_host(sp_ctx* ctx, uint64_t seed, uint64_t shot_begin, uint64_t 
       const uint64_t n = std::min(chunk, n_shots - done);
       if (i >= 2) ck(cudaStreamWaitEvent(ctx->stream, ctx->ev_free[b], 0), "cudaStreamWaitEvent");
       int r = SP_OK;
-      if (ctx->rng == SP_RNG_PHILOX && n_meas && ctx->fused_ok && !ctx->unfused) {
+      if (ctx->rng == SP_RNG_PHILOX && n_meas && ctx->fused_ok && !ctx->unfused && !ctx->k5_ok) {
         // tiled records: coalesced stores for any row count
         if ((r = sp_sample_tiled(ctx, seed, shot_begin + done, n, d_m[b], nullptr))) return r;
         if ((r = sp_encode_tiled(ctx, d_m[b], n, fmt, d_b[b]))) return r;

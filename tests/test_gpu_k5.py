@@ -114,3 +114,20 @@ def test_k5_pattern_marginals_1M(gpu_sampler_factory, force_k5):
             if abs(hits / N - q) > 5 * sd + 1e-12:
                 bad.append((gi, d, p, pat, hits / N))
     assert not bad, bad
+
+
+def test_k5_host_path_and_tiled(gpu_sampler_factory, port, force_k5):
+    """sp_sample_to_host serves a K5 model through the same sampler as
+    sp_sample (its b8 bytes equal the encoded records), and the tiled layout,
+    which only the fused kernel produces, is refused."""
+    from paper_2311_03906_b200._native import SymphaseError
+    model = mixed_dense_model(150, 300, 0.3, seed=9)
+    s = gpu_sampler_factory(model)
+    assert s.plan_info()["fused_ok"] == 2
+    n = 3000
+    out = s.sample(n, 4)
+    want = s.encode(out, n, "b8").cpu().numpy().tobytes()
+    buf, w = s.sample_to_host(n, 4, "b8")
+    assert bytes(buf[:w]) == want
+    with pytest.raises(SymphaseError):
+        s.sample_tiled(n, 4)
