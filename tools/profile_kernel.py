@@ -22,20 +22,22 @@ def main():
     ap.add_argument("--what", default="sample", choices=["sample", "counts", "draw", "given",
                                                          "encode", "compat"])
     ap.add_argument("--reps", type=int, default=2)
+    ap.add_argument("--tiled", action="store_true", help="tiled record layout (sample/counts)")
     a = ap.parse_args()
     init = run_initialization(circuits.CONFIGS[a.config]["text"]())
     n = a.shots or circuits.CONFIGS[a.config]["shots"]
     s = Sampler(init, rng="compat" if a.what == "compat" else "philox")
     T = s.shot_tile
     n = (n + T - 1) // T * T
-    out = s.empty_bits(init.n_meas, n)
+    out = (torch.empty(s.tiled_words(n), dtype=torch.int64, device="cuda") if a.tiled
+           else s.empty_bits(init.n_meas, n))
     counts = torch.zeros(init.n_meas, dtype=torch.int64, device="cuda")
     S = s.draw_assignments(n, 1) if a.what == "given" else None
     for i in range(a.reps):
         if a.what in ("sample", "compat"):
-            s.sample(n, 10 + i, out=out)
+            (s.sample_tiled if a.tiled else s.sample)(n, 10 + i, out=out)
         elif a.what == "counts":
-            s.sample(n, 10 + i, out=out, counts=counts)
+            (s.sample_tiled if a.tiled else s.sample)(n, 10 + i, out=out, counts=counts)
         elif a.what == "draw":
             s.draw_assignments(n, 10 + i)
         elif a.what == "given":
