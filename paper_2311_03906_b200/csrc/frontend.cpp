@@ -127,8 +127,10 @@ class SymTableau {
  public:
   // dev: keep the phase matrix in device memory (frontend_dev.cu); row XORs
   // of measurements run as kernels, single-bit flips are queued.
-  SymTableau(size_t n, size_t capacity, bool dev)
-      : n_(n), wq_((n + 63) / 64), ws_((capacity + 63) / 64),
+  // may_move: start on the host and move the phase matrix to the device
+  // once the row XORs are heavy (see note_op).
+  SymTableau(size_t n, size_t capacity, bool dev, bool may_move = false)
+      : may_move_(may_move && !dev), n_(n), wq_((n + 63) / 64), ws_((capacity + 63) / 64),
         rw_((2 * n + 63) / 64), xc_(n * ((2 * n + 63) / 64), 0), zc_(n * ((2 * n + 63) / 64), 0),
         x_(2 * n * wq_, 0), z_(2 * n * wq_, 0), ph_(dev ? 0 : n * ws_, 0), hi_(n, 0) {
     for (size_t i = 0; i < n; ++i) {
@@ -192,9 +194,38 @@ class SymTableau {
     flip_rows(sym, [&](size_t w) { return (mx & za[w]) ^ (mz & xa[w]); });
   }
 
+  // A reset's X conditioned on every symbol of its measurement's outcome
+  // (tableau.cpp:355-362 applies one conditional X per symbol): the rows it
+  // anticommutes with are the same for all symbols, so find them once and
+  // flip the whole expression into each (same XORs, reordered).
+  void pauli_x_all(uint32_t a, const std::vector<uint32_t>& syms) {
+    if (syms.empty()) return;
+    if (syms.size() == 1) return pauli(a, true, false, syms[0]);
+    rows_.clear();
+    if (!cols_) {
+      const size_t w = a / 64; const uint64_t m = bit(a);
+      for (size_t i = 0; i < n_; ++i)
+        if (z_[(n_ + i) * wq_ + w] & m) rows_.push_back(static_cast<uint32_t>(i));
+    } else {
+      const uint64_t* za = &zc_[a * rw_];
+      for_rows([&](size_t w) { return za[w]; }, [&](size_t i) { rows_.push_back(static_cast<uint32_t>(i)); });
+    }
+    const uint32_t top = *std::max_element(syms.begin(), syms.end()) / 64 + 1;
+    for (uint32_t i : rows_) {
+      if (dev_) {
+        for (uint32_t s : syms) flips_.push_back(static_cast<uint64_t>(i) << 32 | s);
+      } else {
+        uint64_t* p = &ph_[i * ws_];
+        for (uint32_t s : syms) p[s / 64] ^= bit(s);
+      }
+      hi_[i] = std::max(hi_[i], top);
+    }
+  }
+
   // Z-basis measurement (tableau.cpp:146-198). Returns sorted symbol ids.
   std::vector<uint32_t> measure(uint32_t a, uint64_t& n_sym, std::vector<Group>& groups) {
     to_rows();
+    if (may_move_ && heavy_ >= kHeavyOps) move_to_device();
     const size_t w = a / 64; const uint64_t m = bit(a);
     size_t pivot = 2 * n_;
     for (size_t r = n_; r < 2 * n_; ++r)
@@ -202,10 +233,15 @@ class SymTableau {
 
     if (pivot < 2 * n_) {
       targets_.clear();
+      size_t n_stab = 0;
       for (size_t r = 0; r < 2 * n_; ++r) {
         if (r == pivot || r + n_ == pivot) continue;
-        if (x_[r * wq_ + w] & m) rowsum(r, pivot);
+        if (x_[r * wq_ + w] & m) {
+          rowsum(r, pivot);
+          n_stab += r >= n_;
+        }
       }
+      if (!dev_) note_op(n_stab * hi_[pivot - n_]);
       if (dev_ && !targets_.empty()) {  // the phase XORs rowsum deferred, in one launch
         flush_flips();
         phase_dev_xor_rows(dev_, static_cast<uint32_t>(pivot - n_), targets_.data(), targets_.size(),
@@ -255,6 +291,12 @@ class SymTableau {
       if (res == 2) const_flip ^= 1;
     }
     const uint64_t* spp = sp.data();
+    if (!dev_) {
+      size_t words = 0;
+      for (size_t i = 0; i < n_; ++i)
+        if (x_[i * wq_ + w] & m) words += hi_[i];
+      note_op(words);
+    }
     if (dev_) {
       flush_flips();
       spp = phase_dev_reduce(dev_, targets_.data(), targets_.size(),
@@ -284,6 +326,11 @@ class SymTableau {
   // the column-form mask fn(word).
   template <class F>
   void flip_rows(uint32_t sym, F&& fn) {
+    for_rows(fn, [&](size_t i) { flip_phase(i, sym); });
+  }
+  // visit(row - n) for every stabilizer row whose bit is set in fn(word)
+  template <class F, class V>
+  void for_rows(F&& fn, V&& visit) {
     for (size_t w = n_ / 64; w < rw_; ++w) {
       uint64_t v = fn(w);
       const size_t r0 = w * 64;
@@ -292,7 +339,7 @@ class SymTableau {
       while (v) {
         const size_t r = r0 + static_cast<size_t>(__builtin_ctzll(v));
         v &= v - 1;
-        flip_phase(r - n_, sym);
+        visit(r - n_);
       }
     }
   }
@@ -346,6 +393,28 @@ class SymTableau {
     }
   }
 
+  // Host or device phase matrix: a device row operation costs a launch (and,
+  // for a determined outcome, a round trip: ~15-50 us), a host one about
+  // 0.25 ns per 64-bit word XORed. Start on the host (small circuits, surface
+  // codes: few rows per operation) and move the matrix to the device after
+  // kHeavyOps consecutive measurements each XORing more than kHeavyWords
+  // (wide random circuits: hundreds of rows x thousands of words).
+  static constexpr size_t kHeavyWords = size_t{1} << 17;
+  static constexpr int kHeavyOps = 4;
+  void note_op(size_t words) { heavy_ = words > kHeavyWords ? heavy_ + 1 : 0; }
+  void move_to_device() {
+    may_move_ = false;
+    try {
+      dev_ = phase_dev_create(n_, ws_);
+      phase_dev_upload(dev_, ph_.data());
+    } catch (const std::runtime_error&) {  // no device memory: stay on the host
+      phase_dev_destroy(dev_);
+      dev_ = nullptr;
+      return;
+    }
+    std::vector<uint64_t>().swap(ph_);
+  }
+
   void flip_phase(size_t i, uint32_t sym) {
     if (dev_) {
       flips_.push_back(static_cast<uint64_t>(i) << 32 | sym);
@@ -397,6 +466,8 @@ class SymTableau {
     for (size_t k = 0; k < wq_; ++k) { xd[k] ^= xs[k]; zd[k] ^= zs[k]; }
   }
 
+  bool may_move_ = false;
+  int heavy_ = 0;          // consecutive heavy host row operations
   size_t n_, wq_, ws_;
   size_t rw_ = 0;          // words per qubit column (2n rows)
   bool cols_ = false;      // the qubit-major copy is current (row-major stale)
@@ -406,6 +477,7 @@ class SymTableau {
   PhaseDev* dev_ = nullptr;
   std::vector<uint64_t> flips_;    // queued (row << 32 | symbol) flips (dev_)
   std::vector<uint32_t> targets_;  // rows of the current device row operation
+  std::vector<uint32_t> rows_;     // scratch (pauli_x_all)
 };
 
 }  // namespace
@@ -428,15 +500,20 @@ Model run_initialization(const std::vector<Instr>& prog) {
   M.n_qubits = n;
   if (n == 0) return M;
 
-  // The phase matrix goes to the device when it is large (n x capacity
-  // bits >= 2^28, 32 MB) and a GPU is present; SP_FRONTEND_DEV=0/1 forces.
+  // Phase matrix: on the host, moved to the device when its row operations
+  // turn heavy (SymTableau::note_op), or from the start when it is very large
+  // (n x capacity bits >= 2^30, 128 MB) — if a GPU is present.
+  // SP_FRONTEND_DEV=0 keeps it on the host, =1 puts it on the device.
   const char* env = std::getenv("SP_FRONTEND_DEV");
   const double bits = static_cast<double>(n) * static_cast<double>(cap);
-  bool dev = env ? std::atoi(env) != 0 : bits >= static_cast<double>(1ull << 28);
-  if (dev && !phase_dev_available()) dev = false;
+  bool dev = env ? std::atoi(env) != 0 : bits >= static_cast<double>(1ull << 30);
+  // (a smaller matrix never has a row operation heavy enough to move)
+  const bool gpu = (dev || bits >= static_cast<double>(1ull << 24)) && phase_dev_available();
+  if (dev && !gpu) dev = false;
+  const bool may_move = !env && gpu;
   std::unique_ptr<SymTableau> tp;
   try {
-    tp = std::make_unique<SymTableau>(n, cap, dev);
+    tp = std::make_unique<SymTableau>(n, cap, dev, may_move);
   } catch (const std::runtime_error&) {  // no device memory for the phase matrix
     if (!dev) throw;
     tp = std::make_unique<SymTableau>(n, cap, false);
@@ -467,8 +544,7 @@ Model run_initialization(const std::vector<Instr>& prog) {
       case Op::R:
         // Reset = measure + X conditioned on the outcome (tableau.cpp:355-362).
         for (uint32_t a : q) {
-          auto e = t.measure(a, n_sym, M.groups);
-          for (uint32_t s : e) t.pauli(a, true, false, s);
+          t.pauli_x_all(a, t.measure(a, n_sym, M.groups));
         }
         break;
       // decompose_noise (circuit.cpp:228-281): one group per channel target.

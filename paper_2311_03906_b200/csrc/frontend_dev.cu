@@ -141,6 +141,11 @@ void phase_dev_xor_rows(PhaseDev* p, uint32_t src, const uint32_t* targets, size
   ck(cudaGetLastError(), "xor launch");
 }
 
+void phase_dev_upload(PhaseDev* p, const uint64_t* host) {
+  ck(cudaMemcpyAsync(p->ph, host, p->n_rows * p->ws * 8, cudaMemcpyHostToDevice, p->stream), "H2D");
+  ck(cudaStreamSynchronize(p->stream), "sync");
+}
+
 void phase_dev_clear_row(PhaseDev* p, uint32_t row, uint32_t words) {
   if (words == 0) return;
   ck(cudaMemsetAsync(p->ph + static_cast<uint64_t>(row) * p->ws, 0, words * 8ull, p->stream),

@@ -42,3 +42,18 @@ def test_device_phase_store_structured(monkeypatch, which):
             "padded": lambda: CI.gate_padding_pair()[1]}[which]()
     a, b = both(text, monkeypatch)
     assert same(a, b)
+
+
+@pytest.mark.parametrize("which", ["fig3c_300", "fig3b_400", "surface9"])
+def test_phase_store_moves_to_device_mid_pass(monkeypatch, which):
+    """Default mode: the pass starts on the host and moves its phase matrix
+    to the device once measurements XOR > 2^17 words each (fig3c n=300 after
+    a few layers); surface codes stay on the host. Same InitResult either way."""
+    text = {"fig3c_300": lambda: CI.bench_family("c", 300, 4),
+            "fig3b_400": lambda: CI.bench_family("b", 400, 5),
+            "surface9": lambda: CI.surface_code(9, 9, 1e-3)}[which]()
+    monkeypatch.setenv("SP_FRONTEND_DEV", "0")
+    a = run_initialization(text)
+    monkeypatch.delenv("SP_FRONTEND_DEV")
+    b = run_initialization(text)
+    assert same(a, b)
