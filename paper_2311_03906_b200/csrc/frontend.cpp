@@ -121,6 +121,33 @@ std::vector<Instr> parse_circuit(std::string_view text) {
 
 namespace {
 
+// The pass's inner loops, compiled for AVX-512 and AVX2 as well as the
+// baseline (picked at load time by the CPU): the word XOR of phase rows and
+// the x/z part of a rowsum (i-exponent of the product, then the XOR).
+#define SP_CLONES __attribute__((target_clones("avx512f", "avx2", "default")))
+SP_CLONES void xor_words(uint64_t* __restrict__ d, const uint64_t* __restrict__ s, size_t n) {
+  for (size_t k = 0; k < n; ++k) d[k] ^= s[k];
+}
+// i-exponent of (x1,z1) * (x2,z2) (single_qubit_phase_exponent, pauli.cpp:7-12,
+// summed over qubits) mod 4; then (x2,z2) ^= (x1,z1) when xor_in.
+SP_CLONES int product_exponent(const uint64_t* __restrict__ x1, const uint64_t* __restrict__ z1,
+                               uint64_t* __restrict__ x2, uint64_t* __restrict__ z2, size_t n,
+                               bool xor_in) {
+  int64_t plus = 0, minus = 0;
+  for (size_t k = 0; k < n; ++k) {
+    const uint64_t a = x1[k], b = z1[k], c = x2[k], d = z2[k];
+    const uint64_t p = (a & ~b & ~c & d) | (a & b & c & ~d) | (~a & b & c & d);
+    const uint64_t q = (a & ~b & c & d) | (a & b & ~c & d) | (~a & b & c & ~d);
+    plus += __builtin_popcountll(p);
+    minus += __builtin_popcountll(q);
+    if (xor_in) {
+      x2[k] = c ^ a;
+      z2[k] = d ^ b;
+    }
+  }
+  return static_cast<int>((((plus - minus) % 4) + 4) % 4);
+}
+
 // Stabilizer tableau with symbolic phases on the stabilizer half only.
 // Rows [0, n) destabilizers, [n, 2n) stabilizers; x/z row-major packed.
 class SymTableau {
@@ -278,14 +305,13 @@ class SymTableau {
       if (!(x_[i * wq_ + w] & m)) continue;
       const uint64_t* x1 = &x_[(n_ + i) * wq_];
       const uint64_t* z1 = &z_[(n_ + i) * wq_];
-      int res = phase_exponent(x1, z1, sx.data(), sz.data());
+      int res = product_exponent(x1, z1, sx.data(), sz.data(), wq_, true);
       if (res & 1) throw std::logic_error("non-hermitian generator product: tableau corrupt");
-      for (size_t k = 0; k < wq_; ++k) { sx[k] ^= x1[k]; sz[k] ^= z1[k]; }
       if (dev_) {
         targets_.push_back(static_cast<uint32_t>(i));
       } else {
         const uint64_t* p1 = &ph_[i * ws_];
-        for (size_t k = 0; k < hi_[i]; ++k) sp[k] ^= p1[k];
+        xor_words(sp.data(), p1, hi_[i]);
       }
       shi = std::max<size_t>(shi, hi_[i]);
       if (res == 2) const_flip ^= 1;
@@ -429,41 +455,29 @@ class SymTableau {
     flips_.clear();
   }
 
-  // i-exponent of (source * target), single_qubit_phase_exponent summed over
-  // qubits (pauli.cpp:7-12), mod 4.
-  int phase_exponent(const uint64_t* x1, const uint64_t* z1, const uint64_t* x2,
-                     const uint64_t* z2) const {
-    int64_t plus = 0, minus = 0;
-    for (size_t k = 0; k < wq_; ++k) {
-      uint64_t a = x1[k], b = z1[k], c = x2[k], d = z2[k];
-      uint64_t p = (a & ~b & ~c & d) | (a & b & c & ~d) | (~a & b & c & d);
-      uint64_t q = (a & ~b & c & d) | (a & b & ~c & d) | (~a & b & c & ~d);
-      plus += __builtin_popcountll(p);
-      minus += __builtin_popcountll(q);
-    }
-    return static_cast<int>((((plus - minus) % 4) + 4) % 4);
-  }
-
   // dst := src * dst (rowsum_rows, tableau.cpp:113-144). Destabilizer phases
   // are not tracked (they never reach an outcome), so only stabilizer targets
   // pay for the phase.
   void rowsum(size_t dst, size_t src) {
     uint64_t* xd = &x_[dst * wq_]; uint64_t* zd = &z_[dst * wq_];
     const uint64_t* xs = &x_[src * wq_]; const uint64_t* zs = &z_[src * wq_];
-    if (dst >= n_) {
-      int res = phase_exponent(xs, zs, xd, zd);
+    if (dst < n_) {
+      for (size_t k = 0; k < wq_; ++k) { xd[k] ^= xs[k]; zd[k] ^= zs[k]; }
+      return;
+    }
+    {
+      int res = product_exponent(xs, zs, xd, zd, wq_, true);
       if (res & 1) throw std::logic_error("non-hermitian generator product: tableau corrupt");
       size_t di = dst - n_, si = src - n_;
       if (dev_) {
         targets_.push_back(static_cast<uint32_t>(di));  // XORed by the caller in one launch
       } else {
         uint64_t* pd = &ph_[di * ws_]; const uint64_t* ps = &ph_[si * ws_];
-        for (size_t k = 0; k < hi_[si]; ++k) pd[k] ^= ps[k];
+        xor_words(pd, ps, hi_[si]);
       }
       hi_[di] = std::max(hi_[di], hi_[si]);
       if (res == 2) flip_phase(di, 0);
     }
-    for (size_t k = 0; k < wq_; ++k) { xd[k] ^= xs[k]; zd[k] ^= zs[k]; }
   }
 
   bool may_move_ = false;
