@@ -39,13 +39,38 @@ __global__ void k_flips(uint64_t* ph, uint64_t ws, const uint64_t* flips, size_t
   }
 }
 
+// Row lists of up to kParamRows rows travel in the kernel parameters (no
+// host->device copy per operation; CUDA 12.1+ takes 32 KB of parameters).
+constexpr uint32_t kParamRows = 2048;
+struct RowList {
+  uint32_t r[kParamRows];
+};
+
 // ph[t] ^= ph[src] over words [0, words) for every target t (blockIdx.y).
-__global__ void k_xor_rows(uint64_t* ph, uint64_t ws, uint32_t src, const uint32_t* targets,
-                           uint32_t words) {
+__device__ __forceinline__ void xor_row(uint64_t* ph, uint64_t ws, uint32_t src, uint32_t dst,
+                                        uint32_t words) {
   const uint64_t* s = ph + static_cast<uint64_t>(src) * ws;
-  uint64_t* d = ph + static_cast<uint64_t>(targets[blockIdx.y]) * ws;
+  uint64_t* d = ph + static_cast<uint64_t>(dst) * ws;
   for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < words; w += gridDim.x * blockDim.x)
     d[w] ^= s[w];
+}
+__global__ void k_xor_rows(uint64_t* ph, uint64_t ws, uint32_t src, const uint32_t* targets,
+                           uint32_t words) {
+  xor_row(ph, ws, src, targets[blockIdx.y], words);
+}
+__global__ void k_xor_rows_p(uint64_t* ph, uint64_t ws, uint32_t src, const __grid_constant__ RowList t,
+                             uint32_t words) {
+  xor_row(ph, ws, src, t.r[blockIdx.y], words);
+}
+
+// out[w] = XOR over the listed rows of ph[row][w], words [0, words).
+__global__ void k_reduce_rows_p(const uint64_t* ph, uint64_t ws, const __grid_constant__ RowList rows,
+                                uint32_t n_rows, uint32_t words, uint64_t* out) {
+  for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < words; w += gridDim.x * blockDim.x) {
+    uint64_t a = 0;
+    for (uint32_t r = 0; r < n_rows; ++r) a ^= ph[static_cast<uint64_t>(rows.r[r]) * ws + w];
+    out[w] = a;
+  }
 }
 
 // out[w] = XOR over rows of ph[row][w], words [0, words).
@@ -132,8 +157,15 @@ void phase_dev_flips(PhaseDev* p, const uint64_t* flips, size_t n) {
 void phase_dev_xor_rows(PhaseDev* p, uint32_t src, const uint32_t* targets, size_t n_t,
                         uint32_t words) {
   if (n_t == 0 || words == 0) return;
-  stage(p, p->d_rows, p->rows_cap, targets, n_t);
   const unsigned gx = std::max(1u, std::min(64u, (words + 255) / 256));
+  if (n_t <= kParamRows) {
+    RowList t;
+    std::copy(targets, targets + n_t, t.r);
+    k_xor_rows_p<<<dim3(gx, static_cast<unsigned>(n_t)), 256, 0, p->stream>>>(p->ph, p->ws, src, t, words);
+    ck(cudaGetLastError(), "xor launch");
+    return;
+  }
+  stage(p, p->d_rows, p->rows_cap, targets, n_t);
   for (size_t t0 = 0; t0 < n_t; t0 += 65535) {
     const unsigned gy = static_cast<unsigned>(std::min<size_t>(65535, n_t - t0));
     k_xor_rows<<<dim3(gx, gy), 256, 0, p->stream>>>(p->ph, p->ws, src, p->d_rows + t0, words);
@@ -158,10 +190,17 @@ const uint64_t* phase_dev_reduce(PhaseDev* p, const uint32_t* rows, size_t n_r, 
     std::fill(p->h_out, p->h_out + words, 0ull);
     return p->h_out;
   }
-  stage(p, p->d_rows, p->rows_cap, rows, n_r);
   const int grid = static_cast<int>(std::min<uint32_t>((words + 255) / 256, 1024));
-  k_reduce_rows<<<grid, 256, 0, p->stream>>>(p->ph, p->ws, p->d_rows, static_cast<uint32_t>(n_r),
-                                             words, p->d_out);
+  if (n_r <= kParamRows) {
+    RowList t;
+    std::copy(rows, rows + n_r, t.r);
+    k_reduce_rows_p<<<grid, 256, 0, p->stream>>>(p->ph, p->ws, t, static_cast<uint32_t>(n_r), words,
+                                                 p->d_out);
+  } else {
+    stage(p, p->d_rows, p->rows_cap, rows, n_r);
+    k_reduce_rows<<<grid, 256, 0, p->stream>>>(p->ph, p->ws, p->d_rows, static_cast<uint32_t>(n_r),
+                                               words, p->d_out);
+  }
   ck(cudaGetLastError(), "reduce launch");
   ck(cudaMemcpyAsync(p->h_out, p->d_out, words * 8ull, cudaMemcpyDeviceToHost, p->stream), "D2H");
   ck(cudaStreamSynchronize(p->stream), "sync");
