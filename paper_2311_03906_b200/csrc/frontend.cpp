@@ -202,6 +202,66 @@ class SymTableau {
     for (size_t w = 0; w < rw_; ++w) { xb[w] ^= xa[w]; za[w] ^= zb[w]; }
   }
 
+  // One gate instruction while the row-major form is current: applied in
+  // place instead of converting to the qubit-major form (a conversion is
+  // 2 x rw x wq 64 x 64 transposes; in the paper's Fig. 3 families every
+  // layer would otherwise convert twice: gates, then measurements).
+  // H/S/S_DAG on distinct qubits: one sweep over the rows with a qubit mask
+  // (the gates act on different qubits, so each row's constant-phase flips
+  // add up: their parity is flipped in). CX on distinct qubits: per pair
+  // over the rows, when that is cheaper than the conversion.
+  // Returns false when the instruction should go the qubit-major way.
+  bool layer_in_rows(Op op, const std::vector<uint32_t>& q) {
+    if (cols_ || q.empty()) return false;
+    // Work in the row-major form since the last conversion stays below one
+    // conversion's (ops: ~1,500 per 64 x 64 block, ~8 per swept row word,
+    // ~12 per row per CX), so a run of small instructions cannot cost more
+    // than converting would have.
+    const double conv = 2.0 * rw_ * wq_ * 1500.0;
+    const double cost = op == Op::CX ? static_cast<double>(q.size() / 2) * 2.0 * n_ * 12.0
+                                     : 2.0 * n_ * wq_ * 8.0;
+    if (row_work_ + cost > conv) return false;
+    row_work_ += cost;
+    mask_.assign(wq_, 0);
+    for (uint32_t a : q) {
+      if (mask_[a / 64] & bit(a)) return false;  // a repeated qubit: apply gate by gate
+      mask_[a / 64] |= bit(a);
+    }
+    const uint64_t* mk = mask_.data();
+    if (op == Op::CX) {
+      for (size_t i = 0; i + 1 < q.size(); i += 2) {
+        const uint32_t a = q[i], b = q[i + 1];
+        const size_t wa = a / 64, wb = b / 64;
+        const uint64_t ma = bit(a), mb = bit(b);
+        for (size_t r = 0; r < 2 * n_; ++r) {
+          uint64_t* x = &x_[r * wq_]; uint64_t* z = &z_[r * wq_];
+          const bool xa = x[wa] & ma, za = z[wa] & ma, xb = x[wb] & mb, zb = z[wb] & mb;
+          if (r >= n_ && xa && zb && !(xb ^ za)) flip_phase(r - n_, 0);
+          if (xa) x[wb] ^= mb;
+          if (zb) z[wa] ^= ma;
+        }
+      }
+      return true;
+    }
+    for (size_t r = 0; r < 2 * n_; ++r) {
+      uint64_t* x = &x_[r * wq_]; uint64_t* z = &z_[r * wq_];
+      int par = 0;
+      for (size_t k = 0; k < wq_; ++k) {
+        const uint64_t xv = x[k], zv = z[k], m = mk[k];
+        if (op == Op::H) {
+          par += __builtin_popcountll(xv & zv & m);
+          x[k] = (xv & ~m) | (zv & m);
+          z[k] = (zv & ~m) | (xv & m);
+        } else {
+          par += __builtin_popcountll((op == Op::S ? xv & zv : xv & ~zv) & m);
+          z[k] = zv ^ (xv & m);
+        }
+      }
+      if (r >= n_ && (par & 1)) flip_phase(r - n_, 0);
+    }
+    return true;
+  }
+
   // Symbol-conditioned Paulis (tableau.cpp:80-100): XOR symbol s into the
   // phase of every stabilizer row the Pauli anticommutes with.
   // Works in whichever layout is current (a reset's conditional X follows
@@ -391,6 +451,7 @@ class SymTableau {
     if (!cols_) return;
     convert(false);
     cols_ = false;
+    row_work_ = 0;
   }
   void convert(bool to_c) {
     uint64_t blk[64];
@@ -492,6 +553,8 @@ class SymTableau {
   std::vector<uint64_t> flips_;    // queued (row << 32 | symbol) flips (dev_)
   std::vector<uint32_t> targets_;  // rows of the current device row operation
   std::vector<uint32_t> rows_;     // scratch (pauli_x_all)
+  std::vector<uint64_t> mask_;     // scratch (layer_in_rows)
+  double row_work_ = 0;            // layer_in_rows work since the last to_rows
 };
 
 }  // namespace
@@ -547,13 +610,16 @@ Model run_initialization(const std::vector<Instr>& prog) {
   for (const auto& in : prog) {
     const auto& q = in.targets;
     switch (in.op) {
-      case Op::H: for (uint32_t a : q) t.h(a); break;
-      case Op::S: for (uint32_t a : q) t.s(a); break;
-      case Op::SDag: for (uint32_t a : q) t.s_dag(a); break;
+      case Op::H: if (!t.layer_in_rows(in.op, q)) for (uint32_t a : q) t.h(a); break;
+      case Op::S: if (!t.layer_in_rows(in.op, q)) for (uint32_t a : q) t.s(a); break;
+      case Op::SDag: if (!t.layer_in_rows(in.op, q)) for (uint32_t a : q) t.s_dag(a); break;
       case Op::X: for (uint32_t a : q) t.pauli(a, true, false, 0); break;
       case Op::Y: for (uint32_t a : q) t.pauli(a, true, true, 0); break;
       case Op::Z: for (uint32_t a : q) t.pauli(a, false, true, 0); break;
-      case Op::CX: for (size_t i = 0; i + 1 < q.size(); i += 2) t.cx(q[i], q[i + 1]); break;
+      case Op::CX:
+        if (!t.layer_in_rows(in.op, q))
+          for (size_t i = 0; i + 1 < q.size(); i += 2) t.cx(q[i], q[i + 1]);
+        break;
       case Op::M: for (uint32_t a : q) push_row(t.measure(a, n_sym, M.groups)); break;
       case Op::R:
         // Reset = measure + X conditioned on the outcome (tableau.cpp:355-362).
