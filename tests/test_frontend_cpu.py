@@ -141,3 +141,42 @@ def test_frontend_matches_live_reference_wide_random(ref):
         got = run_initialization(text)
         assert got.n_sym == c.n_sym
         assert np.array_equal(got.row_ptr, c.row_ptr) and np.array_equal(got.sym_idx, c.sym_idx)
+
+
+def test_row_form_gate_layers_match_reference(ref):
+    """Gate instructions right after measurements run in the row-major form
+    (masked sweep for H/S/S_DAG, per pair for CX) while cheaper than a layout
+    conversion; repeated qubits and long CX layers go the qubit-major way.
+    Layers mixing all of these, with noise and resets, agree with the
+    reference's pass."""
+    rng = CI.MT19937_64(6060)
+    for n in (70, 130, 200):
+        qs = list(range(n))
+        lines = []
+
+        def subset(frac):
+            return [q for q in qs if rng.below(1000) < frac * 1000]
+
+        for layer in range(12):
+            for name in ("H", "S_DAG", "S"):
+                t = subset(0.4)
+                if t and layer % 3 == 2:
+                    t = t + t[:1]  # a repeated qubit
+                if t:
+                    lines.append(f"{name} " + " ".join(map(str, t)))
+            for i in range(n - 1, 0, -1):
+                j = rng.below(i + 1)
+                qs[i], qs[j] = qs[j], qs[i]
+            k = 3 if layer % 2 else n // 2
+            lines.append("CX " + " ".join(map(str, qs[: 2 * k])))
+            qs.sort()
+            lines.append("DEPOLARIZE1(0.01) " + " ".join(map(str, subset(0.3) or [0])))
+            lines.append("M " + " ".join(map(str, subset(0.2) or [1])))
+            if layer % 4 == 1:
+                lines.append("R " + " ".join(map(str, subset(0.1) or [2])))
+        lines.append("M " + " ".join(map(str, range(n))))
+        text = "\n".join(lines) + "\n"
+        c = ref.circuit(text)
+        got = run_initialization(text)
+        assert got.n_sym == c.n_sym
+        assert np.array_equal(got.row_ptr, c.row_ptr) and np.array_equal(got.sym_idx, c.sym_idx)
