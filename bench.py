@@ -1,12 +1,12 @@
 #!/usr/bin/env python
 """Benchmark of the fused SymPhase sampling hot path on B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg3] [--impl ours|reference]
 
 A step = one fused sampling pass (Philox draws + GF(2) product + bit-packed
 measurement records written to HBM) over this rank's shot range of the
-workload. Default workload: BASELINE.json configs[1] (rotated surface code
-d=5, 5 rounds, p=1e-3, 10^7 shots per GPU). For N > 1 every rank samples a
+workload. Default workload: BASELINE.json configs[2] (rotated surface code
+d=15, 15 rounds, p=1e-3, 10^8 shots per GPU). For N > 1 every rank samples a
 disjoint global shot range (weak scaling) and the per-measurement flip counts
 are all-reduced over NCCL (the path's only exchange).
 
@@ -30,7 +30,7 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "sampled measurement bits/sec"
 UNIT = "bits/s"
-R_INT_PLANNING = 148 * 64 * 1.965e9  # LOP3-class ops/s (SURVEY §8(d) planning value)
+R_INT = 1.8426e13  # LOP3 ops/s measured on the B200 box (tools/microbench.cu, profiles/microbench_r01.jsonl)
 
 WORKLOADS = {
     "cfg1": ("cfg1: repetition code d=5, 5 rounds, p=0.01 (BASELINE.json configs[0])", 10**6),
@@ -43,9 +43,33 @@ WORKLOADS = {
 }
 
 
+def circuits_module():
+    """circuits.py loaded on its own (pure Python, no package import), so the
+    reference arm never loads the repo's native library."""
+    import importlib.util
+    name = "_sp_circuits_standalone"
+    if name in sys.modules:
+        return sys.modules[name]
+    spec = importlib.util.spec_from_file_location(
+        name, ROOT / "paper_2311_03906_b200" / "circuits.py")
+    mod = importlib.util.module_from_spec(spec)
+    sys.modules[name] = mod
+    spec.loader.exec_module(mod)
+    return mod
+
+
 def circuit_text(cfg: str) -> str:
-    from paper_2311_03906_b200 import circuits as CI
-    return CI.CONFIGS[cfg]["text"]()
+    return circuits_module().CONFIGS[cfg]["text"]()
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def measured_peaks():
@@ -144,64 +168,110 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def cpu_reference_rate(init_text: str, n_meas: int, target_s: float, seed: int = 42):
-    """The reference CPU sampler on this host: oracle/_ref (the unmodified
-    reference library), draw_assignments + sample + encode_shots(b8) per
-    shot chunk on every host thread; else the C port (1 thread)."""
-    import oracle
-    threads = os.cpu_count() or 1
-    if oracle.have_ref():
-        c = oracle.Ref().circuit(init_text)
-        chunk = 16384
-        probe = max(chunk * threads, chunk)
-        t = c.time(probe, chunk, threads, seed, 1)
+class ReferenceCPU:
+    """The reference CPU sampler on this host: oracle/_ref, the unmodified
+    reference library built from its sources (kind "reference"). The circuit
+    goes through the reference's own parse_circuit + run_initialization once
+    (tens of seconds at cfg3); every timing below is then the reference's
+    sampling API only.
+
+    figure (a) "as shipped": one draw_assignments(n) (single-threaded, as
+        written) + sample(threads = all host threads) + encode_shots(b8) —
+        cmd_sample's timed region, cliffsym.cpp:108-113 — on n shots.
+    figure (b) "API over shot chunks": every host thread runs
+        draw_assignments(chunk, seed + c) + sample(.., 1) + encode_shots(b8)
+        over its share of 16,384-shot chunks (the faster of the two; the
+        reported reference value).
+    Sampling cost is linear in the shot count (sampler.cpp:52-57, 88-104), so
+    a bounded sample of the workload's shots gives its rate."""
+
+    CHUNK = 16384
+
+    def __init__(self, text: str):
+        import oracle
+        if not oracle.have_ref():
+            raise RuntimeError("oracle/_ref not built (make -C oracle where /root/reference "
+                               "exists; the .so then travels with the repo)")
+        t0 = time.perf_counter()
+        self.c = oracle.Ref().circuit(text)
+        self.init_s = time.perf_counter() - t0
+        self.n_meas = self.c.n_meas
+        self.threads = os.cpu_count() or 1
+
+    def _sized(self, mode, target_s, seed, probe):
+        t = self.c.time(probe, self.CHUNK, self.threads, seed, mode)
+        if t < 0:
+            raise RuntimeError("reference timing failed")
         shots = int(max(probe, min(probe * target_s / max(t, 1e-6), 2e8)))
-        shots = (shots + chunk - 1) // chunk * chunk
-        t = c.time(shots, chunk, threads, seed, 1)
-        sample = (f"{shots} shots of the workload circuit, {chunk}-shot chunks over {threads} "
-                  f"threads; each chunk = reference draw_assignments + sample(threads=1) + "
-                  f"encode_shots(b8) (cliffsym.cpp:108-113 timed region)")
-        return n_meas * shots / t, threads, "reference", sample, t
-    from paper_2311_03906_b200 import run_initialization
-    port = oracle.Port()
-    init = run_initialization(init_text)
-    shots = 20000
-    t0 = time.perf_counter()
-    S = port.draw_assignments(init, shots, seed)
-    m = port.sample(init.row_ptr, init.sym_idx, S, shots)
-    port.encode(m, init.n_meas, shots, "b8")
-    t = time.perf_counter() - t0
-    return n_meas * shots / t, 1, "port", f"{shots} shots, oracle C port, 1 thread", t
+        shots = (shots + self.CHUNK - 1) // self.CHUNK * self.CHUNK
+        return shots
+
+    def figure_b(self, target_s: float, seed: int, shots: int | None = None):
+        if shots is None:
+            shots = self._sized(1, target_s, seed, self.CHUNK * self.threads)
+        t = self.c.time(shots, self.CHUNK, self.threads, seed, 1)
+        return self.n_meas * shots / t, shots, t
+
+    def figure_a(self, target_s: float, seed: int, shots: int | None = None):
+        if shots is None:
+            shots = self._sized(0, target_s, seed, 4096)
+        t = self.c.time(shots, shots, self.threads, seed, 0)
+        return self.n_meas * shots / t, shots, t
+
+    def describe(self, shots_b: int, shots_a: int) -> str:
+        return (f"oracle/_ref (unmodified reference library), host {cpu_model()} x "
+                f"{self.threads} threads; figure (b): {shots_b} shots of the workload in "
+                f"{self.CHUNK}-shot chunks, each draw_assignments + sample(threads=1) + "
+                f"encode_shots(b8) on one thread; figure (a): one cmd_sample timed region "
+                f"(cliffsym.cpp:108-113: draw_assignments + sample(threads={self.threads}) + "
+                f"encode_shots(b8)) on {shots_a} shots")
 
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
-        return
+        return  # one CPU measurement per job, on rank 0
     desc, shots_per_gpu = WORKLOADS[args.config]
-    text = circuit_text(args.config)
-    from paper_2311_03906_b200 import run_initialization
-    n_meas = run_initialization(text).n_meas
-    rates, secs, cores, kind, sample = [], [], 1, "port", ""
+    if args.shots:
+        shots_per_gpu = args.shots
+    ref = ReferenceCPU(circuit_text(args.config))
     per_step = float(os.environ.get("SP_REF_STEP_SECONDS", "4"))
+    shots_b = ref._sized(1, per_step, 41, ref.CHUNK * ref.threads)
+    shots_a = ref._sized(0, per_step / 2, 41, 4096)
+    rates, secs, rates_a = [], [], []
     for i in range(args.warmup + args.steps):
-        r, cores, kind, sample, t = cpu_reference_rate(text, n_meas, per_step, seed=42 + i)
+        r, _, t = ref.figure_b(per_step, 42 + i, shots_b)
         if i >= args.warmup:
             rates.append(r)
             secs.append(t)
+    for i in range(2):
+        r, _, _ = ref.figure_a(per_step / 2, 900 + i, shots_a)
+        rates_a.append(r)
     value = statistics.median(rates)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "n_gpus": args.gpus, "gpus_used": 0, "cpu_threads": ref.threads,
+        "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": statistics.mean(secs) * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-        "config": {"workload": desc, "shots_per_gpu": shots_per_gpu,
-                   "parallelism": "host threads (reference has no GPU path)"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
-                         "sample": sample},
+        "config": bench_config(args, desc, shots_per_gpu),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": ref.threads,
+                         "kind": "reference", "cpu_model": cpu_model(),
+                         "sample": ref.describe(shots_b, shots_a),
+                         "figure_a_as_shipped": statistics.median(rates_a),
+                         "figure_b_chunked": value},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "details": {"reference_init_seconds": round(ref.init_s, 3),
+                    "parallelism": "host threads (the reference has no GPU path)",
+                    "timed_shots_per_step": shots_b},
     }
     print(json.dumps(line), flush=True)
+
+
+def bench_config(args, desc, shots_per_gpu):
+    """The `config` object both arms print (identical for the same flags)."""
+    return {"workload": desc, "shots_per_gpu": shots_per_gpu, "records": args.records,
+            "seed_base": 1000}
 
 
 def run_ours(args):
@@ -217,6 +287,7 @@ def run_ours(args):
     dev = torch.device(f"cuda:{local}")
 
     from paper_2311_03906_b200 import Sampler, run_initialization
+    from paper_2311_03906_b200.distributed import CountPipeline
 
     desc, shots = WORKLOADS[args.config]
     if args.shots:
@@ -234,8 +305,10 @@ def run_ours(args):
     init_s = time.perf_counter() - t0
     smp = Sampler(init, device=local)
     T = smp.shot_tile
-    shots = (shots + T - 1) // T * T
-    shot_begin = rank * shots  # disjoint global shot ranges, tile-aligned
+    # rank r samples global shots [r * span, r * span + shots): disjoint,
+    # tile-aligned ranges (streams are keyed by the global tile)
+    span = (shots + T - 1) // T * T
+    shot_begin = rank * span
     # auto: the tiled layout when a tile's rows are short (T < 1024: 16-128
     # bytes per row per tile, scattered across measurement-major rows), like
     # the reference's own 512 x 512 tiles; measurement-major otherwise
@@ -248,27 +321,13 @@ def run_ours(args):
     run = ((lambda n, seed, **kw: smp.sample_tiled(n, seed, out=out, **kw)) if tiled else
            (lambda n, seed, **kw: smp.sample(n, seed, out=out, **kw)))
     # Per-measurement counts, double-buffered: step i's NCCL all-reduce runs
-    # asynchronously (NCCL's stream) while step i+1 samples into the other
-    # buffer; a buffer's previous reduce completes before it is reused, and
-    # the last step waits for both before its end event.
-    counts2 = [torch.zeros(init.n_meas, dtype=torch.int64, device=dev) for _ in range(2)]
-    pending = [None, None]
+    # asynchronously while step i+1 samples into the other buffer.
+    pipe = CountPipeline(init.n_meas, dev, world)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
     stream = torch.cuda.current_stream()
 
     def step(i, last=False):
-        b = i % 2
-        if pending[b] is not None:
-            pending[b].wait()
-            pending[b] = None
-        run(shots, 1000 + i, shot_begin=shot_begin, counts=counts2[b])
-        if world > 1:
-            pending[b] = dist.all_reduce(counts2[b], async_op=True)
-        if last:
-            for k in range(2):
-                if pending[k] is not None:
-                    pending[k].wait()
-                    pending[k] = None
+        pipe.step(i, lambda c: run(shots, 1000 + i, shot_begin=shot_begin, counts=c), last=last)
 
     for i in range(args.warmup):
         step(i, last=i == args.warmup - 1)
@@ -313,7 +372,7 @@ def run_ours(args):
     t_max = float(t_tensor.item())
     value = init.n_meas * shots * world / t_max
 
-    # Kernel-only timing (no collective) for the roofline, same stream.
+    # Kernel-only timing (no counts, no collective) for the roofline, same stream.
     kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(max(3, args.steps))]
     for i, (a, b) in enumerate(kev):
@@ -327,8 +386,10 @@ def run_ours(args):
     # End to end through the public API with HOST buffers: each step uploads
     # the model (M_sym CSR + group table) from host memory, samples, encodes
     # the reference's b8 records on the device and copies them to pinned host
-    # memory (cmd_sample's timed region, cliffsym.cpp:108-113).
-    e2e_n = shots
+    # memory (cmd_sample's timed region, cliffsym.cpp:108-113). The rate is
+    # per shot, so a bounded shot count (<= 2^23 per step) keeps the pinned
+    # buffer small at cfg3.
+    e2e_n = min(shots, 1 << 23)
     host_out = torch.empty(smp.encoded_size(e2e_n, "b8"), dtype=torch.uint8, pin_memory=True)
     h2d = init.row_ptr.nbytes + init.sym_idx.nbytes + init.groups.nbytes
     e2e_t = []
@@ -350,7 +411,7 @@ def run_ours(args):
         peak, peak_src = measured_peaks()
         nbytes, ops = algorithmic(init, shots)
         achieved = nbytes / (k_ms / 1e3) / 1e9
-        t_hbm, t_int = nbytes / (peak * 1e9), ops / R_INT_PLANNING
+        t_hbm, t_int = nbytes / (peak * 1e9), ops / R_INT
         traffic = None
         tp = ROOT / "profiles" / "ncu_traffic.json"
         if tp.exists():
@@ -364,13 +425,12 @@ def run_ours(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
             "data": "synthetic (seeded circuit generators, SURVEY Appendix A; seeds 1000+i)",
-            "config": {
-                "workload": desc, "shots_per_gpu": shots, "n_meas": init.n_meas,
-                "n_sym": init.n_sym, "nnz": init.nnz, "shot_tile": T,
+            "config": bench_config(args, desc, shots),
+            "details": {
+                "n_meas": init.n_meas, "n_sym": init.n_sym, "nnz": init.nnz, "shot_tile": T,
                 "parallelism": f"shot-range sharding x{world}" + (
                     f", NCCL all_reduce of per-{args.records[:-1]} counts per step (async, "
                     "overlapping the next step)" if world > 1 else ""),
-                "records": args.records,
                 "output": ("tiled [tile][row][T/64]" if tiled else "measurement-major") +
                           " u64 bit-sliced records in HBM + per-row counts",
                 "l2": "flushed between timed steps (256 MiB memset outside the events); "
@@ -382,13 +442,13 @@ def run_ours(args):
                 "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                 "kernel": "k1_fused", "kernel_ms": k_ms, "alg_bytes": nbytes,
                 "alg_int_ops": ops, "t_hbm_ms": t_hbm * 1e3, "t_int_ms": t_int * 1e3,
-                "frac_of_roofline_time": max(t_hbm, t_int) * 1e3 / k_ms,
+                "r_int": R_INT, "frac_of_roofline_time": max(t_hbm, t_int) * 1e3 / k_ms,
                 "frac_vs_8TBs": (nbytes / (k_ms / 1e3)) / 8.0e12,
                 "peak_source": peak_src,
             },
             "clocks": clk.summary(),
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-                    "d2h_bytes_per_step": int(written),
+                    "d2h_bytes_per_step": int(written), "shots_per_step": e2e_n,
                     "path": "Sampler.load + Sampler.sample_to_host (C ABI sp_load_msym_csr/"
                             "sp_load_groups/sp_sample_to_host), b8 records to pinned host; "
                             "each step re-uploads the model arrays (the derived plan is reused "
@@ -397,12 +457,39 @@ def run_ours(args):
             "wall_s_timed": wall,
         }
         if world == 1 and not args.no_cpu_baseline and args.records == "measurements":
-            r, cores, kind, sample, t = cpu_reference_rate(text, init.n_meas, 10.0)
-            line["cpu_baseline"] = {"value": r, "unit": UNIT, "cores": cores, "kind": kind,
-                                    "sample": sample, "seconds": round(t, 3)}
+            ref = ReferenceCPU(text)
+            rb, sb, tb = ref.figure_b(10.0, 42)
+            ra, sa, _ = ref.figure_a(5.0, 43)
+            line["cpu_baseline"] = {"value": rb, "unit": UNIT, "cores": ref.threads,
+                                    "kind": "reference", "cpu_model": cpu_model(),
+                                    "sample": ref.describe(sb, sa), "seconds": round(tb, 3),
+                                    "figure_a_as_shipped": ra, "figure_b_chunked": rb}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def free_port() -> int:
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def relaunch_if_needed(args) -> None:
+    """`--gpus N` without a launcher: re-exec under torchrun, one rank per GPU."""
+    if "WORLD_SIZE" in os.environ:
+        world = int(os.environ["WORLD_SIZE"])
+        if args.impl == "ours" and world != args.gpus:
+            raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+        return
+    if args.gpus > 1 and args.impl == "ours":
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+               f"--master-port={free_port()}", str(Path(__file__).resolve()), *sys.argv[1:]]
+        raise SystemExit(subprocess.call(cmd))
 
 
 def main():
@@ -410,7 +497,9 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="cfg2", choices=sorted(WORKLOADS))
+    ap.add_argument("--config", default="cfg3", choices=sorted(WORKLOADS),
+                    help="BASELINE.json workload; cfg3 (configs[2], the 1/2/4/8-GPU config) "
+                         "by default")
     ap.add_argument("--shots", type=int, default=0, help="override shots per GPU")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -422,6 +511,9 @@ def main():
                          "orientation), tiled (sp_sample_tiled), or auto (tiled when the shot "
                          "tile is under 1024 shots)")
     args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3  # timing rule: at least 3 untimed warm-up steps
+    relaunch_if_needed(args)
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -50,3 +50,51 @@ def sample_sharded(sampler, total_shots: int, seed: int, out=None, counts=None, 
     if counts is not None:
         all_reduce_counts(counts, group)
     return begin, count, out
+
+
+class CountPipeline:
+    """Per-step count reduction, double-buffered (the bench's step loop).
+
+    Step i samples into buffer i % 2 (zeroed first: the sampler adds into it)
+    and starts an asynchronous all-reduce of it; step i+1 samples into the
+    other buffer while that reduce runs. A buffer's previous reduce is waited
+    for before the buffer is reused, and `on_reduced(step, counts)` then sees
+    the step's global counts. `flush()` waits for everything in flight.
+    """
+
+    def __init__(self, n: int, device, world: int, group=None, on_reduced=None):
+        import torch
+        self.world, self.group, self.on_reduced = world, group, on_reduced
+        self.bufs = [torch.zeros(n, dtype=torch.int64, device=device) for _ in range(2)]
+        self.pending = [None, None]  # (work handle or None, step index)
+
+    def _finish(self, b: int):
+        work, i = self.pending[b]
+        if work is not None:
+            work.wait()
+        self.pending[b] = None
+        if self.on_reduced is not None:
+            self.on_reduced(i, self.bufs[b])
+
+    def step(self, i: int, sample_into, last: bool = False):
+        """sample_into(counts) adds this rank's step-i counts into `counts`."""
+        import torch.distributed as dist
+        b = i % 2
+        if self.pending[b] is not None:
+            self._finish(b)
+        buf = self.bufs[b]
+        buf.zero_()
+        sample_into(buf)
+        work = None
+        if self.world > 1:
+            work = dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=self.group, async_op=True)
+        self.pending[b] = (work, i)
+        if last:
+            self.flush()
+        return buf
+
+    def flush(self):
+        for b in sorted(range(2), key=lambda k: -1 if self.pending[k] is None
+                        else self.pending[k][1]):
+            if self.pending[b] is not None:
+                self._finish(b)

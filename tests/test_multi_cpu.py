@@ -76,3 +76,73 @@ def test_gloo_two_rank_counts_match_single_process(port):
     for rank, b, n, counts in res:
         assert np.array_equal(counts, want), rank
     assert sorted((b, n) for _, b, n, _ in res)[0][0] == 0
+
+
+class _FakeSampler:
+    """CPU stand-in for Sampler: deterministic per-(global shot) outcomes, so
+    the union of the ranks' shards equals one single-process run."""
+
+    shot_tile = 64
+
+    def __init__(self, n_meas):
+        self.n_meas = n_meas
+
+    def counts_for(self, begin, count, seed):
+        shots = np.arange(begin, begin + count, dtype=np.int64)
+        rows = np.arange(self.n_meas, dtype=np.int64)[:, None]
+        bits = ((shots[None, :] * 2654435761 + rows * 40503 + seed) >> 7) & 1
+        return bits.sum(axis=1)
+
+    def sample(self, count, seed, shot_begin=0, out=None, counts=None):
+        if counts is not None:
+            counts += torch.from_numpy(self.counts_for(shot_begin, count, seed))
+        return out
+
+
+def _pipeline_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2311_03906_b200.distributed import CountPipeline, sample_sharded
+
+    smp = _FakeSampler(5)
+    total = 1000
+    # sample_sharded: this rank's shard + the count all-reduce
+    c = torch.zeros(5, dtype=torch.int64)
+    b, n, _ = sample_sharded(smp, total, 3, counts=c)
+    # bench's step loop: double-buffered async reduces, buffers reused
+    seen = {}
+    pipe = CountPipeline(5, "cpu", world,
+                         on_reduced=lambda i, t: seen.__setitem__(i, t.clone().numpy()))
+    for i in range(6):
+        pipe.step(i, lambda cnt, i=i: smp.sample(n, 100 + i, shot_begin=b, counts=cnt),
+                  last=i == 5)
+    q.put((rank, b, n, c.numpy(), seen))
+    dist.destroy_process_group()
+
+
+def test_gloo_sample_sharded_and_step_pipeline():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p_port = _free_port()
+    procs = [ctx.Process(target=_pipeline_worker, args=(r, world, p_port, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    smp = _FakeSampler(5)
+    total = 1000
+    spans = sorted((b, n) for _, b, n, _, _ in res)
+    assert spans[0][0] == 0 and sum(n for _, n in spans) == total
+    want = smp.counts_for(0, total, 3)
+    for rank, b, n, c, seen in res:
+        assert np.array_equal(c, want), rank
+        assert sorted(seen) == list(range(6))
+        for i, got in seen.items():
+            # each step's reduced counts = the sum over ranks of that step
+            # only (the buffer is zeroed before reuse, nothing accumulates)
+            want_i = sum(smp.counts_for(bb, nn, 100 + i) for bb, nn in spans)
+            assert np.array_equal(got, want_i), (rank, i)
