@@ -232,13 +232,34 @@ class Sampler:
         return self._torch.empty((rows, max(words(n_shots), 1)), dtype=self._torch.int64,
                                  device=f"cuda:{self.device}")
 
+    def _check_dev(self, t, min_words: int, what: str):
+        """The C ABI takes raw device pointers and cannot see buffer sizes:
+        check dtype, device and size here before any device write."""
+        if t is None:
+            return
+        if t.dtype != self._torch.int64 and t.dtype != self._torch.uint64:
+            raise TypeError(f"{what}: expected int64/uint64 words, got {t.dtype}")
+        if t.device.type != "cuda" or t.device.index != self.device:
+            raise ValueError(f"{what}: expected a tensor on cuda:{self.device}, got {t.device}")
+        if not t.is_contiguous():
+            raise ValueError(f"{what}: must be contiguous")
+        if t.numel() < min_words:
+            raise ValueError(f"{what}: needs >= {min_words} words, has {t.numel()}")
+
+    def _check_matrix(self, t, rows: int, n_shots: int, what: str):
+        self._check_dev(t, 0, what)
+        if t.dim() != 2 or t.shape[0] < rows or t.shape[1] < words(n_shots):
+            raise ValueError(f"{what}: needs shape >= ({rows}, {words(n_shots)}), "
+                             f"got {tuple(t.shape)}")
+
     # -- hot path -------------------------------------------------------------
     def sample(self, n_shots: int, seed: int, shot_begin: int = 0, out=None, counts=None):
         """Fused draw_assignments + sample (K1/K4): measurement-major records."""
         if out is None:
             out = self.empty_bits(self.n_meas, n_shots)
-        N.check(self._L.sp_sample(self._h, seed, shot_begin, n_shots, _ptr(out),
-                                  out.shape[1] if out.dim() == 2 else words(n_shots),
+        self._check_matrix(out, self.n_meas, n_shots, "out")
+        self._check_dev(counts, self.n_meas, "counts")
+        N.check(self._L.sp_sample(self._h, seed, shot_begin, n_shots, _ptr(out), out.shape[1],
                                   _ptr(counts)))
         return out
 
@@ -251,6 +272,8 @@ class Sampler:
         if out is None:
             out = self._torch.empty(max(self.tiled_words(n_shots), 1), dtype=self._torch.int64,
                                     device=f"cuda:{self.device}")
+        self._check_dev(out, self.tiled_words(n_shots), "out")
+        self._check_dev(counts, self.n_meas, "counts")
         N.check(self._L.sp_sample_tiled(self._h, seed, shot_begin, n_shots, _ptr(out),
                                         _ptr(counts)))
         return out
@@ -259,6 +282,8 @@ class Sampler:
         """Tiled records -> measurement-major words [n_meas, ceil(n/64)]."""
         if out is None:
             out = self.empty_bits(self.n_meas, n_shots)
+        self._check_dev(tiled, self.tiled_words(n_shots), "tiled")
+        self._check_matrix(out, self.n_meas, n_shots, "out")
         N.check(self._L.sp_untile(self._h, _ptr(tiled), n_shots, _ptr(out), out.shape[1]))
         return out
 
@@ -274,6 +299,7 @@ class Sampler:
         """draw_assignments: the symbol assignment matrix S (row 0 = ones)."""
         if out is None:
             out = self.empty_bits(self.n_sym, n_shots)
+        self._check_matrix(out, self.n_sym, n_shots, "out")
         N.check(self._L.sp_draw_assignments(self._h, seed, shot_begin, n_shots, _ptr(out),
                                             out.shape[1]))
         return out
@@ -283,6 +309,8 @@ class Sampler:
         n_sym_S = S.shape[0] if n_sym_S is None else n_sym_S
         if out is None:
             out = self.empty_bits(self.n_meas, n_shots)
+        self._check_matrix(S, n_sym_S, n_shots, "S")
+        self._check_matrix(out, self.n_meas, n_shots, "out")
         N.check(self._L.sp_sample_given_S(self._h, _ptr(S), n_sym_S, S.shape[1], n_shots,
                                           _ptr(out), out.shape[1]))
         return out

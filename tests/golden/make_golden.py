@@ -10,7 +10,11 @@ Fixtures (all produced by the reference's own public API):
                  i.e. cliffsym sample --seed S --shots N (cliffsym.cpp:108-113)
   given_s.npz    sample(expressions, batch) on seeded random batches shaped like
                  acceptance.cpp:312-361 (criterion 6) and tile-straddling sizes
+  large.json     run_initialization of the BASELINE workloads cfg2-cfg4 (too
+                 large to store): sha256 + length of every InitResult array
+                 and of the circuit text (`python make_golden.py large`)
 """
+import hashlib
 import json
 import sys
 from pathlib import Path
@@ -111,7 +115,32 @@ def given_s():
     np.savez_compressed(OUT / "given_s.npz", **d)
 
 
-if __name__ == "__main__":
+def digest(a) -> dict:
+    a = np.ascontiguousarray(a)
+    return {"len": int(a.size), "dtype": str(a.dtype),
+            "sha256": hashlib.sha256(a.tobytes()).hexdigest()}
+
+
+def large():
+    d = {}
+    for cfg in ("cfg2", "cfg3", "cfg4"):
+        text = CI.CONFIGS[cfg]["text"]()
+        c = ref.circuit(text)  # the reference's own pass (~1 min at cfg3/cfg4)
+        d[cfg] = {"text": digest(np.frombuffer(text.encode(), dtype=np.uint8)),
+                  "n_meas": int(c.n_meas), "n_sym": int(c.n_sym),
+                  "row_ptr": digest(c.row_ptr.astype(np.uint64)),
+                  "sym_idx": digest(c.sym_idx.astype(np.uint32)),
+                  "dist": digest(c.dist.astype(np.uint8)),
+                  "param": digest(c.param.astype(np.float64)),
+                  "first": digest(c.first.astype(np.uint32)),
+                  "arity": digest(c.arity.astype(np.uint32))}
+        print(cfg, d[cfg]["n_meas"], d[cfg]["n_sym"], flush=True)
+    (OUT / "large.json").write_text(json.dumps(d, indent=1) + "\n")
+
+
+if __name__ == "__main__" and sys.argv[1:] == ["large"]:
+    large()
+elif __name__ == "__main__":
     named = circuits()
     frontend(named)
     draws(named)

@@ -180,3 +180,17 @@ def test_row_form_gate_layers_match_reference(ref):
         got = run_initialization(text)
         assert got.n_sym == c.n_sym
         assert np.array_equal(got.row_ptr, c.row_ptr) and np.array_equal(got.sym_idx, c.sym_idx)
+
+
+@pytest.mark.parametrize("cfg", ["cfg2", "cfg3", "cfg4"])
+def test_baseline_workloads_match_reference_pass(cfg):
+    """cfg2-cfg4 are too large to store: tests/golden/large.json holds sha256
+    digests of the reference pass's arrays (make_golden.py large); the
+    circuit text is pinned by its digest too."""
+    import hashlib
+    from pathlib import Path
+    want = json.loads((Path(__file__).resolve().parent / "golden" / "large.json").read_text())[cfg]
+    text = CI.CONFIGS[cfg]["text"]()
+    assert hashlib.sha256(text.encode()).hexdigest() == want["text"]["sha256"]
+    from test_gpu_large import digest_ok
+    assert digest_ok(run_initialization(text), want)
