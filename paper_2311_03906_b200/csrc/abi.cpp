@@ -114,7 +114,7 @@ struct sp_ctx {
   DevPlan dp;
   // plan buffers
   DBuf b_row_ptr, b_sym_idx, b_col_ptr, b_col_rows, b_dense, b_dense_gm, b_first, b_arity, b_dist, b_param,
-      b_row_const_compat, b_ones, b_dense_sym, b_coin_ptr, b_coin_rows, b_cls, b_cls_groups, b_thin_src, b_g_masks,
+      b_row_const_compat, b_ones, b_dense_sym, b_coin_ptr, b_coin_rows, b_cls, b_cls_groups, b_thin_src, b_mech_pat, b_len_bnd, b_g_masks,
       b_desc, b_colrow, b_live_groups, b_path_rows, b_path_ptr, b_path_par, b_round_ptr, b_plist, b_keep_rows, b_timers;
   uint64_t dnnz = 0;  // nnz of D (chain transform), for reports
   // K2's own copy of the rows (independent of the group table)
@@ -464,6 +464,7 @@ void build_plan(sp_ctx* c) {
     double p;
     uint32_t lpc;  // flip-list length class (live): every pattern's D list has <= lpc rows
     std::vector<uint32_t> groups;
+    bool runs = false;  // one-list groups sorted by list length (length runs, ClassInfo::bnd)
   };
   std::vector<Cls> live_cls, dead_cls, null_cls;
   std::map<std::tuple<uint8_t, uint64_t, uint32_t>, size_t> live_key, dead_key, null_key;
@@ -471,6 +472,7 @@ void build_plan(sp_ctx* c) {
   // D columns of the pattern's symbols), rounded up to 2, 4, 8, 16 (0: longer).
   std::vector<uint32_t> mrg_a, mrg_b;
   const bool split_lists = env_long("SP_LIST_CLASSES", 1) != 0;
+  const bool len_runs = env_long("SP_LEN_RUNS", 1) != 0;
   auto list_class = [&](const sp_group& gr) -> uint32_t {
     const uint32_t npat = (1u << gr.arity) - 1;
     size_t mx = 0;
@@ -597,6 +599,66 @@ void build_plan(sp_ctx* c) {
       for (uint32_t g : bk.first) merged[g] = 1;
     }
   }
+  // Mechanism decomposition (exact). DEPOLARIZE1(p) is the composition of
+  // three independent Pauli channels X, Y, Z each firing with q1 =
+  // (1 - sqrt(1 - 4p/3)) / 2, and DEPOLARIZE2(p) of fifteen independent ones
+  // (one per non-identity two-qubit Pauli) with q2 = (1 - (1 - 16p/15)^(1/8))
+  // / 2: the XOR of the fired patterns' symplectic vectors is uniform over the
+  // non-zero vectors with total rate p (Fourier over GF(2)^n: each non-trivial
+  // character sees the factor (1 - 2q) from exactly half of the patterns). So
+  // every remaining multi-list DEPOLARIZE group becomes one Bernoulli(q)
+  // pseudo variable per pattern, whose D column is that pattern's flip list:
+  // no pattern digits (four skips per Philox block), and classes of one exact
+  // list length (no padded XORs). Patterns that flip nothing become dead
+  // pseudo variables, walked only by the draw kernel, which XORs each firing's
+  // pattern into the source group's symbols (mech_pat) — so S is exactly
+  // DEPOLARIZE-distributed and K1 == M_sym . S(draw) still holds bit for bit.
+  // Valid while q < 1/2 (p < 3/4, resp. 15/16); SP_MECH=0 turns it off.
+  std::vector<uint32_t> mech_pat;      // pseudo j -> pattern of its source group (0: not a mechanism)
+  std::vector<uint8_t> mech(G, 0);
+  if (env_long("SP_MECH", 1) != 0) {
+    std::vector<uint32_t> la, lb;
+    for (uint64_t g = 1; g < G; ++g) {
+      const sp_group& gr = h.groups[g];
+      const double p = gr.param;
+      if (merged[g] || !(p > 0.0)) continue;
+      double q;
+      if (gr.dist == SP_DIST_DEPOLARIZE1 && p < 0.75) q = 0.5 * (1.0 - std::sqrt(1.0 - 4.0 * p / 3.0));
+      else if (gr.dist == SP_DIST_DEPOLARIZE2 && p < 15.0 / 16.0)
+        q = 0.5 * (1.0 - std::pow(1.0 - 16.0 * p / 15.0, 0.125));
+      else continue;
+      if (!(q > 0.0 && q < 0.5)) continue;
+      bool live = false;
+      for (uint32_t b = 0; b < gr.arity; ++b) live |= col_len(gr.first_symbol + b) > 0;
+      if (!live) continue;  // a dead group keeps its plain dead class
+      const uint32_t npat = (1u << gr.arity) - 1;
+      for (uint32_t pat = 1; pat <= npat; ++pat) {
+        la.clear();
+        for (uint32_t b = 0; b < gr.arity; ++b) {
+          if (!((pat >> b) & 1u)) continue;
+          const uint64_t sidx = gr.first_symbol + b;
+          lb.clear();
+          std::set_symmetric_difference(la.begin(), la.end(), dcol_rows.begin() + dcol_ptr[sidx],
+                                        dcol_rows.begin() + dcol_ptr[sidx + 1], std::back_inserter(lb));
+          la.swap(lb);
+        }
+        const uint64_t sym = dcol_ptr.size() - 1;
+        dcol_rows.insert(dcol_rows.end(), la.begin(), la.end());
+        dcol_ptr.push_back(dcol_rows.size());
+        sp_group pg{};
+        pg.dist = SP_DIST_BERNOULLI;
+        pg.param = q;
+        pg.first_symbol = static_cast<uint32_t>(sym);
+        pg.arity = 1;
+        pseudo.push_back(pg);
+        thin_src.push_back(static_cast<uint32_t>(g));
+        mech_pat.resize(pseudo.size(), 0);
+        mech_pat.back() = pat;
+      }
+      mech[g] = 1;
+    }
+  }
+  mech_pat.resize(pseudo.size(), 0);
   const bool merged_any =
       std::any_of(thin_src.begin(), thin_src.end(), [](uint32_t v) { return v == UINT32_MAX; });
   auto grp = [&](uint64_t g) -> const sp_group& { return g < G ? h.groups[g] : pseudo[g - G]; };
@@ -609,10 +671,12 @@ void build_plan(sp_ctx* c) {
     bool live = false;
     uint64_t flips = 0;
     for (uint32_t b = 0; b < gr.arity; ++b) {
-      live |= is_pseudo || col_len(gr.first_symbol + b) > 0;
+      // (a pseudo variable is live when its flip list is not empty)
+      live |= is_pseudo ? dcol_len(gr.first_symbol + b) > 0 : col_len(gr.first_symbol + b) > 0;
       flips += dcol_len(gr.first_symbol + b);
     }
     if (live && !is_pseudo) live_groups.push_back(static_cast<uint32_t>(g));  // compat (M space)
+    if (!is_pseudo && mech[g]) continue;  // sampled and drawn through its mechanisms
     if (!is_pseudo && thinned[g]) {
       // fires through its pseudo variable; the draw kernel's second pass
       // draws its null patterns (Bernoulli null_p over the trials it did not fire)
@@ -661,7 +725,11 @@ void build_plan(sp_ctx* c) {
     std::memcpy(&pbits, &p, 8);
     // Live classes are split by flip-list length, so a slice's warp only
     // runs as many list entries as its class needs.
-    const uint32_t lpc = live && split_lists ? list_class(gr) : 0u;
+    // One-list (Bernoulli) groups of one p form one class whatever their
+    // list lengths: they are sorted by length below and the kernel bounds
+    // each step by the longest list of its run (SP_LEN_RUNS=0: split).
+    const bool runs = live && len_runs && gr.arity == 1;
+    const uint32_t lpc = runs ? 99u : live && split_lists ? list_class(gr) : 0u;
     auto key = std::make_tuple(gr.dist, pbits, lpc);
     auto& keymap = live ? live_key : dead_key;
     auto& cls = live ? live_cls : dead_cls;
@@ -677,7 +745,7 @@ void build_plan(sp_ctx* c) {
     // into the next longer class (or the longest one into its neighbour),
     // so no class is too small to fill its slices. lpc 0 (lists > 16) is
     // the longest.
-    auto rank = [](uint32_t l) { return l == 0 ? 99u : l; };
+    auto rank = [](uint32_t l) { return l == 0 ? 98u : l; };  // 99: a length-run family
     std::stable_sort(live_cls.begin(), live_cls.end(), [&](const Cls& a, const Cls& b) {
       if (a.dist != b.dist) return a.dist < b.dist;
       if (a.p != b.p) return a.p < b.p;
@@ -707,6 +775,14 @@ void build_plan(sp_ctx* c) {
       }
       for (Cls& c : f) {
         std::sort(c.groups.begin(), c.groups.end());
+        if (c.lpc == 99u) {  // length runs: groups by (list length, id)
+          std::stable_sort(c.groups.begin(), c.groups.end(), [&](uint32_t a, uint32_t b) {
+            return dcol_len(grp(a).first_symbol) < dcol_len(grp(b).first_symbol);
+          });
+          const uint64_t mx = dcol_len(grp(c.groups.back()).first_symbol);
+          c.lpc = mx <= 16 ? static_cast<uint32_t>(std::max<uint64_t>(mx, 1)) : 0u;
+          c.runs = mx <= 16;
+        }
         merged.push_back(std::move(c));
       }
       i = j;
@@ -917,6 +993,7 @@ void build_plan(sp_ctx* c) {
   const double E = std::min(std::max(ev_tile / d.gen_warps, 32.0), 2048.0);
   std::vector<ClassInfo> cls_info;
   std::vector<uint32_t> cls_groups;
+  std::vector<uint32_t> len_bnd;
   std::vector<uint4> desc;
   std::vector<uint16_t> colrow16;
   // Exact flip lists per (group, pattern): XOR of the D columns of the
@@ -939,6 +1016,16 @@ void build_plan(sp_ctx* c) {
       ci.npat = cl.dist == SP_DIST_DEPOLARIZE2 ? 15 : cl.dist == SP_DIST_DEPOLARIZE1 ? 3 : 1;
       ci.lp = cl.lpc;  // the kernel runs min(lp, plan lp) list entries for this class
       ci.pbase = static_cast<uint32_t>(pl_off.size() - 1);
+      if (live && cl.runs) {  // (first position << 5 | length) per run, then a sentinel
+        ci.bnd = static_cast<uint32_t>(len_bnd.size());
+        uint64_t prev = UINT64_MAX;
+        for (size_t i = 0; i < cl.groups.size(); ++i) {
+          const uint64_t len = std::max<uint64_t>(dcol_len(grp(cl.groups[i]).first_symbol), 1);
+          if (len != prev) len_bnd.push_back(static_cast<uint32_t>(i << 5) | static_cast<uint32_t>(len));
+          prev = len;
+        }
+        len_bnd.push_back(0xFFFFFFFFu);
+      }
       cls_info.push_back(ci);
       for (uint32_t g : cl.groups) {
         cls_groups.push_back(g);
@@ -1062,6 +1149,10 @@ void build_plan(sp_ctx* c) {
   apply_segments(live_nseg);
   if (thin_src.empty()) thin_src.push_back(UINT32_MAX);  // never read; keeps the buffer non-null
   d.thin_src = c->b_thin_src.upload(thin_src, s);
+  if (len_bnd.empty()) len_bnd.push_back(0xFFFFFFFFu);
+  d.len_bnd = c->b_len_bnd.upload(len_bnd, s);
+  if (mech_pat.empty()) mech_pat.push_back(0);
+  d.mech_pat = c->b_mech_pat.upload(mech_pat, s);
   d.g_masks = c->b_g_masks.upload(g_masks, s);
   d.cls_groups = c->b_cls_groups.upload(cls_groups, s);
   d.desc = c->b_desc.upload(desc, s);
@@ -1177,6 +1268,7 @@ void build_plan(sp_ctx* c) {
   d.live_groups = c->b_live_groups.upload(live_groups, s);
   d.debug_mode = static_cast<uint32_t>(env_long("SP_DEBUG_MODE", 0));
   d.wait_ns = static_cast<uint32_t>(std::max<long>(32, env_long("SP_WAIT_NS", 256)));
+  d.bulk_store = static_cast<uint32_t>(env_long("SP_BULK", 1));
   if (env_long("SP_PHASE_TIMERS", 0)) {
     std::vector<long long> z(8, 0);
     d.timers = c->b_timers.upload(z, s);

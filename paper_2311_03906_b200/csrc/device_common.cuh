@@ -99,7 +99,9 @@ __device__ __forceinline__ uint32_t group_bits_compat(uint32_t dist, double p, u
 struct Segment {
   uint32_t g0, s0;  // first trial = (class position g0, shot s0 in the tile)
   uint32_t len, seg, goff, dist, pbase, npat;
-  uint32_t lp;      // list entries the class needs (ClassInfo::lp)
+  uint32_t lp;      // list entries the class needs (ClassInfo::lp), or of the current run
+  uint32_t bnd;     // next length run in len_bnd (0xFFFFFFFF: none)
+  uint32_t nbp;     // first class position of that run (0xFFFFFFFF: none)
   float clg;
 };
 
@@ -133,6 +135,35 @@ __device__ __forceinline__ void segment_init(Segment& sg, const ClassInfo* cls, 
   sg.npat = ci.npat;
   sg.lp = ci.lp;
   sg.clg = ci.clg;
+  sg.bnd = ci.bnd;
+  sg.nbp = 0xFFFFFFFFu;
+}
+
+// Length runs of a sorted class: the run holding class position g0 sets
+// sg.lp, and sg.nbp is where the next run starts.
+__device__ __forceinline__ void segment_runs(Segment& sg, const uint32_t* len_bnd) {
+  if (sg.bnd == 0xFFFFFFFFu) return;
+  uint32_t e = len_bnd[sg.bnd];
+  sg.lp = e & 31u;
+  for (;;) {
+    const uint32_t n = len_bnd[sg.bnd + 1];
+    if ((n >> 5) > sg.g0) {
+      sg.nbp = n >> 5;
+      ++sg.bnd;
+      return;
+    }
+    ++sg.bnd;
+    sg.lp = n & 31u;
+  }
+}
+// Advance the runs to class position g (non-decreasing along a walk).
+__device__ __forceinline__ void segment_runs_to(Segment& sg, const uint32_t* len_bnd, uint32_t g) {
+  while (g >= sg.nbp) {
+    const uint32_t e = len_bnd[sg.bnd];
+    sg.lp = e & 31u;
+    const uint32_t n = len_bnd[++sg.bnd];
+    sg.nbp = n >> 5;
+  }
 }
 
 __device__ __forceinline__ uint4 segment_philox(const Segment& sg, const RoundKeys& K,
@@ -317,6 +348,23 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity, uint32
   }
 }
 
+
+// Bulk (TMA) copies shared -> global for the drain: the async proxy reads the
+// tile, so threads that wrote it (generic proxy) fence first; completion is
+// tracked per issuing thread with bulk groups.
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_store(void* gdst, uint32_t ssrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(ssrc),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit_and_wait_read() {
+  asm volatile(
+      "cp.async.bulk.commit_group;\n\t"
+      "cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
 
 // 16-byte shared store of v (keep != 0) or of zeros, as two predicated
 // stores instead of four selects.

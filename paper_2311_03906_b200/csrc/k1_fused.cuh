@@ -33,7 +33,7 @@ template <bool kStaged, bool kRowStaged, int kLp, bool kPadPred, int kEB>
 __global__ void __launch_bounds__(kFusedThreads, 1)
 k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, uint64_t n_shots,
          uint64_t* __restrict__ out, uint64_t ld, uint64_t tile_stride,
-         unsigned long long* __restrict__ counts, bool vec) {
+         unsigned long long* __restrict__ counts, bool vec, uint32_t bulk) {
   extern __shared__ __align__(16) uint8_t smem[];
   const uint32_t tw = P.tw, tw4_log2 = P.t_log2 - 7, tw4 = 1u << tw4_log2;
   // Tile rows, then a spare region (never read) that absorbs the XORs of
@@ -108,6 +108,15 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
     CLS = s_cls;
     DESC = s_desc;
     COLROW = s_col;
+  }
+  if (!kStaged && P.cls_staged) {  // class table (a few hundred bytes): searched at every slice
+    ClassInfo* s_cls = reinterpret_cast<ClassInfo*>(p);
+    p += align16(sizeof(ClassInfo) * P.n_cls_live);
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(P.cls);
+    uint32_t* dst = reinterpret_cast<uint32_t*>(s_cls);
+    for (uint32_t i = threadIdx.x; i < P.n_cls_live * (sizeof(ClassInfo) / 4); i += blockDim.x)
+      dst[i] = src[i];
+    CLS = s_cls;
   }
   if (P.coins_staged) {  // coin columns and symbols: small, read every tile
     uint32_t* s_cptr = reinterpret_cast<uint32_t*>(p);
@@ -251,6 +260,13 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
           return;
         }
         if constexpr (kLp > 0) {
+          if (sg.nbp != 0xFFFFFFFFu) {  // length runs: the step's longest list is at its last firing
+            uint32_t gm = 0;
+#pragma unroll
+            for (int k = 0; k < kSlots; ++k)
+              if ((f.v >> k) & 1u) gm = max(gm, f.g[k]);
+            segment_runs_to(sg, P.len_bnd, __reduce_max_sync(kFull, gm));
+          }
           const uint32_t lpu = sg.lp == 0 ? static_cast<uint32_t>(kLp) : sg.lp;
           if constexpr (kPre > 0 && kPre < kSlots) load_lists(bern_tag, f, kPre, kSlots);
 #pragma unroll
@@ -262,9 +278,11 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
               const uint32_t bit = ((f.v >> k) & 1u) << (f.shot[k] & 31);
 #pragma unroll
               for (int e = 0; e < kLp; ++e) {
-                // the class's lists end by entry lpu (warp-uniform): skip the
-                // padding in power-of-two blocks
-                if (e >= 2 && (e & (e - 1)) == 0 && lpu <= static_cast<uint32_t>(e)) break;
+                // the class's (or length run's) lists end by entry lpu
+                // (warp-uniform): skip the padding
+                // (checked per pair of entries: an odd length runs one
+                // padding entry, which XORs the spare region)
+                if (e >= 2 && (e & 1) == 0 && lpu <= static_cast<uint32_t>(e)) break;
                 uint32_t a;
                 bool real;
                 if constexpr (kEB == 1) {
@@ -322,6 +340,7 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
         seg = __shfl_sync(kFull, seg, 0);
         if (seg >= P.n_seg_live || (P.debug_mode & 2u)) return false;
         segment_init(sn, CLS, P.n_cls_live, seg, P.t_log2);
+        segment_runs(sn, P.len_bnd);
         return true;
       };
       uint4 r[kBlocks];
@@ -335,6 +354,8 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
         atomicAdd(reinterpret_cast<unsigned long long*>(P.timers) + 0, tw1 - tw0);
         atomicAdd(reinterpret_cast<unsigned long long*>(P.timers) + 1, clock64() - tw1);
       }
+      // the drain's TMA copy (async proxy) reads what these XORs wrote
+      if (bulk) fence_proxy_async_smem();
       mbar_arrive(mbar_full + b);
     }
   } else {
@@ -406,6 +427,101 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
           }
         }
       };
+      if (bulk && valid == (static_cast<uint64_t>(1) << P.t_log2) && !(P.debug_mode & 8u)) {
+        // TMA drain: rows are rebuilt in place (every final row value stays
+        // in the tile), then the tile leaves for HBM as bulk copies — one
+        // for the whole tile in the tiled layout, one per row segment in the
+        // measurement-major one — and is cleared once the copy engine has
+        // read it. No per-thread global stores or address arithmetic.
+        auto count_item = [&](auto wp_tag, uint32_t k, uint4 v) {
+          constexpr bool kWarpPath = decltype(wp_tag)::value;  // a warp per row (T = 4096)
+          uint32_t pc = __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
+          if constexpr (kWarpPath) {
+            if (cnt_lanes == 32) {
+              asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(cnt_s + ((k * 32 + lane) << 2)),
+                           "r"(pc)
+                           : "memory");
+            } else {
+              pc = __reduce_add_sync(kFull, pc);
+              if (lane == 0) atomicAdd(&cnt[k], pc);
+            }
+          } else {
+            if (pc) atomicAdd(&cnt[k], pc);
+          }
+        };
+        auto rebuild = [&](auto wp_tag) {
+          if (P.flat_rows) {  // no parents: the tile already holds the records
+            if (with_counts)
+              for (uint32_t j = ct; j < (P.n_meas << tw4_log2); j += nct)
+                count_item(wp_tag, j >> tw4_log2, t4[j]);
+            return;
+          }
+          for (uint32_t rd = 0; rd < P.n_rounds; ++rd) {
+            const uint32_t p0 = P.round_ptr[rd], p1 = P.round_ptr[rd + 1];
+            const uint32_t tasks = (p1 - p0) << tw4_log2;
+            const uint32_t tasks_rounded = (tasks + 31) & ~31u;
+            for (uint32_t j = ct; j < tasks_rounded; j += nct) {
+              const bool act = j < tasks;
+              const uint32_t pth = act ? p0 + (j >> tw4_log2) : p0;
+              const uint32_t q = j & (tw4 - 1);
+              const int32_t par = act ? PPAR[pth] : -1;
+              uint4 prev = par >= 0 ? t4[(static_cast<uint32_t>(par) << tw4_log2) + q]
+                                    : make_uint4(0, 0, 0, 0);
+              const uint32_t xe = act ? PPTR[pth + 1] : 0;
+              uint32_t x = act ? PPTR[pth] : 0;
+              // two rows per iteration, the next row's tile word prefetched
+              // (path_rows is padded, so x + 2 <= n_meas is readable)
+              uint32_t ka = PROWS[x] & 0xFFFFu;
+              uint4 ca = t4[(ka << tw4_log2) + q];
+              for (; x + 2 <= xe; x += 2) {
+                const uint32_t kb = PROWS[x + 1] & 0xFFFFu;
+                const uint4 cb = t4[(kb << tw4_log2) + q];
+                const uint4 va = xor4(ca, prev);
+                t4[(ka << tw4_log2) + q] = va;
+                if (with_counts) count_item(wp_tag, ka, va);
+                ka = PROWS[x + 2] & 0xFFFFu;
+                ca = t4[(ka << tw4_log2) + q];
+                prev = xor4(cb, va);
+                t4[(kb << tw4_log2) + q] = prev;
+                if (with_counts) count_item(wp_tag, kb, prev);
+              }
+              if (x < xe) {
+                const uint4 va = xor4(ca, prev);
+                t4[(ka << tw4_log2) + q] = va;
+                if (with_counts) count_item(wp_tag, ka, va);
+              }
+            }
+            if (rd + 1 < P.n_rounds) named_sync(kBarDrain, nct);
+          }
+        };
+        if (tw4 >= 32) rebuild(std::true_type{});
+        else rebuild(std::false_type{});
+        fence_proxy_async_smem();
+        named_sync(kBarDrain, nct);
+        const uint32_t row_bytes = tw * 4u;
+        if (bulk == 1) {
+          if (ct == 0) {
+            bulk_store(tbase, t4_s, P.n_meas * row_bytes);
+            bulk_commit_and_wait_read();
+          }
+        } else {
+          bool issued = false;
+          for (uint32_t k = ct; k < P.n_meas; k += nct) {
+            bulk_store(tbase + static_cast<uint64_t>(k) * ld, t4_s + k * row_bytes, row_bytes);
+            issued = true;
+          }
+          if (issued) bulk_commit_and_wait_read();
+        }
+        named_sync(kBarDrain, nct);  // the copy engine has read the whole tile
+        for (uint32_t j = ct; j < (P.n_meas << tw4_log2); j += nct) t4[j] = make_uint4(0, 0, 0, 0);
+        if (ct == 0) segctr[b] = 0;
+        if (P.timers && lane == 0) {
+          atomicAdd(reinterpret_cast<unsigned long long*>(P.timers) + 2, td1 - td0);
+          atomicAdd(reinterpret_cast<unsigned long long*>(P.timers) + 3, clock64() - td1);
+        }
+        if (i + n_buf < n_my) mbar_arrive(mbar_empty + b);
+        continue;
+      }
       if (P.flat_rows && !(P.debug_mode & 8u)) {
         // No parents (every row its own path, nothing kept): one pass over
         // the tile in row order, clearing as it goes.
@@ -515,13 +631,25 @@ int launch_k1(const DevPlan& P, const LaunchCfg& L, const RoundKeys& K, uint64_t
               uint32_t n_tiles, uint64_t n_shots, uint64_t* out, uint64_t ld, uint64_t tstride,
               unsigned long long* cnt) {
   auto kern = k1_fused<kStaged, kRowStaged, kLp, kPadPred, kEB>;
-  const size_t smem = fused_smem_bytes(P, P.t_log2, kStaged, kRowStaged, P.n_buf);
+  size_t smem = fused_smem_bytes(P, P.t_log2, kStaged, kRowStaged, P.n_buf);
+  DevPlan Q = P;
+  const size_t cls_bytes = align16(sizeof(ClassInfo) * P.n_cls_live);
+  Q.cls_staged = !kStaged && smem + cls_bytes <= L.smem_optin;
+  if (Q.cls_staged) smem += cls_bytes;
   int grid = 0;
   const int threads = static_cast<int>(P.cta_threads);
   if (persistent_grid(kern, L, smem, n_tiles, P.cta_per_sm, &grid, threads)) return -1;
   const bool vec = (ld % 2 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0);
-  kern<<<grid, threads, smem, L.stream>>>(P, K, tile0, n_tiles, n_shots, out, ld, tstride, cnt,
-                                          vec);
+  // TMA bulk stores of finished tiles: 1 = the whole tile is one contiguous
+  // block (tiled layout), 2 = one copy per row segment (measurement-major,
+  // worth it from 128-byte segments up), 0 = per-thread 16-byte stores.
+  // (per-row copies measured slower than the 16-byte stores at cfg2: 145
+  // rows x 512 bytes per tile; SP_BULK=2 forces them)
+  const uint32_t bulk = !P.bulk_store || !vec ? 0u
+                        : (ld * 2 == P.tw && tstride == static_cast<uint64_t>(P.n_meas) * ld) ? 1u
+                        : P.bulk_store == 2 && P.tw * 4 >= 128 ? 2u : 0u;
+  kern<<<grid, threads, smem, L.stream>>>(Q, K, tile0, n_tiles, n_shots, out, ld, tstride, cnt,
+                                          vec, bulk);
   return check_launch() ? -1 : 1;
 }
 

@@ -156,12 +156,18 @@ __global__ void d_segments(const DevPlan P, const RoundKeys K, uint64_t tile0, u
         if (j >= n_shots) continue;
         uint32_t gid = P.cls_groups[sg.goff + f.g[k]];
         uint32_t pat = f.pat[k];
+        bool mech = false;
         if (pass == 0 && gid >= P.n_groups) {
+          const uint32_t mp = P.mech_pat[gid - P.n_groups];
           gid = P.thin_src[gid - P.n_groups];
           if (gid == UINT32_MAX) continue;  // a merged pseudo group: not a symbol of S
+          if (mp) {  // one mechanism (Pauli pattern) of its source group
+            pat = mp;
+            mech = true;
+          }
         }
         const uint32_t first = P.g_first[gid];
-        if (pass == 1 || P.g_masks[gid] != 0) {
+        if (!mech && (pass == 1 || P.g_masks[gid] != 0)) {
           const uint64_t gj = shot0 + j;
           const uint32_t h = philox10(make_uint4(gid, static_cast<uint32_t>(gj),
                                                  (static_cast<uint32_t>(gj >> 32) & 0xFFFFFFu) |

@@ -30,6 +30,10 @@ struct ClassInfo {
   uint32_t pbase = 0;   // first flip list of the class (lists in plist)
   uint32_t npat = 1;    // non-identity patterns per group: 1, 3 or 15
   uint32_t lp = 0;      // longest flip list of the class (2/4/8/16; 0 = longer)
+  // Bernoulli classes hold their groups sorted by flip-list length; len_bnd
+  // [bnd ..] lists (first class position << 5 | length) of each length run,
+  // ending with a sentinel, so a walk knows the longest list of its step.
+  uint32_t bnd = 0xFFFFFFFFu;  // none: every list runs lp entries
 };
 
 // Everything a kernel needs about the loaded model, all device pointers.
@@ -97,6 +101,10 @@ struct DevPlan {
   // second pass.
   uint32_t n_cls_null = 0, n_seg_null = 0;
   const uint32_t* thin_src = nullptr;
+  // Mechanism pseudo variables (abi.cpp): pseudo j >= n_groups with
+  // mech_pat[j - n_groups] != 0 is one Pauli pattern of source group
+  // thin_src[j - n_groups], drawn as an independent Bernoulli mechanism.
+  const uint32_t* mech_pat = nullptr;
   const uint32_t* g_masks = nullptr;
   // Fused-kernel event tables in D space (M_sym = L·D, see abi.cpp), class-
   // position order: desc = {colrow base, len0 | len1 << 16, len2 | len3 << 16,
@@ -115,6 +123,7 @@ struct DevPlan {
   uint32_t plist_dummy = 0;  // index of an all-padding list (invalid slots load it)
   uint32_t entry_bytes = 4;  // 1: u8 row indices, 2: u16 / 4: u32 tile byte offsets
   const uint4* plist = nullptr;
+  const uint32_t* len_bnd = nullptr;  // length runs of the sorted Bernoulli classes (ClassInfo::bnd)
   // Row reconstruction out[k] = d[k] ^ out[parent[k]] along the paths of a
   // heavy-path decomposition of the parent forest: path p lists rows
   // path_rows[path_ptr[p] .. path_ptr[p+1]) top-down; path_par[p] is the head's
@@ -138,6 +147,14 @@ struct DevPlan {
   uint32_t cta_per_sm = 1;
   uint32_t cta_threads = 512;
   uint32_t n_buf = 2;        // shot-tile buffers in shared memory (1 or 2)
+  // Drain stores finished tiles with TMA bulk copies (rows rebuilt in place,
+  // then one copy per tile in the tiled layout or one per row segment of
+  // >= 128 bytes in the measurement-major layout) instead of per-thread
+  // 16-byte stores (SP_BULK=0 turns it off).
+  uint32_t bulk_store = 1;
+  // Class table copied into shared memory (set at launch when it fits): the
+  // segment dispenser's class search then reads shared memory, not L2.
+  uint32_t cls_staged = 0;
   // Profiling switches (SP_DEBUG_MODE): bit 0 skips the firing XORs, bit 1
   // skips the segment walks, bit 2 skips the coin words, bit 3 skips the row
   // rebuild. Results are wrong when set.
