@@ -320,14 +320,31 @@ def run_ours(args):
         out = smp.empty_bits(init.n_meas, shots)
     run = ((lambda n, seed, **kw: smp.sample_tiled(n, seed, out=out, **kw)) if tiled else
            (lambda n, seed, **kw: smp.sample(n, seed, out=out, **kw)))
-    # Per-measurement counts, double-buffered: step i's NCCL all-reduce runs
-    # asynchronously while step i+1 samples into the other buffer.
-    pipe = CountPipeline(init.n_meas, dev, world)
+    # The reduced quantity: per-detector flip counts for the surface-code
+    # workloads (BASELINE configs[2]: "NCCL reduce of per-detector flip
+    # counts"), counted by the sampling kernel's drain from the finished rows
+    # (sp_sample_ex); per-measurement counts otherwise.
+    dd = {"cfg2": (5, 5), "cfg3": (15, 15)}.get(args.config)
+    count_kind = "measurement"
+    if dd is not None and args.records == "measurements" and args.counts == "detectors":
+        from paper_2311_03906_b200 import circuits as CI
+        dets, obs = CI.surface_code_detectors(*dd)
+        smp.set_detectors(dets + obs)
+        count_kind = "detector"
+        n_counts = len(dets) + len(obs)
+        counted = (lambda n, seed, counts=None, **kw:
+                   smp.sample_counted(n, seed, out=out, det_counts=counts, tiled=tiled, **kw))
+    else:
+        n_counts = init.n_meas
+        counted = run
+    # Counts double-buffered: step i's NCCL all-reduce runs asynchronously
+    # while step i+1 samples into the other buffer.
+    pipe = CountPipeline(n_counts, dev, world)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
     stream = torch.cuda.current_stream()
 
     def step(i, last=False):
-        pipe.step(i, lambda c: run(shots, 1000 + i, shot_begin=shot_begin, counts=c), last=last)
+        pipe.step(i, lambda c: counted(shots, 1000 + i, shot_begin=shot_begin, counts=c), last=last)
 
     for i in range(args.warmup):
         step(i, last=i == args.warmup - 1)
@@ -429,10 +446,14 @@ def run_ours(args):
             "details": {
                 "n_meas": init.n_meas, "n_sym": init.n_sym, "nnz": init.nnz, "shot_tile": T,
                 "parallelism": f"shot-range sharding x{world}" + (
-                    f", NCCL all_reduce of per-{args.records[:-1]} counts per step (async, "
+                    f", NCCL all_reduce of per-{count_kind} flip counts per step (async, "
                     "overlapping the next step)" if world > 1 else ""),
+                "counts": f"per-{count_kind} flip counts ({n_counts}) accumulated by the "
+                          "sampling kernel every step" + (
+                              " (detectors: surface_code_detectors + logical observable)"
+                              if count_kind == "detector" else ""),
                 "output": ("tiled [tile][row][T/64]" if tiled else "measurement-major") +
-                          " u64 bit-sliced records in HBM + per-row counts",
+                          " u64 bit-sliced records in HBM + flip counts",
                 "l2": "flushed between timed steps (256 MiB memset outside the events); "
                       "output per step > L2",
                 "init_seconds": round(init_s, 4),
@@ -506,6 +527,9 @@ def main():
     ap.add_argument("--records", default="measurements", choices=["measurements", "detectors"],
                     help="sample measurement records (the metric) or, for the surface-code "
                          "workloads, detector + observable records (D_sym = A . M_sym)")
+    ap.add_argument("--counts", default="detectors", choices=["detectors", "measurements"],
+                    help="counts each step reduces: per-detector (surface-code workloads, "
+                         "BASELINE configs[2]) or per-measurement")
     ap.add_argument("--layout", default="auto", choices=["auto", "mm", "tiled"],
                     help="record layout in HBM: measurement-major (the reference's SampleMatrix "
                          "orientation), tiled (sp_sample_tiled), or auto (tiled when the shot "

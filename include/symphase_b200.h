@@ -167,6 +167,21 @@ int sp_sample(sp_ctx* ctx, uint64_t seed, uint64_t shot_begin, uint64_t n_shots,
 uint64_t sp_tiled_words(sp_ctx* ctx, uint64_t n_shots);
 int sp_sample_tiled(sp_ctx* ctx, uint64_t seed, uint64_t shot_begin, uint64_t n_shots,
                     uint64_t* d_out, uint64_t* d_counts);
+/* Detector counts in the sampling launch (not in the reference: its parser
+ * has no DETECTOR, circuit.cpp:117-121; the multi-GPU reduction of
+ * BASELINE configs[2] needs per-detector flip counts). sp_set_detectors
+ * registers detectors as sets of measurement indices (CSR, host pointers;
+ * a measurement listed twice cancels); sp_sample_ex then samples the
+ * records exactly like sp_sample (ld > 0, measurement-major) or
+ * sp_sample_tiled (ld == 0) and, when d_det_counts is not NULL, adds to
+ * d_det_counts[k] (u64, device) the number of shots in which detector k is
+ * 1 — counted by the fused kernel's drain from the finished rows, with no
+ * pass over the records. Fused Philox sampler only (SP_ERR_UNSUPPORTED
+ * otherwise); SP_ERR_NOT_LOADED without registered detectors. */
+int sp_set_detectors(sp_ctx* ctx, uint64_t n_det, const uint64_t* det_ptr,
+                     const uint32_t* det_meas);
+int sp_sample_ex(sp_ctx* ctx, uint64_t seed, uint64_t shot_begin, uint64_t n_shots,
+                 uint64_t* d_out, uint64_t ld, uint64_t* d_counts, uint64_t* d_det_counts);
 /* Tiled records -> measurement-major [n_meas][ld]. */
 int sp_untile(sp_ctx* ctx, const uint64_t* d_tiled, uint64_t n_shots, uint64_t* d_out,
               uint64_t ld);

@@ -60,6 +60,8 @@ SIGNATURES = [
     ("sp_draw_assignments", _i, [_p, _u64, _u64, _u64, _p, _u64]),
     ("sp_tiled_words", _u64, [_p, _u64]),
     ("sp_sample_tiled", _i, [_p, _u64, _u64, _u64, _p, _p]),
+    ("sp_set_detectors", _i, [_p, _u64, _p, _p]),
+    ("sp_sample_ex", _i, [_p, _u64, _u64, _u64, _p, _u64, _p, _p]),
     ("sp_untile", _i, [_p, _p, _u64, _p, _u64]),
     ("sp_encode_tiled", _i, [_p, _p, _u64, _i, _p]),
     ("sp_sample_given_S", _i, [_p, _p, _u64, _u64, _u64, _p, _u64]),

@@ -88,6 +88,9 @@ struct HostPlan {
   std::vector<sp_group> groups;
   std::vector<uint64_t> dense_words;  // only if dense product requested / loaded
   uint64_t ldm = 0;
+  // detectors registered by sp_set_detectors (CSR over measurement indices)
+  std::vector<uint64_t> det_ptr{0};
+  std::vector<uint32_t> det_meas;
 };
 
 }  // namespace
@@ -115,7 +118,8 @@ struct sp_ctx {
   // plan buffers
   DBuf b_row_ptr, b_sym_idx, b_col_ptr, b_col_rows, b_dense, b_dense_gm, b_first, b_arity, b_dist, b_param,
       b_row_const_compat, b_ones, b_dense_sym, b_coin_ptr, b_coin_rows, b_cls, b_cls_groups, b_thin_src, b_mech_pat, b_len_bnd, b_g_masks,
-      b_desc, b_colrow, b_live_groups, b_path_rows, b_path_ptr, b_path_par, b_round_ptr, b_plist, b_keep_rows, b_timers;
+      b_desc, b_colrow, b_live_groups, b_path_rows, b_path_ptr, b_path_par, b_round_ptr, b_plist, b_keep_rows, b_timers,
+      b_gdet_ptr, b_gdet_rows, b_gdet_id;
   uint64_t dnnz = 0;  // nnz of D (chain transform), for reports
   // K2's own copy of the rows (independent of the group table)
   bool prod_ready = false;
@@ -237,6 +241,8 @@ uint64_t model_fingerprint(const HostPlan& h) {
   mix(h.sym_idx.data(), h.sym_idx.size() * 4);
   mix(h.dense_words.data(), h.dense_words.size() * 8);
   mix(h.groups.data(), h.groups.size() * sizeof(sp_group));
+  mix(h.det_ptr.data(), h.det_ptr.size() * 8);
+  mix(h.det_meas.data(), h.det_meas.size() * 4);
   for (char** e = environ; e && *e; ++e)
     if (std::strncmp(*e, "SP_", 3) == 0) mix(*e, std::strlen(*e));
   return fp;
@@ -1239,13 +1245,55 @@ void build_plan(sp_ctx* c) {
       const int32_t pa = X.parent[k];
       if (pa >= 0 && heavy[pa] != static_cast<int32_t>(k)) keep[pa] = 1;  // light child
     }
+    // Detectors: {k, parent(k)} (or {k} for a root row) is counted from row
+    // k's D value during the rebuild; the others are "general".
+    const uint64_t n_det = h.det_ptr.size() - 1;
+    std::vector<uint32_t> det_of_row(n_meas, 0);  // detector index + 1
+    std::vector<uint32_t> gdet_ptr{0}, gdet_id;
+    std::vector<uint16_t> gdet_rows;
+    const bool flat = paths.size() == n_meas && std::all_of(keep.begin(), keep.end(), [](uint8_t v) { return !v; });
+    for (uint64_t j = 0; j < n_det; ++j) {
+      std::vector<uint32_t> m(h.det_meas.begin() + h.det_ptr[j], h.det_meas.begin() + h.det_ptr[j + 1]);
+      std::sort(m.begin(), m.end());
+      std::vector<uint32_t> odd;  // a measurement listed twice cancels
+      for (size_t i = 0; i < m.size();) {
+        size_t e = i;
+        while (e < m.size() && m[e] == m[i]) ++e;
+        if ((e - i) & 1) odd.push_back(m[i]);
+        i = e;
+      }
+      int64_t row = -1;
+      if (!flat && n_det < 0x7FFF) {
+        if (odd.size() == 1 && X.parent[odd[0]] < 0) row = odd[0];
+        if (odd.size() == 2 && X.parent[odd[1]] == static_cast<int32_t>(odd[0])) row = odd[1];
+        if (row >= 0 && det_of_row[row]) row = -1;  // the row already counts another detector
+      }
+      if (row >= 0) {
+        det_of_row[row] = static_cast<uint32_t>(j + 1);
+      } else {
+        for (uint32_t r : odd) gdet_rows.push_back(static_cast<uint16_t>(r));
+        gdet_ptr.push_back(static_cast<uint32_t>(gdet_rows.size()));
+        gdet_id.push_back(static_cast<uint32_t>(j));
+      }
+    }
+    // the legacy drain clears rows as it goes: keep the general detectors'
+    // rows until the tile ends
+    if (!flat)
+      for (uint16_t r : gdet_rows) keep[r] = 1;
+    d.n_det = static_cast<uint32_t>(n_det);
+    d.n_gdet = static_cast<uint32_t>(gdet_id.size());
+    if (gdet_rows.empty()) gdet_rows.push_back(0);
+    if (gdet_id.empty()) gdet_id.push_back(0);
+    d.gdet_ptr = c->b_gdet_ptr.upload(gdet_ptr, s);
+    d.gdet_rows = c->b_gdet_rows.upload(gdet_rows, s);
+    d.gdet_id = c->b_gdet_id.upload(gdet_id, s);
     std::vector<uint32_t> path_rows;
     std::vector<uint32_t> path_ptr{0}, round_ptr(n_rounds + 1, 0);
     std::vector<uint16_t> keep_rows;
     std::vector<int32_t> path_par;
     for (uint32_t id : order) {
       for (uint16_t r : paths[id]) {
-        path_rows.push_back(r | (keep[r] ? 0x80000000u : 0u));
+        path_rows.push_back(r | (det_of_row[r] << 16) | (keep[r] ? 0x80000000u : 0u));
         if (keep[r]) keep_rows.push_back(r);
       }
       path_ptr.push_back(static_cast<uint32_t>(path_rows.size()));
@@ -1253,7 +1301,7 @@ void build_plan(sp_ctx* c) {
       round_ptr[round_of_path[id] + 1]++;
     }
     for (uint32_t r = 0; r < n_rounds; ++r) round_ptr[r + 1] += round_ptr[r];
-    path_rows.push_back(0);  // prefetch padding: the walk reads one entry past a path
+    for (int i = 0; i < 4; ++i) path_rows.push_back(0);  // prefetch padding: walks read past a path
     d.n_paths = static_cast<uint32_t>(paths.size());
     d.n_rounds = n_rounds;
     d.n_keep = static_cast<uint32_t>(keep_rows.size());
@@ -1783,6 +1831,44 @@ int sp_sample(sp_ctx* ctx, uint64_t seed, uint64_t shot_begin, uint64_t n_shots,
   int r = ctx->rng == SP_RNG_PHILOX
               ? launch_fused_sample(ctx->dp, ctx->L, seed, tile0, n_shots, d_out, ld, d_counts)
               : launch_fused_sample_compat(ctx->dp, ctx->L, seed, tile0, n_shots, d_out, ld, d_counts);
+  return launched(ctx, r, "fused sampler launch");
+}
+
+int sp_set_detectors(sp_ctx* ctx, uint64_t n_det, const uint64_t* det_ptr, const uint32_t* det_meas) {
+  if (!ctx) return fail(SP_ERR_INVALID_ARGUMENT, "null ctx");
+  if (n_det && (!det_ptr || det_ptr[0] != 0 || (det_ptr[n_det] && !det_meas)))
+    return fail(SP_ERR_INVALID_ARGUMENT, "detector CSR: det_ptr[0] must be 0 and det_meas non-null");
+  if (n_det > 0xFFFFFFFFull) return fail(SP_ERR_INVALID_ARGUMENT, "too many detectors");
+  for (uint64_t j = 0; j < n_det; ++j)
+    if (det_ptr[j + 1] < det_ptr[j]) return fail(SP_ERR_INVALID_ARGUMENT, "det_ptr must not decrease");
+  if (ctx->have_msym)
+    for (uint64_t i = 0; i < (n_det ? det_ptr[n_det] : 0); ++i)
+      if (det_meas[i] >= ctx->hp.n_meas)
+        return fail(SP_ERR_OUT_OF_RANGE, "detector refers to a measurement out of range");
+  ctx->hp.det_ptr.assign(det_ptr ? det_ptr : nullptr, det_ptr ? det_ptr + n_det + 1 : nullptr);
+  if (ctx->hp.det_ptr.empty()) ctx->hp.det_ptr.push_back(0);
+  ctx->hp.det_meas.assign(det_meas, det_meas + (n_det ? det_ptr[n_det] : 0));
+  ctx->plan_ready = false;
+  return SP_OK;
+}
+
+int sp_sample_ex(sp_ctx* ctx, uint64_t seed, uint64_t shot_begin, uint64_t n_shots, uint64_t* d_out,
+                 uint64_t ld, uint64_t* d_counts, uint64_t* d_det_counts) {
+  if (!d_det_counts)
+    return ld ? sp_sample(ctx, seed, shot_begin, n_shots, d_out, ld, d_counts)
+              : sp_sample_tiled(ctx, seed, shot_begin, n_shots, d_out, d_counts);
+  if (!ctx) return fail(SP_ERR_INVALID_ARGUMENT, "null ctx");
+  if (n_shots == 0) return fail(SP_ERR_INVALID_ARGUMENT, "need at least one shot");
+  if (int r = set_device(ctx)) return r;
+  if (int r = ensure_plan(ctx)) return r;
+  if (ctx->hp.det_ptr.size() < 2) return fail(SP_ERR_NOT_LOADED, "no detectors registered (sp_set_detectors)");
+  if (!ctx->fused_ok || ctx->k5_ok || ctx->unfused || ctx->rng != SP_RNG_PHILOX)
+    return fail(SP_ERR_UNSUPPORTED, "detector counts are produced by the fused Philox sampler only");
+  const uint64_t T = 1ull << ctx->dp.t_log2;
+  if (shot_begin % T) return fail(SP_ERR_INVALID_ARGUMENT, "shot_begin must be a multiple of the shot tile");
+  if (!d_out || (ld && ld < (n_shots + 63) / 64)) return fail(SP_ERR_INVALID_ARGUMENT, "output too small");
+  const int r = launch_fused_sample(ctx->dp, ctx->L, seed, shot_begin / T, n_shots, d_out, ld,
+                                    d_counts, ld == 0, d_det_counts);
   return launched(ctx, r, "fused sampler launch");
 }
 

@@ -33,7 +33,8 @@ template <bool kStaged, bool kRowStaged, int kLp, bool kPadPred, int kEB>
 __global__ void __launch_bounds__(kFusedThreads, 1)
 k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, uint64_t n_shots,
          uint64_t* __restrict__ out, uint64_t ld, uint64_t tile_stride,
-         unsigned long long* __restrict__ counts, bool vec, uint32_t bulk) {
+         unsigned long long* __restrict__ counts, bool vec, uint32_t bulk,
+         unsigned long long* __restrict__ det_counts) {
   extern __shared__ __align__(16) uint8_t smem[];
   const uint32_t tw = P.tw, tw4_log2 = P.t_log2 - 7, tw4 = 1u << tw4_log2;
   // Tile rows, then a spare region (never read) that absorbs the XORs of
@@ -51,6 +52,10 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
   const uint32_t cnt_lanes = count_lanes(P.t_log2, P.n_buf);
   uint32_t* cnt = reinterpret_cast<uint32_t*>(p);
   p += align16(4ull * P.n_meas * cnt_lanes);
+  // Detector flip counts (sp_sample_ex): one u32 per detector.
+  const bool with_dets = det_counts != nullptr && P.n_det > 0;
+  uint32_t* det_cnt = reinterpret_cast<uint32_t*>(p);  // [n_det][cnt_lanes]
+  p += align16(4ull * P.n_det * cnt_lanes);
   uint32_t* segctr = reinterpret_cast<uint32_t*>(p);  // per-buffer segment dispensers
   p += 16;
   // Tile hand-off: full[b] completes when every generator thread finished
@@ -75,14 +80,14 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
   const uint32_t* CSYM = P.dense_sym;
   if (kRowStaged) {
     uint32_t* s_prows = reinterpret_cast<uint32_t*>(p);
-    p += align16(4ull * (P.n_meas + 1));
+    p += align16(4ull * (P.n_meas + 4));
     uint32_t* s_pptr = reinterpret_cast<uint32_t*>(p);
     p += align16(4ull * (P.n_paths + 1));
     int32_t* s_ppar = reinterpret_cast<int32_t*>(p);
     p += align16(4ull * P.n_paths);
     uint16_t* s_keep = reinterpret_cast<uint16_t*>(p);
     p += align16(2ull * P.n_keep);
-    for (uint32_t i = threadIdx.x; i <= P.n_meas; i += blockDim.x) s_prows[i] = P.path_rows[i];
+    for (uint32_t i = threadIdx.x; i < P.n_meas + 4; i += blockDim.x) s_prows[i] = P.path_rows[i];
     for (uint32_t i = threadIdx.x; i <= P.n_paths; i += blockDim.x) s_pptr[i] = P.path_ptr[i];
     for (uint32_t i = threadIdx.x; i < P.n_paths; i += blockDim.x) s_ppar[i] = P.path_par[i];
     for (uint32_t i = threadIdx.x; i < P.n_keep; i += blockDim.x) s_keep[i] = P.keep_rows[i];
@@ -138,6 +143,8 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
       t4[i] = make_uint4(0, 0, 0, 0);
     if (with_counts)
       for (uint32_t i = threadIdx.x; i < P.n_meas * cnt_lanes; i += blockDim.x) cnt[i] = 0;
+    if (with_dets)
+      for (uint32_t i = threadIdx.x; i < P.n_det * cnt_lanes; i += blockDim.x) det_cnt[i] = 0;
     if (threadIdx.x < kMaxBuf) {
       segctr[threadIdx.x] = 0;
       mbar_init(mbar_full + threadIdx.x, P.gen_warps * 32);
@@ -381,58 +388,29 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
       uint64_t* const tbase = out + t_local * tile_stride;  // this tile's records
       // Row k's 128-shot column q is final: store 16 bytes to HBM (masked in a
       // partial tile), optionally count its ones.
-      auto store_row = [&](auto fast_tag, auto wp_tag, uint32_t k, uint32_t q, uint4 v) {
-        constexpr bool kFast = decltype(fast_tag)::value;  // full tile, aligned, ldb < 2^32
-        constexpr bool kWarpPath = decltype(wp_tag)::value;  // a warp per row (T = 4096)
-        uint64_t* obase = tbase + 2 * q;
-        uint32_t pc = 0;
-        if constexpr (kFast) {
-          *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(obase) +
-                                    static_cast<uint64_t>(k) * ldb) = v;
-          if (with_counts) pc = __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
-        } else if (q < vq) {
-          uint64_t* o = obase + static_cast<uint64_t>(k) * ld;
-          bool two = true;  // whether the item's second u64 word is inside the tile
-          if (q == vq - 1 && rem) {
-            const uint32_t m[4] = {
-                rem >= 32 ? kFull : (1u << rem) - 1,
-                rem >= 64 ? kFull : rem > 32 ? (1u << (rem - 32)) - 1 : 0u,
-                rem >= 96 ? kFull : rem > 64 ? (1u << (rem - 64)) - 1 : 0u,
-                rem > 96 ? (1u << (rem - 96)) - 1 : 0u};
-            v.x &= m[0]; v.y &= m[1]; v.z &= m[2]; v.w &= m[3];
-            two = rem > 64;
-          }
-          const uint64_t w0 = (static_cast<uint64_t>(v.y) << 32) | v.x;
-          const uint64_t w1 = (static_cast<uint64_t>(v.w) << 32) | v.z;
-          if (vec && two) {
-            *reinterpret_cast<ulonglong2*>(o) = make_ulonglong2(w0, w1);
-          } else {
-            o[0] = w0;
-            if (two) o[1] = w1;
-          }
-          if (with_counts) pc = __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
-        }
-        if (with_counts) {
-          if constexpr (kWarpPath) {
-            if (cnt_lanes == 32) {  // per-lane partials, no reduction here
-              asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(cnt_s + ((k * 32 + lane) << 2)),
-                           "r"(pc)
-                           : "memory");
-            } else {  // the warp holds this row: one add per row
-              pc = __reduce_add_sync(kFull, pc);
-              if (lane == 0) atomicAdd(&cnt[k], pc);
+      if ((bulk || (with_dets && P.flat_rows)) && !(P.debug_mode & 8u)) {
+        // In-place drain: rows are rebuilt in place (every final row value
+        // stays in the tile), detectors are counted from the finished rows,
+        // then the tile leaves for HBM — as TMA bulk copies (one for the
+        // whole tile in the tiled layout, one per row segment in the
+        // measurement-major one) or 16-byte stores — and is cleared.
+        const bool full = valid == (static_cast<uint64_t>(1) << P.t_log2);
+        if (!full) {  // a partial tile: shots past the end become zero
+          for (uint32_t j = ct; j < (P.n_meas << tw4_log2); j += nct) {
+            const uint32_t q = j & (tw4 - 1);
+            if (q >= vq) {
+              t4[j] = make_uint4(0, 0, 0, 0);
+            } else if (q == vq - 1 && rem) {
+              uint4 v = t4[j];
+              v.x &= rem >= 32 ? kFull : (1u << rem) - 1;
+              v.y &= rem >= 64 ? kFull : rem > 32 ? (1u << (rem - 32)) - 1 : 0u;
+              v.z &= rem >= 96 ? kFull : rem > 64 ? (1u << (rem - 64)) - 1 : 0u;
+              v.w &= rem > 96 ? (1u << (rem - 96)) - 1 : 0u;
+              t4[j] = v;
             }
-          } else {
-            if (pc) atomicAdd(&cnt[k], pc);
           }
+          named_sync(kBarDrain, nct);
         }
-      };
-      if (bulk && valid == (static_cast<uint64_t>(1) << P.t_log2) && !(P.debug_mode & 8u)) {
-        // TMA drain: rows are rebuilt in place (every final row value stays
-        // in the tile), then the tile leaves for HBM as bulk copies — one
-        // for the whole tile in the tiled layout, one per row segment in the
-        // measurement-major one — and is cleared once the copy engine has
-        // read it. No per-thread global stores or address arithmetic.
         auto count_item = [&](auto wp_tag, uint32_t k, uint4 v) {
           constexpr bool kWarpPath = decltype(wp_tag)::value;  // a warp per row (T = 4096)
           uint32_t pc = __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
@@ -449,11 +427,55 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
             if (pc) atomicAdd(&cnt[k], pc);
           }
         };
-        auto rebuild = [&](auto wp_tag) {
+        // detector {k, parent(k)} (or {k} for a root row): the row's D value
+        auto count_det = [&](auto wp_tag, uint32_t e, uint4 d) {
+          constexpr bool kWarpPath = decltype(wp_tag)::value;  // the warp holds one row
+          const uint32_t id = (e >> 16) & 0x7FFFu;
+          if (id) {
+            uint32_t pc = __popc(d.x) + __popc(d.y) + __popc(d.z) + __popc(d.w);
+            if constexpr (kWarpPath) {
+              if (cnt_lanes == 32) {  // per-lane partials
+                atomicAdd(&det_cnt[(id - 1) * 32 + lane], pc);
+              } else {
+                pc = __reduce_add_sync(kFull, pc);
+                if (lane == 0 && pc) atomicAdd(&det_cnt[id - 1], pc);
+              }
+            } else {
+              if (pc) atomicAdd(&det_cnt[id - 1], pc);
+            }
+          }
+        };
+        // measurement-major records without TMA: each finished 16-byte item
+        // is stored as the rebuild produces it (valid words only)
+        const bool direct = bulk == 0 || (bulk == 2 && !full);
+        auto store_item = [&](uint32_t k, uint32_t q, uint4 v) {
+          if (q >= vq) return;
+          const uint64_t w0 = (static_cast<uint64_t>(v.y) << 32) | v.x;
+          const uint64_t w1 = (static_cast<uint64_t>(v.w) << 32) | v.z;
+          if (fast) {
+            *reinterpret_cast<ulonglong2*>(reinterpret_cast<uint8_t*>(tbase + 2 * q) +
+                                           static_cast<uint64_t>(k) * ldb) = make_ulonglong2(w0, w1);
+            return;
+          }
+          uint64_t* o = tbase + static_cast<uint64_t>(k) * ld + 2 * q;
+          const bool two = q < vq - 1 || rem == 0 || rem > 64;
+          if (vec && two) {
+            *reinterpret_cast<ulonglong2*>(o) = make_ulonglong2(w0, w1);
+          } else {
+            o[0] = w0;
+            if (two) o[1] = w1;
+          }
+        };
+        // (counting modes are compile-time tags: no per-row flag checks)
+        auto rebuild = [&](auto wp_tag, auto cnt_tag, auto det_tag) {
+          constexpr bool kCnt = decltype(cnt_tag)::value, kDet = decltype(det_tag)::value;
           if (P.flat_rows) {  // no parents: the tile already holds the records
-            if (with_counts)
-              for (uint32_t j = ct; j < (P.n_meas << tw4_log2); j += nct)
-                count_item(wp_tag, j >> tw4_log2, t4[j]);
+            if (kCnt || direct)
+              for (uint32_t j = ct; j < (P.n_meas << tw4_log2); j += nct) {
+                const uint4 v = t4[j];
+                if constexpr (kCnt) count_item(wp_tag, j >> tw4_log2, v);
+                if (direct) store_item(j >> tw4_log2, j & (tw4 - 1), v);
+              }
             return;
           }
           for (uint32_t rd = 0; rd < P.n_rounds; ++rd) {
@@ -469,50 +491,82 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
                                     : make_uint4(0, 0, 0, 0);
               const uint32_t xe = act ? PPTR[pth + 1] : 0;
               uint32_t x = act ? PPTR[pth] : 0;
-              // two rows per iteration, the next row's tile word prefetched
-              // (path_rows is padded, so x + 2 <= n_meas is readable)
-              uint32_t ka = PROWS[x] & 0xFFFFu;
-              uint4 ca = t4[(ka << tw4_log2) + q];
-              for (; x + 2 <= xe; x += 2) {
-                const uint32_t kb = PROWS[x + 1] & 0xFFFFu;
-                const uint4 cb = t4[(kb << tw4_log2) + q];
-                const uint4 va = xor4(ca, prev);
-                t4[(ka << tw4_log2) + q] = va;
-                if (with_counts) count_item(wp_tag, ka, va);
-                ka = PROWS[x + 2] & 0xFFFFu;
-                ca = t4[(ka << tw4_log2) + q];
-                prev = xor4(cb, va);
-                t4[(kb << tw4_log2) + q] = prev;
-                if (with_counts) count_item(wp_tag, kb, prev);
-              }
-              if (x < xe) {
-                const uint4 va = xor4(ca, prev);
-                t4[(ka << tw4_log2) + q] = va;
-                if (with_counts) count_item(wp_tag, ka, va);
+              // four rows per group: the group's entries and tile words are
+              // loaded together (path_rows is padded by four entries), then
+              // the parent chain runs through them
+              auto row = [&](uint32_t e, uint4 c) {
+                const uint32_t k = e & 0xFFFFu;
+                prev = xor4(c, prev);
+                t4[(k << tw4_log2) + q] = prev;
+                if constexpr (kCnt) count_item(wp_tag, k, prev);
+                if constexpr (kDet) count_det(wp_tag, e, c);
+                if (direct) store_item(k, q, prev);
+              };
+              for (; x < xe; x += 4) {
+                const uint32_t e0 = PROWS[x], e1 = PROWS[x + 1], e2 = PROWS[x + 2], e3 = PROWS[x + 3];
+                const uint4 c0 = t4[((e0 & 0xFFFFu) << tw4_log2) + q];
+                const uint4 c1 = t4[((e1 & 0xFFFFu) << tw4_log2) + q];
+                const uint4 c2 = t4[((e2 & 0xFFFFu) << tw4_log2) + q];
+                const uint4 c3 = t4[((e3 & 0xFFFFu) << tw4_log2) + q];
+                row(e0, c0);
+                if (x + 1 < xe) row(e1, c1);
+                if (x + 2 < xe) row(e2, c2);
+                if (x + 3 < xe) row(e3, c3);
               }
             }
             if (rd + 1 < P.n_rounds) named_sync(kBarDrain, nct);
           }
         };
-        if (tw4 >= 32) rebuild(std::true_type{});
-        else rebuild(std::false_type{});
-        fence_proxy_async_smem();
+        auto rebuild_wp = [&](auto wp_tag) {
+          if (with_counts) {
+            if (with_dets) rebuild(wp_tag, std::true_type{}, std::true_type{});
+            else rebuild(wp_tag, std::true_type{}, std::false_type{});
+          } else {
+            if (with_dets) rebuild(wp_tag, std::false_type{}, std::true_type{});
+            else rebuild(wp_tag, std::false_type{}, std::false_type{});
+          }
+        };
+        if (tw4 >= 32) rebuild_wp(std::true_type{});
+        else rebuild_wp(std::false_type{});
+        // other detectors: XOR of their measurements' finished rows (read
+        // while the copy engine reads the same tile)
+        auto general_dets = [&]() {
+          for (uint32_t j = ct; j < (P.n_gdet << tw4_log2); j += nct) {
+            const uint32_t gd = j >> tw4_log2, q = j & (tw4 - 1);
+            uint4 v = make_uint4(0, 0, 0, 0);
+            for (uint32_t m = P.gdet_ptr[gd]; m < P.gdet_ptr[gd + 1]; ++m)
+              v = xor4(v, t4[(static_cast<uint32_t>(P.gdet_rows[m]) << tw4_log2) + q]);
+            uint32_t pc = __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
+            if (tw4 >= 32) {  // the warp holds one detector: one add
+              if (cnt_lanes == 32) {  // per-lane partials
+                atomicAdd(&det_cnt[P.gdet_id[gd] * 32 + lane], pc);
+              } else {
+                pc = __reduce_add_sync(kFull, pc);
+                if (lane == 0 && pc) atomicAdd(&det_cnt[P.gdet_id[gd]], pc);
+              }
+            } else if (pc) {
+              atomicAdd(&det_cnt[P.gdet_id[gd]], pc);
+            }
+          }
+        };
+        if (bulk) fence_proxy_async_smem();
         named_sync(kBarDrain, nct);
         const uint32_t row_bytes = tw * 4u;
-        if (bulk == 1) {
+        bool issued = false;
+        if (bulk == 1) {  // the tiled layout allocates whole tiles
           if (ct == 0) {
             bulk_store(tbase, t4_s, P.n_meas * row_bytes);
-            bulk_commit_and_wait_read();
+            issued = true;
           }
-        } else {
-          bool issued = false;
+        } else if (bulk == 2 && full) {
           for (uint32_t k = ct; k < P.n_meas; k += nct) {
             bulk_store(tbase + static_cast<uint64_t>(k) * ld, t4_s + k * row_bytes, row_bytes);
             issued = true;
           }
-          if (issued) bulk_commit_and_wait_read();
         }
-        named_sync(kBarDrain, nct);  // the copy engine has read the whole tile
+        if (with_dets && P.n_gdet) general_dets();
+        if (issued) bulk_commit_and_wait_read();
+        named_sync(kBarDrain, nct);  // every row has left the tile
         for (uint32_t j = ct; j < (P.n_meas << tw4_log2); j += nct) t4[j] = make_uint4(0, 0, 0, 0);
         if (ct == 0) segctr[b] = 0;
         if (P.timers && lane == 0) {
@@ -522,84 +576,198 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
         if (i + n_buf < n_my) mbar_arrive(mbar_empty + b);
         continue;
       }
-      if (P.flat_rows && !(P.debug_mode & 8u)) {
-        // No parents (every row its own path, nothing kept): one pass over
-        // the tile in row order, clearing as it goes.
-        auto flat = [&](auto fast_tag, auto wp_tag) {
-          for (uint32_t j = ct; j < (P.n_meas << tw4_log2); j += nct) {
-            const uint4 v = t4[j];
-            t4[j] = make_uint4(0, 0, 0, 0);
-            store_row(fast_tag, wp_tag, j >> tw4_log2, j & (tw4 - 1), v);
+      // Legacy drain (16-byte stores while the rows are rebuilt, rows
+      // cleared as soon as no later row reads them); the counting modes
+      // are compile-time tags, so no per-row flag checks.
+      auto legacy = [&](auto cnt_tag, auto det_tag) {
+        constexpr bool kCntL = decltype(cnt_tag)::value, kDetL = decltype(det_tag)::value;
+        auto store_row = [&](auto fast_tag, auto wp_tag, uint32_t k, uint32_t q, uint4 v) {
+          constexpr bool kFast = decltype(fast_tag)::value;  // full tile, aligned, ldb < 2^32
+          constexpr bool kWarpPath = decltype(wp_tag)::value;  // a warp per row (T = 4096)
+          uint64_t* obase = tbase + 2 * q;
+          uint32_t pc = 0;
+          if constexpr (kFast) {
+            *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(obase) +
+                                      static_cast<uint64_t>(k) * ldb) = v;
+            if constexpr (kCntL) pc = __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
+          } else if (q < vq) {
+            uint64_t* o = obase + static_cast<uint64_t>(k) * ld;
+            bool two = true;  // whether the item's second u64 word is inside the tile
+            if (q == vq - 1 && rem) {
+              const uint32_t m[4] = {
+                  rem >= 32 ? kFull : (1u << rem) - 1,
+                  rem >= 64 ? kFull : rem > 32 ? (1u << (rem - 32)) - 1 : 0u,
+                  rem >= 96 ? kFull : rem > 64 ? (1u << (rem - 64)) - 1 : 0u,
+                  rem > 96 ? (1u << (rem - 96)) - 1 : 0u};
+              v.x &= m[0]; v.y &= m[1]; v.z &= m[2]; v.w &= m[3];
+              two = rem > 64;
+            }
+            const uint64_t w0 = (static_cast<uint64_t>(v.y) << 32) | v.x;
+            const uint64_t w1 = (static_cast<uint64_t>(v.w) << 32) | v.z;
+            if (vec && two) {
+              *reinterpret_cast<ulonglong2*>(o) = make_ulonglong2(w0, w1);
+            } else {
+              o[0] = w0;
+              if (two) o[1] = w1;
+            }
+            if constexpr (kCntL) pc = __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
+          }
+          if constexpr (kCntL) {
+            if constexpr (kWarpPath) {
+              if (cnt_lanes == 32) {  // per-lane partials, no reduction here
+                asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(cnt_s + ((k * 32 + lane) << 2)),
+                             "r"(pc)
+                             : "memory");
+              } else {  // the warp holds this row: one add per row
+                pc = __reduce_add_sync(kFull, pc);
+                if (lane == 0) atomicAdd(&cnt[k], pc);
+              }
+            } else {
+              if (pc) atomicAdd(&cnt[k], pc);
+            }
           }
         };
-        if (tw4 >= 32) {
-          if (fast) flat(std::true_type{}, std::true_type{});
-          else flat(std::false_type{}, std::true_type{});
-        } else {
-          if (fast) flat(std::true_type{}, std::false_type{});
-          else flat(std::false_type{}, std::false_type{});
-        }
-      }
-      // Rows along parent paths (heavy-path decomposition of the L forest):
-      // one thread walks a path top-down for one 128-shot column, carrying
-      // the running row value; a path's head waits only for its parent's
-      // path, which ran in an earlier round.
-      for (uint32_t rd = 0; rd < ((P.debug_mode & 8u) || P.flat_rows ? 0u : P.n_rounds); ++rd) {
-        const uint32_t p0 = P.round_ptr[rd], p1 = P.round_ptr[rd + 1];
-        const uint32_t tasks = (p1 - p0) << tw4_log2;
-        const uint32_t tasks_rounded = (tasks + 31) & ~31u;
-        for (uint32_t j = ct; j < tasks_rounded; j += nct) {
-          const bool act = j < tasks;
-          const uint32_t pth = act ? p0 + (j >> tw4_log2) : p0;
-          const uint32_t q = j & (tw4 - 1);
-          const int32_t par = act ? PPAR[pth] : -1;
-          uint4 prev = par >= 0 ? t4[(static_cast<uint32_t>(par) << tw4_log2) + q]
-                                : make_uint4(0, 0, 0, 0);
-          const uint32_t xe = act ? PPTR[pth + 1] : 0;
-          uint32_t x = act ? PPTR[pth] : 0;
-          // One row of the path: row = tile word ^ parent row; keep or clear
-          // the tile word, then store it (and count it).
-          auto row_step = [&](auto fast_tag, auto wp_tag, uint32_t e, uint4 c) {
-            const uint32_t k = e & 0xFFFFu;
-            const uint4 v = xor4(c, prev);
-            // Rows with light children keep their final value for a later
-            // round; all others are cleared for tile i+2 right away.
-            sts_or_zero(t4_s + (((k << tw4_log2) + q) << 4), v, e >> 31);
-            prev = v;
-            store_row(fast_tag, wp_tag, k, q, v);
-          };
-          // Two rows per iteration with the next row's entry and tile word
-          // prefetched (path_rows is padded, so x + 2 <= n_meas is readable).
-          auto walk = [&](auto fast_tag, auto wp_tag) {
-            uint32_t ea = PROWS[x];
-            uint4 ca = t4[((ea & 0xFFFFu) << tw4_log2) + q];
-            for (; x + 2 <= xe; x += 2) {
-              const uint32_t eb = PROWS[x + 1];
-              const uint4 cb = t4[((eb & 0xFFFFu) << tw4_log2) + q];
-              row_step(fast_tag, wp_tag, ea, ca);
-              ea = PROWS[x + 2];
-              ca = t4[((ea & 0xFFFFu) << tw4_log2) + q];
-              row_step(fast_tag, wp_tag, eb, cb);
+        if (P.flat_rows && !(P.debug_mode & 8u)) {
+          // No parents (every row its own path, nothing kept): one pass over
+          // the tile in row order, clearing as it goes.
+          auto flat = [&](auto fast_tag, auto wp_tag) {
+            for (uint32_t j = ct; j < (P.n_meas << tw4_log2); j += nct) {
+              const uint4 v = t4[j];
+              t4[j] = make_uint4(0, 0, 0, 0);
+              store_row(fast_tag, wp_tag, j >> tw4_log2, j & (tw4 - 1), v);
             }
-            if (x < xe) row_step(fast_tag, wp_tag, ea, ca);
           };
           if (tw4 >= 32) {
-            if (fast) walk(std::true_type{}, std::true_type{});
-            else walk(std::false_type{}, std::true_type{});
+            if (fast) flat(std::true_type{}, std::true_type{});
+            else flat(std::false_type{}, std::true_type{});
           } else {
-            if (fast) walk(std::true_type{}, std::false_type{});
-            else walk(std::false_type{}, std::false_type{});
+            if (fast) flat(std::true_type{}, std::false_type{});
+            else flat(std::false_type{}, std::false_type{});
           }
         }
-        // A later round must not start before every row a light child
-        // reads is final.
-        if (rd + 1 < P.n_rounds) named_sync(kBarDrain, nct);
-      }
-      if (P.n_keep) {
-        named_sync(kBarDrain, nct);  // all light children have read their parents
-        for (uint32_t j = ct; j < (P.n_keep << tw4_log2); j += nct)
-          t4[(static_cast<uint32_t>(KEEP[j >> tw4_log2]) << tw4_log2) + (j & (tw4 - 1))] =
-              make_uint4(0, 0, 0, 0);
+        // Rows along parent paths (heavy-path decomposition of the L forest):
+        // one thread walks a path top-down for one 128-shot column, carrying
+        // the running row value; a path's head waits only for its parent's
+        // path, which ran in an earlier round.
+        for (uint32_t rd = 0; rd < ((P.debug_mode & 8u) || P.flat_rows ? 0u : P.n_rounds); ++rd) {
+          const uint32_t p0 = P.round_ptr[rd], p1 = P.round_ptr[rd + 1];
+          const uint32_t tasks = (p1 - p0) << tw4_log2;
+          const uint32_t tasks_rounded = (tasks + 31) & ~31u;
+          for (uint32_t j = ct; j < tasks_rounded; j += nct) {
+            const bool act = j < tasks;
+            const uint32_t pth = act ? p0 + (j >> tw4_log2) : p0;
+            const uint32_t q = j & (tw4 - 1);
+            const int32_t par = act ? PPAR[pth] : -1;
+            uint4 prev = par >= 0 ? t4[(static_cast<uint32_t>(par) << tw4_log2) + q]
+                                  : make_uint4(0, 0, 0, 0);
+            const uint32_t xe = act ? PPTR[pth + 1] : 0;
+            uint32_t x = act ? PPTR[pth] : 0;
+            // One row of the path: row = tile word ^ parent row; keep or clear
+            // the tile word, then store it (and count it).
+            auto row_step = [&](auto fast_tag, auto wp_tag, uint32_t e, uint4 c) {
+              const uint32_t k = e & 0xFFFFu;
+              const uint4 v = xor4(c, prev);
+              if constexpr (kDetL) {  // detector {k, parent(k)} or {k}: the row's D value
+                const uint32_t id = (e >> 16) & 0x7FFFu;
+                if (id) {
+                  uint4 dv = c;
+                  if (!decltype(fast_tag)::value) {  // a partial tile: valid shots only
+                    if (q >= vq) dv = make_uint4(0, 0, 0, 0);
+                    else if (q == vq - 1 && rem) {
+                      dv.x &= rem >= 32 ? kFull : (1u << rem) - 1;
+                      dv.y &= rem >= 64 ? kFull : rem > 32 ? (1u << (rem - 32)) - 1 : 0u;
+                      dv.z &= rem >= 96 ? kFull : rem > 64 ? (1u << (rem - 64)) - 1 : 0u;
+                      dv.w &= rem > 96 ? (1u << (rem - 96)) - 1 : 0u;
+                    }
+                  }
+                  uint32_t pc = __popc(dv.x) + __popc(dv.y) + __popc(dv.z) + __popc(dv.w);
+                  if constexpr (decltype(wp_tag)::value) {
+                    if (cnt_lanes == 32) {  // per-lane partials
+                      atomicAdd(&det_cnt[(id - 1) * 32 + lane], pc);
+                    } else {
+                      pc = __reduce_add_sync(kFull, pc);
+                      if (lane == 0 && pc) atomicAdd(&det_cnt[id - 1], pc);
+                    }
+                  } else if (pc) {
+                    atomicAdd(&det_cnt[id - 1], pc);
+                  }
+                }
+              }
+              // Rows with light children keep their final value for a later
+              // round; all others are cleared for tile i+2 right away.
+              sts_or_zero(t4_s + (((k << tw4_log2) + q) << 4), v, e >> 31);
+              prev = v;
+              store_row(fast_tag, wp_tag, k, q, v);
+            };
+            // Two rows per iteration with the next row's entry and tile word
+            // prefetched (path_rows is padded, so x + 2 <= n_meas is readable).
+            auto walk = [&](auto fast_tag, auto wp_tag) {
+              uint32_t ea = PROWS[x];
+              uint4 ca = t4[((ea & 0xFFFFu) << tw4_log2) + q];
+              for (; x + 2 <= xe; x += 2) {
+                const uint32_t eb = PROWS[x + 1];
+                const uint4 cb = t4[((eb & 0xFFFFu) << tw4_log2) + q];
+                row_step(fast_tag, wp_tag, ea, ca);
+                ea = PROWS[x + 2];
+                ca = t4[((ea & 0xFFFFu) << tw4_log2) + q];
+                row_step(fast_tag, wp_tag, eb, cb);
+              }
+              if (x < xe) row_step(fast_tag, wp_tag, ea, ca);
+            };
+            if (tw4 >= 32) {
+              if (fast) walk(std::true_type{}, std::true_type{});
+              else walk(std::false_type{}, std::true_type{});
+            } else {
+              if (fast) walk(std::true_type{}, std::false_type{});
+              else walk(std::false_type{}, std::false_type{});
+            }
+          }
+          // A later round must not start before every row a light child
+          // reads is final.
+          if (rd + 1 < P.n_rounds) named_sync(kBarDrain, nct);
+        }
+        if (kDetL && P.n_gdet && !P.flat_rows) {
+          // other detectors: their measurement rows are kept (planner) until
+          // the tile ends; XOR them and count
+          named_sync(kBarDrain, nct);
+          for (uint32_t j = ct; j < (P.n_gdet << tw4_log2); j += nct) {
+            const uint32_t gd = j >> tw4_log2, q = j & (tw4 - 1);
+            uint4 v = make_uint4(0, 0, 0, 0);
+            for (uint32_t m = P.gdet_ptr[gd]; m < P.gdet_ptr[gd + 1]; ++m)
+              v = xor4(v, t4[(static_cast<uint32_t>(P.gdet_rows[m]) << tw4_log2) + q]);
+            if (q >= vq) v = make_uint4(0, 0, 0, 0);
+            else if (q == vq - 1 && rem) {
+              v.x &= rem >= 32 ? kFull : (1u << rem) - 1;
+              v.y &= rem >= 64 ? kFull : rem > 32 ? (1u << (rem - 32)) - 1 : 0u;
+              v.z &= rem >= 96 ? kFull : rem > 64 ? (1u << (rem - 64)) - 1 : 0u;
+              v.w &= rem > 96 ? (1u << (rem - 96)) - 1 : 0u;
+            }
+            uint32_t pc = __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
+            if (tw4 >= 32) {
+              if (cnt_lanes == 32) {  // per-lane partials
+                atomicAdd(&det_cnt[P.gdet_id[gd] * 32 + lane], pc);
+              } else {
+                pc = __reduce_add_sync(kFull, pc);
+                if (lane == 0 && pc) atomicAdd(&det_cnt[P.gdet_id[gd]], pc);
+              }
+            } else if (pc) {
+              atomicAdd(&det_cnt[P.gdet_id[gd]], pc);
+            }
+          }
+        }
+        if (P.n_keep) {
+          named_sync(kBarDrain, nct);  // all light children have read their parents
+          for (uint32_t j = ct; j < (P.n_keep << tw4_log2); j += nct)
+            t4[(static_cast<uint32_t>(KEEP[j >> tw4_log2]) << tw4_log2) + (j & (tw4 - 1))] =
+                make_uint4(0, 0, 0, 0);
+        }
+      };
+      if (with_counts) {
+        if (with_dets) legacy(std::true_type{}, std::true_type{});
+        else legacy(std::true_type{}, std::false_type{});
+      } else {
+        if (with_dets) legacy(std::false_type{}, std::true_type{});
+        else legacy(std::false_type{}, std::false_type{});
       }
       if (ct == 0) segctr[b] = 0;  // all generators are past tile i (full[b] completed)
       if (P.timers && lane == 0) {  // drain: [2] waiting FULL, [3] working
@@ -607,6 +775,18 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
         atomicAdd(reinterpret_cast<unsigned long long*>(P.timers) + 3, clock64() - td1);
       }
       if (i + n_buf < n_my) mbar_arrive(mbar_empty + b);
+    }
+  }
+  if (with_dets) {
+    __syncthreads();
+    if (cnt_lanes == 32) {  // per-lane partials: one warp per detector
+      for (uint32_t k = threadIdx.x >> 5; k < P.n_det; k += blockDim.x >> 5) {
+        const uint32_t c = __reduce_add_sync(kFull, det_cnt[k * 32 + lane]);
+        if (lane == 0 && c) atomicAdd(&det_counts[k], static_cast<unsigned long long>(c));
+      }
+    } else {
+      for (uint32_t i = threadIdx.x; i < P.n_det; i += blockDim.x)
+        if (det_cnt[i]) atomicAdd(&det_counts[i], static_cast<unsigned long long>(det_cnt[i]));
     }
   }
   if (with_counts) {
@@ -629,7 +809,7 @@ namespace k1 {
 template <bool kStaged, bool kRowStaged, int kLp, bool kPadPred, int kEB>
 int launch_k1(const DevPlan& P, const LaunchCfg& L, const RoundKeys& K, uint64_t tile0,
               uint32_t n_tiles, uint64_t n_shots, uint64_t* out, uint64_t ld, uint64_t tstride,
-              unsigned long long* cnt) {
+              unsigned long long* cnt, unsigned long long* det_cnt) {
   auto kern = k1_fused<kStaged, kRowStaged, kLp, kPadPred, kEB>;
   size_t smem = fused_smem_bytes(P, P.t_log2, kStaged, kRowStaged, P.n_buf);
   DevPlan Q = P;
@@ -649,7 +829,7 @@ int launch_k1(const DevPlan& P, const LaunchCfg& L, const RoundKeys& K, uint64_t
                         : (ld * 2 == P.tw && tstride == static_cast<uint64_t>(P.n_meas) * ld) ? 1u
                         : P.bulk_store == 2 && P.tw * 4 >= 128 ? 2u : 0u;
   kern<<<grid, threads, smem, L.stream>>>(Q, K, tile0, n_tiles, n_shots, out, ld, tstride, cnt,
-                                          vec, bulk);
+                                          vec, bulk, det_cnt);
   return check_launch() ? -1 : 1;
 }
 

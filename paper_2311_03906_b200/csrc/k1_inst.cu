@@ -8,7 +8,7 @@ namespace k1 {
 
 #define SP_ARGS                                                                              \
   const DevPlan&, const LaunchCfg&, const RoundKeys&, uint64_t, uint32_t, uint64_t, uint64_t*, \
-      uint64_t, uint64_t, unsigned long long*
+      uint64_t, uint64_t, unsigned long long*, unsigned long long*
 #if SP_LP == 0
 template int launch_k1<true, true, 0, false, 4>(SP_ARGS);
 template int launch_k1<true, false, 0, false, 4>(SP_ARGS);

@@ -557,7 +557,7 @@ namespace k1 {
 template <bool kStaged, bool kRowStaged, int kLp, bool kPadPred, int kEB>
 int launch_k1(const DevPlan& P, const LaunchCfg& L, const RoundKeys& K, uint64_t tile0,
               uint32_t n_tiles, uint64_t n_shots, uint64_t* out, uint64_t ld, uint64_t tstride,
-              unsigned long long* cnt);
+              unsigned long long* cnt, unsigned long long* det_cnt);
 }  // namespace k1
 
 size_t fused_smem_bytes(const DevPlan& P, uint32_t t_log2, bool staged, bool row_staged,
@@ -565,12 +565,13 @@ size_t fused_smem_bytes(const DevPlan& P, uint32_t t_log2, bool staged, bool row
   const size_t tw = size_t{1} << (t_log2 - 5);
   size_t b = n_buf * (static_cast<size_t>(P.n_meas) * tw + spare_words(tw)) * 4;  // tiles + spare
   b += align16(4ull * P.n_meas * count_lanes(t_log2, n_buf)) + 16;  // counts, dispensers
+  b += align16(4ull * P.n_det * count_lanes(t_log2, n_buf));           // detector counts
   b += 16 * kMaxBufHost;                                               // tile mbarriers
   if (P.coins_staged)
     b += align16(4ull * (P.n_dense_live + 2)) + align16(4ull * P.n_dense_live) +
          align16(2ull * P.n_coin_rows);                                 // coin tables
   if (row_staged) {
-    b += align16(4ull * (P.n_meas + 1));
+    b += align16(4ull * (P.n_meas + 4));
     b += align16(4ull * (P.n_paths + 1));
     b += align16(4ull * P.n_paths);
     b += align16(2ull * P.n_keep);
@@ -585,15 +586,16 @@ size_t fused_smem_bytes(const DevPlan& P, uint32_t t_log2, bool staged, bool row
 
 int launch_fused_sample(const DevPlan& P, const LaunchCfg& L, uint64_t seed, uint64_t tile0,
                         uint64_t n_shots, uint64_t* out, uint64_t ld, uint64_t* counts,
-                        bool tiled) {
+                        bool tiled, uint64_t* det_counts) {
   const uint64_t T = 1ull << P.t_log2;
   const uint64_t tstride = tiled ? static_cast<uint64_t>(P.n_meas) * (T / 64) : T / 64;
   if (tiled) ld = T / 64;
   const uint32_t n_tiles = static_cast<uint32_t>((n_shots + T - 1) / T);
   const RoundKeys K = expand_keys(seed);
   auto* cnt = reinterpret_cast<unsigned long long*>(counts);
+  auto* dcnt = reinterpret_cast<unsigned long long*>(det_counts);
 #define SP_K1(st, rs, lp, pp, eb) \
-  k1::launch_k1<st, rs, lp, pp, eb>(P, L, K, tile0, n_tiles, n_shots, out, ld, tstride, cnt)
+  k1::launch_k1<st, rs, lp, pp, eb>(P, L, K, tile0, n_tiles, n_shots, out, ld, tstride, cnt, dcnt)
 #define SP_K1R(lp, pp, eb) \
   (P.row_staged ? SP_K1(false, true, lp, pp, eb) : SP_K1(false, false, lp, pp, eb))
 #define SP_K1P(lp, eb) (P.pad_pred ? SP_K1R(lp, true, eb) : SP_K1R(lp, false, eb))

@@ -139,6 +139,14 @@ struct DevPlan {
   const uint32_t* round_ptr = nullptr;  // [n_rounds + 1] over paths
   uint32_t n_paths = 0, n_rounds = 1, n_keep = 0;
   uint32_t flat_rows = 0;  // no parents at all: the drain is one pass in row order
+  // Detector counts (sp_sample_ex): a detector equal to {k, parent(k)} (or
+  // {k} for a root row) is counted from row k's D value while the drain
+  // rebuilds the row (its index + 1 in bits 16..30 of k's path_rows entry);
+  // the others ("general") XOR their measurements' finished rows.
+  uint32_t n_det = 0, n_gdet = 0;
+  const uint32_t* gdet_ptr = nullptr;   // [n_gdet + 1]
+  const uint16_t* gdet_rows = nullptr;  // measurement rows
+  const uint32_t* gdet_id = nullptr;    // detector index
 
   // Fused-kernel launch shape (chosen by the planner).
   uint32_t staged = 0;       // event tables copied into shared memory
@@ -224,7 +232,7 @@ size_t fused_smem_bytes(const DevPlan& P, uint32_t t_log2, bool staged, bool row
 // K1 fused sampler (Philox). Returns number of launches issued, <0 on error.
 int launch_fused_sample(const DevPlan& P, const LaunchCfg& L, uint64_t seed, uint64_t tile0,
                         uint64_t n_shots, uint64_t* out, uint64_t ld, uint64_t* counts,
-                        bool tiled = false);
+                        bool tiled = false, uint64_t* det_counts = nullptr);
 // K4 fused sampler, compat RNG (bit-exact keyed_draw / fill_group).
 int launch_fused_sample_compat(const DevPlan& P, const LaunchCfg& L, uint64_t seed,
                                uint64_t tile0, uint64_t n_shots, uint64_t* out, uint64_t ld,

@@ -278,6 +278,41 @@ class Sampler:
                                         _ptr(counts)))
         return out
 
+    def set_detectors(self, detectors):
+        """Registers detectors (lists of measurement indices) whose flip counts
+        sample_counted() accumulates in the sampling launch."""
+        import ctypes as C
+        import numpy as np
+        ptr = np.zeros(len(detectors) + 1, dtype=np.uint64)
+        for i, d in enumerate(detectors):
+            ptr[i + 1] = ptr[i] + len(d)
+        meas = np.fromiter((m for d in detectors for m in d), dtype=np.uint32, count=int(ptr[-1]))
+        self._det_arrays = (ptr, meas)
+        N.check(self._L.sp_set_detectors(self._h, len(detectors),
+                                         ptr.ctypes.data_as(C.c_void_p),
+                                         meas.ctypes.data_as(C.c_void_p) if meas.size else None))
+        self.n_det = len(detectors)
+
+    def sample_counted(self, n_shots: int, seed: int, shot_begin: int = 0, out=None, counts=None,
+                       det_counts=None, tiled: bool = False):
+        """sample / sample_tiled plus per-detector counts (sp_sample_ex):
+        det_counts[k] += number of shots in which detector k is 1."""
+        if out is None:
+            out = (self._torch.empty(max(self.tiled_words(n_shots), 1), dtype=self._torch.int64,
+                                     device=f"cuda:{self.device}") if tiled
+                   else self.empty_bits(self.n_meas, n_shots))
+        if tiled:
+            self._check_dev(out, self.tiled_words(n_shots), "out")
+            ld = 0
+        else:
+            self._check_matrix(out, self.n_meas, n_shots, "out")
+            ld = out.shape[1]
+        self._check_dev(counts, self.n_meas, "counts")
+        self._check_dev(det_counts, getattr(self, "n_det", 0), "det_counts")
+        N.check(self._L.sp_sample_ex(self._h, seed, shot_begin, n_shots, _ptr(out), ld,
+                                     _ptr(counts), _ptr(det_counts)))
+        return out
+
     def untile(self, tiled, n_shots: int, out=None):
         """Tiled records -> measurement-major words [n_meas, ceil(n/64)]."""
         if out is None:

@@ -20,6 +20,7 @@ def main():
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--counts", action="store_true")
     ap.add_argument("--tiled", action="store_true", help="tiled record layout")
+    ap.add_argument("--dets", action="store_true", help="per-detector counts (surface codes)")
     a = ap.parse_args()
     init = run_initialization(circuits.CONFIGS[a.config]["text"]())
     n = a.shots or circuits.CONFIGS[a.config]["shots"]
@@ -31,6 +32,13 @@ def main():
     run = (lambda seed: s.sample_tiled(n, seed, out=out, counts=counts)) if a.tiled else \
           (lambda seed: s.sample(n, seed, out=out, counts=counts))
     counts = torch.zeros(init.n_meas, dtype=torch.int64, device="cuda") if a.counts else None
+    if a.dets:
+        dd = {"cfg2": (5, 5), "cfg3": (15, 15)}[a.config]
+        dets, obs = circuits.surface_code_detectors(*dd)
+        s.set_detectors(dets + obs)
+        dc = torch.zeros(len(dets) + 1, dtype=torch.int64, device="cuda")
+        run = lambda seed: s.sample_counted(n, seed, out=out, counts=counts, det_counts=dc,  # noqa: E731
+                                            tiled=a.tiled)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     for i in range(3):
         run(i)
