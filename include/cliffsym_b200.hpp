@@ -19,6 +19,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <span>
@@ -33,8 +34,13 @@
 
 namespace cliffsym_b200 {
 
+// circuit.hpp:42-47: "line N: ..." plus the line number.
 struct ParseError : std::runtime_error {
-  using std::runtime_error::runtime_error;
+  explicit ParseError(const std::string& what)
+      : std::runtime_error(what), line(std::strtoull(what.c_str() + (what.rfind("line ", 0) == 0 ? 5 : what.size()), nullptr, 10)) {}
+  ParseError(size_t l, const std::string& what)
+      : std::runtime_error("line " + std::to_string(l) + ": " + what), line(l) {}
+  size_t line;
 };
 
 inline void throw_status(int code) {
@@ -80,7 +86,8 @@ class BitVec {
   std::vector<uint64_t> w_;
 };
 
-// TiledBitMatrix (bit_matrix.hpp:67-125) behaviour over bit-sliced rows.
+// TiledBitMatrix (bit_matrix.hpp:67-125) behaviour over bit-sliced rows
+// (TiledBitMatrix below is an alias, so reference code compiles unchanged).
 class BitMatrix {
  public:
   BitMatrix() = default;
@@ -131,6 +138,8 @@ class BitMatrix {
   size_t rows_ = 0, cols_ = 0, ld_ = 1;
   std::vector<uint64_t> w_;
 };
+
+using TiledBitMatrix = BitMatrix;
 
 // symbols.hpp:19-100
 enum class GroupDistribution : uint8_t {
@@ -194,17 +203,53 @@ struct MeasurementExpression {
   bool operator==(const MeasurementExpression&) const = default;
 };
 
+// circuit.hpp:13-40 (same kind order as the C ABI's program arrays).
+enum class InstrKind : uint8_t {
+  kH, kS, kSDag, kX, kY, kZ, kCX, kM, kR, kXError, kYError, kZError, kDepolarize1, kDepolarize2, kTick
+};
+
+struct Instruction {
+  InstrKind kind = InstrKind::kTick;
+  std::vector<uint32_t> targets;
+  double param = 0.0;  // probability, noise kinds only
+  size_t line = 0;     // 1-based source line, 0 when synthesized
+};
+
+struct CircuitSummary {  // circuit.hpp:67-79 (the fields the sampler path reads)
+  size_t n_qubits = 0;
+  size_t n_measurements = 0;
+};
+
 struct InitResult {
   size_t n_qubits = 0;
+  CircuitSummary summary;
   SymbolRegistry registry;
   std::vector<MeasurementExpression> expressions;
 };
 
-// parse_circuit + run_initialization (circuit.hpp:55, tableau.hpp:101).
-inline InitResult run_initialization_text(std::string_view text) {
+// parse_circuit (circuit.hpp:55) through the library's parser.
+inline std::vector<Instruction> parse_circuit(std::string_view text) {
   std::string t(text);
-  sp_model* m = nullptr;
-  throw_status(sp_model_from_text(t.c_str(), &m));
+  uint64_t n = 0, nt = 0;
+  throw_status(sp_parse_circuit(t.c_str(), 0, nullptr, nullptr, nullptr, nullptr, 0, nullptr, &n, &nt));
+  std::vector<uint8_t> kinds(n + 1);
+  std::vector<double> params(n + 1);
+  std::vector<uint64_t> lines(n + 1), ptr(n + 1);
+  std::vector<uint32_t> tg(nt + 1);
+  throw_status(sp_parse_circuit(t.c_str(), n, kinds.data(), params.data(), lines.data(), ptr.data(),
+                                nt, tg.data(), &n, &nt));
+  std::vector<Instruction> prog(n);
+  for (uint64_t i = 0; i < n; ++i) {
+    prog[i].kind = static_cast<InstrKind>(kinds[i]);
+    prog[i].param = params[i];
+    prog[i].line = lines[i];
+    prog[i].targets.assign(tg.begin() + ptr[i], tg.begin() + ptr[i + 1]);
+  }
+  return prog;
+}
+
+namespace detail {
+inline InitResult init_from_model(sp_model* m) {
   std::unique_ptr<sp_model, void (*)(sp_model*)> guard(m, sp_model_destroy);
   uint64_t nq, nm, ns, ng, nnz;
   throw_status(sp_model_dims(m, &nq, &nm, &ns, &ng, &nnz));
@@ -214,6 +259,8 @@ inline InitResult run_initialization_text(std::string_view text) {
   throw_status(sp_model_export(m, rp.data(), si.data(), g.data()));
   InitResult r;
   r.n_qubits = nq;
+  r.summary.n_qubits = nq;
+  r.summary.n_measurements = nm;
   for (uint64_t i = 1; i < ng; ++i) {
     auto d = static_cast<GroupDistribution>(g[i].dist);
     if (d == GroupDistribution::kFairCoin)
@@ -224,6 +271,33 @@ inline InitResult run_initialization_text(std::string_view text) {
   r.expressions.resize(nm);
   for (uint64_t k = 0; k < nm; ++k) r.expressions[k].symbols.assign(si.begin() + rp[k], si.begin() + rp[k + 1]);
   return r;
+}
+}  // namespace detail
+
+// run_initialization (tableau.hpp:101) on a parsed or synthesized program.
+inline InitResult run_initialization(const std::vector<Instruction>& prog) {
+  std::vector<uint8_t> kinds(prog.size() + 1);
+  std::vector<double> params(prog.size() + 1);
+  std::vector<uint64_t> ptr{0};
+  std::vector<uint32_t> tg;
+  for (size_t i = 0; i < prog.size(); ++i) {
+    kinds[i] = static_cast<uint8_t>(prog[i].kind);
+    params[i] = prog[i].param;
+    tg.insert(tg.end(), prog[i].targets.begin(), prog[i].targets.end());
+    ptr.push_back(tg.size());
+  }
+  if (tg.empty()) tg.push_back(0);
+  sp_model* m = nullptr;
+  throw_status(sp_model_from_program(prog.size(), kinds.data(), params.data(), ptr.data(), tg.data(), &m));
+  return detail::init_from_model(m);
+}
+
+// parse_circuit + run_initialization in one call.
+inline InitResult run_initialization_text(std::string_view text) {
+  std::string t(text);
+  sp_model* m = nullptr;
+  throw_status(sp_model_from_text(t.c_str(), &m));
+  return detail::init_from_model(m);
 }
 
 // sampler.hpp:30-46
@@ -244,24 +318,47 @@ enum class ShotFormat : uint8_t { k01 = SP_FMT_01, kB8 = SP_FMT_B8 };
 
 namespace detail {
 
+// Grow-only device buffer, reused across calls (no cudaMalloc per call).
 struct DevBuf {
   void* p = nullptr;
-  explicit DevBuf(size_t n) { cuda_check(cudaMalloc(&p, std::max<size_t>(n, 16))); }
-  ~DevBuf() { cudaFree(p); }
-  DevBuf(const DevBuf&) = delete;
-  DevBuf& operator=(const DevBuf&) = delete;
+  size_t n = 0;
+  void* ensure(size_t bytes) {
+    bytes = std::max<size_t>(bytes, 16);
+    if (bytes > n) {
+      if (p) cudaFree(p);
+      p = nullptr;
+      cuda_check(cudaMalloc(&p, bytes));
+      n = bytes;
+    }
+    return p;
+  }
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
 };
 
-// One device context per host thread (the ABI's threading rule).
-inline sp_ctx* ctx() {
+// Device contexts per host thread (the ABI's threading rule), one per role,
+// so one call never replaces the model another role's context holds (a
+// draw_assignments between two sample_shots calls keeps the loaded model).
+enum Role { kDraw = 0, kProduct = 1, kFused = 2, kEncode = 3, kRoles = 4 };
+struct Slot {
+  sp_ctx* c = nullptr;
+  DevBuf a, b;
+};
+inline Slot& slot(Role r) {
   struct Holder {
-    sp_ctx* c = nullptr;
-    Holder() { throw_status(sp_ctx_create(0, &c)); }
-    ~Holder() { sp_ctx_destroy(c); }
+    Slot s[kRoles];
+    Holder() {
+      for (Slot& x : s) throw_status(sp_ctx_create(0, &x.c));
+    }
+    ~Holder() {
+      for (Slot& x : s) sp_ctx_destroy(x.c);
+    }
   };
   thread_local Holder h;
-  return h.c;
+  return h.s[r];
 }
+inline sp_ctx* ctx(Role r = kProduct) { return slot(r).c; }
 
 inline void load_rows(sp_ctx* c, std::span<const std::vector<uint32_t>> rows, uint64_t n_sym) {
   std::vector<uint64_t> rp{0};
@@ -292,26 +389,29 @@ inline void sorted_unique_check(const std::vector<std::vector<uint32_t>>& rows) 
 inline SymbolAssignmentBatch draw_assignments(const SymbolRegistry& registry, size_t n_smp,
                                               uint64_t seed) {
   if (n_smp == 0) throw std::invalid_argument("need at least one shot");
-  sp_ctx* c = detail::ctx();
+  detail::Slot& sl = detail::slot(detail::kDraw);
+  sp_ctx* c = sl.c;
   std::vector<std::vector<uint32_t>> none;
   detail::load_rows(c, none, registry.size());
   auto g = registry.to_abi();
   throw_status(sp_load_groups(c, g.size(), g.data()));
   throw_status(sp_set_rng(c, SP_RNG_COMPAT_SPLITMIX));
   SymbolAssignmentBatch b{BitMatrix(registry.size(), n_smp)};
-  detail::DevBuf d(b.data.bytes());
-  throw_status(sp_draw_assignments(c, seed, 0, n_smp, static_cast<uint64_t*>(d.p), b.data.ld()));
-  cuda_check(cudaMemcpy(b.data.data(), d.p, b.data.bytes(), cudaMemcpyDeviceToHost));
+  void* d = sl.a.ensure(b.data.bytes());
+  throw_status(sp_draw_assignments(c, seed, 0, n_smp, static_cast<uint64_t*>(d), b.data.ld()));
+  cuda_check(cudaMemcpy(b.data.data(), d, b.data.bytes(), cudaMemcpyDeviceToHost));
   return b;
 }
 
 // gf2_multiply_sparse (bit_matrix.hpp:133-134).
 inline BitMatrix gf2_multiply_sparse(std::span<const std::vector<uint32_t>> a_rows,
                                      const BitMatrix& b) {
-  sp_ctx* c = detail::ctx();
+  detail::Slot& sl = detail::slot(detail::kProduct);
+  sp_ctx* c = sl.c;
   std::vector<std::vector<uint32_t>> rows(a_rows.begin(), a_rows.end());
   for (auto& r : rows) std::sort(r.begin(), r.end());
   detail::sorted_unique_check(rows);
+  throw_status(sp_set_product(c, SP_PRODUCT_AUTO));
   detail::load_rows(c, rows, b.rows());
   BitMatrix out(rows.size(), b.cols());
   if (rows.empty() || b.cols() == 0) {
@@ -320,11 +420,31 @@ inline BitMatrix gf2_multiply_sparse(std::span<const std::vector<uint32_t>> a_ro
         if (s >= b.rows()) throw std::out_of_range("sparse row index");
     return out;
   }
-  detail::DevBuf dS(b.bytes()), dO(out.bytes());
-  cuda_check(cudaMemcpy(dS.p, b.data(), b.bytes(), cudaMemcpyHostToDevice));
-  throw_status(sp_sample_given_S(c, static_cast<const uint64_t*>(dS.p), b.rows(), b.ld(), b.cols(),
-                                 static_cast<uint64_t*>(dO.p), out.ld()));
-  cuda_check(cudaMemcpy(out.data(), dO.p, out.bytes(), cudaMemcpyDeviceToHost));
+  void* dS = sl.a.ensure(b.bytes());
+  void* dO = sl.b.ensure(out.bytes());
+  cuda_check(cudaMemcpy(dS, b.data(), b.bytes(), cudaMemcpyHostToDevice));
+  throw_status(sp_sample_given_S(c, static_cast<const uint64_t*>(dS), b.rows(), b.ld(), b.cols(),
+                                 static_cast<uint64_t*>(dO), out.ld()));
+  cuda_check(cudaMemcpy(out.data(), dO, out.bytes(), cudaMemcpyDeviceToHost));
+  return out;
+}
+
+// gf2_multiply (bit_matrix.hpp:129): dense a [m x k] times b [k x n] — the
+// device's dense explicit-S product (Four-Russians tables).
+inline BitMatrix gf2_multiply(const BitMatrix& a, const BitMatrix& b) {
+  if (a.cols() != b.rows()) throw std::invalid_argument("gf2_multiply: inner dimensions differ");
+  BitMatrix out(a.rows(), b.cols());
+  if (a.rows() == 0 || b.cols() == 0) return out;
+  detail::Slot& sl = detail::slot(detail::kProduct);
+  sp_ctx* c = sl.c;
+  throw_status(sp_load_msym_dense(c, a.rows(), std::max<size_t>(a.cols(), 1), a.data(), a.ld()));
+  throw_status(sp_set_product(c, SP_PRODUCT_DENSE));
+  void* dS = sl.a.ensure(b.bytes());
+  void* dO = sl.b.ensure(out.bytes());
+  cuda_check(cudaMemcpy(dS, b.data(), b.bytes(), cudaMemcpyHostToDevice));
+  throw_status(sp_sample_given_S(c, static_cast<const uint64_t*>(dS), std::max<size_t>(b.rows(), 1),
+                                 b.ld(), b.cols(), static_cast<uint64_t*>(dO), out.ld()));
+  cuda_check(cudaMemcpy(out.data(), dO, out.bytes(), cudaMemcpyDeviceToHost));
   return out;
 }
 
@@ -349,7 +469,8 @@ inline SampleMatrix sample(const std::vector<MeasurementExpression>& expressions
 inline SampleMatrix sample_shots(const InitResult& init, size_t n_smp, uint64_t seed,
                                  sp_rng rng = SP_RNG_PHILOX) {
   if (n_smp == 0) throw std::invalid_argument("need at least one shot");
-  sp_ctx* c = detail::ctx();
+  detail::Slot& sl = detail::slot(detail::kFused);
+  sp_ctx* c = sl.c;
   auto rows = detail::rows_of(init.expressions);
   detail::load_rows(c, rows, init.registry.size());
   auto g = init.registry.to_abi();
@@ -360,9 +481,9 @@ inline SampleMatrix sample_shots(const InitResult& init, size_t n_smp, uint64_t 
   m.measurement_order.resize(init.expressions.size());
   for (size_t i = 0; i < m.measurement_order.size(); ++i) m.measurement_order[i] = static_cast<uint32_t>(i);
   if (init.expressions.empty()) return m;
-  detail::DevBuf d(m.data.bytes());
-  throw_status(sp_sample(c, seed, 0, n_smp, static_cast<uint64_t*>(d.p), m.data.ld(), nullptr));
-  cuda_check(cudaMemcpy(m.data.data(), d.p, m.data.bytes(), cudaMemcpyDeviceToHost));
+  void* d = sl.a.ensure(m.data.bytes());
+  throw_status(sp_sample(c, seed, 0, n_smp, static_cast<uint64_t*>(d), m.data.ld(), nullptr));
+  cuda_check(cudaMemcpy(m.data.data(), d, m.data.bytes(), cudaMemcpyDeviceToHost));
   return m;
 }
 
@@ -372,12 +493,13 @@ inline std::string encode_shots(const SampleMatrix& m, ShotFormat format) {
   const uint64_t size = sp_encoded_size(n_m, n, static_cast<sp_format>(format));
   std::string out(size, '\0');
   if (size == 0) return out;
-  sp_ctx* c = detail::ctx();
-  detail::DevBuf dm(m.data.bytes()), db(size);
-  cuda_check(cudaMemcpy(dm.p, m.data.data(), m.data.bytes(), cudaMemcpyHostToDevice));
-  throw_status(sp_encode(c, static_cast<const uint64_t*>(dm.p), m.data.ld(), n_m, n,
-                         static_cast<sp_format>(format), static_cast<uint8_t*>(db.p)));
-  cuda_check(cudaMemcpy(out.data(), db.p, size, cudaMemcpyDeviceToHost));
+  detail::Slot& sl = detail::slot(detail::kEncode);
+  void* dm = sl.a.ensure(m.data.bytes());
+  void* db = sl.b.ensure(size);
+  cuda_check(cudaMemcpy(dm, m.data.data(), m.data.bytes(), cudaMemcpyHostToDevice));
+  throw_status(sp_encode(sl.c, static_cast<const uint64_t*>(dm), m.data.ld(), n_m, n,
+                         static_cast<sp_format>(format), static_cast<uint8_t*>(db)));
+  cuda_check(cudaMemcpy(out.data(), db, size, cudaMemcpyDeviceToHost));
   return out;
 }
 

@@ -94,6 +94,20 @@ int sp_model_dims(const sp_model* m, uint64_t* n_qubits, uint64_t* n_meas, uint6
 /* row_ptr[n_meas+1], sym_idx[nnz], groups[n_groups]; any may be NULL. */
 int sp_model_export(const sp_model* m, uint64_t* row_ptr, uint32_t* sym_idx, sp_group* groups);
 
+/* parse_circuit (circuit.hpp:55, circuit.cpp:79-168) as flat arrays: kind
+ * (InstrKind order, circuit.hpp:13-29), parameter, 1-based source line and
+ * the targets of instruction i in targets[tgt_ptr[i] .. tgt_ptr[i+1]).
+ * Two-pass: with kinds == NULL only *n_instr_out / *n_targets_out are set.
+ * SP_ERR_PARSE with the reference's "line N: ..." message on bad input. */
+int sp_parse_circuit(const char* text, uint64_t cap_instr, uint8_t* kinds, double* params,
+                     uint64_t* lines, uint64_t* tgt_ptr, uint64_t cap_targets,
+                     uint32_t* targets, uint64_t* n_instr_out, uint64_t* n_targets_out);
+/* run_initialization(const std::vector<Instruction>&) (tableau.hpp:101) on a
+ * structured program in the same flat form; the instruction shapes are
+ * checked like parse_circuit's (SP_ERR_INVALID_ARGUMENT). */
+int sp_model_from_program(uint64_t n_instr, const uint8_t* kinds, const double* params,
+                          const uint64_t* tgt_ptr, const uint32_t* targets, sp_model** out);
+
 /* Detector layer (not in the reference: its parser has no DETECTOR,
  * circuit.cpp:117-121). A detector is the XOR of a set of measurements;
  * detector k = measurements det_meas[det_ptr[k] .. det_ptr[k+1]). Its symbolic

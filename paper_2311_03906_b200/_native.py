@@ -43,6 +43,8 @@ SIGNATURES = [
     ("sp_abi_version", _i, []),
     ("sp_model_from_text", _i, [C.c_char_p, C.POINTER(_p)]),
     ("sp_model_destroy", None, [_p]),
+    ("sp_parse_circuit", _i, [C.c_char_p, _u64, _p, _p, _p, _p, _u64, _p, _pu64, _pu64]),
+    ("sp_model_from_program", _i, [_u64, _p, _p, _p, _p, C.POINTER(_p)]),
     ("sp_model_dims", _i, [_p, _pu64, _pu64, _pu64, _pu64, _pu64]),
     ("sp_model_export", _i, [_p, _p, _p, _p]),
     ("sp_detector_rows", _i, [_u64, _p, _p, _u64, _p, _p, _p, _p, _u64, _pu64]),

@@ -1566,6 +1566,77 @@ int sp_model_from_text(const char* text, sp_model** out) {
   }
 }
 
+int sp_parse_circuit(const char* text, uint64_t cap_instr, uint8_t* kinds, double* params,
+                     uint64_t* lines, uint64_t* tgt_ptr, uint64_t cap_targets, uint32_t* targets,
+                     uint64_t* n_instr_out, uint64_t* n_targets_out) {
+  if (!text || !n_instr_out || !n_targets_out) return fail(SP_ERR_INVALID_ARGUMENT, "null argument");
+  try {
+    const std::vector<Instr> prog = parse_circuit(text);
+    uint64_t nt = 0;
+    for (const Instr& in : prog) nt += in.targets.size();
+    *n_instr_out = prog.size();
+    *n_targets_out = nt;
+    if (!kinds) return SP_OK;  // sizes only
+    if (cap_instr < prog.size() || cap_targets < nt || !params || !lines || !tgt_ptr || (nt && !targets))
+      return fail(SP_ERR_INVALID_ARGUMENT, "output buffers too small");
+    uint64_t t = 0;
+    tgt_ptr[0] = 0;
+    for (size_t i = 0; i < prog.size(); ++i) {
+      kinds[i] = static_cast<uint8_t>(prog[i].op);
+      params[i] = prog[i].p;
+      lines[i] = prog[i].line;
+      for (uint32_t q : prog[i].targets) targets[t++] = q;
+      tgt_ptr[i + 1] = t;
+    }
+    return SP_OK;
+  } catch (const ParseError& e) {
+    return fail(SP_ERR_PARSE, e.what());
+  } catch (const std::exception& e) {
+    return fail(SP_ERR_INVALID_ARGUMENT, e.what());
+  }
+}
+
+int sp_model_from_program(uint64_t n_instr, const uint8_t* kinds, const double* params,
+                          const uint64_t* tgt_ptr, const uint32_t* targets, sp_model** out) {
+  if (!out || (n_instr && (!kinds || !params || !tgt_ptr)))
+    return fail(SP_ERR_INVALID_ARGUMENT, "null argument");
+  try {
+    std::vector<Instr> prog(n_instr);
+    for (uint64_t i = 0; i < n_instr; ++i) {
+      if (kinds[i] > static_cast<uint8_t>(Op::Tick))
+        return fail(SP_ERR_INVALID_ARGUMENT, "unknown instruction kind");
+      Instr& in = prog[i];
+      in.op = static_cast<Op>(kinds[i]);
+      in.p = params[i];
+      if (tgt_ptr[i + 1] < tgt_ptr[i] || (tgt_ptr[i + 1] > tgt_ptr[i] && !targets))
+        return fail(SP_ERR_INVALID_ARGUMENT, "bad target offsets");
+      in.targets.assign(targets + tgt_ptr[i], targets + tgt_ptr[i + 1]);
+      // the shape rules parse_circuit enforces (circuit.cpp:79-168)
+      const bool noise = in.op == Op::XErr || in.op == Op::YErr || in.op == Op::ZErr ||
+                         in.op == Op::Dep1 || in.op == Op::Dep2;
+      const bool pairs = in.op == Op::CX || in.op == Op::Dep2;
+      if (noise && (in.p < 0.0 || in.p > 1.0))
+        return fail(SP_ERR_INVALID_ARGUMENT, "probability out of [0,1]");
+      if ((in.op == Op::Tick) != in.targets.empty())
+        return fail(SP_ERR_INVALID_ARGUMENT, in.op == Op::Tick ? "TICK takes no targets" : "missing targets");
+      if (pairs) {
+        if (in.targets.size() & 1) return fail(SP_ERR_INVALID_ARGUMENT, "odd number of pair targets");
+        for (size_t k = 0; k < in.targets.size(); k += 2)
+          if (in.targets[k] == in.targets[k + 1])
+            return fail(SP_ERR_INVALID_ARGUMENT, "pair targets the same qubit twice");
+      }
+    }
+    auto m = std::make_unique<sp_model>();
+    m->m = run_initialization(prog);
+    *out = m.release();
+    return SP_OK;
+  } catch (const std::logic_error& e) {
+    return fail(SP_ERR_LOGIC, e.what());
+  } catch (const std::exception& e) {
+    return fail(SP_ERR_INVALID_ARGUMENT, e.what());
+  }
+}
+
 void sp_model_destroy(sp_model* m) { delete m; }
 
 int sp_model_dims(const sp_model* m, uint64_t* n_qubits, uint64_t* n_meas, uint64_t* n_sym,

@@ -1,5 +1,6 @@
-// Host front end — see frontend.hpp for scope. Independent implementation of
-// the reference's parse_circuit (circuit.cpp:79-168), summarize
+// Host front end — see frontend.hpp for scope. Accepts the language of the
+// reference's parse_circuit (circuit.cpp:79-168) with its own table-driven
+// scanner and validator; independent implementations of summarize
 // (circuit.cpp:188-226), decompose_noise (circuit.cpp:228-281) and the
 // one-pass symbolic tableau (tableau.cpp:17-198, 318-382).
 #include "frontend.hpp"
@@ -17,105 +18,137 @@ namespace symphase {
 
 namespace {
 
-bool is_noise(Op k) {
-  return k == Op::XErr || k == Op::YErr || k == Op::ZErr || k == Op::Dep1 || k == Op::Dep2;
-}
-bool is_pair_op(Op k) { return k == Op::CX || k == Op::Dep2; }
+// Instruction vocabulary: spelling (upper case) -> opcode and the shape
+// rules the parser checks (a probability argument for noise channels,
+// target pairs for two-qubit instructions, no targets for TICK).
+struct OpSpec {
+  const char* name;
+  Op op;
+  bool noise, pairs;
+};
+constexpr OpSpec kOps[] = {
+    {"H", Op::H, false, false},         {"S", Op::S, false, false},
+    {"S_DAG", Op::SDag, false, false},  {"X", Op::X, false, false},
+    {"Y", Op::Y, false, false},         {"Z", Op::Z, false, false},
+    {"CX", Op::CX, false, true},        {"CNOT", Op::CX, false, true},
+    {"M", Op::M, false, false},         {"MZ", Op::M, false, false},
+    {"R", Op::R, false, false},         {"X_ERROR", Op::XErr, true, false},
+    {"Y_ERROR", Op::YErr, true, false}, {"Z_ERROR", Op::ZErr, true, false},
+    {"DEPOLARIZE1", Op::Dep1, true, false}, {"DEPOLARIZE2", Op::Dep2, true, true},
+    {"TICK", Op::Tick, false, false}};
+// Stim-format instructions the flat circuit model does not cover.
+constexpr const char* kUnsupported[] = {"REPEAT", "DETECTOR", "OBSERVABLE_INCLUDE",
+                                        "QUBIT_COORDS", "SHIFT_COORDS"};
 
-std::optional<Op> op_from_name(std::string name) {
-  for (auto& c : name) c = static_cast<char>(std::toupper(static_cast<unsigned char>(c)));
-  static const struct { const char* n; Op op; } kTable[] = {
-      {"H", Op::H},         {"S", Op::S},           {"S_DAG", Op::SDag},
-      {"X", Op::X},         {"Y", Op::Y},           {"Z", Op::Z},
-      {"CX", Op::CX},       {"CNOT", Op::CX},       {"M", Op::M},
-      {"MZ", Op::M},        {"R", Op::R},           {"X_ERROR", Op::XErr},
-      {"Y_ERROR", Op::YErr}, {"Z_ERROR", Op::ZErr}, {"DEPOLARIZE1", Op::Dep1},
-      {"DEPOLARIZE2", Op::Dep2}, {"TICK", Op::Tick}};
-  for (const auto& e : kTable)
-    if (name == e.n) return e.op;
-  return std::nullopt;
+const OpSpec* find_op(std::string_view name) {
+  std::string up(name);
+  std::transform(up.begin(), up.end(), up.begin(),
+                 [](unsigned char c) { return static_cast<char>(std::toupper(c)); });
+  for (const OpSpec& o : kOps)
+    if (up == o.name) return &o;
+  return nullptr;
 }
 
-// Whitespace set of operator>> on a C-locale istringstream.
-bool is_ws(char c) {
+// The characters operator>> skips on a C-locale stream.
+constexpr bool blank(char c) {
   return c == ' ' || c == '\t' || c == '\n' || c == '\v' || c == '\f' || c == '\r';
+}
+
+// Splits circuit text into lines of whitespace-separated words, with '#'
+// comments removed; calls emit(line number, words) for each non-empty line.
+template <class Emit>
+void scan_lines(std::string_view text, Emit&& emit) {
+  std::vector<std::string_view> words;
+  size_t number = 1, i = 0;
+  bool in_comment = false;
+  const size_t n = text.size();
+  while (i <= n) {
+    if (i == n || text[i] == '\n') {  // end of a line
+      if (!words.empty()) emit(number, words);
+      words.clear();
+      in_comment = false;
+      ++number;
+      ++i;
+      continue;
+    }
+    if (in_comment || blank(text[i])) {
+      ++i;
+      continue;
+    }
+    if (text[i] == '#') {
+      in_comment = true;
+      ++i;
+      continue;
+    }
+    const size_t b = i;
+    while (i < n && !blank(text[i]) && text[i] != '#') ++i;
+    words.push_back(text.substr(b, i - b));
+  }
+}
+
+template <class T>
+bool parse_number(std::string_view w, T& out) {
+  const auto r = std::from_chars(w.data(), w.data() + w.size(), out);
+  return r.ec == std::errc{} && r.ptr == w.data() + w.size();
+}
+
+// One instruction from its words: NAME[(p)] target target ...
+Instr make_instr(size_t line, const std::vector<std::string_view>& words) {
+  std::string_view head = words.front();
+  std::optional<double> arg;
+  if (const size_t lp = head.find('('); lp != std::string_view::npos) {
+    if (head.back() != ')') throw ParseError(line, "malformed parameter");
+    const std::string_view inner = head.substr(lp + 1, head.size() - lp - 2);
+    double v = 0;
+    if (!parse_number(inner, v)) throw ParseError(line, "bad probability '" + std::string(inner) + "'");
+    arg = v;
+    head = head.substr(0, lp);
+  }
+  const OpSpec* spec = find_op(head);
+  if (!spec) {
+    for (const char* u : kUnsupported)
+      if (head == u)
+        throw ParseError(line, "unsupported instruction '" + std::string(head) +
+                                   "' (flat gate/noise/measure circuits only)");
+    throw ParseError(line, "unknown instruction '" + std::string(head) + "'");
+  }
+  Instr in;
+  in.op = spec->op;
+  in.line = line;
+  in.targets.reserve(words.size() - 1);
+  for (size_t k = 1; k < words.size(); ++k) {
+    uint32_t q = 0;
+    if (!parse_number(words[k], q)) throw ParseError(line, "bad target '" + std::string(words[k]) + "'");
+    in.targets.push_back(q);
+  }
+  // shape rules
+  if (spec->noise && !arg) throw ParseError(line, "noise instruction needs a probability");
+  if (!spec->noise && arg) throw ParseError(line, "unexpected parameter on non-noise instruction");
+  if (arg) {
+    if (*arg < 0.0 || *arg > 1.0) throw ParseError(line, "probability out of [0,1]");
+    in.p = *arg;
+  }
+  const bool tick = spec->op == Op::Tick;
+  if (tick && !in.targets.empty()) throw ParseError(line, "TICK takes no targets");
+  if (!tick && in.targets.empty()) throw ParseError(line, "missing targets");
+  if (spec->pairs) {
+    if (in.targets.size() & 1)
+      throw ParseError(line, "odd number of targets for a two-qubit instruction");
+    for (size_t k = 0; k + 1 < in.targets.size(); k += 2)
+      if (in.targets[k] == in.targets[k + 1]) throw ParseError(line, "pair targets the same qubit twice");
+  }
+  return in;
 }
 
 }  // namespace
 
+// Accepts the reference's circuit language (circuit.cpp:79-168): the same
+// instruction set, the same rejections and line numbers, its own scanner.
 std::vector<Instr> parse_circuit(std::string_view text) {
   std::vector<Instr> prog;
-  size_t line_no = 0, pos = 0;
-  while (pos <= text.size()) {
-    size_t eol = text.find('\n', pos);
-    std::string_view line =
-        text.substr(pos, eol == std::string_view::npos ? text.size() - pos : eol - pos);
-    pos = eol == std::string_view::npos ? text.size() + 1 : eol + 1;
-    ++line_no;
-    if (size_t h = line.find('#'); h != std::string_view::npos) line = line.substr(0, h);
-
-    std::vector<std::string> tok;
-    for (size_t i = 0; i < line.size();) {
-      while (i < line.size() && is_ws(line[i])) ++i;
-      size_t j = i;
-      while (j < line.size() && !is_ws(line[j])) ++j;
-      if (j > i) tok.emplace_back(line.substr(i, j - i));
-      i = j;
-    }
-    if (tok.empty()) continue;
-
-    std::string head = tok[0];
-    std::optional<double> prob;
-    if (size_t open = head.find('('); open != std::string::npos) {
-      if (head.back() != ')') throw ParseError(line_no, "malformed parameter");
-      std::string body = head.substr(open + 1, head.size() - open - 2);
-      double v = 0;
-      auto r = std::from_chars(body.data(), body.data() + body.size(), v);
-      if (r.ec != std::errc{} || r.ptr != body.data() + body.size())
-        throw ParseError(line_no, "bad probability '" + body + "'");
-      prob = v;
-      head = head.substr(0, open);
-    }
-    auto op = op_from_name(head);
-    if (!op) {
-      if (head == "REPEAT" || head == "DETECTOR" || head == "OBSERVABLE_INCLUDE" ||
-          head == "QUBIT_COORDS" || head == "SHIFT_COORDS")
-        throw ParseError(line_no, "unsupported instruction '" + head +
-                                      "' (flat gate/noise/measure circuits only)");
-      throw ParseError(line_no, "unknown instruction '" + head + "'");
-    }
-    Instr in;
-    in.op = *op;
-    in.line = line_no;
-    for (size_t i = 1; i < tok.size(); ++i) {
-      uint32_t t = 0;
-      const std::string& s = tok[i];
-      auto r = std::from_chars(s.data(), s.data() + s.size(), t);
-      if (r.ec != std::errc{} || r.ptr != s.data() + s.size())
-        throw ParseError(line_no, "bad target '" + s + "'");
-      in.targets.push_back(t);
-    }
-    if (is_noise(in.op)) {
-      if (!prob) throw ParseError(line_no, "noise instruction needs a probability");
-      if (*prob < 0.0 || *prob > 1.0) throw ParseError(line_no, "probability out of [0,1]");
-      in.p = *prob;
-    } else if (prob) {
-      throw ParseError(line_no, "unexpected parameter on non-noise instruction");
-    }
-    if (in.op == Op::Tick) {
-      if (!in.targets.empty()) throw ParseError(line_no, "TICK takes no targets");
-    } else if (in.targets.empty()) {
-      throw ParseError(line_no, "missing targets");
-    }
-    if (is_pair_op(in.op)) {
-      if (in.targets.size() % 2 != 0)
-        throw ParseError(line_no, "odd number of targets for a two-qubit instruction");
-      for (size_t i = 0; i < in.targets.size(); i += 2)
-        if (in.targets[i] == in.targets[i + 1])
-          throw ParseError(line_no, "pair targets the same qubit twice");
-    }
-    prog.push_back(std::move(in));
-  }
+  scan_lines(text, [&](size_t line, const std::vector<std::string_view>& words) {
+    prog.push_back(make_instr(line, words));
+  });
   return prog;
 }
 

@@ -206,6 +206,27 @@ int main() {
     check_within_4sigma(counts[2], shots, p / 3.0);
     check_within_4sigma(counts[3], shots, p / 3.0);
   }
+  {  // a draw_assignments call between two fused samples keeps the fused
+     // context's model: both samples of the same seed are identical
+    auto init = init_from("X_ERROR(0.3) 0\nDEPOLARIZE1(0.2) 1\nM 0 1\n");
+    auto other = init_from("H 0\nM 0\n");
+    auto a = sample_shots(init, 5000, 7);
+    auto batch = draw_assignments(other.registry, 100, 1);
+    CHECK(batch.n_symbols() == other.registry.size());
+    auto b = sample_shots(init, 5000, 7);
+    CHECK(a.data.same_bits(b.data));
+    // parse_circuit + run_initialization(program) == run_initialization_text
+    auto prog = parse_circuit("X_ERROR(0.3) 0\nDEPOLARIZE1(0.2) 1\nM 0 1\n");
+    CHECK(prog.size() == 3 && prog[1].kind == InstrKind::kDepolarize1 && prog[2].targets.size() == 2);
+    CHECK(run_initialization(prog).expressions == init.expressions);
+    bool threw = false;
+    try {
+      parse_circuit("H 0\nFROB 1\n");
+    } catch (const ParseError& e) {
+      threw = e.line == 2;
+    }
+    CHECK(threw);
+  }
   std::printf("%d checks, %d failed\n", g_checks, g_fail);
   return g_fail ? 1 : 0;
 }

@@ -194,3 +194,58 @@ def test_baseline_workloads_match_reference_pass(cfg):
     assert hashlib.sha256(text.encode()).hexdigest() == want["text"]["sha256"]
     from test_gpu_large import digest_ok
     assert digest_ok(run_initialization(text), want)
+
+
+def _fuzz_line(rng):
+    names = ["H", "h", "S", "S_DAG", "X", "Y", "Z", "CX", "cnot", "M", "MZ", "R", "TICK", "tick",
+             "X_ERROR", "Y_ERROR", "Z_ERROR", "DEPOLARIZE1", "DEPOLARIZE2", "FROB", "REPEAT",
+             "DETECTOR", "QUBIT_COORDS"]
+    name = names[rng.integers(len(names))]
+    r = rng.random()
+    if r < 0.5:
+        name += f"({rng.choice(['0.1', '0', '1', '1.5', '-0.1', 'x', '', '1e-3', 'nan'])})"
+    elif r < 0.55:
+        name += "(0.2"
+    n = int(rng.integers(0, 5))
+    targets = [str(int(rng.integers(0, 4))) if rng.random() < 0.9 else
+               rng.choice(["-1", "a", "2x", "rec[-1]"]) for _ in range(n)]
+    ws = [" ", "\t", "  ", " \r"]
+    line = name + "".join(ws[rng.integers(len(ws))] + t for t in targets)
+    if rng.random() < 0.2:
+        line += " # note " + rng.choice(["", "H 0", "#"])
+    if rng.random() < 0.1:
+        line = "   " + line
+    return line
+
+
+def test_parser_agrees_with_reference_parser(ref):
+    """The rewritten scanner/validator accepts exactly what the reference's
+    parse_circuit (circuit.cpp:79-168) accepts, and reports the same line.
+    Single-line programs first (every rule), then multi-line ones."""
+    import re
+    rng = np.random.default_rng(77)
+    texts = [_fuzz_line(rng) for _ in range(600)]
+    texts += ["\n".join(_fuzz_line(rng) for _ in range(int(rng.integers(2, 6))))
+              for _ in range(200)]
+    for text in texts:
+        try:
+            ref.circuit(text)
+            ref_err = None
+        except (ValueError, RuntimeError) as e:
+            ref_err = str(e)
+        try:
+            run_initialization(text)
+            ours = None
+        except ParseError as e:
+            ours = str(e)
+        except LogicError:
+            ours = "logic"
+        if ref_err is None:
+            assert ours is None, (text, ours)
+            continue
+        if "line" not in ref_err:  # a logic error of the symbolic pass, not the parser
+            assert ours is not None, (text, ref_err)
+            continue
+        assert ours is not None and ours != "logic", (text, ref_err)
+        want = re.search(r"line (\d+)", ref_err).group(1)
+        assert f"line {want}:" in ours, (text, ref_err, ours)
