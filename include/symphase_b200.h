@@ -75,7 +75,9 @@ typedef enum { SP_FMT_01 = 0, SP_FMT_B8 = 1 } sp_format; /* ShotFormat, sampler.
 typedef enum {
   SP_PRODUCT_AUTO = 0,   /* DENSE when nnz(M_sym) > 0.15 n_meas n_sym (measured crossover), else SPARSE */
   SP_PRODUCT_SPARSE = 1, /* CSR over measurements (expression lists) */
-  SP_PRODUCT_DENSE = 2   /* dense row-major M_sym words, Four-Russians tables */
+  SP_PRODUCT_DENSE = 2,  /* dense row-major M_sym words, Four-Russians tables */
+  SP_PRODUCT_TENSOR = 3  /* dense M_sym as an integer GEMM on the tensor cores (tcgen05.mma
+                            kind::i8, int32 counts in TMEM, parity of each count) */
 } sp_product;
 
 typedef struct sp_ctx sp_ctx;

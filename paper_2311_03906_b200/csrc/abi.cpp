@@ -125,6 +125,8 @@ struct sp_ctx {
   bool prod_ready = false;
   DevPlan pp;
   DBuf p_row_ptr, p_sym_idx, p_dense, p_dense_gm, p_seg_ptr, p_seg_row, p_split_rows;
+  DBuf p_tc_a;          // K6: M_sym bytes in the tensor-core tile layout
+  bool tc_ready = false;
   // sp_sample_to_host: double-buffered records/bytes, a copy stream and the
   // events that hand each buffer between the compute and copy streams
   DBuf s_out[2], s_bytes[2];
@@ -266,7 +268,7 @@ struct PlanTimer {
 // Measured on B200 at cfg5's shape the two cross at density ~0.15.
 constexpr double kDenseProductDensity = 0.15;
 bool dense_product(const sp_ctx* c) {
-  if (c->product == SP_PRODUCT_DENSE) return true;
+  if (c->product == SP_PRODUCT_DENSE || c->product == SP_PRODUCT_TENSOR) return true;
   if (c->product != SP_PRODUCT_AUTO) return false;
   const double cells = static_cast<double>(c->hp.n_meas) * static_cast<double>(c->hp.n_sym);
   return cells > 0 && static_cast<double>(c->hp.nnz) > kDenseProductDensity * cells;
@@ -1750,7 +1752,7 @@ int sp_set_rng(sp_ctx* ctx, sp_rng rng) {
 
 int sp_set_product(sp_ctx* ctx, sp_product v) {
   if (!ctx) return fail(SP_ERR_INVALID_ARGUMENT, "null ctx");
-  if (v != SP_PRODUCT_AUTO && v != SP_PRODUCT_SPARSE && v != SP_PRODUCT_DENSE)
+  if (v != SP_PRODUCT_AUTO && v != SP_PRODUCT_SPARSE && v != SP_PRODUCT_DENSE && v != SP_PRODUCT_TENSOR)
     return fail(SP_ERR_INVALID_ARGUMENT, "unknown product variant");
   ctx->product = v;
   if (dense_product(ctx) && ctx->hp.dense_words.empty() && ctx->have_msym) {
@@ -2066,11 +2068,29 @@ int sp_sample_given_S(sp_ctx* ctx, const uint64_t* d_S, uint64_t n_sym_S, uint64
         ck(cudaStreamSynchronize(ctx->stream), "dense upload");
       }
       ctx->prod_ready = true;
+      ctx->tc_ready = false;
     } catch (const CudaError& e) {
       return fail(SP_ERR_CUDA, e.what());
     }
   }
   if (dense && !ctx->pp.dense) return fail(SP_ERR_NOT_LOADED, "dense M_sym words not built");
+  if (ctx->product == SP_PRODUCT_TENSOR) {
+    if (!ctx->tc_ready) {
+      try {
+        const uint64_t bytes = tc_a_bytes(ctx->pp.n_meas, ctx->pp.n_sym);
+        auto* at = static_cast<uint8_t*>(ctx->p_tc_a.ensure(bytes));
+        const int rp = launch_tc_prep(ctx->L, ctx->pp.dense, ctx->pp.ldm, ctx->pp.n_meas,
+                                      ctx->pp.n_sym, at);
+        if (int e = launched(ctx, rp, "tensor-core operand layout")) return e;
+        ctx->tc_ready = true;
+      } catch (const CudaError& e) {
+        return fail(SP_ERR_CUDA, e.what());
+      }
+    }
+    const int r = launch_tc_product(ctx->L, static_cast<const uint8_t*>(ctx->p_tc_a.p), ctx->pp.n_meas,
+                                    ctx->pp.n_sym, d_S, ldS, n_shots, d_out, ld);
+    return launched(ctx, r, "tensor-core product launch");
+  }
   int r = launch_product(ctx->pp, ctx->L, dense, d_S, ldS, n_shots, d_out, ld);
   return launched(ctx, r, "product launch");
 }

@@ -251,6 +251,14 @@ int launch_k5(const K5Plan& P, const LaunchCfg& L, uint64_t seed, uint64_t shot_
 // draw_assignments for the K5 streams (S must be zeroed, ones/coins filled).
 int launch_k5_draw(const K5Plan& P, const LaunchCfg& L, uint64_t seed, uint64_t shot_begin,
                    uint64_t n_shots, uint64_t* S, uint64_t ldS);
+// K6 — the dense explicit-S product on the tensor cores (k6_tcgen05.cu):
+// A = M_sym bytes in the core-matrix tile layout (tc_a_bytes, built once per
+// model from the dense words by launch_tc_prep), then the GEMM + parity.
+uint64_t tc_a_bytes(uint32_t n_meas, uint32_t n_sym);
+int launch_tc_prep(const LaunchCfg& L, const uint64_t* dense, uint64_t ldm, uint32_t n_meas,
+                   uint32_t n_sym, uint8_t* At);
+int launch_tc_product(const LaunchCfg& L, const uint8_t* At, uint32_t n_meas, uint32_t n_sym,
+                      const uint64_t* S, uint64_t ldS, uint64_t n_shots, uint64_t* out, uint64_t ld);
 // K3 encode (fmt 0 = '01', 1 = 'b8').
 // tile_shots == 0: measurement-major input; else tiled blocks of tile_shots.
 int launch_encode(const LaunchCfg& L, const uint64_t* m, uint64_t ld, uint64_t n_meas,

@@ -33,7 +33,7 @@ assert GROUP_DTYPE.itemsize == C.sizeof(N.sp_group)
 DIST_NAMES = {0: "constant", 1: "bernoulli", 2: "coin", 3: "depolarize1", 4: "depolarize2"}
 FORMATS = {"01": 0, "b8": 1}
 RNGS = {"philox": 0, "compat": 1}
-PRODUCTS = {"auto": 0, "sparse": 1, "dense": 2}
+PRODUCTS = {"auto": 0, "sparse": 1, "dense": 2, "tensor": 3}
 
 
 def _ptr(a) -> int:
