@@ -40,7 +40,42 @@ WORKLOADS = {
              "(BASELINE.json configs[2])", 10**8),
     "cfg4": ("cfg4: random Clifford n=1000, 100 layers, DEPOLARIZE1(1e-3) "
              "(BASELINE.json configs[3])", 10**6),
+    "cfg5": ("cfg5: raw GF(2) sampling, random M_sym m=10^4 x v=10^5 (density --dens), "
+             "Bernoulli(--p) faults, N=2^20 (BASELINE.json configs[4])", 1 << 20),
 }
+
+
+class Model:
+    """InitResult-shaped model (row_ptr, sym_idx, groups) built without the
+    repo's library, so the reference arm can use it too."""
+
+    def __init__(self, n_sym, row_ptr, sym_idx, groups):
+        self.n_qubits, self.n_sym = 0, n_sym
+        self.row_ptr, self.sym_idx, self.groups = row_ptr, sym_idx, groups
+
+    @property
+    def n_meas(self):
+        return len(self.row_ptr) - 1
+
+    @property
+    def nnz(self):
+        return int(self.row_ptr[-1])
+
+
+def cfg5_model(dens: float, p: float) -> Model:
+    """BASELINE configs[4]: random M_sym 10^4 x 10^5 at density `dens` (seed 7)
+    + 10^5 Bernoulli(p) fault symbols (circuits.random_msym_rows)."""
+    cm = circuits_module()
+    v = 10**5
+    row_ptr, sym_idx = cm.random_msym_rows(10**4, v, dens, 7)
+    gdt = np.dtype([("dist", np.uint8), ("reserved", np.uint8, 7), ("param", np.float64),
+                    ("first_symbol", np.uint32), ("arity", np.uint32)])
+    groups = np.zeros(v + 1, dtype=gdt)
+    groups["dist"][1:] = 1
+    groups["param"][1:] = p
+    groups["first_symbol"] = np.arange(v + 1, dtype=np.uint32)
+    groups["arity"] = 1
+    return Model(v + 1, row_ptr, sym_idx, groups)
 
 
 def circuits_module():
@@ -185,15 +220,14 @@ class ReferenceCPU:
     Sampling cost is linear in the shot count (sampler.cpp:52-57, 88-104), so
     a bounded sample of the workload's shots gives its rate."""
 
-    CHUNK = 16384
-
-    def __init__(self, text: str):
+    def __init__(self, text: str, model=None, chunk: int = 16384):
         import oracle
         if not oracle.have_ref():
             raise RuntimeError("oracle/_ref not built (make -C oracle where /root/reference "
                                "exists; the .so then travels with the repo)")
         t0 = time.perf_counter()
-        self.c = oracle.Ref().circuit(text)
+        self.CHUNK = chunk
+        self.c = oracle.Ref().model(model) if model is not None else oracle.Ref().circuit(text)
         self.init_s = time.perf_counter() - t0
         self.n_meas = self.c.n_meas
         self.threads = os.cpu_count() or 1
@@ -234,10 +268,13 @@ def run_reference(args):
     desc, shots_per_gpu = WORKLOADS[args.config]
     if args.shots:
         shots_per_gpu = args.shots
-    ref = ReferenceCPU(circuit_text(args.config))
+    if args.config == "cfg5":  # dense rows: a 1024-shot chunk already takes seconds at density 0.5
+        ref = ReferenceCPU("", model=cfg5_model(args.dens, args.p), chunk=1024 if args.dens > 0.1 else 16384)
+    else:
+        ref = ReferenceCPU(circuit_text(args.config))
     per_step = float(os.environ.get("SP_REF_STEP_SECONDS", "4"))
     shots_b = ref._sized(1, per_step, 41, ref.CHUNK * ref.threads)
-    shots_a = ref._sized(0, per_step / 2, 41, 4096)
+    shots_a = ref._sized(0, per_step / 2, 41, min(4096, ref.CHUNK))
     rates, secs, rates_a = [], [], []
     for i in range(args.warmup + args.steps):
         r, _, t = ref.figure_b(per_step, 42 + i, shots_b)
@@ -270,8 +307,11 @@ def run_reference(args):
 
 def bench_config(args, desc, shots_per_gpu):
     """The `config` object both arms print (identical for the same flags)."""
-    return {"workload": desc, "shots_per_gpu": shots_per_gpu, "records": args.records,
-            "seed_base": 1000}
+    c = {"workload": desc, "shots_per_gpu": shots_per_gpu, "records": args.records,
+         "seed_base": 1000}
+    if args.config == "cfg5":
+        c.update({"density": args.dens, "p": args.p})
+    return c
 
 
 def run_ours(args):
@@ -292,9 +332,14 @@ def run_ours(args):
     desc, shots = WORKLOADS[args.config]
     if args.shots:
         shots = args.shots
-    text = circuit_text(args.config)
+    text = circuit_text(args.config) if args.config != "cfg5" else ""
     t0 = time.perf_counter()
-    init = run_initialization(text)
+    if args.config == "cfg5":
+        from paper_2311_03906_b200.sampler import InitResult
+        mdl = cfg5_model(args.dens, args.p)
+        init = InitResult(0, mdl.n_sym, mdl.row_ptr, mdl.sym_idx, mdl.groups)
+    else:
+        init = run_initialization(text)
     if args.records == "detectors":  # detector layer: D_sym = A . M_sym
         from paper_2311_03906_b200 import circuits as CI
         dd = {"cfg2": (5, 5), "cfg3": (15, 15)}.get(args.config)
@@ -427,8 +472,14 @@ def run_ours(args):
     if rank == 0:
         peak, peak_src = measured_peaks()
         nbytes, ops = algorithmic(init, shots)
-        achieved = nbytes / (k_ms / 1e3) / 1e9
         t_hbm, t_int = nbytes / (peak * 1e9), ops / R_INT
+        fo = smp.plan_info()["fused_ok"]
+        kernel = {1: "k1_fused", 2: "k5_columns"}.get(fo, "d_segments + k2 product")
+        int_bound = t_int > t_hbm
+        # achieved = algorithmic bytes (HBM-bound) or LOP3 ops (INT-bound) per
+        # second of the kernel's CUDA-event time, against the measured peak
+        achieved = (ops / (k_ms / 1e3) / 1e12) if int_bound else nbytes / (k_ms / 1e3) / 1e9
+        r_peak, r_unit = (R_INT / 1e12, "Tops/s (LOP3)") if int_bound else (peak, "GB/s")
         traffic = None
         tp = ROOT / "profiles" / "ncu_traffic.json"
         if tp.exists():
@@ -459,13 +510,14 @@ def run_ours(args):
                 "init_seconds": round(init_s, 4),
             },
             "roofline": {
-                "bound": "hbm" if t_hbm >= t_int else "int", "achieved": achieved,
-                "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
-                "kernel": "k1_fused", "kernel_ms": k_ms, "alg_bytes": nbytes,
+                "bound": "int" if int_bound else "hbm", "achieved": achieved,
+                "peak": r_peak, "unit": r_unit, "frac": achieved / r_peak, "traffic": traffic,
+                "kernel": kernel, "kernel_ms": k_ms, "alg_bytes": nbytes,
                 "alg_int_ops": ops, "t_hbm_ms": t_hbm * 1e3, "t_int_ms": t_int * 1e3,
                 "r_int": R_INT, "frac_of_roofline_time": max(t_hbm, t_int) * 1e3 / k_ms,
                 "frac_vs_8TBs": (nbytes / (k_ms / 1e3)) / 8.0e12,
-                "peak_source": peak_src,
+                "peak_source": peak_src if not int_bound else
+                "measured LOP3 rate (tools/microbench.cu, profiles/microbench_r01.jsonl)",
             },
             "clocks": clk.summary(),
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
@@ -478,9 +530,10 @@ def run_ours(args):
             "wall_s_timed": wall,
         }
         if world == 1 and not args.no_cpu_baseline and args.records == "measurements":
-            ref = ReferenceCPU(text)
+            ref = (ReferenceCPU("", model=init, chunk=1024 if args.dens > 0.1 else 16384)
+                   if args.config == "cfg5" else ReferenceCPU(text))
             rb, sb, tb = ref.figure_b(10.0, 42)
-            ra, sa, _ = ref.figure_a(5.0, 43)
+            ra, sa, _ = ref.figure_a(5.0, 43) if args.config != "cfg5" else (None, 0, 0)
             line["cpu_baseline"] = {"value": rb, "unit": UNIT, "cores": ref.threads,
                                     "kind": "reference", "cpu_model": cpu_model(),
                                     "sample": ref.describe(sb, sa), "seconds": round(tb, 3),
@@ -527,6 +580,8 @@ def main():
     ap.add_argument("--records", default="measurements", choices=["measurements", "detectors"],
                     help="sample measurement records (the metric) or, for the surface-code "
                          "workloads, detector + observable records (D_sym = A . M_sym)")
+    ap.add_argument("--dens", type=float, default=0.5, help="cfg5: M_sym density")
+    ap.add_argument("--p", type=float, default=1e-3, help="cfg5: fault probability")
     ap.add_argument("--counts", default="detectors", choices=["detectors", "measurements"],
                     help="counts each step reduces: per-detector (surface-code workloads, "
                          "BASELINE configs[2]) or per-measurement")

@@ -123,19 +123,35 @@ class Ref:
         L.ref_sample_encode.argtypes = [_p, _u64, _u64, _i, C.c_uint, _p, _u64]
         L.ref_encode.restype = C.c_int64
         L.ref_encode.argtypes = [_u64, _u64, _p, _u64, _i, _p, _u64]
+        L.ref_init_model.restype = _i
+        L.ref_init_model.argtypes = [_u64, _p, _p, _u64, _p, _p, _p, C.POINTER(_p)]
         L.ref_time.restype = _d
         L.ref_time.argtypes = [_p, _u64, _u64, C.c_uint, _u64, _i]
         self.L = L
 
     class Circuit:
-        def __init__(self, ref: "Ref", text: str):
+        def __init__(self, ref: "Ref", text: str | None, model=None):
             self.ref = ref
             h = _p()
-            err = C.create_string_buffer(512)
-            rc = ref.L.ref_init(text.encode(), C.byref(h), err, 512)
-            if rc != 0:
-                kind = {1: ValueError, 2: RuntimeError}[rc]
-                raise kind(err.value.decode())
+            if model is not None:  # explicit expressions + group table (cfg5)
+                rp = np.ascontiguousarray(model.row_ptr, dtype=np.uint64)
+                si = np.ascontiguousarray(model.sym_idx, dtype=np.uint32)
+                if si.size == 0:
+                    si = np.zeros(1, dtype=np.uint32)
+                g = model.groups
+                dist = np.ascontiguousarray(g["dist"], dtype=np.uint8)
+                param = np.ascontiguousarray(g["param"], dtype=np.float64)
+                arity = np.ascontiguousarray(g["arity"], dtype=np.uint32)
+                rc = ref.L.ref_init_model(len(rp) - 1, _ptr(rp), _ptr(si), len(dist), _ptr(dist),
+                                          _ptr(param), _ptr(arity), C.byref(h))
+                if rc != 0:
+                    raise ValueError("ref_init_model failed")
+            else:
+                err = C.create_string_buffer(512)
+                rc = ref.L.ref_init(text.encode(), C.byref(h), err, 512)
+                if rc != 0:
+                    kind = {1: ValueError, 2: RuntimeError}[rc]
+                    raise kind(err.value.decode())
             self.h = h
             d = [_u64() for _ in range(5)]
             ref.L.ref_dims(h, *[C.byref(x) for x in d])
@@ -179,6 +195,10 @@ class Ref:
 
     def circuit(self, text: str) -> "Ref.Circuit":
         return Ref.Circuit(self, text)
+
+    def model(self, init) -> "Ref.Circuit":
+        """A reference InitResult from an InitResult-like model (no circuit)."""
+        return Ref.Circuit(self, None, model=init)
 
     def sample_given(self, row_ptr, sym_idx, S: np.ndarray, n_shots: int, threads: int = 1):
         rp = np.ascontiguousarray(row_ptr, dtype=np.uint64)

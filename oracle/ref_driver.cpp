@@ -103,6 +103,29 @@ int ref_init(const char* text, ref_ctx** out, char* err, size_t errlen) {
   }
 }
 
+// An InitResult from explicit expressions + a group table (cfg5's random
+// M_sym has no circuit): the reference's own SymbolRegistry and
+// MeasurementExpression, so draw_assignments / sample run unchanged on it.
+int ref_init_model(uint64_t n_meas, const uint64_t* row_ptr, const uint32_t* sym_idx,
+                   uint64_t n_groups, const uint8_t* dist, const double* param,
+                   const uint32_t* arity, ref_ctx** out) {
+  try {
+    auto ctx = new ref_ctx;
+    for (uint64_t g = 1; g < n_groups; ++g) {
+      const auto d = static_cast<GroupDistribution>(dist[g]);
+      if (d == GroupDistribution::kFairCoin) ctx->init.registry.add_measurement_symbol(0);
+      else ctx->init.registry.add_fault_group(d, param[g], arity[g], 0);
+    }
+    ctx->init.expressions.resize(n_meas);
+    for (uint64_t k = 0; k < n_meas; ++k)
+      ctx->init.expressions[k].symbols.assign(sym_idx + row_ptr[k], sym_idx + row_ptr[k + 1]);
+    *out = ctx;
+    return 0;
+  } catch (const std::exception&) {
+    return 1;
+  }
+}
+
 void ref_free(ref_ctx* c) { delete c; }
 
 void ref_dims(const ref_ctx* c, uint64_t* n_meas, uint64_t* n_sym, uint64_t* n_groups,

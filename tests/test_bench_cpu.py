@@ -58,4 +58,4 @@ def test_reference_arm_never_loads_repo_library(tmp_path):
     line = json.loads(r.stdout.strip().splitlines()[-1])
     assert line["impl"] == "reference" and line["cpu_baseline"]["kind"] == "reference"
     assert line["config"] == bench.bench_config(
-        SimpleNamespace(records="measurements"), bench.WORKLOADS["cfg1"][0], 10**6)
+        SimpleNamespace(records="measurements", config="cfg1"), bench.WORKLOADS["cfg1"][0], 10**6)
