@@ -1365,14 +1365,16 @@ void build_plan(sp_ctx* c) {
     const uint64_t cal_shots = cal_tiles * T_;
     const uint64_t ldw = cal_shots / 64;
     uint64_t* buf = nullptr;
+    uint64_t* dcnt = nullptr;  // registered detectors: tune with their counting on
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     ck(cudaMalloc(reinterpret_cast<void**>(&buf), n_meas * ldw * 8), "cudaMalloc (autotune)");
+    if (d.n_det) ck(cudaMalloc(reinterpret_cast<void**>(&dcnt), d.n_det * 8ull), "cudaMalloc (autotune)");
     ck(cudaEventCreate(&e0), "cudaEventCreate");
     ck(cudaEventCreate(&e1), "cudaEventCreate");
     auto launch_once = [&](uint64_t seed) {
       ck(cudaEventRecord(e0, s), "cudaEventRecord");
       // tiled layout: contiguous stores, so the kernel's own balance decides
-      if (launch_fused_sample(d, c->L, seed, 0, cal_shots, buf, ldw, nullptr, true) < 0)
+      if (launch_fused_sample(d, c->L, seed, 0, cal_shots, buf, ldw, nullptr, true, dcnt) < 0)
         throw CudaError("autotune launch failed");
       ck(cudaEventRecord(e1, s), "cudaEventRecord");
       ck(cudaEventSynchronize(e1), "cudaEventSynchronize");
@@ -1458,11 +1460,13 @@ void build_plan(sp_ctx* c) {
       }
     } catch (...) {
       cudaFree(buf);
+      if (dcnt) cudaFree(dcnt);
       cudaEventDestroy(e0);
       cudaEventDestroy(e1);
       throw;
     }
     cudaFree(buf);
+    if (dcnt) cudaFree(dcnt);
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     if (d.timers) d.timers = c->b_timers.upload(std::vector<long long>(8, 0), s);
