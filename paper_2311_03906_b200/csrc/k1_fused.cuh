@@ -54,8 +54,9 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
   p += align16(4ull * P.n_meas * cnt_lanes);
   // Detector flip counts (sp_sample_ex): one u32 per detector.
   const bool with_dets = det_counts != nullptr && P.n_det > 0;
-  uint32_t* det_cnt = reinterpret_cast<uint32_t*>(p);  // [n_det][cnt_lanes]
-  p += align16(4ull * P.n_det * cnt_lanes);
+  uint32_t* det_cnt = reinterpret_cast<uint32_t*>(p);  // [n_det + 1 spare][cnt_lanes]
+  p += align16(4ull * (P.n_det + (P.n_det ? 1 : 0)) * cnt_lanes);
+  const uint32_t det_s = static_cast<uint32_t>(__cvta_generic_to_shared(det_cnt));
   uint32_t* segctr = reinterpret_cast<uint32_t*>(p);  // per-buffer segment dispensers
   p += 16;
   // Tile hand-off: full[b] completes when every generator thread finished
@@ -144,7 +145,7 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
     if (with_counts)
       for (uint32_t i = threadIdx.x; i < P.n_meas * cnt_lanes; i += blockDim.x) cnt[i] = 0;
     if (with_dets)
-      for (uint32_t i = threadIdx.x; i < P.n_det * cnt_lanes; i += blockDim.x) det_cnt[i] = 0;
+      for (uint32_t i = threadIdx.x; i < (P.n_det + 1) * cnt_lanes; i += blockDim.x) det_cnt[i] = 0;
     if (threadIdx.x < kMaxBuf) {
       segctr[threadIdx.x] = 0;
       mbar_init(mbar_full + threadIdx.x, P.gen_warps * 32);
@@ -423,26 +424,27 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
               pc = __reduce_add_sync(kFull, pc);
               if (lane == 0) atomicAdd(&cnt[k], pc);
             }
-          } else {
-            if (pc) atomicAdd(&cnt[k], pc);
+          } else {  // branch-free: one shared add per row item
+            asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(cnt_s + (k << 2)), "r"(pc) : "memory");
           }
         };
-        // detector {k, parent(k)} (or {k} for a root row): the row's D value
+        // detector {k, parent(k)} (or {k} for a root row): the row's D value;
+        // rows without a detector add into the spare slot n_det (branch-free)
         auto count_det = [&](auto wp_tag, uint32_t e, uint4 d) {
           constexpr bool kWarpPath = decltype(wp_tag)::value;  // the warp holds one row
-          const uint32_t id = (e >> 16) & 0x7FFFu;
-          if (id) {
-            uint32_t pc = __popc(d.x) + __popc(d.y) + __popc(d.z) + __popc(d.w);
-            if constexpr (kWarpPath) {
-              if (cnt_lanes == 32) {  // per-lane partials
-                atomicAdd(&det_cnt[(id - 1) * 32 + lane], pc);
-              } else {
-                pc = __reduce_add_sync(kFull, pc);
-                if (lane == 0 && pc) atomicAdd(&det_cnt[id - 1], pc);
-              }
+          const uint32_t slot = min(((e >> 16) & 0x7FFFu) - 1u, P.n_det);
+          uint32_t pc = __popc(d.x) + __popc(d.y) + __popc(d.z) + __popc(d.w);
+          if constexpr (kWarpPath) {
+            if (cnt_lanes == 32) {  // per-lane partials
+              asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(det_s + ((slot * 32 + lane) << 2)),
+                           "r"(pc)
+                           : "memory");
             } else {
-              if (pc) atomicAdd(&det_cnt[id - 1], pc);
+              pc = __reduce_add_sync(kFull, pc);
+              if (lane == 0) atomicAdd(&det_cnt[slot], pc);
             }
+          } else {
+            asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(det_s + (slot << 2)), "r"(pc) : "memory");
           }
         };
         // measurement-major records without TMA: each finished 16-byte item
@@ -467,14 +469,15 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
           }
         };
         // (counting modes are compile-time tags: no per-row flag checks)
-        auto rebuild = [&](auto wp_tag, auto cnt_tag, auto det_tag) {
+        auto rebuild = [&](auto wp_tag, auto cnt_tag, auto det_tag, auto dir_tag) {
           constexpr bool kCnt = decltype(cnt_tag)::value, kDet = decltype(det_tag)::value;
+          constexpr bool direct = decltype(dir_tag)::value;
           if (P.flat_rows) {  // no parents: the tile already holds the records
             if (kCnt || direct)
               for (uint32_t j = ct; j < (P.n_meas << tw4_log2); j += nct) {
                 const uint4 v = t4[j];
                 if constexpr (kCnt) count_item(wp_tag, j >> tw4_log2, v);
-                if (direct) store_item(j >> tw4_log2, j & (tw4 - 1), v);
+                if constexpr (direct) store_item(j >> tw4_log2, j & (tw4 - 1), v);
               }
             return;
           }
@@ -500,31 +503,39 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
                 t4[(k << tw4_log2) + q] = prev;
                 if constexpr (kCnt) count_item(wp_tag, k, prev);
                 if constexpr (kDet) count_det(wp_tag, e, c);
-                if (direct) store_item(k, q, prev);
+                if constexpr (direct) store_item(k, q, prev);
               };
-              for (; x < xe; x += 4) {
+              for (; x + 4 <= xe; x += 4) {  // whole groups: no per-row checks
                 const uint32_t e0 = PROWS[x], e1 = PROWS[x + 1], e2 = PROWS[x + 2], e3 = PROWS[x + 3];
                 const uint4 c0 = t4[((e0 & 0xFFFFu) << tw4_log2) + q];
                 const uint4 c1 = t4[((e1 & 0xFFFFu) << tw4_log2) + q];
                 const uint4 c2 = t4[((e2 & 0xFFFFu) << tw4_log2) + q];
                 const uint4 c3 = t4[((e3 & 0xFFFFu) << tw4_log2) + q];
                 row(e0, c0);
-                if (x + 1 < xe) row(e1, c1);
-                if (x + 2 < xe) row(e2, c2);
-                if (x + 3 < xe) row(e3, c3);
+                row(e1, c1);
+                row(e2, c2);
+                row(e3, c3);
+              }
+              for (; x < xe; ++x) {
+                const uint32_t e0 = PROWS[x];
+                row(e0, t4[((e0 & 0xFFFFu) << tw4_log2) + q]);
               }
             }
             if (rd + 1 < P.n_rounds) named_sync(kBarDrain, nct);
           }
         };
-        auto rebuild_wp = [&](auto wp_tag) {
+        auto rebuild_dir = [&](auto wp_tag, auto dir_tag) {
           if (with_counts) {
-            if (with_dets) rebuild(wp_tag, std::true_type{}, std::true_type{});
-            else rebuild(wp_tag, std::true_type{}, std::false_type{});
+            if (with_dets) rebuild(wp_tag, std::true_type{}, std::true_type{}, dir_tag);
+            else rebuild(wp_tag, std::true_type{}, std::false_type{}, dir_tag);
           } else {
-            if (with_dets) rebuild(wp_tag, std::false_type{}, std::true_type{});
-            else rebuild(wp_tag, std::false_type{}, std::false_type{});
+            if (with_dets) rebuild(wp_tag, std::false_type{}, std::true_type{}, dir_tag);
+            else rebuild(wp_tag, std::false_type{}, std::false_type{}, dir_tag);
           }
+        };
+        auto rebuild_wp = [&](auto wp_tag) {
+          if (direct) rebuild_dir(wp_tag, std::true_type{});
+          else rebuild_dir(wp_tag, std::false_type{});
         };
         if (tw4 >= 32) rebuild_wp(std::true_type{});
         else rebuild_wp(std::false_type{});
@@ -668,29 +679,30 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
               const uint32_t k = e & 0xFFFFu;
               const uint4 v = xor4(c, prev);
               if constexpr (kDetL) {  // detector {k, parent(k)} or {k}: the row's D value
-                const uint32_t id = (e >> 16) & 0x7FFFu;
-                if (id) {
-                  uint4 dv = c;
-                  if (!decltype(fast_tag)::value) {  // a partial tile: valid shots only
-                    if (q >= vq) dv = make_uint4(0, 0, 0, 0);
-                    else if (q == vq - 1 && rem) {
-                      dv.x &= rem >= 32 ? kFull : (1u << rem) - 1;
-                      dv.y &= rem >= 64 ? kFull : rem > 32 ? (1u << (rem - 32)) - 1 : 0u;
-                      dv.z &= rem >= 96 ? kFull : rem > 64 ? (1u << (rem - 64)) - 1 : 0u;
-                      dv.w &= rem > 96 ? (1u << (rem - 96)) - 1 : 0u;
-                    }
+                // (rows without a detector add into the spare slot n_det)
+                const uint32_t slot = min(((e >> 16) & 0x7FFFu) - 1u, P.n_det);
+                uint4 dv = c;
+                if (!decltype(fast_tag)::value) {  // a partial tile: valid shots only
+                  if (q >= vq) dv = make_uint4(0, 0, 0, 0);
+                  else if (q == vq - 1 && rem) {
+                    dv.x &= rem >= 32 ? kFull : (1u << rem) - 1;
+                    dv.y &= rem >= 64 ? kFull : rem > 32 ? (1u << (rem - 32)) - 1 : 0u;
+                    dv.z &= rem >= 96 ? kFull : rem > 64 ? (1u << (rem - 64)) - 1 : 0u;
+                    dv.w &= rem > 96 ? (1u << (rem - 96)) - 1 : 0u;
                   }
-                  uint32_t pc = __popc(dv.x) + __popc(dv.y) + __popc(dv.z) + __popc(dv.w);
-                  if constexpr (decltype(wp_tag)::value) {
-                    if (cnt_lanes == 32) {  // per-lane partials
-                      atomicAdd(&det_cnt[(id - 1) * 32 + lane], pc);
-                    } else {
-                      pc = __reduce_add_sync(kFull, pc);
-                      if (lane == 0 && pc) atomicAdd(&det_cnt[id - 1], pc);
-                    }
-                  } else if (pc) {
-                    atomicAdd(&det_cnt[id - 1], pc);
+                }
+                uint32_t pc = __popc(dv.x) + __popc(dv.y) + __popc(dv.z) + __popc(dv.w);
+                if constexpr (decltype(wp_tag)::value) {
+                  if (cnt_lanes == 32) {  // per-lane partials
+                    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(det_s + ((slot * 32 + lane) << 2)),
+                                 "r"(pc)
+                                 : "memory");
+                  } else {
+                    pc = __reduce_add_sync(kFull, pc);
+                    if (lane == 0) atomicAdd(&det_cnt[slot], pc);
                   }
+                } else {
+                  asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(det_s + (slot << 2)), "r"(pc) : "memory");
                 }
               }
               // Rows with light children keep their final value for a later

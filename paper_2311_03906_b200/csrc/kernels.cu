@@ -565,7 +565,7 @@ size_t fused_smem_bytes(const DevPlan& P, uint32_t t_log2, bool staged, bool row
   const size_t tw = size_t{1} << (t_log2 - 5);
   size_t b = n_buf * (static_cast<size_t>(P.n_meas) * tw + spare_words(tw)) * 4;  // tiles + spare
   b += align16(4ull * P.n_meas * count_lanes(t_log2, n_buf)) + 16;  // counts, dispensers
-  b += align16(4ull * P.n_det * count_lanes(t_log2, n_buf));           // detector counts
+  b += align16(4ull * (P.n_det + (P.n_det ? 1 : 0)) * count_lanes(t_log2, n_buf));  // detector counts + spare
   b += 16 * kMaxBufHost;                                               // tile mbarriers
   if (P.coins_staged)
     b += align16(4ull * (P.n_dense_live + 2)) + align16(4ull * P.n_dense_live) +

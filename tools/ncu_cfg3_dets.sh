@@ -10,6 +10,6 @@ out=torch.empty(s.tiled_words(n),dtype=torch.int64,device="cuda"); dc=torch.zero
 for i in range(2): s.sample_counted(n, 10+i, out=out, det_counts=dc, tiled=True)
 torch.cuda.synchronize(); print("ok", s.plan_info())
 PY
-SP_AUTOTUNE=0 SP_GEN_WARPS=11 ncu --set full --import-source on --clock-control none -k regex:k1_fused -s 1 -c 1 -o $o/k1 python $o/prof.py > $o/ncu.log 2>&1
+SP_AUTOTUNE=0 SP_GEN_WARPS=${GW:-10} SP_PAD_PRED=${PP:-0} ncu --set full --import-source on --clock-control none -k regex:k1_fused -s 1 -c 1 -o $o/k1 python $o/prof.py > $o/ncu.log 2>&1
 python tools/ncu_summarize.py $o/k1.ncu-rep > $o/summary.txt 2>&1
 python tools/ncu_regions.py $o/k1.ncu-rep > $o/regions.txt 2>&1
