@@ -118,7 +118,7 @@ struct sp_ctx {
   DevPlan dp;
   // plan buffers
   DBuf b_row_ptr, b_sym_idx, b_col_ptr, b_col_rows, b_dense, b_dense_gm, b_first, b_arity, b_dist, b_param,
-      b_row_const_compat, b_ones, b_dense_sym, b_coin_ptr, b_coin_rows, b_cls, b_cls_groups, b_thin_src, b_mech_pat, b_len_bnd, b_g_masks,
+      b_row_const_compat, b_ones, b_dense_sym, b_coin_ptr, b_coin_rows, b_cls, b_cls_groups, b_thin_src, b_mech_pat, b_len_bnd, b_seg_desc, b_g_masks,
       b_desc, b_colrow, b_live_groups, b_path_rows, b_path_ptr, b_path_par, b_round_ptr, b_plist, b_keep_rows, b_timers,
       b_gdet_ptr, b_gdet_rows, b_gdet_id;
   uint64_t dnnz = 0;  // nnz of D (chain transform), for reports
@@ -1037,6 +1037,35 @@ void build_plan(sp_ctx* c) {
     if (n_chains >= (1ull << 32)) throw std::invalid_argument("too many sampling chains");
     d.n_seg_null = static_cast<uint32_t>(n_chains) - d.n_seg_all;
     d.cls = c->b_cls.upload(cls_info, s);
+    // the live slices resolved on the host (the kernel's dispenser reads
+    // them instead of searching the classes and length runs)
+    std::vector<SegDesc> sd;
+    const uint64_t T_ = uint64_t{1} << d.t_log2;
+    for (size_t cc = 0; cc < live_cls.size(); ++cc) {
+      const ClassInfo& ci = cls_info[cc];
+      for (uint32_t i = 0; i < ci.n_seg; ++i) {
+        SegDesc e{};
+        const uint64_t first = static_cast<uint64_t>(i) * ci.L;
+        e.g0 = static_cast<uint32_t>(first / T_);
+        e.s0 = static_cast<uint32_t>(first % T_);
+        e.len = static_cast<uint32_t>(std::min(first + ci.L, ci.trials) - first);
+        e.goff = ci.goff;
+        e.pbase = ci.pbase;
+        e.clg = ci.clg;
+        uint32_t lp = ci.lp;
+        if (ci.bnd != 0xFFFFFFFFu) {  // the length run holding g0, and where the next starts
+          uint32_t b = ci.bnd;
+          lp = len_bnd[b] & 31u;
+          while ((len_bnd[b + 1] >> 5) <= e.g0) lp = len_bnd[++b] & 31u;
+          e.bnd = b + 1;
+          e.nbp = len_bnd[b + 1] >> 5;
+        }
+        e.meta = ci.npat | (ci.dist << 8) | (lp << 16);
+        sd.push_back(e);
+      }
+    }
+    if (sd.empty()) sd.push_back(SegDesc{});
+    d.seg_desc = c->b_seg_desc.upload(sd, s);
   };
 
   std::vector<uint32_t> g_first(G), g_arity(G);
@@ -1088,6 +1117,7 @@ void build_plan(sp_ctx* c) {
   d.thin_src = c->b_thin_src.upload(thin_src, s);
   if (len_bnd.empty()) len_bnd.push_back(0xFFFFFFFFu);
   d.len_bnd = c->b_len_bnd.upload(len_bnd, s);
+  d.n_len_bnd = static_cast<uint32_t>(len_bnd.size());
   if (mech_pat.empty()) mech_pat.push_back(0);
   d.mech_pat = c->b_mech_pat.upload(mech_pat, s);
   d.g_masks = c->b_g_masks.upload(g_masks, s);

@@ -124,6 +124,23 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
       dst[i] = src[i];
     CLS = s_cls;
   }
+  // Slice descriptors and length runs (set at launch when they fit): the
+  // slice dispenser then resolves a slice with three shared loads.
+  const SegDesc* SEGD = P.seg_desc;
+  const uint32_t* LENB = P.len_bnd;
+  if (P.seg_staged) {
+    SegDesc* s_seg = reinterpret_cast<SegDesc*>(p);
+    p += align16(sizeof(SegDesc) * P.n_seg_live);
+    uint32_t* s_lenb = reinterpret_cast<uint32_t*>(p);
+    p += align16(4ull * P.n_len_bnd);
+    const uint4* src = reinterpret_cast<const uint4*>(P.seg_desc);
+    uint4* dst = reinterpret_cast<uint4*>(s_seg);
+    for (uint32_t i = threadIdx.x; i < P.n_seg_live * (sizeof(SegDesc) / 16); i += blockDim.x)
+      dst[i] = src[i];
+    for (uint32_t i = threadIdx.x; i < P.n_len_bnd; i += blockDim.x) s_lenb[i] = P.len_bnd[i];
+    SEGD = s_seg;
+    LENB = s_lenb;
+  }
   if (P.coins_staged) {  // coin columns and symbols: small, read every tile
     uint32_t* s_cptr = reinterpret_cast<uint32_t*>(p);
     p += align16(4ull * (P.n_dense_live + 2));
@@ -273,7 +290,7 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
 #pragma unroll
             for (int k = 0; k < kSlots; ++k)
               if ((f.v >> k) & 1u) gm = max(gm, f.g[k]);
-            segment_runs_to(sg, P.len_bnd, __reduce_max_sync(kFull, gm));
+            segment_runs_to(sg, LENB, __reduce_max_sync(kFull, gm));
           }
           const uint32_t lpu = sg.lp == 0 ? static_cast<uint32_t>(kLp) : sg.lp;
           if constexpr (kPre > 0 && kPre < kSlots) load_lists(bern_tag, f, kPre, kSlots);
@@ -347,8 +364,24 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
         if (lane == 0) seg = atomicAdd(&segctr[b], 1u);
         seg = __shfl_sync(kFull, seg, 0);
         if (seg >= P.n_seg_live || (P.debug_mode & 2u)) return false;
-        segment_init(sn, CLS, P.n_cls_live, seg, P.t_log2);
-        segment_runs(sn, P.len_bnd);
+        if (P.seg_staged) {
+          const SegDesc& e = SEGD[seg];
+          sn.g0 = e.g0;
+          sn.s0 = e.s0;
+          sn.len = e.len;
+          sn.seg = seg;
+          sn.goff = e.goff;
+          sn.pbase = e.pbase;
+          sn.npat = e.meta & 0xFFu;
+          sn.dist = (e.meta >> 8) & 0xFFu;
+          sn.lp = e.meta >> 16;
+          sn.bnd = e.bnd;
+          sn.nbp = e.nbp;
+          sn.clg = e.clg;
+        } else {
+          segment_init(sn, CLS, P.n_cls_live, seg, P.t_log2);
+          segment_runs(sn, LENB);
+        }
         return true;
       };
       uint4 r[kBlocks];
@@ -828,6 +861,9 @@ int launch_k1(const DevPlan& P, const LaunchCfg& L, const RoundKeys& K, uint64_t
   const size_t cls_bytes = align16(sizeof(ClassInfo) * P.n_cls_live);
   Q.cls_staged = !kStaged && smem + cls_bytes <= L.smem_optin;
   if (Q.cls_staged) smem += cls_bytes;
+  const size_t seg_bytes = align16(sizeof(SegDesc) * P.n_seg_live) + align16(4ull * P.n_len_bnd);
+  Q.seg_staged = P.seg_desc != nullptr && P.n_seg_live > 0 && smem + seg_bytes <= L.smem_optin;
+  if (Q.seg_staged) smem += seg_bytes;
   int grid = 0;
   const int threads = static_cast<int>(P.cta_threads);
   if (persistent_grid(kern, L, smem, n_tiles, P.cta_per_sm, &grid, threads)) return -1;

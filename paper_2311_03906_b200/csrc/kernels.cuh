@@ -36,6 +36,18 @@ struct ClassInfo {
   uint32_t bnd = 0xFFFFFFFFu;  // none: every list runs lp entries
 };
 
+// One sampling slice of a tile, resolved on the host (the fused kernel's
+// slice dispenser reads it from shared memory instead of searching the class
+// table): first trial (class position g0, shot s0), length, the class's
+// fields, and the flip-list length run holding g0 (lp, next run bnd/nbp).
+struct SegDesc {
+  uint32_t g0 = 0, s0 = 0, len = 0, goff = 0;
+  uint32_t pbase = 0, meta = 0;  // meta = npat | dist << 8 | lp << 16
+  uint32_t bnd = 0xFFFFFFFFu, nbp = 0xFFFFFFFFu;
+  float clg = 0.f;
+  uint32_t pad[3] = {0, 0, 0};
+};
+
 // Everything a kernel needs about the loaded model, all device pointers.
 // Built once per model by abi.cpp (build_plan).
 struct DevPlan {
@@ -124,6 +136,9 @@ struct DevPlan {
   uint32_t entry_bytes = 4;  // 1: u8 row indices, 2: u16 / 4: u32 tile byte offsets
   const uint4* plist = nullptr;
   const uint32_t* len_bnd = nullptr;  // length runs of the sorted Bernoulli classes (ClassInfo::bnd)
+  uint32_t n_len_bnd = 0;
+  const SegDesc* seg_desc = nullptr;  // [n_seg_live]
+  uint32_t seg_staged = 0;            // seg_desc and len_bnd copied to shared memory (set at launch)
   // Row reconstruction out[k] = d[k] ^ out[parent[k]] along the paths of a
   // heavy-path decomposition of the parent forest: path p lists rows
   // path_rows[path_ptr[p] .. path_ptr[p+1]) top-down; path_par[p] is the head's
