@@ -1196,6 +1196,7 @@ void build_plan(sp_ctx* c) {
   d.debug_mode = static_cast<uint32_t>(env_long("SP_DEBUG_MODE", 0));
   d.wait_ns = static_cast<uint32_t>(std::max<long>(32, env_long("SP_WAIT_NS", 256)));
   d.bulk_store = static_cast<uint32_t>(env_long("SP_BULK", 1));
+  d.seg_stage_ok = static_cast<uint32_t>(env_long("SP_SEG_STAGE", 1));
   if (env_long("SP_PHASE_TIMERS", 0)) {
     std::vector<long long> z(8, 0);
     d.timers = c->b_timers.upload(z, s);

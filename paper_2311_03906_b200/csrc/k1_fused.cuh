@@ -103,6 +103,7 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
     uint4* s_desc = reinterpret_cast<uint4*>(p);
     p += 16ull * P.n_desc_live;
     uint16_t* s_col = reinterpret_cast<uint16_t*>(p);
+    p += align16(2ull * P.n_colrow);  // (what is staged after the tables starts here)
     {
       const uint32_t* src = reinterpret_cast<const uint32_t*>(P.cls);
       uint32_t* dst = reinterpret_cast<uint32_t*>(s_cls);
@@ -862,7 +863,8 @@ int launch_k1(const DevPlan& P, const LaunchCfg& L, const RoundKeys& K, uint64_t
   Q.cls_staged = !kStaged && smem + cls_bytes <= L.smem_optin;
   if (Q.cls_staged) smem += cls_bytes;
   const size_t seg_bytes = align16(sizeof(SegDesc) * P.n_seg_live) + align16(4ull * P.n_len_bnd);
-  Q.seg_staged = P.seg_desc != nullptr && P.n_seg_live > 0 && smem + seg_bytes <= L.smem_optin;
+  Q.seg_staged = P.seg_stage_ok && P.seg_desc != nullptr && P.n_seg_live > 0 &&
+                 smem + seg_bytes <= L.smem_optin;
   if (Q.seg_staged) smem += seg_bytes;
   int grid = 0;
   const int threads = static_cast<int>(P.cta_threads);

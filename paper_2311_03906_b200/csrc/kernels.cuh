@@ -139,6 +139,7 @@ struct DevPlan {
   uint32_t n_len_bnd = 0;
   const SegDesc* seg_desc = nullptr;  // [n_seg_live]
   uint32_t seg_staged = 0;            // seg_desc and len_bnd copied to shared memory (set at launch)
+  uint32_t seg_stage_ok = 1;          // SP_SEG_STAGE=0 keeps them in global memory
   // Row reconstruction out[k] = d[k] ^ out[parent[k]] along the paths of a
   // heavy-path decomposition of the parent forest: path p lists rows
   // path_rows[path_ptr[p] .. path_ptr[p+1]) top-down; path_par[p] is the head's
