@@ -118,7 +118,7 @@ struct sp_ctx {
   DevPlan dp;
   // plan buffers
   DBuf b_row_ptr, b_sym_idx, b_col_ptr, b_col_rows, b_dense, b_dense_gm, b_first, b_arity, b_dist, b_param,
-      b_row_const_compat, b_ones, b_dense_sym, b_coin_ptr, b_coin_rows, b_cls, b_cls_groups, b_thin_src, b_mech_pat, b_len_bnd, b_seg_desc, b_g_masks,
+      b_row_const_compat, b_ones, b_dense_sym, b_coin_ptr, b_coin_rows, b_cls, b_cls_groups, b_thin_src, b_mech_pat, b_len_bnd, b_seg_desc, b_zero, b_g_masks,
       b_desc, b_colrow, b_live_groups, b_path_rows, b_path_ptr, b_path_par, b_round_ptr, b_plist, b_keep_rows, b_timers,
       b_gdet_ptr, b_gdet_rows, b_gdet_id;
   uint64_t dnnz = 0;  // nnz of D (chain transform), for reports
@@ -1197,6 +1197,11 @@ void build_plan(sp_ctx* c) {
   d.wait_ns = static_cast<uint32_t>(std::max<long>(32, env_long("SP_WAIT_NS", 256)));
   d.bulk_store = static_cast<uint32_t>(env_long("SP_BULK", 1));
   d.seg_stage_ok = static_cast<uint32_t>(env_long("SP_SEG_STAGE", 1));
+  if (env_long("SP_TMA_ZERO", 1) != 0) {
+    const size_t zb = static_cast<size_t>(n_meas) * d.tw * 4;
+    d.zero_src = static_cast<const uint32_t*>(c->b_zero.ensure(std::max<size_t>(zb, 16)));
+    ck(cudaMemsetAsync(const_cast<uint32_t*>(d.zero_src), 0, std::max<size_t>(zb, 16), s), "zero tile");
+  }
   if (env_long("SP_PHASE_TIMERS", 0)) {
     std::vector<long long> z(8, 0);
     d.timers = c->b_timers.upload(z, s);

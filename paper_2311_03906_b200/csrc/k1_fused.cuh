@@ -41,6 +41,8 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
   // padded flip-list entries, spread over 32 banks.
   const uint32_t tile_words = P.n_meas * tw + spare_words(tw);
   const bool with_counts = counts != nullptr;
+  // tiled-layout TMA drain: the stored tile is cleared by a bulk copy of zeros
+  const bool tma_zero = bulk == 1 && P.zero_src != nullptr;
   uint32_t* tiles = reinterpret_cast<uint32_t*>(smem);
   // n_buf tile buffers (1..4): with 2+ the generators fill tiles ahead while
   // the drains empty tile i; 1 when two do not fit (very many rows)
@@ -167,7 +169,8 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
     if (threadIdx.x < kMaxBuf) {
       segctr[threadIdx.x] = 0;
       mbar_init(mbar_full + threadIdx.x, P.gen_warps * 32);
-      mbar_init(mbar_empty + threadIdx.x, blockDim.x - P.gen_warps * 32);
+      // TMA drain: one elected arrival + the zero-fill copy's bytes
+      mbar_init(mbar_empty + threadIdx.x, tma_zero ? 1u : blockDim.x - P.gen_warps * 32);
     }
   }
   __syncthreads();
@@ -610,15 +613,37 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
           }
         }
         if (with_dets && P.n_gdet) general_dets();
-        if (issued) bulk_commit_and_wait_read();
-        named_sync(kBarDrain, nct);  // every row has left the tile
-        for (uint32_t j = ct; j < (P.n_meas << tw4_log2); j += nct) t4[j] = make_uint4(0, 0, 0, 0);
-        if (ct == 0) segctr[b] = 0;
+        if (tma_zero) {
+          // every thread is done reading the tile; the elected thread waits
+          // until the copy engine has read it and then refills it with zeros
+          // by TMA, completing `empty` — the others move on to the next tile
+          if (issued) asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          named_sync(kBarDrain, nct);
+          if (ct == 0) {
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            segctr[b] = 0;
+            if (i + n_buf < n_my) {
+              const uint32_t bytes = P.n_meas * row_bytes;
+              const uint32_t bar = static_cast<uint32_t>(__cvta_generic_to_shared(mbar_empty + b));
+              asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+                           : "memory");
+              asm volatile(
+                  "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(t4_s),
+                  "l"(P.zero_src), "r"(bytes), "r"(bar)
+                  : "memory");
+            }
+          }
+        } else {
+          if (issued) bulk_commit_and_wait_read();
+          named_sync(kBarDrain, nct);  // every row has left the tile
+          for (uint32_t j = ct; j < (P.n_meas << tw4_log2); j += nct) t4[j] = make_uint4(0, 0, 0, 0);
+          if (ct == 0) segctr[b] = 0;
+          if (i + n_buf < n_my) mbar_arrive(mbar_empty + b);
+        }
         if (P.timers && lane == 0) {
           atomicAdd(reinterpret_cast<unsigned long long*>(P.timers) + 2, td1 - td0);
           atomicAdd(reinterpret_cast<unsigned long long*>(P.timers) + 3, clock64() - td1);
         }
-        if (i + n_buf < n_my) mbar_arrive(mbar_empty + b);
         continue;
       }
       // Legacy drain (16-byte stores while the rows are rebuilt, rows

@@ -140,6 +140,9 @@ struct DevPlan {
   const SegDesc* seg_desc = nullptr;  // [n_seg_live]
   uint32_t seg_staged = 0;            // seg_desc and len_bnd copied to shared memory (set at launch)
   uint32_t seg_stage_ok = 1;          // SP_SEG_STAGE=0 keeps them in global memory
+  // Zeros (n_meas * tw u32, device): the TMA drain clears a stored tile with a
+  // bulk copy from here, completing on the tile's `empty` barrier (SP_TMA_ZERO=0: threads clear it)
+  const uint32_t* zero_src = nullptr;
   // Row reconstruction out[k] = d[k] ^ out[parent[k]] along the paths of a
   // heavy-path decomposition of the parent forest: path p lists rows
   // path_rows[path_ptr[p] .. path_ptr[p+1]) top-down; path_par[p] is the head's
