@@ -310,6 +310,16 @@ void build_k5(sp_ctx* c, const std::vector<uint64_t>& col_ptr, const std::vector
   P.cls_sym = c->b_k5_sym.upload(csym, s);
   P.cols = c->b_k5_cols.upload(cols, s);
   P.row_const = c->b_k5_rc.upload(rc, s);
+  {  // ~32 MB of columns per chunk (a quarter of the L2) when the columns
+     // outgrow the L2 and a shot fires tens to hundreds of times (measured at
+     // cfg5 density 0.5: p = 1e-3 27 -> 18 ms with 4 chunks; p = 1e-4 and
+     // 1e-2 are faster unchunked: too few firings per chunk walk, resp. not
+     // bound by column misses)
+    const double col_bytes = static_cast<double>(n_sym) * ncw * 4;
+    long dflt = std::max<long>(1, static_cast<long>(std::ceil(col_bytes / (32.0 * (1 << 20)))));
+    if (events_per_shot < 30.0 || events_per_shot > 300.0) dflt = 1;
+    P.n_chunks = static_cast<uint32_t>(std::min<long>(std::max<long>(env_long("SP_K5_CHUNKS", dflt), 1), 32767));
+  }
   ck(cudaStreamSynchronize(s), "K5 plan upload");
   c->k5_ok = true;
 }

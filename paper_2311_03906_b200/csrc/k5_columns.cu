@@ -75,16 +75,24 @@ k5_columns(const K5Plan P, const RoundKeys K, uint64_t shot_begin, uint64_t n_sh
       for (uint32_t i = threadIdx.x; i < T * q; i += blockDim.x) r4[i] = __ldg(c4 + i % q);
       __syncthreads();
     }
+    // Symbol chunks (chunk-major over the warp's shots): every warp of every
+    // CTA walks the same slice of the model's columns at about the same
+    // time, so that slice stays L2-resident; a class's walk restarts at each
+    // chunk (its own stream), which the draw mode follows too.
+    for (uint32_t ch = 0; ch < P.n_chunks; ++ch)
     for (uint32_t s = warp; s < valid; s += kK5Warps) {
       const uint64_t gs = shot_begin + j0 + s;  // global shot: the stream key
       uint4* r4 = reinterpret_cast<uint4*>(rec + s * ncw);
       for (uint32_t c = 0; c < n_cls; ++c) {
         const ClassInfo ci = P.cls[c];
+        const uint32_t g_lo = static_cast<uint32_t>(ci.trials * ch / P.n_chunks);
+        const uint32_t g_hi = static_cast<uint32_t>(ci.trials * (ch + 1) / P.n_chunks);
+        if (g_lo == g_hi) continue;
         Segment sg;
-        sg.g0 = 0;
+        sg.g0 = g_lo;
         sg.s0 = 0;
-        sg.len = static_cast<uint32_t>(ci.trials);
-        sg.seg = 0x80000000u | c;
+        sg.len = g_hi - g_lo;
+        sg.seg = 0x80000000u | (ch << 16) | c;
         sg.goff = ci.goff;
         sg.dist = ci.dist;
         sg.pbase = 0;

@@ -208,6 +208,7 @@ struct K5Plan {
   const uint32_t* cls_sym = nullptr;    // class position -> first symbol of its group
   const uint32_t* cols = nullptr;       // [n_sym][ncw] dense M_sym columns
   const uint32_t* row_const = nullptr;  // [ncw] rows that are one in every shot
+  uint32_t n_chunks = 1;  // symbol chunks walked in turn (columns of a chunk stay L2-resident)
 };
 
 // Philox4x32-10 round keys for one seed (host-expanded, read from the
