@@ -26,16 +26,13 @@
 
 #include <algorithm>
 
-// column XORs flushed SP_K5Q at a time (their loads in flight together)
-#ifndef SP_K5Q
-#define SP_K5Q 4
-#endif
-
 namespace symphase {
 namespace {
 
 constexpr int kK5Threads = 512;
 constexpr int kK5Warps = kK5Threads / 32;
+constexpr uint32_t kK5G = 8;        // columns XORed per record pass (their loads in flight together)
+constexpr uint32_t kK5Scratch = 128;  // per-warp list of one slot's fired symbols (32 lanes x 4 bits)
 
 __device__ __forceinline__ uint32_t transpose32_k5(uint32_t x, uint32_t lane) {
   constexpr uint32_t kLow[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
@@ -58,6 +55,7 @@ k5_columns(const K5Plan P, const RoundKeys K, uint64_t shot_begin, uint64_t n_sh
   const uint32_t T = 1u << P.t_log2, ncw = P.ncw;
   uint32_t* rec = reinterpret_cast<uint32_t*>(smem);  // [T][ncw]
   uint32_t* cnt = rec + (kDraw ? 0u : T * ncw);       // [n_meas]
+  uint32_t* scratch = cnt + (kDraw ? 0u : P.n_meas) + (threadIdx.x >> 5) * kK5Scratch;  // this warp's list
   const bool with_counts = !kDraw && counts != nullptr;
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (with_counts)
@@ -99,63 +97,83 @@ k5_columns(const K5Plan P, const RoundKeys K, uint64_t shot_begin, uint64_t n_sh
         sg.npat = ci.npat;
         sg.lp = 0;
         sg.clg = ci.clg;
-        segment_walk(sg, K, gs, 0u, lane, [&](auto, const Fired& f) {
-          // each lane looks up its own firings' first symbols at once (one
-          // load latency for the step), then the warp takes the firings one
-          // by one, two columns in flight
-          uint32_t symk[kSlots];
+        // XOR the compacted symbols scratch[0 .. total) into the record
+        // kK5G columns at a time: each lane owns 16-byte chunks of the
+        // record, the group's column loads are in flight together, and the
+        // record is read and written once per group.
+        auto xor_list = [&](uint32_t total) {
+          const uint32_t q = ncw / 4;
+          for (uint32_t i0 = 0; i0 < total; i0 += kK5G) {
+            const uint32_t n = min(kK5G, total - i0);
+            uint32_t cs[kK5G];
 #pragma unroll
-          for (int k = 0; k < kSlots; ++k)
-            symk[k] = ((f.v >> k) & 1u) ? __ldg(P.cls_sym + sg.goff + f.g[k]) : 0u;
-          // pending column XORs (up to kQ symbols), flushed kQ at a time so
-          // kQ columns' loads are in flight together (the loads are the bound)
-          constexpr int kQ = SP_K5Q;
-          uint32_t pend[kQ];  // a shift register (static indices only)
-          int np = 0;
-          auto flush = [&](int cnt) {
-            const uint32_t q = ncw / 4;
+            for (uint32_t t = 0; t < kK5G; ++t) cs[t] = scratch[i0 + (t < n ? t : 0)];
             for (uint32_t w4 = lane; w4 < q; w4 += 32) {
-              uint4 c[kQ];
+              uint4 acc = make_uint4(0, 0, 0, 0);
 #pragma unroll
-              for (int t = 0; t < kQ; ++t)
-                c[t] = t < cnt ? __ldg(reinterpret_cast<const uint4*>(P.cols + static_cast<uint64_t>(pend[t]) * ncw) + w4)
-                               : make_uint4(0, 0, 0, 0);
-              uint4 r = r4[w4];
-#pragma unroll
-              for (int t = 0; t < kQ; ++t) {
-                r.x ^= c[t].x; r.y ^= c[t].y; r.z ^= c[t].z; r.w ^= c[t].w;
-              }
-              r4[w4] = r;
-            }
-          };
-#pragma unroll
-          for (int k = 0; k < kSlots; ++k) {
-            uint32_t m = __ballot_sync(kFull, (f.v >> k) & 1u);
-            while (m) {
-              const uint32_t src = __ffs(m) - 1;
-              m &= m - 1;
-              uint32_t sym = __shfl_sync(kFull, symk[k], src);
-              uint32_t pat = __shfl_sync(kFull, f.pat[k], src);
-              for (; pat; pat >>= 1, ++sym) {
-                if (!(pat & 1u)) continue;
-                if (kDraw) {
-                  if (lane == 0) {
-                    const uint64_t j = j0 + s;
-                    atomicOr(&S32[sym * ld32 + (j >> 5)], 1u << (j & 31));
-                  }
-                } else {
-#pragma unroll
-                  for (int t = kQ - 1; t > 0; --t) pend[t] = pend[t - 1];
-                  pend[0] = sym;
-                  if (++np == kQ) {
-                    flush(kQ);
-                    np = 0;
-                  }
+              for (uint32_t t = 0; t < kK5G; ++t) {
+                if (t < n) {
+                  const uint4 c = __ldg(reinterpret_cast<const uint4*>(P.cols + static_cast<uint64_t>(cs[t]) * ncw) + w4);
+                  acc.x ^= c.x; acc.y ^= c.y; acc.z ^= c.z; acc.w ^= c.w;
                 }
               }
+              uint4 r = r4[w4];
+              r.x ^= acc.x; r.y ^= acc.y; r.z ^= acc.z; r.w ^= acc.w;
+              r4[w4] = r;
             }
           }
-          if (!kDraw && np > 0) flush(np);
+        };
+        auto warp_excl = [&](uint32_t mine, uint32_t& total) {  // exclusive prefix + total
+          uint32_t incl = mine;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(kFull, incl, o);
+            if (lane >= static_cast<uint32_t>(o)) incl += y;
+          }
+          total = __shfl_sync(kFull, incl, 31);
+          return incl - mine;
+        };
+        segment_walk(sg, K, gs, 0u, lane, [&](auto tag, const Fired& f) {
+          constexpr bool kBern = decltype(tag)::value;
+          if (kDraw) {  // the symbol bits this firing sets, straight into S
+            const uint64_t j = j0 + s;
+#pragma unroll
+            for (int k = 0; k < kSlots; ++k) {
+              if (!((f.v >> k) & 1u)) continue;
+              uint32_t sym = __ldg(P.cls_sym + sg.goff + f.g[k]);
+              for (uint32_t pp = f.pat[k]; pp; pp >>= 1, ++sym)
+                if (pp & 1u) atomicOr(&S32[sym * ld32 + (j >> 5)], 1u << (j & 31));
+            }
+            return;
+          }
+          if constexpr (kBern) {
+            // one symbol per firing: the whole step (<= 128) in one list
+            if (!__any_sync(kFull, f.v != 0)) return;
+            uint32_t total;
+            uint32_t at = warp_excl(__popc(f.v), total);
+#pragma unroll
+            for (int k = 0; k < kSlots; ++k)
+              if ((f.v >> k) & 1u) scratch[at++] = __ldg(P.cls_sym + sg.goff + f.g[k]);
+            __syncwarp();
+            xor_list(total);
+            __syncwarp();  // the list is reused by the next step
+          } else {
+            // DEPOLARIZE: one symbol per pattern bit, a slot at a time (<= 128)
+#pragma unroll
+            for (int k = 0; k < kSlots; ++k) {
+              const bool on = (f.v >> k) & 1u;
+              const uint32_t pat = on ? f.pat[k] : 0u;
+              if (!__any_sync(kFull, pat != 0)) continue;
+              uint32_t total;
+              uint32_t at = warp_excl(__popc(pat), total);
+              uint32_t sym = on ? __ldg(P.cls_sym + sg.goff + f.g[k]) : 0u;
+              for (uint32_t pp = pat; pp; pp >>= 1, ++sym)
+                if (pp & 1u) scratch[at++] = sym;
+              __syncwarp();
+              xor_list(total);
+              __syncwarp();
+            }
+          }
         });
       }
     }
@@ -210,7 +228,8 @@ k5_columns(const K5Plan P, const RoundKeys K, uint64_t shot_begin, uint64_t n_sh
 }  // namespace
 
 size_t k5_smem_bytes(uint32_t ncw, uint32_t t_log2, uint32_t n_meas) {
-  return (static_cast<size_t>(ncw) << t_log2) * 4 + static_cast<size_t>(n_meas) * 4;
+  return (static_cast<size_t>(ncw) << t_log2) * 4 + static_cast<size_t>(n_meas) * 4 +
+         static_cast<size_t>(kK5Warps) * kK5Scratch * 4;
 }
 
 int launch_k5(const K5Plan& P, const LaunchCfg& L, uint64_t seed, uint64_t shot_begin,
