@@ -114,6 +114,7 @@ constexpr int kSlots = 4 * kBlocks;
 struct Fired {
   uint32_t v;
   uint32_t g[kSlots], shot[kSlots], pat[kSlots];  // class position, shot in tile, pattern
+  uint32_t glast;  // class position of the step's last trial (warp-uniform)
 };
 
 __device__ __forceinline__ void segment_init(Segment& sg, const ClassInfo* cls, uint32_t n_cls,
@@ -260,6 +261,7 @@ __device__ __forceinline__ bool segment_walk_t(Segment& sg, uint4 (&r)[kBlocks],
         f.v |= (base + incl[sl] < sg.len ? 1u : 0u) << sl;
       }
     }
+    f.glast = sg.g0 + ((sg.s0 + min(pos + total, sg.len) - 1) >> t_log2);
     pos += total;
     const bool more = pos < sg.len;
     pre(std::integral_constant<bool, kBern>{}, f);

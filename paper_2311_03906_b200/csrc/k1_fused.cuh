@@ -289,13 +289,9 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
           return;
         }
         if constexpr (kLp > 0) {
-          if (sg.nbp != 0xFFFFFFFFu) {  // length runs: the step's longest list is at its last firing
-            uint32_t gm = 0;
-#pragma unroll
-            for (int k = 0; k < kSlots; ++k)
-              if ((f.v >> k) & 1u) gm = max(gm, f.g[k]);
-            segment_runs_to(sg, LENB, __reduce_max_sync(kFull, gm));
-          }
+          // length runs: the step's longest list is at its last trial
+          // (warp-uniform; a run boundary is crossed rarely)
+          if (f.glast >= sg.nbp) segment_runs_to(sg, LENB, f.glast);
           const uint32_t lpu = sg.lp == 0 ? static_cast<uint32_t>(kLp) : sg.lp;
           if constexpr (kPre > 0 && kPre < kSlots) load_lists(bern_tag, f, kPre, kSlots);
 #pragma unroll
