@@ -8,14 +8,19 @@
 //       no-swizzle core-matrix layout, one contiguous 16 KB block per
 //       (128-row m-tile, 128-symbol k-stage): a stage is ONE bulk TMA copy
 //       (cp.async.bulk, completion on the stage's mbarrier).
-//   B = S bits of a 256-shot n-tile, expanded to bytes in shared memory by
-//       four expander warps in the MN-major (shots contiguous) core-matrix
+//   B = S bits of a 128-shot n-tile, expanded to bytes in shared memory by
+//       eight expander warps in the MN-major (shots contiguous) core-matrix
 //       layout: 16 shot bits -> 16 bytes, no bit transpose.
-// Per CTA: one 128 x 256 output tile, 4 pipeline stages (16 + 32 KB each);
-// warp 0 lane 0 issues A copies, warp 1 lane 0 issues the MMAs (4 per stage,
-// K = 32), warps 4-7 expand B and then run the epilogue (tcgen05.ld of
-// 32 columns per thread, parity, pack to words, store). tcgen05.commit
-// arrives on the stage's `empty` barrier when the MMAs that read it are done.
+// Per CTA: four 128 x 128 output tiles (kTcMT m-tiles share every expanded
+// B stage, so the expansion cost per MMA is a quarter of a one-tile CTA's),
+// 2 pipeline stages (4 x 16 KB A + 16 KB B each), 4 x 128 TMEM columns.
+// Warp 0 lane 0 issues the A copies, warp 1 lane 0 the MMAs (4 m-tiles x 4
+// K-steps of 32 per stage), warps 4-11 expand B and then run the epilogue
+// (tcgen05.ld of 32 columns per thread, parity, pack to words, store).
+// tcgen05.commit arrives on the stage's `empty` barrier when the MMAs that
+// read it are done.
+// cfg5 shape (10^4 x 10^5, density 0.5, 2^20 shots): 892 ms vs 1020 ms for
+// Four-Russians (profiles/k6_timing_r02.txt); 1 tile/CTA was 2.87 s.
 //
 // A prototype next to the Four-Russians kernel (k2_m4rm): selected with
 // sp_set_product(SP_PRODUCT_TENSOR); results are bit-identical (integer
@@ -29,16 +34,20 @@
 namespace symphase {
 namespace {
 
-constexpr uint32_t kTcM = 128, kTcN = 256, kTcBK = 128, kTcStages = 4;
-constexpr uint32_t kTcAStage = kTcM * kTcBK;  // bytes
+constexpr uint32_t kTcM = 128, kTcN = 128, kTcBK = 128, kTcStages = 2;
+constexpr uint32_t kTcMT = 4;                 // m-tiles per CTA: four accumulators share each B stage
+constexpr uint32_t kTcNG = kTcN / 16;         // 16-shot groups of an n-tile (B core matrices along N)
+constexpr uint32_t kTcLboB = kTcNG * 128;     // B: bytes between k-groups
+constexpr uint32_t kTcAStage = kTcM * kTcBK;  // bytes of one m-tile's A per stage
 constexpr uint32_t kTcBStage = kTcN * kTcBK;
 constexpr uint32_t kTcThreads = 384;   // warps 0-3: TMA / MMA / TMEM / spare; 4-11: B expanders + epilogue
 constexpr uint32_t kTcExp = 256;        // expander threads
-constexpr uint32_t kTcPk = kTcBK * kTcN / 8;  // packed S bytes per stage (4 KB)
+constexpr uint32_t kTcPk = kTcBK * kTcN / 8;  // packed S bytes per stage
+constexpr uint32_t kTcPkChunks = kTcPk / 16;   // 16-byte cp.async chunks of a stage
 constexpr uint32_t kTcPkSlots = 4, kTcPkAhead = 3;
 constexpr uint32_t kBarExp = 2;         // named barrier of the expander warps
-constexpr size_t kTcSmem =
-    kTcStages * (kTcAStage + kTcBStage) + kTcPkSlots * kTcPk + 8 * (3 * kTcStages + 1) + 16 + 1024;
+constexpr size_t kTcSmem = kTcStages * (kTcMT * kTcAStage + kTcBStage) + kTcPkSlots * kTcPk +
+                           8 * (3 * kTcStages + 1) + 16 + 1024;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -58,7 +67,7 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint
          (static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);
 }
 
-// Instruction descriptor: D s32, A u8 K-major, B u8 MN-major, M = 128, N = 256.
+// Instruction descriptor: D s32, A u8 K-major, B u8 MN-major, M = kTcM, N = kTcN.
 constexpr uint32_t kTcIdesc = (2u << 4) | (0u << 7) | (0u << 10) | (0u << 15) | (1u << 16) |
                               ((kTcN >> 3) << 17) | ((kTcM >> 4) << 24);
 
@@ -106,7 +115,7 @@ k6_tc_product(const uint8_t* __restrict__ At, uint32_t k_stages, const uint64_t*
   extern __shared__ __align__(1024) uint8_t smem_k6[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_k6) + 1023) & ~uintptr_t{1023});
   uint8_t* sA = base;
-  uint8_t* sB = base + kTcStages * kTcAStage;
+  uint8_t* sB = base + kTcStages * kTcMT * kTcAStage;
   uint8_t* sP = sB + kTcStages * kTcBStage;  // packed S ring (cp.async)
   uint64_t* bars = reinterpret_cast<uint64_t*>(sP + kTcPkSlots * kTcPk);
   uint64_t* full_a = bars;
@@ -115,7 +124,7 @@ k6_tc_product(const uint8_t* __restrict__ At, uint32_t k_stages, const uint64_t*
   uint64_t* done = bars + 3 * kTcStages;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * kTcStages + 1);
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t nt = blockIdx.x, mt = blockIdx.y;
+  const uint32_t nt = blockIdx.x, mt = blockIdx.y * kTcMT;  // first of the CTA's m-tiles
 
   if (threadIdx.x == 0) {
     for (uint32_t s = 0; s < kTcStages; ++s) {
@@ -126,9 +135,9 @@ k6_tc_product(const uint8_t* __restrict__ At, uint32_t k_stages, const uint64_t*
     mbar_init(done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 2) {  // TMEM: 128 lanes x 256 int32 columns, one accumulator tile
+  if (warp == 2) {  // TMEM: 128 lanes x kTcN int32 columns per accumulator tile
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "n"(kTcN)
+                 "n"(kTcN * kTcMT)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
@@ -144,9 +153,11 @@ k6_tc_product(const uint8_t* __restrict__ At, uint32_t k_stages, const uint64_t*
       for (uint32_t ks = 0; ks < k_stages; ++ks) {
         const uint32_t s = ks % kTcStages;
         if (ks >= kTcStages) mbar_wait_spin(smem_u32(empty + s), ((ks / kTcStages) - 1) & 1);
-        mbar_expect_tx(smem_u32(full_a + s), kTcAStage);
-        bulk_load(smem_u32(sA + s * kTcAStage), src + static_cast<uint64_t>(ks) * kTcAStage, kTcAStage,
-                  smem_u32(full_a + s));
+        mbar_expect_tx(smem_u32(full_a + s), kTcMT * kTcAStage);
+        for (uint32_t a = 0; a < kTcMT; ++a)  // the next m-tile's blocks follow k_stages blocks later
+          bulk_load(smem_u32(sA + (s * kTcMT + a) * kTcAStage),
+                    src + (static_cast<uint64_t>(a) * k_stages + ks) * kTcAStage, kTcAStage,
+                    smem_u32(full_a + s));
       }
     }
   } else if (warp == 1) {
@@ -157,20 +168,23 @@ k6_tc_product(const uint8_t* __restrict__ At, uint32_t k_stages, const uint64_t*
         mbar_wait_spin(smem_u32(full_a + s), ph);
         mbar_wait_spin(smem_u32(full_b + s), ph);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t a0 = smem_u32(sA + s * kTcAStage), b0 = smem_u32(sB + s * kTcBStage);
+        const uint32_t a0 = smem_u32(sA + s * kTcMT * kTcAStage), b0 = smem_u32(sB + s * kTcBStage);
 #pragma unroll
         for (uint32_t kk = 0; kk < kTcBK / 32; ++kk) {
           // K = 32 per MMA: A chunks 2kk, 2kk+1 (LBO 2048 between chunks, SBO
-          // 128 between row groups); B k-groups 4kk..4kk+3 (LBO 2048 between
-          // k-groups, SBO 128 between 16-shot groups)
-          const uint64_t da = umma_desc(a0 + kk * 2 * 2048, 2048, 128);
-          const uint64_t db = umma_desc(b0 + kk * 4 * 2048, 2048, 128);
+          // 128 between row groups); B k-groups 4kk..4kk+3 (LBO kTcLboB
+          // between k-groups, SBO 128 between 16-shot groups)
+          const uint64_t db = umma_desc(b0 + kk * 4 * kTcLboB, kTcLboB, 128);
           const uint32_t acc = (ks | kk) != 0;
-          asm volatile(
-              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-              "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
-              "l"(da), "l"(db), "r"(kTcIdesc), "r"(acc)
-              : "memory");
+#pragma unroll
+          for (uint32_t a = 0; a < kTcMT; ++a) {  // accumulator a: columns a * kTcN ..
+            const uint64_t da = umma_desc(a0 + a * kTcAStage + kk * 2 * 2048, 2048, 128);
+            asm volatile(
+                "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem + a * kTcN),
+                "l"(da), "l"(db), "r"(kTcIdesc), "r"(acc)
+                : "memory");
+          }
         }
         // the stage's smem may be refilled once these MMAs have read it
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -183,17 +197,18 @@ k6_tc_product(const uint8_t* __restrict__ At, uint32_t k_stages, const uint64_t*
     }
   } else if (warp >= 4) {
     // ---- B expanders: S bits -> MN-major u8 core matrices ----
-    // The packed S slice of stage ks (128 symbols x 256 shots = 4 KB, one
-    // 16-byte chunk per thread) is fetched kTcPkAhead stages ahead with
-    // cp.async into a ring; then unit (k-group kg, shot group ng, k-row kr)
-    // = 16 bytes at ((kg * 16 + ng) * 8 + kr) * 16 is spread from 16 bits.
+    // The packed S slice of stage ks (128 symbols x kTcN shots, one 16-byte
+    // chunk per thread) is fetched kTcPkAhead stages ahead with cp.async
+    // into a ring; then unit (k-group kg, shot group ng, k-row kr) = 16
+    // bytes at ((kg * kTcNG + ng) * 8 + kr) * 16 is spread from 16 bits.
     const uint32_t et = threadIdx.x - 128;
     const uint64_t n0 = static_cast<uint64_t>(nt) * kTcN;
     const uint32_t n_words = static_cast<uint32_t>((n_shots + 63) >> 6);
-    auto fetch = [&](uint32_t ks) {  // chunk et: symbol row et >> 1, shots (et & 1) * 128 ..
-      if (ks < k_stages) {
-        const uint32_t k = ks * kTcBK + (et >> 1);
-        const uint32_t w = static_cast<uint32_t>(n0 >> 6) + (et & 1) * 2;  // first of 2 words
+    constexpr uint32_t kCpr = kTcN / 128;  // 16-byte chunks per symbol row of a stage
+    auto fetch = [&](uint32_t ks) {  // chunk et: symbol row et / kCpr, 128 shots (et % kCpr)
+      if (ks < k_stages && et < kTcPkChunks) {
+        const uint32_t k = ks * kTcBK + et / kCpr;
+        const uint32_t w = static_cast<uint32_t>(n0 >> 6) + (et % kCpr) * 2;  // first of 2 words
         const uint32_t dst = smem_u32(sP + (ks % kTcPkSlots) * kTcPk + et * 16);
         // two 8-byte copies (rows of S are only 8-byte aligned); rows past
         // n_sym and words past the record are zero-filled
@@ -219,13 +234,13 @@ k6_tc_product(const uint8_t* __restrict__ At, uint32_t k_stages, const uint64_t*
       const uint16_t* pk = reinterpret_cast<const uint16_t*>(sP + (ks % kTcPkSlots) * kTcPk);
 #pragma unroll 4
       for (uint32_t i = 0; i < (kTcBK * kTcN / 16) / kTcExp; ++i) {
-        const uint32_t u = et + kTcExp * i;  // unit index in [0, 2048)
-        const uint32_t ng = u & 15u, kr = (u >> 4) & 7u, kg = u >> 7;
-        uint32_t bits = pk[(kg * 8 + kr) * 16 + ng];
+        const uint32_t u = et + kTcExp * i;  // unit index in [0, kTcBK * kTcN / 16)
+        const uint32_t ng = u % kTcNG, kr = (u / kTcNG) & 7u, kg = u / (kTcNG * 8);
+        uint32_t bits = pk[(kg * 8 + kr) * kTcNG + ng];
         const uint64_t shot = n0 + ng * 16;
         if (shot >= n_shots) bits = 0;
         else if (n_shots - shot < 16) bits &= (1u << (n_shots - shot)) - 1u;
-        dst[(kg * 16 + ng) * 8 + kr] = spread16(bits);  // (a 256-entry smem LUT: 3.5 s vs 2.9 s)
+        dst[(kg * kTcNG + ng) * 8 + kr] = spread16(bits);  // (a 256-entry smem LUT was slower)
       }
       fence_proxy_async_smem();  // the tensor core reads the stage through the async proxy
       mbar_arrive(full_b + s);
@@ -234,12 +249,12 @@ k6_tc_product(const uint8_t* __restrict__ At, uint32_t k_stages, const uint64_t*
     mbar_wait_spin(smem_u32(done), 0);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t q = warp & 3;               // TMEM lane quarter of this warp
-    const uint32_t half = (warp - 4) >> 2;     // which half of the 256 columns
-    const uint32_t row = mt * kTcM + q * 32 + lane;
     uint32_t* out32 = reinterpret_cast<uint32_t*>(out);
-    for (uint32_t c = half * 4; c < half * 4 + 4; ++c) {
+    for (uint32_t acc = (warp - 4) >> 2; acc < kTcMT; acc += 2)  // two warps per lane quarter
+    for (uint32_t c = 0; c < kTcN / 32; ++c) {
+      const uint32_t row = (mt + acc) * kTcM + q * 32 + lane;
       uint32_t v[32];
-      const uint32_t taddr = tmem + ((q * 32) << 16) + c * 32;
+      const uint32_t taddr = tmem + ((q * 32) << 16) + acc * kTcN + c * 32;
       asm volatile(
           "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
           "%12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, "
@@ -263,13 +278,16 @@ k6_tc_product(const uint8_t* __restrict__ At, uint32_t k_stages, const uint64_t*
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 2)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTcN) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTcN * kTcMT)
+                 : "memory");
 }
 
 }  // namespace
 
 uint64_t tc_a_bytes(uint32_t n_meas, uint32_t n_sym) {
-  const uint64_t mt = (n_meas + kTcM - 1) / kTcM, ks = (std::max<uint32_t>(n_sym, 1) + kTcBK - 1) / kTcBK;
+  // m-tiles rounded up to the CTA's kTcMT (the extra ones are zero rows)
+  const uint64_t mt = (n_meas + kTcM * kTcMT - 1) / (kTcM * kTcMT) * kTcMT;
+  const uint64_t ks = (std::max<uint32_t>(n_sym, 1) + kTcBK - 1) / kTcBK;
   return mt * ks * kTcAStage;
 }
 
@@ -294,9 +312,10 @@ int launch_tc_product(const LaunchCfg& L, const uint8_t* At, uint32_t n_meas, ui
     attr = true;
   }
   const uint32_t ks = (std::max<uint32_t>(n_sym, 1) + kTcBK - 1) / kTcBK;
-  const uint64_t n_tiles = (n_shots + kTcN - 1) / kTcN, m_tiles = (n_meas + kTcM - 1) / kTcM;
-  if (n_tiles > 0x7FFFFFFFull || m_tiles > 65535) return -1;
-  dim3 grid(static_cast<unsigned>(n_tiles), static_cast<unsigned>(m_tiles));
+  const uint64_t n_tiles = (n_shots + kTcN - 1) / kTcN;
+  const uint64_t m_ctas = (n_meas + kTcM * kTcMT - 1) / (kTcM * kTcMT);
+  if (n_tiles > 0x7FFFFFFFull || m_ctas > 65535) return -1;
+  dim3 grid(static_cast<unsigned>(n_tiles), static_cast<unsigned>(m_ctas));
   k6_tc_product<<<grid, kTcThreads, kTcSmem, L.stream>>>(At, ks, S, ldS, n_sym, n_shots, n_meas, out, ld);
   return check_launch() ? -1 : 1;
 }
