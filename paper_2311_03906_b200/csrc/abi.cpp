@@ -206,6 +206,17 @@ bool dense_product(const sp_ctx* c) {
   const double cells = static_cast<double>(c->hp.n_meas) * static_cast<double>(c->hp.n_sym);
   return cells > 0 && static_cast<double>(c->hp.nnz) > kDenseProductDensity * cells;
 }
+// K6 (tcgen05 int8 GEMM) vs K2 (Four-Russians) for a dense product: K6 wins
+// at every measured shape with >= 4096 symbols and loses at 1000 symbols
+// (profiles/k6_shapes_r02.txt); its u8 operand copy of M_sym is capped.
+constexpr uint64_t kTensorMinSym = 4096;
+constexpr uint64_t kTensorMaxABytes = 16ull << 30;
+bool tensor_product(const sp_ctx* c) {
+  if (c->product == SP_PRODUCT_TENSOR) return true;
+  return c->product == SP_PRODUCT_AUTO && dense_product(c) && c->hp.n_sym >= kTensorMinSym &&
+         tc_a_bytes(static_cast<uint32_t>(c->hp.n_meas), static_cast<uint32_t>(c->hp.n_sym)) <=
+             kTensorMaxABytes;
+}
 // Dense row-major M_sym words from the CSR rows (first use only).
 void ensure_dense_words(HostPlan& h) {
   if (!h.dense_words.empty()) return;
@@ -214,6 +225,24 @@ void ensure_dense_words(HostPlan& h) {
   for (uint64_t k = 0; k < h.n_meas; ++k)
     for (uint64_t i = h.row_ptr[k]; i < h.row_ptr[k + 1]; ++i)
       h.dense_words[k * h.ldm + h.sym_idx[i] / 64] |= uint64_t{1} << (h.sym_idx[i] % 64);
+}
+
+// The explicit-S product of plan d (whose dense words are M_sym's): K6 when
+// tensor_product() picks it (the u8 operand layout is built on first use and
+// kept until the model changes), else K2. Returns launch_* codes.
+int run_product(sp_ctx* c, const DevPlan& d, const uint64_t* S, uint64_t ldS, uint64_t n_shots,
+                uint64_t* out, uint64_t ld) {
+  if (!tensor_product(c) || !d.dense) return launch_product(d, c->L, dense_product(c), S, ldS, n_shots, out, ld);
+  int prep = 0;
+  if (!c->tc_ready) {
+    auto* at = static_cast<uint8_t*>(c->p_tc_a.ensure(tc_a_bytes(d.n_meas, d.n_sym)));
+    prep = launch_tc_prep(c->L, d.dense, d.ldm, d.n_meas, d.n_sym, at);
+    if (prep < 0) return prep;
+    c->tc_ready = true;
+  }
+  const int r = launch_tc_product(c->L, static_cast<const uint8_t*>(c->p_tc_a.p), d.n_meas, d.n_sym, S,
+                                  ldS, n_shots, out, ld);
+  return r < 0 ? r : r + prep;
 }
 
 // K5 column sampler plan (k5_columns.cu): for models the fused kernel does
@@ -1337,7 +1366,7 @@ void build_plan(sp_ctx* c) {
         for (int rep = 0; rep < 3; ++rep) {
           ck(cudaEventRecord(e0, s), "cudaEventRecord");
           const int r1 = launch_draw(d, c->L, false, 0x5EEDull + rep, 0, n_u, S, ldS);
-          const int r2 = launch_product(d, c->L, dense_product(c), S, ldS, n_u, buf, ldS);
+          const int r2 = run_product(c, d, S, ldS, n_u, buf, ldS);
           ck(cudaEventRecord(e1, s), "cudaEventRecord");
           ck(cudaEventSynchronize(e1), "cudaEventSynchronize");
           if (r1 < 0 || r2 < 0) {
@@ -1657,6 +1686,7 @@ int sp_set_product(sp_ctx* ctx, sp_product v) {
     ensure_dense_words(ctx->hp);
     ctx->plan_ready = false;
     ctx->prod_ready = false;
+    ctx->tc_ready = false;
   }
   return SP_OK;
 }
@@ -1687,6 +1717,7 @@ int sp_load_msym_csr(sp_ctx* ctx, uint64_t n_meas, uint64_t n_sym, const uint64_
   ctx->have_msym = true;
   ctx->plan_ready = false;
   ctx->prod_ready = false;
+  ctx->tc_ready = false;
   if (ctx->product == SP_PRODUCT_DENSE) sp_set_product(ctx, SP_PRODUCT_DENSE);
   return SP_OK;
 }
@@ -1719,6 +1750,7 @@ int sp_load_msym_dense(sp_ctx* ctx, uint64_t n_meas, uint64_t n_sym, const uint6
     for (uint64_t k = 0; k < n_meas; ++k)
       h.dense_words[k * h.ldm + (n_sym - 1) / 64] &= (uint64_t{1} << (n_sym % 64)) - 1;
   ctx->prod_ready = false;
+  ctx->tc_ready = false;
   return SP_OK;
 }
 
@@ -1926,6 +1958,7 @@ int sp_sample_given_S(sp_ctx* ctx, const uint64_t* d_S, uint64_t n_sym_S, uint64
   if (dense && ctx->hp.dense_words.empty()) {
     ensure_dense_words(ctx->hp);
     ctx->prod_ready = false;
+    ctx->tc_ready = false;
   }
   if (!ctx->prod_ready) {
     try {
@@ -1971,25 +2004,11 @@ int sp_sample_given_S(sp_ctx* ctx, const uint64_t* d_S, uint64_t n_sym_S, uint64
     }
   }
   if (dense && !ctx->pp.dense) return fail(SP_ERR_NOT_LOADED, "dense M_sym words not built");
-  if (ctx->product == SP_PRODUCT_TENSOR) {
-    if (!ctx->tc_ready) {
-      try {
-        const uint64_t bytes = tc_a_bytes(ctx->pp.n_meas, ctx->pp.n_sym);
-        auto* at = static_cast<uint8_t*>(ctx->p_tc_a.ensure(bytes));
-        const int rp = launch_tc_prep(ctx->L, ctx->pp.dense, ctx->pp.ldm, ctx->pp.n_meas,
-                                      ctx->pp.n_sym, at);
-        if (int e = launched(ctx, rp, "tensor-core operand layout")) return e;
-        ctx->tc_ready = true;
-      } catch (const CudaError& e) {
-        return fail(SP_ERR_CUDA, e.what());
-      }
-    }
-    const int r = launch_tc_product(ctx->L, static_cast<const uint8_t*>(ctx->p_tc_a.p), ctx->pp.n_meas,
-                                    ctx->pp.n_sym, d_S, ldS, n_shots, d_out, ld);
-    return launched(ctx, r, "tensor-core product launch");
+  try {
+    return launched(ctx, run_product(ctx, ctx->pp, d_S, ldS, n_shots, d_out, ld), "product launch");
+  } catch (const CudaError& e) {
+    return fail(SP_ERR_CUDA, e.what());
   }
-  int r = launch_product(ctx->pp, ctx->L, dense, d_S, ldS, n_shots, d_out, ld);
-  return launched(ctx, r, "product launch");
 }
 
 uint64_t sp_encoded_size(uint64_t n_meas, uint64_t n_shots, sp_format fmt) {

@@ -49,3 +49,22 @@ def test_tensor_product_cfg5_shape(gpu_sampler_factory, port, dens):
     assert np.array_equal(host(s.sample_given(dev(S), n)), want)
     s.set_product("dense")
     assert np.array_equal(host(s.sample_given(dev(S), n)), want)
+
+
+def test_auto_picks_tensor_and_rebuilds_on_reload(gpu_sampler_factory, port):
+    """AUTO routes a dense product with >= 4096 symbols to K6; loading another
+    model of the same shape must rebuild the u8 operand layout (the buffer is
+    reused, so a stale layout would still have the right size)."""
+    n = 3 * 4096 + 5
+    rng = np.random.default_rng(3)
+    s = gpu_sampler_factory()
+    for seed in (11, 12):
+        model = CI.random_msym_model(700, 5000, 0.5, 1e-3, seed=seed)
+        S = pack_bits(rng.integers(0, 2, size=(model.n_sym, n), dtype=np.uint8))
+        s.load_csr(model.row_ptr, model.sym_idx, model.n_sym)
+        before = s.launches
+        got = host(s.sample_given(dev(S), n))
+        assert np.array_equal(got, port.sample(model.row_ptr, model.sym_idx, S, n))
+        assert s.launches - before == 2  # operand layout + K6
+        s.sample_given(dev(S), n)
+        assert s.launches - before == 3

@@ -14,7 +14,9 @@ from paper_2311_03906_b200 import circuits as CI  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 1 << 20
 dens = float(sys.argv[2]) if len(sys.argv) > 2 else 0.5
-model = CI.random_msym_model(10**4, 10**5, dens, 1e-3, seed=7)
+m = int(sys.argv[3]) if len(sys.argv) > 3 else 10**4
+v = int(sys.argv[4]) if len(sys.argv) > 4 else 10**5
+model = CI.random_msym_model(m, v, dens, 1e-3, seed=7)
 g = torch.Generator(device="cuda").manual_seed(42)
 S = torch.randint(-(2**63), 2**63 - 1, (model.n_sym, n // 64), dtype=torch.int64, device="cuda",
                   generator=g)
@@ -35,6 +37,6 @@ for variant in ("tensor", "dense"):
         ts.append(a.elapsed_time(b))
     outs[variant] = out
     ops = 2.0 * model.n_meas * model.n_sym * n
-    print(json.dumps({"variant": variant, "n_shots": n, "density": dens, "ms": min(ts),
+    print(json.dumps({"variant": variant, "m": m, "v": v, "n_shots": n, "density": dens, "ms": min(ts),
                       "int8_tops": ops / (min(ts) / 1e3) / 1e12}), flush=True)
 print(json.dumps({"equal": bool(torch.equal(outs["tensor"], outs["dense"]))}))
