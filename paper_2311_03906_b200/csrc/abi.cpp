@@ -314,8 +314,9 @@ void build_k5(sp_ctx* c, const std::vector<uint64_t>& col_ptr, const std::vector
       cls.push_back(ci);
       cg.insert(cg.end(), k.groups.begin(), k.groups.end());
     }
-  // dense columns, and the rows that are one in every shot (s0, p >= 1)
-  std::vector<uint32_t> cols(static_cast<size_t>(n_sym) * ncw, 0), rc(ncw, 0);
+  // dense columns (plus an all-zero column n_sym that pads K5's column
+  // groups), and the rows that are one in every shot (s0, p >= 1)
+  std::vector<uint32_t> cols(static_cast<size_t>(n_sym + 1) * ncw, 0), rc(ncw, 0);
   for (uint64_t sidx = 0; sidx < n_sym; ++sidx)
     for (uint64_t i = col_ptr[sidx]; i < col_ptr[sidx + 1]; ++i)
       cols[sidx * ncw + col_rows[i] / 32] ^= 1u << (col_rows[i] % 32);

@@ -31,8 +31,17 @@ namespace {
 
 constexpr int kK5Threads = 512;
 constexpr int kK5Warps = kK5Threads / 32;
-constexpr uint32_t kK5G = 8;        // columns XORed per record pass (their loads in flight together)
-constexpr uint32_t kK5Scratch = 128;  // per-warp list of one slot's fired symbols (32 lanes x 4 bits)
+#ifndef K5_G
+#define K5_G 8
+#endif
+#ifndef K5_UNR
+#define K5_UNR 1
+#endif
+constexpr uint32_t kK5G = K5_G;
+constexpr int kK5Unroll = K5_UNR;     // columns XORed per record pass (their loads in flight together)
+// per-warp list of one step's fired symbols (32 lanes x 4 slots), padded to
+// whole column groups with the zero column n_sym
+constexpr uint32_t kK5Scratch = 128 + kK5G;
 
 __device__ __forceinline__ uint32_t transpose32_k5(uint32_t x, uint32_t lane) {
   constexpr uint32_t kLow[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
@@ -102,21 +111,27 @@ k5_columns(const K5Plan P, const RoundKeys K, uint64_t shot_begin, uint64_t n_sh
         // record, the group's column loads are in flight together, and the
         // record is read and written once per group.
         auto xor_list = [&](uint32_t total) {
+          // pad the list to whole groups with the zero column: every group
+          // issues kK5G loads, branch-free; offsets are u32 (uint4 units)
+          const uint32_t padded = (total + kK5G - 1) / kK5G * kK5G;
+          if (lane < padded - total) scratch[total + lane] = P.n_sym;
+          __syncwarp();
           const uint32_t q = ncw / 4;
-          for (uint32_t i0 = 0; i0 < total; i0 += kK5G) {
-            const uint32_t n = min(kK5G, total - i0);
-            uint32_t cs[kK5G];
+          const uint4* base = reinterpret_cast<const uint4*>(P.cols);
+          for (uint32_t i0 = 0; i0 < padded; i0 += kK5G) {
+            uint32_t off[kK5G];
 #pragma unroll
-            for (uint32_t t = 0; t < kK5G; ++t) cs[t] = scratch[i0 + (t < n ? t : 0)];
+            for (uint32_t t = 0; t < kK5G; ++t) off[t] = scratch[i0 + t] * q + lane;
+#pragma unroll kK5Unroll
             for (uint32_t w4 = lane; w4 < q; w4 += 32) {
-              uint4 acc = make_uint4(0, 0, 0, 0);
+              uint4 acc = __ldg(base + off[0]);
 #pragma unroll
-              for (uint32_t t = 0; t < kK5G; ++t) {
-                if (t < n) {
-                  const uint4 c = __ldg(reinterpret_cast<const uint4*>(P.cols + static_cast<uint64_t>(cs[t]) * ncw) + w4);
-                  acc.x ^= c.x; acc.y ^= c.y; acc.z ^= c.z; acc.w ^= c.w;
-                }
+              for (uint32_t t = 1; t < kK5G; ++t) {
+                const uint4 c = __ldg(base + off[t]);
+                acc.x ^= c.x; acc.y ^= c.y; acc.z ^= c.z; acc.w ^= c.w;
               }
+#pragma unroll
+              for (uint32_t t = 0; t < kK5G; ++t) off[t] += 32;
               uint4 r = r4[w4];
               r.x ^= acc.x; r.y ^= acc.y; r.z ^= acc.z; r.w ^= acc.w;
               r4[w4] = r;
