@@ -20,10 +20,13 @@ def dev(a):
 
 
 @pytest.mark.parametrize("m,v,n,dens", [(1, 1, 1, 0.5), (5, 40, 70, 0.3), (128, 128, 256, 0.5),
+                                        (128, 256, 256, 0.5), (256, 128, 256, 0.5), (128, 128, 512, 0.5),
+                                        (128, 131, 256, 0.5), (128, 128, 257, 0.5), (513, 300, 129, 0.5),
                                         (129, 131, 257, 0.5), (300, 1000, 1000, 0.1),
                                         (200, 300, 4096 + 33, 0.9), (1000, 2000, 300, 0.5)])
 def test_tensor_product_equals_oracle(gpu_sampler_factory, port, m, v, n, dens):
-    """Ragged shapes: rows, symbols and shots off the 128 / 128 / 256 tiles."""
+    """Tile-edge and ragged shapes: rows, symbols and shots on and off the
+    128-row / 512-row-CTA / 128-symbol / 128-shot tiles."""
     model = CI.random_msym_model(m, v, dens, 1e-3, seed=m + v)
     rng = np.random.default_rng(n)
     S = pack_bits(rng.integers(0, 2, size=(model.n_sym, n), dtype=np.uint8))
