@@ -314,6 +314,37 @@ def bench_config(args, desc, shots_per_gpu):
     return c
 
 
+def step_protocol(step, soak, warmup, steps, barrier, sync, clock, timed, on_timed=None):
+    """The step loop both ranks run: `warmup` untimed steps, >= 0.6 s of soak
+    (the clock sampler starts), exactly `steps` timed steps (timed(fn) wraps a
+    step in CUDA events and returns them), then 0.5 s of soak. `step` carries
+    the per-step collective, so it runs exactly warmup + steps times on every
+    rank; `soak` has no collective (its count depends on each rank's clock).
+    on_timed(0) / on_timed(1) run just before / after the timed steps.
+    Returns (events, wall seconds of the timed steps)."""
+    for i in range(warmup):
+        step(i, last=i == warmup - 1)
+    sync()
+    barrier()
+    while clock() < 0.6:
+        soak()
+    sync()
+    barrier()
+    if on_timed is not None:
+        on_timed(0)
+    wall0 = time.perf_counter()
+    evs = [timed(lambda i=i: step(warmup + i, last=i == steps - 1)) for i in range(steps)]
+    sync()
+    barrier()
+    wall = time.perf_counter() - wall0
+    if on_timed is not None:
+        on_timed(1)
+    t_end = clock() + 0.5
+    while clock() < t_end:
+        soak()
+    return evs, wall
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -391,41 +422,35 @@ def run_ours(args):
     def step(i, last=False):
         pipe.step(i, lambda c: counted(shots, 1000 + i, shot_begin=shot_begin, counts=c), last=last)
 
-    for i in range(args.warmup):
-        step(i, last=i == args.warmup - 1)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(args.steps)]
+    scratch = torch.zeros(n_counts, dtype=torch.int64, device=dev)
+    n_soak = [0]
+
+    def soak():
+        # GPU load for the clock sampler: the same launch, counts into a
+        # scratch buffer and NO collective, so ranks may run different numbers
+        scratch.zero_()
+        counted(shots, 7000 + n_soak[0], shot_begin=shot_begin, counts=scratch)
+        torch.cuda.synchronize()
+        n_soak[0] += 1
+
+    def timed(fn):
+        flush.zero_()  # L2 flush between timed iterations, outside the events
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        fn()
+        b.record(stream)
+        return a, b
+
+    barrier = (lambda: dist.barrier()) if world > 1 else (lambda: None)
     with ClockSampler(local) as clk:
-        # Keep the GPU busy (untimed) while nvidia-smi starts sampling.
-        j = 0
-        while clk.elapsed() < 0.6:
-            step(args.warmup + args.steps + j, last=True)
-            torch.cuda.synchronize()
-            j += 1
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        wall0 = time.perf_counter()
-        launches0 = smp.launches
-        for i in range(args.steps):
-            flush.zero_()  # L2 flush between timed iterations, outside the events
-            evs[i][0].record(stream)
-            step(args.warmup + i, last=i == args.steps - 1)
-            evs[i][1].record(stream)
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        wall = time.perf_counter() - wall0
-        launches = smp.launches - launches0
-        # ... and for a short soak after the timed steps, same load.
-        t_end = clk.elapsed() + 0.5
-        while clk.elapsed() < t_end:
-            step(args.warmup + args.steps + j, last=True)
-            torch.cuda.synchronize()
-            j += 1
+        lc = [0, 0]  # the library's launch counter before / after the timed steps
+
+        def mark(k):
+            lc[k] = smp.launches
+
+        evs, wall = step_protocol(step, soak, args.warmup, args.steps, barrier,
+                                  torch.cuda.synchronize, clk.elapsed, timed, on_timed=mark)
+        launches = lc[1] - lc[0]
     step_ms = [a.elapsed_time(b) for a, b in evs]
     t_step = sum(step_ms) / len(step_ms) / 1e3
     t_tensor = torch.tensor([t_step], dtype=torch.float64, device=dev)

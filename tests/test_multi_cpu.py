@@ -146,3 +146,59 @@ def test_gloo_sample_sharded_and_step_pipeline():
             # only (the buffer is zeroed before reuse, nothing accumulates)
             want_i = sum(smp.counts_for(bb, nn, 100 + i) for bb, nn in spans)
             assert np.array_equal(got, want_i), (rank, i)
+
+
+def _protocol_worker(rank, world, port, q):
+    """bench.step_protocol with the bench's CountPipeline on gloo: the soak
+    runs a rank-dependent number of times (rank 1's clock runs slow), yet
+    every rank issues the same collectives, so nothing hangs and each step's
+    reduce pairs with the same step on the other rank."""
+    import time
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import bench
+    from paper_2311_03906_b200.distributed import CountPipeline
+
+    smp = _FakeSampler(5)
+    seen = {}
+    pipe = CountPipeline(5, "cpu", world,
+                         on_reduced=lambda i, t: seen.__setitem__(i, t.clone().numpy()))
+    n_soak = [0]
+
+    def soak():
+        time.sleep(0.01 * (1 + 3 * rank))
+        n_soak[0] += 1
+
+    def step(i, last=False):
+        pipe.step(i, lambda c: smp.sample(100, 100 + i, shot_begin=100 * rank, counts=c), last=last)
+
+    t0 = time.perf_counter()
+    marks = []  # (mark, steps reduced so far): the timed window holds exactly the 4 timed steps
+    evs, wall = bench.step_protocol(step, soak, 3, 4, dist.barrier, lambda: None,
+                                    lambda: time.perf_counter() - t0, lambda fn: fn(),
+                                    on_timed=lambda k: marks.append((k, len(seen))))
+    assert marks == [(0, 3), (1, 7)], marks
+    q.put((rank, n_soak[0], len(evs), seen))
+    dist.destroy_process_group()
+
+
+def test_gloo_bench_step_protocol_ranks_agree():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_protocol_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    smp = _FakeSampler(5)
+    assert res[0][1] != res[1][1]  # different soak counts ...
+    for rank, _, n_ev, seen in res:  # ... same collectives: 3 warm-up + 4 timed steps
+        assert n_ev == 4 and sorted(seen) == list(range(7))
+        for i, got in seen.items():
+            want = sum(smp.counts_for(100 * r, 100, 100 + i) for r in range(world))
+            assert np.array_equal(got, want), (rank, i)
