@@ -135,7 +135,11 @@ struct sp_ctx {
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t ev_ready[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
   uint64_t launches = 0;
+  // texture view of the flip lists (the fused samplers fetch them through the
+  // texture pipe, which leaves the LSU data pipe to the tile's shared atomics)
+  cudaTextureObject_t plist_tex = 0;
   ~sp_ctx() {
+    if (plist_tex) cudaDestroyTextureObject(plist_tex);
     for (int b = 0; b < 2; ++b) {
       if (ev_ready[b]) cudaEventDestroy(ev_ready[b]);
       if (ev_free[b]) cudaEventDestroy(ev_free[b]);
@@ -1206,7 +1210,57 @@ void build_plan(sp_ctx* c) {
       std::vector<uint4> packed(bytes.size() / 16);
       std::memcpy(packed.data(), bytes.data(), bytes.size());
       d.plist = c->b_plist.upload(packed, s);
+      // texel = one list (4, 8 bytes) or a 16-byte piece of it
+      if (c->plist_tex) {
+        cudaDestroyTextureObject(c->plist_tex);
+        c->plist_tex = 0;
+      }
+      d.plist_tex = 0;
+      if (env_long("SP_LIST_TEX", 1) != 0) {
+        const uint32_t lb = d.lp * d.entry_bytes;  // bytes per list
+        const uint32_t tb = lb >= 16 ? 16 : lb;    // bytes per texel
+        cudaResourceDesc rd{};
+        rd.resType = cudaResourceTypeLinear;
+        rd.res.linear.devPtr = const_cast<uint4*>(d.plist);
+        rd.res.linear.sizeInBytes = packed.size() * 16;
+        rd.res.linear.desc = cudaCreateChannelDesc(32, tb >= 8 ? 32 : 0, tb >= 16 ? 32 : 0,
+                                                   tb >= 16 ? 32 : 0, cudaChannelFormatKindUnsigned);
+        cudaTextureDesc td{};
+        td.readMode = cudaReadModeElementType;
+        cudaDeviceProp prop{};
+        int dev = 0;
+        cudaGetDevice(&dev);
+        int max_lin = 0;
+        cudaDeviceGetAttribute(&max_lin, cudaDevAttrMaxTexture1DLinearWidth, dev);
+        if (tb >= 4 && packed.size() * 16 / tb <= static_cast<size_t>(max_lin) &&
+            cudaCreateTextureObject(&c->plist_tex, &rd, &td, nullptr) == cudaSuccess)
+          d.plist_tex = c->plist_tex;
+        else
+          cudaGetLastError();
+        (void)prop;
+      }
     }
+  }
+  {
+    // K7 (k7_queued.cuh) serves plans whose live classes are all one-list
+    // Bernoulli (mechanism) classes with exact flip lists of at most four
+    // words: a firing is then one u32, (list index << t_log2) | shot.
+    // SP_QUEUED=0 keeps K1; SP_Q_WALK / SP_Q_APPLY / SP_Q_DEPTH / SP_Q_THREADS set the shape.
+    bool ok = c->fused_ok && d.lp != 0 && d.lp * d.entry_bytes <= 16 && !live_cls.empty();
+    for (const Cls& cl : live_cls) ok = ok && cl.dist == SP_DIST_BERNOULLI;
+    ok = ok && ((static_cast<uint64_t>(pl_off.size()) + 1) << d.t_log2) < (1ull << 32);
+    d.q_threads = env_long("SP_Q_THREADS", 1024) == 768 ? 768 : 1024;
+    const long warps = d.q_threads / 32;
+    long qw = std::max<long>(1, env_long("SP_Q_WALK", warps / 4));
+    long qa = std::max<long>(1, env_long("SP_Q_APPLY", 2 * qw));
+    qa = std::max<long>(qw, qa / qw * qw);
+    if (qw + qa >= warps) ok = false;
+    long qd = env_long("SP_Q_DEPTH", 8);
+    while (qd & (qd - 1)) ++qd;
+    d.q_walk = static_cast<uint32_t>(qw);
+    d.q_apply = static_cast<uint32_t>(qa);
+    d.q_depth = static_cast<uint32_t>(std::max<long>(2, qd));
+    d.queued = ok && env_long("SP_QUEUED", 0) != 0;
   }
   ptm.mark("uploads");
   {

@@ -560,6 +560,15 @@ int launch_k1(const DevPlan& P, const LaunchCfg& L, const RoundKeys& K, uint64_t
               unsigned long long* cnt, unsigned long long* det_cnt);
 }  // namespace k1
 
+namespace k7 {
+// Defined in k7_queued.cuh, instantiated in k7_inst.cu. Returns 0 when the
+// plan does not fit the variant (the caller runs K1).
+template <int kThreads, bool kRowStaged, int kLp, int kEB>
+int launch_k7(const DevPlan& P, const LaunchCfg& L, const RoundKeys& K, uint64_t tile0,
+              uint32_t n_tiles, uint64_t n_shots, uint64_t* out, uint64_t ld, uint64_t tstride,
+              unsigned long long* cnt, unsigned long long* det_cnt);
+}  // namespace k7
+
 size_t fused_smem_bytes(const DevPlan& P, uint32_t t_log2, bool staged, bool row_staged,
                         uint32_t n_buf) {
   const size_t tw = size_t{1} << (t_log2 - 5);
@@ -594,6 +603,28 @@ int launch_fused_sample(const DevPlan& P, const LaunchCfg& L, uint64_t seed, uin
   const RoundKeys K = expand_keys(seed);
   auto* cnt = reinterpret_cast<unsigned long long*>(counts);
   auto* dcnt = reinterpret_cast<unsigned long long*>(det_counts);
+  if (P.queued) {  // K7: same records; falls through to K1 when the rings do not fit
+    int r = 0;
+#define SP_K7T(th, lp, eb)                                                                      \
+  (P.row_staged ? k7::launch_k7<th, true, lp, eb>(P, L, K, tile0, n_tiles, n_shots, out, ld,    \
+                                                  tstride, cnt, dcnt)                           \
+                : k7::launch_k7<th, false, lp, eb>(P, L, K, tile0, n_tiles, n_shots, out, ld,   \
+                                                   tstride, cnt, dcnt))
+#define SP_K7(lp, eb) (P.q_threads == 768 ? SP_K7T(768, lp, eb) : SP_K7T(1024, lp, eb))
+    const uint32_t key = P.lp * 8 + P.entry_bytes;
+    switch (key) {
+      case 4 * 8 + 1: r = SP_K7(4, 1); break;
+      case 8 * 8 + 1: r = SP_K7(8, 1); break;
+      case 16 * 8 + 1: r = SP_K7(16, 1); break;
+      case 4 * 8 + 2: r = SP_K7(4, 2); break;
+      case 8 * 8 + 2: r = SP_K7(8, 2); break;
+      case 4 * 8 + 4: r = SP_K7(4, 4); break;
+      default: r = 0;
+    }
+#undef SP_K7
+#undef SP_K7T
+    if (r != 0) return r;
+  }
 #define SP_K1(st, rs, lp, pp, eb) \
   k1::launch_k1<st, rs, lp, pp, eb>(P, L, K, tile0, n_tiles, n_shots, out, ld, tstride, cnt, dcnt)
 #define SP_K1R(lp, pp, eb) \

@@ -135,6 +135,9 @@ struct DevPlan {
   uint32_t plist_dummy = 0;  // index of an all-padding list (invalid slots load it)
   uint32_t entry_bytes = 4;  // 1: u8 row indices, 2: u16 / 4: u32 tile byte offsets
   const uint4* plist = nullptr;
+  // the same lists as a linear texture (texel = a list of 4 / 8 bytes, or a
+  // 16-byte piece of a longer one); 0 = none, load through plist
+  cudaTextureObject_t plist_tex = 0;
   const uint32_t* len_bnd = nullptr;  // length runs of the sorted Bernoulli classes (ClassInfo::bnd)
   uint32_t n_len_bnd = 0;
   const SegDesc* seg_desc = nullptr;  // [n_seg_live]
@@ -174,6 +177,12 @@ struct DevPlan {
   uint32_t cta_per_sm = 1;
   uint32_t cta_threads = 512;
   uint32_t n_buf = 2;        // shot-tile buffers in shared memory (1 or 2)
+  // K7 (k7_queued.cuh), the queued form of the fused sampler: walker warps
+  // push firings into shared-memory rings, apply warps XOR their flip lists
+  // (same streams and records as K1). queued = the plan is eligible and K7
+  // serves the launch; q_apply is a multiple of q_walk, q_depth a power of two.
+  uint32_t queued = 0;
+  uint32_t q_walk = 8, q_apply = 16, q_depth = 4, q_threads = 1024;
   // Drain stores finished tiles with TMA bulk copies (rows rebuilt in place,
   // then one copy per tile in the tiled layout or one per row segment of
   // >= 128 bytes in the measurement-major layout) instead of per-thread
