@@ -1255,11 +1255,12 @@ void build_plan(sp_ctx* c) {
     long qa = std::max<long>(1, env_long("SP_Q_APPLY", 2 * qw));
     qa = std::max<long>(qw, qa / qw * qw);
     if (qw + qa >= warps) ok = false;
-    long qd = env_long("SP_Q_DEPTH", 8);
-    while (qd & (qd - 1)) ++qd;
+    const long qd = std::min<long>(std::max<long>(env_long("SP_Q_DEPTH", 8), 2), 64);
+    uint32_t qdl = 1;
+    while ((1l << qdl) < qd) ++qdl;
     d.q_walk = static_cast<uint32_t>(qw);
     d.q_apply = static_cast<uint32_t>(qa);
-    d.q_depth = static_cast<uint32_t>(std::max<long>(2, qd));
+    d.q_depth_log2 = qdl;
     d.queued = ok && env_long("SP_QUEUED", 0) != 0;
   }
   ptm.mark("uploads");

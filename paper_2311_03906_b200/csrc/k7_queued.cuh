@@ -29,8 +29,9 @@ constexpr uint32_t kQEnd = 0xFFFFFFFFu;      // header of a tile-end batch
 
 // Shared-memory bytes of the rings: per walker warp `depth` slots of kQBatch
 // entries, a header word and a full/empty mbarrier pair per slot.
+constexpr uint32_t kQSlotBytes = kQBatch * 4 + 16;  // entries, then the header word (16-byte aligned)
 __host__ __device__ constexpr size_t k7_ring_bytes(uint32_t n_walk, uint32_t depth) {
-  return static_cast<size_t>(n_walk) * depth * (kQBatch * 4 + 16 + 16);
+  return static_cast<size_t>(n_walk) * depth * (kQSlotBytes + 16);
 }
 
 template <int kThreads, bool kRowStaged, int kLp, int kEB>
@@ -41,14 +42,12 @@ k7_queued(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, 
           unsigned long long* __restrict__ det_counts) {
   constexpr bool kStaged = false;
 #include "k1_prologue.inc"
-  // rings: data [walker][slot][128] u32, then headers (16 bytes per slot, word 0 used),
-  // then the slots' full / empty mbarriers
-  const uint32_t n_gen = P.q_walk, n_app = P.q_apply, depth = P.q_depth;
+  // rings: slots [walker][slot] of 128 entries + a header word, then the
+  // slots' full / empty mbarriers
+  const uint32_t n_gen = P.q_walk, n_app = P.q_apply, dlog = P.q_depth_log2, depth = 1u << dlog;
   p = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 15) & ~uintptr_t{15});
-  uint32_t* ring = reinterpret_cast<uint32_t*>(p);
-  p += static_cast<size_t>(n_gen) * depth * kQBatch * 4;
-  uint32_t* ring_hdr = reinterpret_cast<uint32_t*>(p);
-  p += static_cast<size_t>(n_gen) * depth * 16;
+  uint8_t* ring = p;
+  p += static_cast<size_t>(n_gen) * depth * kQSlotBytes;
   uint64_t* ring_full = reinterpret_cast<uint64_t*>(p);
   uint64_t* ring_empty = ring_full + n_gen * depth;
   p += static_cast<size_t>(n_gen) * depth * 16;
@@ -86,22 +85,23 @@ k7_queued(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, 
     // the ring depth, across tile boundaries. Slice s of the CTA's i-th tile
     // is walked by walker (s + i) mod n_gen (the slices are the streams, so
     // who walks them does not change the records).
-    uint32_t* my_ring = ring + warp * depth * kQBatch;
-    const uint32_t ring_s = static_cast<uint32_t>(__cvta_generic_to_shared(my_ring));
-    uint32_t* my_hdr = ring_hdr + warp * depth * 4;
+    const uint32_t ring_s =
+        static_cast<uint32_t>(__cvta_generic_to_shared(ring + warp * depth * kQSlotBytes));
     uint64_t* my_full = ring_full + warp * depth;
     uint64_t* my_empty = ring_empty + warp * depth;
+    const uint32_t segd_s = static_cast<uint32_t>(__cvta_generic_to_shared(SEGD));
     uint32_t bno = 0;  // batches pushed so far (all tiles)
     // claim the slot of batch bno (wait until its previous batch was read)
     auto claim = [&]() {
       const uint32_t slot = bno & dmask;
-      if (bno >= depth) mbar_wait(my_empty + slot, ((bno / depth) - 1) & 1, 32);
+      if (bno >= depth) mbar_wait(my_empty + slot, ((bno >> dlog) - 1) & 1, 32);
       return slot;
     };
     auto publish = [&](uint32_t slot, uint32_t hdr) {
       __syncwarp();
       if (lane == 0) {
-        my_hdr[slot * 4] = hdr;
+        asm volatile("st.shared.u32 [%0], %1;" ::"r"(ring_s + slot * kQSlotBytes + kQBatch * 4), "r"(hdr)
+                     : "memory");
         mbar_arrive(my_full + slot);
       }
       ++bno;
@@ -112,21 +112,24 @@ k7_queued(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, 
       Segment sg;
       auto fetch = [&](Segment& sn) {
         if (seg >= P.n_seg_live || (P.debug_mode & 2u)) return false;
-        if (P.seg_staged) {
-          const SegDesc& e = SEGD[seg];
-          sn.g0 = e.g0;
-          sn.s0 = e.s0;
-          sn.len = e.len;
-          sn.seg = seg;
-          sn.pbase = e.pbase;
-          sn.lp = e.meta >> 16;
-          sn.bnd = e.bnd;
-          sn.nbp = e.nbp;
-          sn.clg = e.clg;
-        } else {
-          segment_init(sn, CLS, P.n_cls_live, seg, P.t_log2);
-          segment_runs(sn, LENB);
-        }
+        // the slice descriptors are staged in shared memory (launch_k7 requires it)
+        uint4 a, b2;
+        uint32_t clg;
+        const uint32_t sa = segd_s + seg * static_cast<uint32_t>(sizeof(SegDesc));
+        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w) : "r"(sa));
+        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(b2.x), "=r"(b2.y), "=r"(b2.z), "=r"(b2.w) : "r"(sa + 16));
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(clg) : "r"(sa + 32));
+        sn.g0 = a.x;
+        sn.s0 = a.y;
+        sn.len = a.z;
+        sn.seg = seg;
+        sn.pbase = b2.x;
+        sn.lp = b2.y >> 16;
+        sn.bnd = b2.z;
+        sn.nbp = b2.w;
+        sn.clg = __uint_as_float(clg);
         seg += n_gen;
         return true;
       };
@@ -179,7 +182,7 @@ k7_queued(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, 
           if (n_valid && !(P.debug_mode & 1u)) {
             const uint32_t slot = claim();
             asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(
-                             ring_s + ((slot * kQBatch + 4 * lane) << 2)),
+                             ring_s + slot * kQSlotBytes + (lane << 4)),
                          "r"(ebase + t0), "r"(ebase + t1), "r"(ebase + t2), "r"(ebase + t3)
                          : "memory");
             publish(slot, n_valid | (lpu << 8));
@@ -202,15 +205,13 @@ k7_queued(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, 
     const uint32_t aw = warp - n_gen;
     const uint32_t src = aw / per, sub = aw - src * per;
     const uint32_t ring_s =
-        static_cast<uint32_t>(__cvta_generic_to_shared(ring + src * depth * kQBatch));
-    const uint32_t* my_hdr = ring_hdr + src * depth * 4;
+        static_cast<uint32_t>(__cvta_generic_to_shared(ring + src * depth * kQSlotBytes));
     uint64_t* my_full = ring_full + src * depth;
     uint64_t* my_empty = ring_empty + src * depth;
     constexpr int kWords = kLp * kEB / 4;  // u32 words per list (<= 4)
     static_assert(kWords >= 1 && kWords <= 4, "K7 keeps a lane's four lists in registers");
     const uint32_t tmask = (1u << P.t_log2) - 1u;
     const uint32_t row_b = tw * 4u;
-    const uint32_t* PL = reinterpret_cast<const uint32_t*>(P.plist);
     const uint32_t coin_tid = threadIdx.x - n_gen * 32, coin_stride = n_app * 32;
     uint32_t cb = sub;  // this warp's next batch of its walker
     for (uint32_t i = 0; i < n_my; ++i) {
@@ -222,14 +223,15 @@ k7_queued(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, 
 #include "k1_coins.inc"
       for (;;) {
         const uint32_t slot = cb & dmask;
-        mbar_wait(my_full + slot, (cb / depth) & 1, 32);
-        const uint32_t hdr = my_hdr[slot * 4];
-        uint4 e = make_uint4(0, 0, 0, 0);
-        if (hdr != kQEnd)
-          asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                       : "=r"(e.x), "=r"(e.y), "=r"(e.z), "=r"(e.w)
-                       : "r"(ring_s + ((slot * kQBatch + 4 * lane) << 2))
-                       : "memory");
+        mbar_wait(my_full + slot, (cb >> dlog) & 1, 32);
+        uint32_t hdr;
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(hdr) : "r"(ring_s + slot * kQSlotBytes + kQBatch * 4)
+                     : "memory");
+        uint4 e;  // (an end batch's entries are stale and unused)
+        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(e.x), "=r"(e.y), "=r"(e.z), "=r"(e.w)
+                     : "r"(ring_s + slot * kQSlotBytes + (lane << 4))
+                     : "memory");
         __syncwarp();
         if (lane == 0) mbar_arrive(my_empty + slot);  // the slot can be refilled
         cb += per;
@@ -237,49 +239,23 @@ k7_queued(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, 
         const uint32_t n_valid = hdr & 0xFFu, lpu = hdr >> 8;
         const uint32_t ent[4] = {e.x, e.y, e.z, e.w};
         uint32_t lst[4][kWords];
-        // 8 bytes of a 16-byte list are enough while the run's lists are short
-        const bool half = kWords == 4 && lpu * kEB <= 8;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           const bool ok = 4 * lane + k < n_valid;
           const uint32_t li = ok ? ent[k] >> P.t_log2 : P.plist_dummy;
-          const uint32_t* s = PL + static_cast<size_t>(li) * kWords;
-          if (P.plist_tex) {  // texture pipe: keeps these scattered loads off the LSU data pipe
-            if constexpr (kWords == 1) {
-              lst[k][0] = tex1Dfetch<unsigned int>(P.plist_tex, static_cast<int>(li));
-            } else if constexpr (kWords == 2) {
-              const uint2 v = tex1Dfetch<uint2>(P.plist_tex, static_cast<int>(li));
-              lst[k][0] = v.x;
-              lst[k][1] = v.y;
-            } else {
-              const uint4 v = tex1Dfetch<uint4>(P.plist_tex, static_cast<int>(li));
-              lst[k][0] = v.x;
-              lst[k][1] = v.y;
-              lst[k][2] = v.z;
-              lst[k][3] = v.w;
-            }
-            continue;
-          }
+          // texture pipe: keeps these scattered loads off the LSU data pipe
           if constexpr (kWords == 1) {
-            lst[k][0] = __ldg(s);
+            lst[k][0] = tex1Dfetch<unsigned int>(P.plist_tex, static_cast<int>(li));
           } else if constexpr (kWords == 2) {
-            const uint2 v = __ldg(reinterpret_cast<const uint2*>(s));
+            const uint2 v = tex1Dfetch<uint2>(P.plist_tex, static_cast<int>(li));
             lst[k][0] = v.x;
             lst[k][1] = v.y;
           } else {
-            if (half) {
-              const uint2 v = __ldg(reinterpret_cast<const uint2*>(s));
-              lst[k][0] = v.x;
-              lst[k][1] = v.y;
-              lst[k][2] = 0;
-              lst[k][3] = 0;
-            } else {
-              const uint4 v = __ldg(reinterpret_cast<const uint4*>(s));
-              lst[k][0] = v.x;
-              lst[k][1] = v.y;
-              lst[k][2] = v.z;
-              lst[k][3] = v.w;
-            }
+            const uint4 v = tex1Dfetch<uint4>(P.plist_tex, static_cast<int>(li));
+            lst[k][0] = v.x;
+            lst[k][1] = v.y;
+            lst[k][2] = v.z;
+            lst[k][3] = v.w;
           }
         }
 #pragma unroll
@@ -328,16 +304,16 @@ int launch_k7(const DevPlan& P, const LaunchCfg& L, const RoundKeys& K, uint64_t
               unsigned long long* cnt, unsigned long long* det_cnt) {
   auto kern = k7_queued<kThreads, kRowStaged, kLp, kEB>;
   size_t smem = fused_smem_bytes(P, P.t_log2, false, kRowStaged, P.n_buf) + 16 +
-                k7_ring_bytes(P.q_walk, P.q_depth);
+                k7_ring_bytes(P.q_walk, 1u << P.q_depth_log2);
   if (smem > L.smem_optin) return 0;
   DevPlan Q = P;
   const size_t cls_bytes = align16(sizeof(ClassInfo) * P.n_cls_live);
   Q.cls_staged = smem + cls_bytes <= L.smem_optin;
   if (Q.cls_staged) smem += cls_bytes;
   const size_t seg_bytes = align16(sizeof(SegDesc) * P.n_seg_live) + align16(4ull * P.n_len_bnd);
-  Q.seg_staged = P.seg_stage_ok && P.seg_desc != nullptr && P.n_seg_live > 0 &&
-                 smem + seg_bytes <= L.smem_optin;
-  if (Q.seg_staged) smem += seg_bytes;
+  Q.seg_staged = P.seg_desc != nullptr && P.n_seg_live > 0 && smem + seg_bytes <= L.smem_optin;
+  if (!Q.seg_staged || !P.plist_tex) return 0;  // the walkers read the slices from shared memory
+  smem += seg_bytes;
   int grid = 0;
   if (persistent_grid(kern, L, smem, n_tiles, 1, &grid, kThreads)) return -1;
   const bool vec = (ld % 2 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0);

@@ -180,9 +180,9 @@ struct DevPlan {
   // K7 (k7_queued.cuh), the queued form of the fused sampler: walker warps
   // push firings into shared-memory rings, apply warps XOR their flip lists
   // (same streams and records as K1). queued = the plan is eligible and K7
-  // serves the launch; q_apply is a multiple of q_walk, q_depth a power of two.
+  // serves the launch; q_apply is a multiple of q_walk; a ring holds 2^q_depth_log2 batches.
   uint32_t queued = 0;
-  uint32_t q_walk = 8, q_apply = 16, q_depth = 4, q_threads = 1024;
+  uint32_t q_walk = 8, q_apply = 16, q_depth_log2 = 2, q_threads = 1024;
   // Drain stores finished tiles with TMA bulk copies (rows rebuilt in place,
   // then one copy per tile in the tiled layout or one per row segment of
   // >= 128 bytes in the measurement-major layout) instead of per-thread
