@@ -245,8 +245,9 @@ int sp_debug_philox(sp_ctx* ctx, const uint32_t* ctr_key, uint32_t* out);
 /* Launch shape and table sizes of the loaded model's fused-sampler plan:
  * {T, gen_warps, cta_threads, staged, row_staged, lp, pad_pred, n_paths,
  *  n_rounds, n_keep, n_segments, n_classes, n_dense, nnz(D), smem_bytes, sampler}
- * with sampler 1 = fused K1, 2 = K5 column sampler (dense M_sym), 0 = draw S
- * + explicit product. */
+ * with sampler 1 = fused K1, 3 = its queued form K7 (same records; gen_warps /
+ * cta_threads are then K7's walker warps / threads), 2 = K5 column sampler
+ * (dense M_sym), 0 = draw S + explicit product. */
 int sp_plan_info(sp_ctx* ctx, uint64_t* out16);
 
 /* Profiling hook: per-role cycle counters of the fused kernel (gen wait,

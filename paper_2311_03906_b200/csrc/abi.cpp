@@ -1251,17 +1251,21 @@ void build_plan(sp_ctx* c) {
     ok = ok && ((static_cast<uint64_t>(pl_off.size()) + 1) << d.t_log2) < (1ull << 32);
     d.q_threads = env_long("SP_Q_THREADS", 1024) == 768 ? 768 : 1024;
     const long warps = d.q_threads / 32;
-    long qw = std::max<long>(1, env_long("SP_Q_WALK", warps / 4));
-    long qa = std::max<long>(1, env_long("SP_Q_APPLY", 2 * qw));
+    long qw = std::max<long>(1, env_long("SP_Q_WALK", 8));
+    long qa = std::max<long>(1, env_long("SP_Q_APPLY", qw));
     qa = std::max<long>(qw, qa / qw * qw);
     if (qw + qa >= warps) ok = false;
-    const long qd = std::min<long>(std::max<long>(env_long("SP_Q_DEPTH", 8), 2), 64);
+    const long qd = std::min<long>(std::max<long>(env_long("SP_Q_DEPTH", 4), 2), 64);
     uint32_t qdl = 1;
     while ((1l << qdl) < qd) ++qdl;
     d.q_walk = static_cast<uint32_t>(qw);
     d.q_apply = static_cast<uint32_t>(qa);
     d.q_depth_log2 = qdl;
-    d.queued = ok && env_long("SP_QUEUED", 0) != 0;
+    d.q_drain_teams = env_long("SP_Q_TEAMS", 2) == 1 ? 1u : 2u;
+    // SP_QUEUED: 1 = K7 whenever eligible, 0 = never, unset = the launch
+    // autotune times it against K1 and keeps the faster
+    d.queued_ok = ok && d.plist_tex != 0 && env_long("SP_QUEUED", -1) != 0;
+    d.queued = d.queued_ok && env_long("SP_QUEUED", -1) == 1;
   }
   ptm.mark("uploads");
   {
@@ -1291,6 +1295,7 @@ void build_plan(sp_ctx* c) {
   d.debug_mode = static_cast<uint32_t>(env_long("SP_DEBUG_MODE", 0));
   d.wait_ns = static_cast<uint32_t>(std::max<long>(32, env_long("SP_WAIT_NS", 256)));
   d.bulk_store = static_cast<uint32_t>(env_long("SP_BULK", 1));
+  d.drain_teams = env_long("SP_DRAIN_TEAMS", 1) == 2 && d.n_buf >= 2 ? 2u : 1u;
   d.seg_stage_ok = static_cast<uint32_t>(env_long("SP_SEG_STAGE", 1));
   if (env_long("SP_TMA_ZERO", 1) != 0) {
     const size_t zb = static_cast<size_t>(n_meas) * d.tw * 4;
@@ -1319,7 +1324,8 @@ void build_plan(sp_ctx* c) {
        0x100000001b3ull) ^
       (d.lp | static_cast<uint64_t>(d.entry_bytes) << 8 | static_cast<uint64_t>(d.cta_threads) << 16);
   static std::mutex tune_mu;
-  static std::map<uint64_t, std::pair<uint32_t, uint32_t>> tune_cache;  // fp -> (gen_warps, pad_pred)
+  // fp -> (gen_warps, pad_pred | unfused << 1 | queued << 2 | q_walk << 8 | q_apply << 16)
+  static std::map<uint64_t, std::pair<uint32_t, uint32_t>> tune_cache;
   bool cached = false;
   if (!fix_gw || !fix_pp) {
     std::lock_guard<std::mutex> lk(tune_mu);
@@ -1328,6 +1334,13 @@ void build_plan(sp_ctx* c) {
       if (!fix_gw) d.gen_warps = it->second.first;
       if (!fix_pp) d.pad_pred = it->second.second & 1u;
       c->unfused = (it->second.second & 2u) != 0;
+      if (d.queued_ok && env_long("SP_QUEUED", -1) < 0) {
+        d.queued = (it->second.second >> 2) & 1u;
+        if (d.queued) {
+          d.q_walk = (it->second.second >> 8) & 0xFFu;
+          d.q_apply = (it->second.second >> 16) & 0xFFu;
+        }
+      }
       cached = true;
     }
   }
@@ -1407,6 +1420,25 @@ void build_plan(sp_ctx* c) {
         d.gen_warps = cand[bi].first;
         d.pad_pred = cand[bi].second;
       }
+      // K7 (queued) against the tuned K1: same records, so the faster one
+      // serves the launches. Two shapes: 8 + 8 warps and 12 + 12 (the rest drain).
+      if (d.queued_ok && env_long("SP_QUEUED", -1) < 0) {
+        const bool fix_shape = std::getenv("SP_Q_WALK") != nullptr;
+        const float t_k1 = time_launch();
+        std::vector<std::pair<uint32_t, uint32_t>> shapes{{d.q_walk, d.q_apply}};
+        if (!fix_shape) shapes.emplace_back(12u, 12u);
+        float t_best = t_k1 * 0.98f;  // K7 must win by 2 %
+        uint32_t bw = 0, ba = 0;
+        d.queued = 1;
+        for (auto [w, a2] : shapes) {
+          d.q_walk = w;
+          d.q_apply = a2;
+          const float t = time_launch();
+          if (t < t_best) { t_best = t; bw = w; ba = a2; }
+        }
+        d.queued = bw != 0;
+        if (bw) { d.q_walk = bw; d.q_apply = ba; } else { d.q_walk = shapes[0].first; d.q_apply = shapes[0].second; }
+      }
       // Fused vs unfused (device draw of S + explicit-S product): the same
       // bits for an unmerged model (K1 == M_sym . S of its own draw), so the
       // faster one serves sp_sample. Unfused wins when firings x list
@@ -1450,7 +1482,8 @@ void build_plan(sp_ctx* c) {
     if (d.timers) d.timers = c->b_timers.upload(std::vector<long long>(8, 0), s);
     ck(cudaStreamSynchronize(s), "plan upload");
     std::lock_guard<std::mutex> lk(tune_mu);
-    tune_cache[fp] = {d.gen_warps, d.pad_pred | (c->unfused ? 2u : 0u)};
+    tune_cache[fp] = {d.gen_warps, d.pad_pred | (c->unfused ? 2u : 0u) | (d.queued ? 4u : 0u) |
+                                       (d.q_walk << 8) | (d.q_apply << 16)};
   }
   ptm.mark("autotune");
   build_k5(c, col_ptr, col_rows, ones, events_per_shot, flips_per_shot, n_dense_live);
@@ -2158,17 +2191,19 @@ int sp_synchronize(sp_ctx* ctx) {
 
 // Launch shape and table sizes of the fused sampler's plan (for reports):
 // {T, gen_warps, cta_threads, staged, row_staged, lp, pad_pred, n_paths,
-//  n_rounds, n_keep, n_seg_live, n_cls_live, n_dense_live, nnz(D), smem bytes, fused_ok}
+//  n_rounds, n_keep, n_seg_live, n_cls_live, n_dense_live, nnz(D), smem bytes,
+//  sampler: 0 draw + product, 1 K1, 2 K5, 3 K7 (then gen_warps / cta_threads are K7's walkers / threads)}
 int sp_plan_info(sp_ctx* ctx, uint64_t* out16) {
   if (!ctx || !out16) return fail(SP_ERR_INVALID_ARGUMENT, "null argument");
   if (int r = set_device(ctx)) return r;
   if (int r = ensure_plan(ctx)) return r;
   const DevPlan& d = ctx->dp;
-  const uint64_t v[16] = {1ull << d.t_log2, d.gen_warps, d.cta_threads, d.staged, d.row_staged,
+  const bool k7 = ctx->fused_ok && !ctx->k5_ok && d.queued;  // K7 serves the fused launches
+  const uint64_t v[16] = {1ull << d.t_log2, k7 ? d.q_walk : d.gen_warps, k7 ? d.q_threads : d.cta_threads, d.staged, d.row_staged,
                           d.lp, d.pad_pred, d.n_paths, d.n_rounds, d.n_keep, d.n_seg_live,
                           d.n_cls_live, d.n_dense_live, ctx->dnnz,
                           fused_smem_bytes(d, d.t_log2, d.staged, d.row_staged, d.n_buf),
-                          ctx->k5_ok ? 2u : ctx->fused_ok ? 1u : 0u};
+                          ctx->k5_ok ? 2u : k7 ? 3u : ctx->fused_ok ? 1u : 0u};
   std::memcpy(out16, v, sizeof(v));
   return SP_OK;
 }

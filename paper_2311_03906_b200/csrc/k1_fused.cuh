@@ -48,7 +48,7 @@ k1_fused(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, u
       segctr[threadIdx.x] = 0;
       mbar_init(mbar_full + threadIdx.x, P.gen_warps * 32);
       // TMA drain: one elected arrival + the zero-fill copy's bytes
-      mbar_init(mbar_empty + threadIdx.x, tma_zero ? 1u : blockDim.x - P.gen_warps * 32);
+      mbar_init(mbar_empty + threadIdx.x, tma_zero ? 1u : (blockDim.x - P.gen_warps * 32) / P.drain_teams);
     }
   }
   __syncthreads();
@@ -279,6 +279,8 @@ int launch_k1(const DevPlan& P, const LaunchCfg& L, const RoundKeys& K, uint64_t
   auto kern = k1_fused<kStaged, kRowStaged, kLp, kPadPred, kEB>;
   size_t smem = fused_smem_bytes(P, P.t_log2, kStaged, kRowStaged, P.n_buf);
   DevPlan Q = P;
+  // drain teams need whole warps each
+  if ((P.cta_threads / 32 - P.gen_warps) % P.drain_teams != 0) Q.drain_teams = 1;
   const size_t cls_bytes = align16(sizeof(ClassInfo) * P.n_cls_live);
   Q.cls_staged = !kStaged && smem + cls_bytes <= L.smem_optin;
   if (Q.cls_staged) smem += cls_bytes;

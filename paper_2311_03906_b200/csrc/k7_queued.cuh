@@ -63,7 +63,7 @@ k7_queued(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, 
       segctr[threadIdx.x] = 0;
       // a tile is complete when every apply thread (coin words, flip lists) is done with it
       mbar_init(mbar_full + threadIdx.x, n_app * 32);
-      mbar_init(mbar_empty + threadIdx.x, tma_zero ? 1u : blockDim.x - (n_gen + n_app) * 32);
+      mbar_init(mbar_empty + threadIdx.x, tma_zero ? 1u : (blockDim.x - (n_gen + n_app) * 32) / P.drain_teams);
     }
     for (uint32_t i = threadIdx.x; i < n_gen * depth; i += blockDim.x) {
       mbar_init(ring_full + i, 1);   // the walker's elected lane
@@ -307,6 +307,8 @@ int launch_k7(const DevPlan& P, const LaunchCfg& L, const RoundKeys& K, uint64_t
                 k7_ring_bytes(P.q_walk, 1u << P.q_depth_log2);
   if (smem > L.smem_optin) return 0;
   DevPlan Q = P;
+  Q.drain_teams = (kThreads / 32 - P.q_walk - P.q_apply) % P.q_drain_teams == 0 && P.n_buf >= 2
+                      ? P.q_drain_teams : 1;
   const size_t cls_bytes = align16(sizeof(ClassInfo) * P.n_cls_live);
   Q.cls_staged = smem + cls_bytes <= L.smem_optin;
   if (Q.cls_staged) smem += cls_bytes;

@@ -177,12 +177,15 @@ struct DevPlan {
   uint32_t cta_per_sm = 1;
   uint32_t cta_threads = 512;
   uint32_t n_buf = 2;        // shot-tile buffers in shared memory (1 or 2)
+  uint32_t drain_teams = 1;  // drain warps split into teams that take alternate tiles (1 or 2)
   // K7 (k7_queued.cuh), the queued form of the fused sampler: walker warps
   // push firings into shared-memory rings, apply warps XOR their flip lists
   // (same streams and records as K1). queued = the plan is eligible and K7
   // serves the launch; q_apply is a multiple of q_walk; a ring holds 2^q_depth_log2 batches.
   uint32_t queued = 0;
-  uint32_t q_walk = 8, q_apply = 16, q_depth_log2 = 2, q_threads = 1024;
+  uint32_t queued_ok = 0;  // the plan is eligible for K7 (the launch autotune decides)
+  uint32_t q_walk = 8, q_apply = 8, q_depth_log2 = 2, q_threads = 1024;
+  uint32_t q_drain_teams = 2;  // K7 has warps to spare for two drain teams
   // Drain stores finished tiles with TMA bulk copies (rows rebuilt in place,
   // then one copy per tile in the tiled layout or one per row segment of
   // >= 128 bytes in the measurement-major layout) instead of per-thread
