@@ -389,7 +389,7 @@ def run_ours(args):
     # bytes per row per tile, scattered across measurement-major rows), like
     # the reference's own 512 x 512 tiles; measurement-major otherwise
     tiled = args.layout == "tiled" or (
-        args.layout == "auto" and T < 1024 and smp.plan_info()["fused_ok"] in (1, 3))
+        args.layout == "auto" and T < 1024 and smp.plan_info()["fused_ok"] in (1, 3, 4, 5))
     if tiled:  # [tile][row][T/64] records: contiguous stores for any row count
         out = torch.empty(smp.tiled_words(shots), dtype=torch.int64, device=dev)
     else:
@@ -499,7 +499,12 @@ def run_ours(args):
         nbytes, ops = algorithmic(init, shots)
         t_hbm, t_int = nbytes / (peak * 1e9), ops / R_INT
         fo = smp.plan_info()["fused_ok"]
-        kernel = {1: "k1_fused", 2: "k5_columns", 3: "k7_queued"}.get(fo, "d_segments + k2 product")
+        # the roofline kernel is the uncounted launch; the step's launch counts detectors
+        # (cfg2/cfg3) or measurements: the autotune picks K1 or K7 per mode (plan_info)
+        kernel = {1: "k1_fused", 2: "k5_columns", 3: "k7_queued", 4: "k1_fused",
+                  5: "k7_queued"}.get(fo, "d_segments + k2 product")
+        step_kernel = {1: "k1_fused", 2: "k5_columns", 3: "k7_queued", 4: "k7_queued",
+                       5: "k1_fused"}.get(fo, "d_segments + k2 product")
         int_bound = t_int > t_hbm
         # achieved = algorithmic bytes (HBM-bound) or LOP3 ops (INT-bound) per
         # second of the kernel's CUDA-event time, against the measured peak
@@ -533,6 +538,7 @@ def run_ours(args):
                 "l2": "flushed between timed steps (256 MiB memset outside the events); "
                       "output per step > L2",
                 "init_seconds": round(init_s, 4),
+                "step_kernel": step_kernel,
             },
             "roofline": {
                 "bound": "int" if int_bound else "hbm", "achieved": achieved,

@@ -246,8 +246,10 @@ int sp_debug_philox(sp_ctx* ctx, const uint32_t* ctr_key, uint32_t* out);
  * {T, gen_warps, cta_threads, staged, row_staged, lp, pad_pred, n_paths,
  *  n_rounds, n_keep, n_segments, n_classes, n_dense, nnz(D), smem_bytes, sampler}
  * with sampler 1 = fused K1, 3 = its queued form K7 (same records; gen_warps /
- * cta_threads are then K7's walker warps / threads), 2 = K5 column sampler
- * (dense M_sym), 0 = draw S + explicit product. */
+ * cta_threads are then K7's walker warps / threads), 4 = K7 for launches that
+ * count detectors and K1 for the others, 5 = the reverse (the launch autotune
+ * decides per mode), 2 = K5 column sampler (dense M_sym), 0 = draw S +
+ * explicit product. */
 int sp_plan_info(sp_ctx* ctx, uint64_t* out16);
 
 /* Profiling hook: per-role cycle counters of the fused kernel (gen wait,

@@ -1266,6 +1266,9 @@ void build_plan(sp_ctx* c) {
     // autotune times it against K1 and keeps the faster
     d.queued_ok = ok && d.plist_tex != 0 && env_long("SP_QUEUED", -1) != 0;
     d.queued = d.queued_ok && env_long("SP_QUEUED", -1) == 1;
+    d.queued_dets = d.queued;
+    d.q_walk_dets = d.q_walk;
+    d.q_apply_dets = d.q_apply;
   }
   ptm.mark("uploads");
   {
@@ -1322,9 +1325,10 @@ void build_plan(sp_ctx* c) {
   const uint64_t fp =
       ((model_fingerprint(h) ^ (static_cast<uint64_t>(c->L.num_sms) << 32 | d.t_log2)) *
        0x100000001b3ull) ^
-      (d.lp | static_cast<uint64_t>(d.entry_bytes) << 8 | static_cast<uint64_t>(d.cta_threads) << 16);
+      (d.lp | static_cast<uint64_t>(d.entry_bytes) << 8 | static_cast<uint64_t>(d.cta_threads) << 16 |
+       static_cast<uint64_t>(d.n_det != 0) << 32);  // detector counting shifts the tuned split
   static std::mutex tune_mu;
-  // fp -> (gen_warps, pad_pred | unfused << 1 | queued << 2 | q_walk << 8 | q_apply << 16)
+  // fp -> (gen_warps, pad_pred | unfused << 1 | K7 without / with detector counts << 2, 3 | their 12 + 12 shapes << 8, 9)
   static std::map<uint64_t, std::pair<uint32_t, uint32_t>> tune_cache;
   bool cached = false;
   if (!fix_gw || !fix_pp) {
@@ -1335,11 +1339,11 @@ void build_plan(sp_ctx* c) {
       if (!fix_pp) d.pad_pred = it->second.second & 1u;
       c->unfused = (it->second.second & 2u) != 0;
       if (d.queued_ok && env_long("SP_QUEUED", -1) < 0) {
-        d.queued = (it->second.second >> 2) & 1u;
-        if (d.queued) {
-          d.q_walk = (it->second.second >> 8) & 0xFFu;
-          d.q_apply = (it->second.second >> 16) & 0xFFu;
-        }
+        const uint32_t v = it->second.second;
+        d.queued = (v >> 2) & 1u;
+        d.queued_dets = (v >> 3) & 1u;
+        d.q_walk = d.q_apply = ((v >> 8) & 1u) ? 12u : d.q_walk;
+        d.q_walk_dets = d.q_apply_dets = ((v >> 9) & 1u) ? 12u : d.q_walk_dets;
       }
       cached = true;
     }
@@ -1421,23 +1425,42 @@ void build_plan(sp_ctx* c) {
         d.pad_pred = cand[bi].second;
       }
       // K7 (queued) against the tuned K1: same records, so the faster one
-      // serves the launches. Two shapes: 8 + 8 warps and 12 + 12 (the rest drain).
+      // serves the launches. Two shapes: 8 + 8 warps and 12 + 12 (the rest
+      // drain). Decided separately for launches with and without detector
+      // counts (the drain's share differs).
       if (d.queued_ok && env_long("SP_QUEUED", -1) < 0) {
         const bool fix_shape = std::getenv("SP_Q_WALK") != nullptr;
-        const float t_k1 = time_launch();
         std::vector<std::pair<uint32_t, uint32_t>> shapes{{d.q_walk, d.q_apply}};
         if (!fix_shape) shapes.emplace_back(12u, 12u);
-        float t_best = t_k1 * 0.98f;  // K7 must win by 2 %
-        uint32_t bw = 0, ba = 0;
-        d.queued = 1;
-        for (auto [w, a2] : shapes) {
-          d.q_walk = w;
-          d.q_apply = a2;
-          const float t = time_launch();
-          if (t < t_best) { t_best = t; bw = w; ba = a2; }
+        auto pick = [&]() {  // -> index into shapes, or -1 for K1
+          d.queued = 0;
+          d.queued_dets = 0;
+          float t_best = time_launch() * 0.98f;  // K7 must win by 2 %
+          int best = -1;
+          d.queued = d.queued_dets = 1;
+          for (size_t i = 0; i < shapes.size(); ++i) {
+            d.q_walk = d.q_walk_dets = shapes[i].first;
+            d.q_apply = d.q_apply_dets = shapes[i].second;
+            const float t = time_launch();
+            if (t < t_best) { t_best = t; best = static_cast<int>(i); }
+          }
+          return best;
+        };
+        int b_dets = -1, b_plain = -1;
+        if (dcnt) b_dets = pick();
+        {
+          uint64_t* const saved = dcnt;
+          dcnt = nullptr;
+          b_plain = pick();
+          dcnt = saved;
         }
-        d.queued = bw != 0;
-        if (bw) { d.q_walk = bw; d.q_apply = ba; } else { d.q_walk = shapes[0].first; d.q_apply = shapes[0].second; }
+        if (!dcnt) b_dets = b_plain;
+        d.queued = b_plain >= 0;
+        d.queued_dets = b_dets >= 0;
+        d.q_walk = shapes[std::max(b_plain, 0)].first;
+        d.q_apply = shapes[std::max(b_plain, 0)].second;
+        d.q_walk_dets = shapes[std::max(b_dets, 0)].first;
+        d.q_apply_dets = shapes[std::max(b_dets, 0)].second;
       }
       // Fused vs unfused (device draw of S + explicit-S product): the same
       // bits for an unmerged model (K1 == M_sym . S of its own draw), so the
@@ -1483,7 +1506,8 @@ void build_plan(sp_ctx* c) {
     ck(cudaStreamSynchronize(s), "plan upload");
     std::lock_guard<std::mutex> lk(tune_mu);
     tune_cache[fp] = {d.gen_warps, d.pad_pred | (c->unfused ? 2u : 0u) | (d.queued ? 4u : 0u) |
-                                       (d.q_walk << 8) | (d.q_apply << 16)};
+                                       (d.queued_dets ? 8u : 0u) | (d.q_walk == 12 ? 256u : 0u) |
+                                       (d.q_walk_dets == 12 ? 512u : 0u)};
   }
   ptm.mark("autotune");
   build_k5(c, col_ptr, col_rows, ones, events_per_shot, flips_per_shot, n_dense_live);
@@ -2192,18 +2216,25 @@ int sp_synchronize(sp_ctx* ctx) {
 // Launch shape and table sizes of the fused sampler's plan (for reports):
 // {T, gen_warps, cta_threads, staged, row_staged, lp, pad_pred, n_paths,
 //  n_rounds, n_keep, n_seg_live, n_cls_live, n_dense_live, nnz(D), smem bytes,
-//  sampler: 0 draw + product, 1 K1, 2 K5, 3 K7 (then gen_warps / cta_threads are K7's walkers / threads)}
+//  sampler: 0 draw + product, 1 K1, 2 K5, 3 K7, 4 K7 for launches counting detectors and K1 for the
+//  others, 5 the reverse (gen_warps / cta_threads are K7's walkers / threads when it serves the
+//  launches of the registered mode)}
 int sp_plan_info(sp_ctx* ctx, uint64_t* out16) {
   if (!ctx || !out16) return fail(SP_ERR_INVALID_ARGUMENT, "null argument");
   if (int r = set_device(ctx)) return r;
   if (int r = ensure_plan(ctx)) return r;
   const DevPlan& d = ctx->dp;
-  const bool k7 = ctx->fused_ok && !ctx->k5_ok && d.queued;  // K7 serves the fused launches
-  const uint64_t v[16] = {1ull << d.t_log2, k7 ? d.q_walk : d.gen_warps, k7 ? d.q_threads : d.cta_threads, d.staged, d.row_staged,
+  // K7 serves the fused launches: 3 = all of them, 4 = only those counting
+  // detectors (sp_sample_ex), 5 = only the others; 1 = K1 serves all
+  const bool fz = ctx->fused_ok && !ctx->k5_ok;
+  const bool k7p = fz && d.queued, k7d = fz && d.queued_dets;
+  const bool k7 = d.n_det ? k7d : k7p;
+  const uint64_t sampler = ctx->k5_ok ? 2u : !ctx->fused_ok ? 0u : k7p && k7d ? 3u : k7d ? 4u : k7p ? 5u : 1u;
+  const uint64_t v[16] = {1ull << d.t_log2, k7 ? (d.n_det ? d.q_walk_dets : d.q_walk) : d.gen_warps, k7 ? d.q_threads : d.cta_threads, d.staged, d.row_staged,
                           d.lp, d.pad_pred, d.n_paths, d.n_rounds, d.n_keep, d.n_seg_live,
                           d.n_cls_live, d.n_dense_live, ctx->dnnz,
                           fused_smem_bytes(d, d.t_log2, d.staged, d.row_staged, d.n_buf),
-                          ctx->k5_ok ? 2u : k7 ? 3u : ctx->fused_ok ? 1u : 0u};
+                          sampler};
   std::memcpy(out16, v, sizeof(v));
   return SP_OK;
 }

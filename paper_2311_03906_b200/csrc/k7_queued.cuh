@@ -217,7 +217,10 @@ k7_queued(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, 
     for (uint32_t i = 0; i < n_my; ++i) {
       const uint32_t b = i % n_buf;
       const uint64_t gtile = tile0 + blockIdx.x + static_cast<uint64_t>(i) * gridDim.x;
+      const long long ta0 = clock64();
       if (i >= n_buf) mbar_wait(mbar_empty + b, ((i / n_buf) - 1) & 1, P.wait_ns);
+      if (P.timers && lane == 0)  // [0] apply warps waiting for an empty tile buffer
+        atomicAdd(reinterpret_cast<unsigned long long*>(P.timers) + 0, clock64() - ta0);
       const uint32_t tile_s =
           static_cast<uint32_t>(__cvta_generic_to_shared(tiles + b * tile_words));
 #include "k1_coins.inc"
@@ -285,6 +288,8 @@ k7_queued(const DevPlan P, const RoundKeys K, uint64_t tile0, uint32_t n_tiles, 
       // tile end: this warp's XORs are done
       if (bulk) fence_proxy_async_smem();
       mbar_arrive(mbar_full + b);
+      if (P.timers && lane == 0)  // [1] apply warps: whole tile, wait included
+        atomicAdd(reinterpret_cast<unsigned long long*>(P.timers) + 1, clock64() - ta0);
     }
   } else {
     // ---------------- drain warps ----------------

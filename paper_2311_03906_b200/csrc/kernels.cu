@@ -603,12 +603,17 @@ int launch_fused_sample(const DevPlan& P, const LaunchCfg& L, uint64_t seed, uin
   const RoundKeys K = expand_keys(seed);
   auto* cnt = reinterpret_cast<unsigned long long*>(counts);
   auto* dcnt = reinterpret_cast<unsigned long long*>(det_counts);
-  if (P.queued) {  // K7: same records; falls through to K1 when the rings do not fit
+  if (dcnt ? P.queued_dets : P.queued) {  // K7: same records; falls through to K1 when the rings do not fit
     int r = 0;
+    DevPlan PQ = P;
+    if (dcnt) {
+      PQ.q_walk = P.q_walk_dets;
+      PQ.q_apply = P.q_apply_dets;
+    }
 #define SP_K7T(th, lp, eb)                                                                      \
-  (P.row_staged ? k7::launch_k7<th, true, lp, eb>(P, L, K, tile0, n_tiles, n_shots, out, ld,    \
+  (P.row_staged ? k7::launch_k7<th, true, lp, eb>(PQ, L, K, tile0, n_tiles, n_shots, out, ld,   \
                                                   tstride, cnt, dcnt)                           \
-                : k7::launch_k7<th, false, lp, eb>(P, L, K, tile0, n_tiles, n_shots, out, ld,   \
+                : k7::launch_k7<th, false, lp, eb>(PQ, L, K, tile0, n_tiles, n_shots, out, ld,  \
                                                    tstride, cnt, dcnt))
 #define SP_K7(lp, eb) (P.q_threads == 768 ? SP_K7T(768, lp, eb) : SP_K7T(1024, lp, eb))
     const uint32_t key = P.lp * 8 + P.entry_bytes;

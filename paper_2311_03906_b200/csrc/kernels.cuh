@@ -183,6 +183,8 @@ struct DevPlan {
   // (same streams and records as K1). queued = the plan is eligible and K7
   // serves the launch; q_apply is a multiple of q_walk; a ring holds 2^q_depth_log2 batches.
   uint32_t queued = 0;
+  // the same choice and shape for launches that count detectors (sp_sample_ex)
+  uint32_t queued_dets = 0, q_walk_dets = 8, q_apply_dets = 8;
   uint32_t queued_ok = 0;  // the plan is eligible for K7 (the launch autotune decides)
   uint32_t q_walk = 8, q_apply = 8, q_depth_log2 = 2, q_threads = 1024;
   uint32_t q_drain_teams = 2;  // K7 has warps to spare for two drain teams

@@ -81,7 +81,7 @@ def test_cfg3_fused_equals_product_of_its_draws(gpu_sampler_factory, port, tiled
     init = init_of("cfg3")
     s = gpu_sampler_factory(init)
     info = s.plan_info()
-    assert info["fused_ok"] in (1, 3), info  # the fused sampler the bench runs (K1 or its queued form K7)
+    assert info["fused_ok"] in (1, 3, 4, 5), info  # the fused sampler the bench runs (K1 or its queued form K7)
     T = s.shot_tile
     for n, seed in ((4 * T + 37, 3), (16 * T, 11), (1, 5)):
         ok, S, want = _product_identity(s, n, seed, tiled)
