@@ -21,7 +21,8 @@ def _pair(init, monkeypatch, **env):
     return k1, k7
 
 
-@pytest.mark.parametrize("cfg,shots", [("cfg1", 100_003), ("cfg2", 300_001), ("cfg3", 40_000)])
+@pytest.mark.parametrize("cfg,shots", [("cfg1", 100_003), ("cfg2", 300_001), ("cfg3", 40_000),
+                                       ("cfg4", 30_001)])
 @pytest.mark.parametrize("tiled", [False, True])
 def test_queued_equals_fused(cfg, shots, tiled, monkeypatch):
     init = run_initialization(circuits.CONFIGS[cfg]["text"]())
@@ -67,3 +68,21 @@ def test_queued_falls_back_when_not_eligible(monkeypatch):
     a = k1.sample(50_000, 3)
     b = k7.sample(50_000, 3)
     assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("cfg,shots", [("cfg2", 200_000), ("cfg3", 20_000)])
+@pytest.mark.parametrize("queued", ["0", "1"])
+def test_texture_list_fetch_equals_global_loads(cfg, shots, queued, monkeypatch):
+    """The flip lists read through the texture pipe (default) or with
+    ld.global.nc (SP_LIST_TEX=0; K7 then falls back to K1) give the same records."""
+    init = run_initialization(circuits.CONFIGS[cfg]["text"]())
+    monkeypatch.setenv("SP_QUEUED", queued)
+    outs = []
+    for tex in ("1", "0"):
+        monkeypatch.setenv("SP_LIST_TEX", tex)
+        s = Sampler(init)
+        out = torch.zeros(s.tiled_words(shots), dtype=torch.int64, device="cuda")
+        s.sample_tiled(shots, 21, out=out)
+        outs.append(out)
+    assert int((outs[0] != 0).sum()) > 0
+    assert torch.equal(outs[0], outs[1])
