@@ -501,10 +501,8 @@ def run_ours(args):
         fo = smp.plan_info()["fused_ok"]
         # the roofline kernel is the uncounted launch; the step's launch counts detectors
         # (cfg2/cfg3) or measurements: the autotune picks K1 or K7 per mode (plan_info)
-        kernel = {1: "k1_fused", 2: "k5_columns", 3: "k7_queued", 4: "k1_fused",
-                  5: "k7_queued"}.get(fo, "d_segments + k2 product")
-        step_kernel = {1: "k1_fused", 2: "k5_columns", 3: "k7_queued", 4: "k7_queued",
-                       5: "k1_fused"}.get(fo, "d_segments + k2 product")
+        kernel = smp.sampler_kernel(tiled, False)  # the uncounted launch
+        step_kernel = smp.sampler_kernel(tiled, count_kind == "detector")
         int_bound = t_int > t_hbm
         # achieved = algorithmic bytes (HBM-bound) or LOP3 ops (INT-bound) per
         # second of the kernel's CUDA-event time, against the measured peak

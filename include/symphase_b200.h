@@ -245,12 +245,17 @@ int sp_debug_philox(sp_ctx* ctx, const uint32_t* ctr_key, uint32_t* out);
 /* Launch shape and table sizes of the loaded model's fused-sampler plan:
  * {T, gen_warps, cta_threads, staged, row_staged, lp, pad_pred, n_paths,
  *  n_rounds, n_keep, n_segments, n_classes, n_dense, nnz(D), smem_bytes, sampler}
- * with sampler 1 = fused K1, 3 = its queued form K7 (same records; gen_warps /
- * cta_threads are then K7's walker warps / threads), 4 = K7 for launches that
+ * with sampler (of tiled launches) 1 = fused K1, 3 = its queued form K7 (same
+ * records; gen_warps / cta_threads are then K7's walker warps / threads), 4 = K7 for launches that
  * count detectors and K1 for the others, 5 = the reverse (the launch autotune
  * decides per mode), 2 = K5 column sampler (dense M_sym), 0 = draw S +
  * explicit product. */
 int sp_plan_info(sp_ctx* ctx, uint64_t* out16);
+/* Which sampler serves one kind of launch (records tiled or measurement-major,
+ * with or without per-detector counts): 0 draw S + explicit product, 1 fused
+ * K1, 2 K5 column sampler, 3 K7 (the queued form of K1, same records). The
+ * launch autotune decides K1 vs K7 per kind on the first load of a model. */
+int sp_sampler_kernel(sp_ctx* ctx, int tiled, int with_detector_counts, uint32_t* out);
 
 /* Profiling hook: per-role cycle counters of the fused kernel (gen wait,
  * gen work, drain wait, drain work), then walk steps, firings and two

@@ -73,6 +73,7 @@ SIGNATURES = [
     ("sp_debug_philox", _i, [_p, _p, _p]),
     ("sp_debug_timers", _i, [_p, _p]),
     ("sp_plan_info", _i, [_p, _p]),
+    ("sp_sampler_kernel", _i, [_p, _i, _i, _pu32]),
     ("sp_launch_count", _u64, [_p]),
     ("sp_synchronize", _i, [_p]),
 ]

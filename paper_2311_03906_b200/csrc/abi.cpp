@@ -1265,10 +1265,11 @@ void build_plan(sp_ctx* c) {
     // SP_QUEUED: 1 = K7 whenever eligible, 0 = never, unset = the launch
     // autotune times it against K1 and keeps the faster
     d.queued_ok = ok && d.plist_tex != 0 && env_long("SP_QUEUED", -1) != 0;
-    d.queued = d.queued_ok && env_long("SP_QUEUED", -1) == 1;
-    d.queued_dets = d.queued;
-    d.q_walk_dets = d.q_walk;
-    d.q_apply_dets = d.q_apply;
+    d.q_fixed_shape = std::getenv("SP_Q_WALK") != nullptr || std::getenv("SP_Q_APPLY") != nullptr;
+    for (int kd = 0; kd < 4; ++kd) {
+      d.q_sel[kd] = d.queued_ok && env_long("SP_QUEUED", -1) == 1;
+      d.q_shape[kd] = d.q_walk;
+    }
   }
   ptm.mark("uploads");
   {
@@ -1328,7 +1329,7 @@ void build_plan(sp_ctx* c) {
       (d.lp | static_cast<uint64_t>(d.entry_bytes) << 8 | static_cast<uint64_t>(d.cta_threads) << 16 |
        static_cast<uint64_t>(d.n_det != 0) << 32);  // detector counting shifts the tuned split
   static std::mutex tune_mu;
-  // fp -> (gen_warps, pad_pred | unfused << 1 | K7 without / with detector counts << 2, 3 | their 12 + 12 shapes << 8, 9)
+  // fp -> (gen_warps, pad_pred | unfused << 1 | K7 per launch kind << 4..7 | its 12 + 12 shape << 8..11)
   static std::map<uint64_t, std::pair<uint32_t, uint32_t>> tune_cache;
   bool cached = false;
   if (!fix_gw || !fix_pp) {
@@ -1340,10 +1341,10 @@ void build_plan(sp_ctx* c) {
       c->unfused = (it->second.second & 2u) != 0;
       if (d.queued_ok && env_long("SP_QUEUED", -1) < 0) {
         const uint32_t v = it->second.second;
-        d.queued = (v >> 2) & 1u;
-        d.queued_dets = (v >> 3) & 1u;
-        d.q_walk = d.q_apply = ((v >> 8) & 1u) ? 12u : d.q_walk;
-        d.q_walk_dets = d.q_apply_dets = ((v >> 9) & 1u) ? 12u : d.q_walk_dets;
+        for (int kd = 0; kd < 4; ++kd) {
+          d.q_sel[kd] = (v >> (4 + kd)) & 1u;
+          d.q_shape[kd] = ((v >> (8 + kd)) & 1u) ? 12u : 8u;
+        }
       }
       cached = true;
     }
@@ -1366,10 +1367,11 @@ void build_plan(sp_ctx* c) {
     if (d.n_det) ck(cudaMalloc(reinterpret_cast<void**>(&dcnt), d.n_det * 8ull), "cudaMalloc (autotune)");
     ck(cudaEventCreate(&e0), "cudaEventCreate");
     ck(cudaEventCreate(&e1), "cudaEventCreate");
+    bool cal_tiled = true;
     auto launch_once = [&](uint64_t seed) {
       ck(cudaEventRecord(e0, s), "cudaEventRecord");
       // tiled layout: contiguous stores, so the kernel's own balance decides
-      if (launch_fused_sample(d, c->L, seed, 0, cal_shots, buf, ldw, nullptr, true, dcnt) < 0)
+      if (launch_fused_sample(d, c->L, seed, 0, cal_shots, buf, ldw, nullptr, cal_tiled, dcnt) < 0)
         throw CudaError("autotune launch failed");
       ck(cudaEventRecord(e1, s), "cudaEventRecord");
       ck(cudaEventSynchronize(e1), "cudaEventSynchronize");
@@ -1426,41 +1428,41 @@ void build_plan(sp_ctx* c) {
       }
       // K7 (queued) against the tuned K1: same records, so the faster one
       // serves the launches. Two shapes: 8 + 8 warps and 12 + 12 (the rest
-      // drain). Decided separately for launches with and without detector
-      // counts (the drain's share differs).
+      // drain). Decided per launch kind — tiled or measurement-major records,
+      // with or without detector counts (the drain's work and share differ).
       if (d.queued_ok && env_long("SP_QUEUED", -1) < 0) {
-        const bool fix_shape = std::getenv("SP_Q_WALK") != nullptr;
-        std::vector<std::pair<uint32_t, uint32_t>> shapes{{d.q_walk, d.q_apply}};
-        if (!fix_shape) shapes.emplace_back(12u, 12u);
-        auto pick = [&]() {  // -> index into shapes, or -1 for K1
-          d.queued = 0;
-          d.queued_dets = 0;
-          float t_best = time_launch() * 0.98f;  // K7 must win by 2 %
-          int best = -1;
-          d.queued = d.queued_dets = 1;
-          for (size_t i = 0; i < shapes.size(); ++i) {
-            d.q_walk = d.q_walk_dets = shapes[i].first;
-            d.q_apply = d.q_apply_dets = shapes[i].second;
-            const float t = time_launch();
-            if (t < t_best) { t_best = t; best = static_cast<int>(i); }
+        std::vector<uint32_t> shapes{d.q_fixed_shape ? d.q_walk : 8u};
+        if (!d.q_fixed_shape) shapes.push_back(12u);
+        uint64_t* const dcnt_reg = dcnt;
+        for (uint32_t kd = 0; kd < 4; ++kd) {
+          if ((kd & 1u) && !dcnt_reg) {  // no detectors registered: as without counts
+            d.q_sel[kd] = d.q_sel[kd - 1];
+            d.q_shape[kd] = d.q_shape[kd - 1];
+            continue;
           }
-          return best;
-        };
-        int b_dets = -1, b_plain = -1;
-        if (dcnt) b_dets = pick();
-        {
-          uint64_t* const saved = dcnt;
-          dcnt = nullptr;
-          b_plain = pick();
-          dcnt = saved;
+          dcnt = (kd & 1u) ? dcnt_reg : nullptr;
+          cal_tiled = (kd & 2u) != 0;
+          // candidates timed round robin (drift hits all alike), min kept;
+          // 4 to 16 rounds: short launches time noisily
+          std::vector<float> best(shapes.size() + 1, 1e30f);
+          d.q_sel[kd] = 0;
+          const float t0 = launch_once(0x5EED);
+          const int reps = static_cast<int>(std::min(16.f, std::max(4.f, std::ceil(3.f / std::max(t0, 1e-3f)))));
+          for (int rep = 0; rep < reps; ++rep)
+            for (size_t i = 0; i <= shapes.size(); ++i) {
+              d.q_sel[kd] = i > 0;
+              if (i > 0) d.q_shape[kd] = shapes[i - 1];
+              best[i] = std::min(best[i], launch_once(0x5EEDull + 11 * rep + i));
+            }
+          int bi = -1;
+          float t_best = best[0] * 0.98f;  // K7 must win by 2 %
+          for (size_t i = 0; i < shapes.size(); ++i)
+            if (best[i + 1] < t_best) { t_best = best[i + 1]; bi = static_cast<int>(i); }
+          d.q_sel[kd] = bi >= 0;
+          d.q_shape[kd] = shapes[std::max(bi, 0)];
         }
-        if (!dcnt) b_dets = b_plain;
-        d.queued = b_plain >= 0;
-        d.queued_dets = b_dets >= 0;
-        d.q_walk = shapes[std::max(b_plain, 0)].first;
-        d.q_apply = shapes[std::max(b_plain, 0)].second;
-        d.q_walk_dets = shapes[std::max(b_dets, 0)].first;
-        d.q_apply_dets = shapes[std::max(b_dets, 0)].second;
+        dcnt = dcnt_reg;
+        cal_tiled = true;
       }
       // Fused vs unfused (device draw of S + explicit-S product): the same
       // bits for an unmerged model (K1 == M_sym . S of its own draw), so the
@@ -1505,9 +1507,10 @@ void build_plan(sp_ctx* c) {
     if (d.timers) d.timers = c->b_timers.upload(std::vector<long long>(8, 0), s);
     ck(cudaStreamSynchronize(s), "plan upload");
     std::lock_guard<std::mutex> lk(tune_mu);
-    tune_cache[fp] = {d.gen_warps, d.pad_pred | (c->unfused ? 2u : 0u) | (d.queued ? 4u : 0u) |
-                                       (d.queued_dets ? 8u : 0u) | (d.q_walk == 12 ? 256u : 0u) |
-                                       (d.q_walk_dets == 12 ? 512u : 0u)};
+    uint32_t qbits = 0;
+    for (int kd = 0; kd < 4; ++kd)
+      qbits |= (d.q_sel[kd] ? 1u << (4 + kd) : 0u) | (d.q_shape[kd] == 12 ? 1u << (8 + kd) : 0u);
+    tune_cache[fp] = {d.gen_warps, d.pad_pred | (c->unfused ? 2u : 0u) | qbits};
   }
   ptm.mark("autotune");
   build_k5(c, col_ptr, col_rows, ones, events_per_shot, flips_per_shot, n_dense_live);
@@ -2216,26 +2219,40 @@ int sp_synchronize(sp_ctx* ctx) {
 // Launch shape and table sizes of the fused sampler's plan (for reports):
 // {T, gen_warps, cta_threads, staged, row_staged, lp, pad_pred, n_paths,
 //  n_rounds, n_keep, n_seg_live, n_cls_live, n_dense_live, nnz(D), smem bytes,
-//  sampler: 0 draw + product, 1 K1, 2 K5, 3 K7, 4 K7 for launches counting detectors and K1 for the
-//  others, 5 the reverse (gen_warps / cta_threads are K7's walkers / threads when it serves the
+//  sampler (for tiled launches): 0 draw + product, 1 K1, 2 K5, 3 K7, 4 K7 for launches counting
+//  detectors and K1 for the others, 5 the reverse (gen_warps / cta_threads are K7's walkers / threads when it serves the
 //  launches of the registered mode)}
 int sp_plan_info(sp_ctx* ctx, uint64_t* out16) {
   if (!ctx || !out16) return fail(SP_ERR_INVALID_ARGUMENT, "null argument");
   if (int r = set_device(ctx)) return r;
   if (int r = ensure_plan(ctx)) return r;
   const DevPlan& d = ctx->dp;
-  // K7 serves the fused launches: 3 = all of them, 4 = only those counting
+  // K7 serves tiled launches: 3 = all of them, 4 = only those counting
   // detectors (sp_sample_ex), 5 = only the others; 1 = K1 serves all
-  const bool fz = ctx->fused_ok && !ctx->k5_ok;
-  const bool k7p = fz && d.queued, k7d = fz && d.queued_dets;
+  // (sp_sampler_kernel answers for any launch kind)
+  const bool fz = ctx->fused_ok && !ctx->k5_ok && d.queued_ok;
+  const bool k7p = fz && d.q_sel[2], k7d = fz && d.q_sel[3];
   const bool k7 = d.n_det ? k7d : k7p;
+  const uint32_t k7w = d.q_fixed_shape ? d.q_walk : d.q_shape[d.n_det ? 3 : 2];
   const uint64_t sampler = ctx->k5_ok ? 2u : !ctx->fused_ok ? 0u : k7p && k7d ? 3u : k7d ? 4u : k7p ? 5u : 1u;
-  const uint64_t v[16] = {1ull << d.t_log2, k7 ? (d.n_det ? d.q_walk_dets : d.q_walk) : d.gen_warps, k7 ? d.q_threads : d.cta_threads, d.staged, d.row_staged,
+  const uint64_t v[16] = {1ull << d.t_log2, k7 ? k7w : d.gen_warps, k7 ? d.q_threads : d.cta_threads, d.staged, d.row_staged,
                           d.lp, d.pad_pred, d.n_paths, d.n_rounds, d.n_keep, d.n_seg_live,
                           d.n_cls_live, d.n_dense_live, ctx->dnnz,
                           fused_smem_bytes(d, d.t_log2, d.staged, d.row_staged, d.n_buf),
                           sampler};
   std::memcpy(out16, v, sizeof(v));
+  return SP_OK;
+}
+
+// Which sampler serves one kind of sp_sample / sp_sample_tiled / sp_sample_ex
+// launch: 0 draw + product, 1 K1, 2 K5, 3 K7.
+int sp_sampler_kernel(sp_ctx* ctx, int tiled, int with_detector_counts, uint32_t* out) {
+  if (!ctx || !out) return fail(SP_ERR_INVALID_ARGUMENT, "null argument");
+  if (int r = set_device(ctx)) return r;
+  if (int r = ensure_plan(ctx)) return r;
+  const DevPlan& d = ctx->dp;
+  const uint32_t kind = (tiled ? 2u : 0u) | (with_detector_counts ? 1u : 0u);
+  *out = ctx->k5_ok ? 2u : !ctx->fused_ok || ctx->unfused ? 0u : d.queued_ok && d.q_sel[kind] ? 3u : 1u;
   return SP_OK;
 }
 

@@ -603,13 +603,13 @@ int launch_fused_sample(const DevPlan& P, const LaunchCfg& L, uint64_t seed, uin
   const RoundKeys K = expand_keys(seed);
   auto* cnt = reinterpret_cast<unsigned long long*>(counts);
   auto* dcnt = reinterpret_cast<unsigned long long*>(det_counts);
-  if (dcnt ? P.queued_dets : P.queued) {  // K7: same records; falls through to K1 when the rings do not fit
+  // K7: same records; the launch autotune decides per launch kind. Falls
+  // through to K1 when the rings do not fit.
+  const uint32_t kind = (tiled ? 2u : 0u) | (dcnt ? 1u : 0u);
+  if (P.queued_ok && P.q_sel[kind]) {
     int r = 0;
     DevPlan PQ = P;
-    if (dcnt) {
-      PQ.q_walk = P.q_walk_dets;
-      PQ.q_apply = P.q_apply_dets;
-    }
+    if (!P.q_fixed_shape) PQ.q_walk = PQ.q_apply = P.q_shape[kind];
 #define SP_K7T(th, lp, eb)                                                                      \
   (P.row_staged ? k7::launch_k7<th, true, lp, eb>(PQ, L, K, tile0, n_tiles, n_shots, out, ld,   \
                                                   tstride, cnt, dcnt)                           \

@@ -180,13 +180,15 @@ struct DevPlan {
   uint32_t drain_teams = 1;  // drain warps split into teams that take alternate tiles (1 or 2)
   // K7 (k7_queued.cuh), the queued form of the fused sampler: walker warps
   // push firings into shared-memory rings, apply warps XOR their flip lists
-  // (same streams and records as K1). queued = the plan is eligible and K7
-  // serves the launch; q_apply is a multiple of q_walk; a ring holds 2^q_depth_log2 batches.
-  uint32_t queued = 0;
-  // the same choice and shape for launches that count detectors (sp_sample_ex)
-  uint32_t queued_dets = 0, q_walk_dets = 8, q_apply_dets = 8;
-  uint32_t queued_ok = 0;  // the plan is eligible for K7 (the launch autotune decides)
-  uint32_t q_walk = 8, q_apply = 8, q_depth_log2 = 2, q_threads = 1024;
+  // (same streams and records as K1). q_sel[kind] says whether K7 serves a
+  // launch kind (kind = 2 * tiled + counts detectors), with q_shape[kind]
+  // walker (= apply) warps: the launch autotune times K7 against the tuned K1
+  // per kind. q_apply is a multiple of q_walk; a ring holds 2^q_depth_log2 batches.
+  uint32_t queued_ok = 0;  // the plan is eligible for K7
+  uint32_t q_sel[4] = {0, 0, 0, 0};
+  uint32_t q_shape[4] = {8, 8, 8, 8};
+  uint32_t q_fixed_shape = 0;  // SP_Q_WALK / SP_Q_APPLY given: q_walk / q_apply as set
+  uint32_t q_walk = 8, q_apply = 8, q_depth_log2 = 2, q_threads = 1024;  // the launch's shape (set from q_shape)
   uint32_t q_drain_teams = 2;  // K7 has warps to spare for two drain teams
   // Drain stores finished tiles with TMA bulk copies (rows rebuilt in place,
   // then one copy per tile in the tiled layout or one per row segment of

@@ -220,6 +220,15 @@ class Sampler:
         N.check(self._L.sp_plan_info(self._h, C.cast(buf, C.c_void_p)))
         return dict(zip(self.PLAN_FIELDS, (int(x) for x in buf)))
 
+    SAMPLER_KERNELS = {0: "d_segments + k2 product", 1: "k1_fused", 2: "k5_columns", 3: "k7_queued"}
+
+    def sampler_kernel(self, tiled: bool = False, detector_counts: bool = False) -> str:
+        """Kernel that serves one kind of sample / sample_tiled / sample_counted
+        launch (the launch autotune picks K1 or its queued form K7 per kind)."""
+        v = C.c_uint32()
+        N.check(self._L.sp_sampler_kernel(self._h, int(tiled), int(detector_counts), C.byref(v)))
+        return self.SAMPLER_KERNELS[int(v.value)]
+
     @property
     def launches(self) -> int:
         return int(self._L.sp_launch_count(self._h))

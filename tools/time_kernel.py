@@ -65,7 +65,8 @@ def main():
                       "ms_median": ms,
                       "ms_min": ts[0], "GBps": bytes_ / ms / 1e6,
                       "bits_per_s": init.n_meas * n / ms * 1e3, "timers": timers,
-                      "plan": s.plan_info()}))
+                      "plan": s.plan_info(),
+                      "kernel": s.sampler_kernel(a.tiled, a.dets)}))
 
 
 if __name__ == "__main__":
