@@ -10,11 +10,16 @@
 //     as one 16-byte shared store per lane into the warp's ring (a batch =
 //     one walk step = up to 128 firings, plus a header word: valid count and
 //     the longest list of the step's length run);
-//   * apply warps pop batches, load the four flip lists of their lane and XOR
-//     them into the tile with shared atomics. Their state is tiny, so many of
-//     them are resident and the list latency hides behind other warps;
-//   * drain warps are K1's (k1_drain.inc).
-// All roles fit 64 registers, so a CTA runs 1,024 threads (50 % occupancy).
+//   * apply warps wait for a free tile buffer, make the tile's fair-coin
+//     words, then pop batches, fetch the four flip lists of their lane through
+//     the texture pipe and XOR them into the tile with shared atomics. Their
+//     state is tiny, so many of them are resident and the list latency hides
+//     behind other warps;
+//   * drain warps are K1's (k1_drain.inc), in two teams on alternate tiles.
+// Walkers never touch a tile, so they run ahead of the apply warps by the ring
+// depth, across tile boundaries. All roles fit 64 registers, so a CTA runs
+// 1,024 threads (50 % occupancy). The launch autotune (abi.cpp) times K7
+// against K1 per launch kind and keeps the faster (K7).
 // Only for plans whose live classes are all one-list Bernoulli (mechanism)
 // classes with exact flip lists of at most four u32 words; other plans run K1.
 #pragma once
